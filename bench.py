@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the element-based P1 hot path (BASELINE.json metric, config C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): 2D P1 triangles on the unit square at level 11
+(n_n = 4,198,401, n_e = 8,388,608), node numbering randomly permuted from the seed,
+x ~ U[-1,1], nu = 1, f = 1; one step = one element-based residual r = b - A x.
+Prints ONE JSON line (rank 0).  `value` = GDoF/s with inputs resident in HBM, timed with
+CUDA events over exactly K steps; `e2e` = the same through the public API
+(`residual(batch, x_host)`) with the host->device copy of x and the device->host copy of r
+inside the timed region.  `--impl reference` times the CPU oracle port of the reference
+residual (oracle/, NumPy, all host threads) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+METRIC = "element matvec GDoF/s & HBM GB/s (fraction of peak); PCG iterations/sec"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+def residual_bytes(n_n, n_e, nb=3):
+    """matvec n_e(8 nb^2 + 4 nb) + 16 n_n, residual + 8 n_n (b pre-assembled)."""
+    return n_e * (8 * nb * nb + 4 * nb) + 24 * n_n
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) in a thread while running."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index=0, period=0.01):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        self._ok = False
+        self._gate = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            self._ok = False
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            if self._gate.is_set():
+                try:
+                    mhz = self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM)
+                    r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                    self.samples.append(mhz)
+                    self.reasons |= int(r)
+                except Exception:
+                    pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self._ok:
+            self._t.start()
+        return self
+
+    def on(self):
+        self._gate.set()
+
+    def off(self):
+        self._gate.clear()
+
+    def stop(self):
+        self._stop.set()
+        if self._ok:
+            self._t.join(timeout=1.0)
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- CPU oracle --
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_residual_rate(A, b_e, indt, x, budget_s=10.0, min_calls=3, threads=None):
+    """Time oracle.residual (the reference algorithm, NumPy, T threads) for ~budget_s."""
+    import oracle as o
+    T = threads or cpu_threads()
+    o.residual(A, b_e, indt, x, threads=T)  # warm
+    t0 = time.perf_counter()
+    calls = 0
+    while calls < min_calls or time.perf_counter() - t0 < budget_s:
+        o.residual(A, b_e, indt, x, threads=T)
+        calls += 1
+    dt = time.perf_counter() - t0
+    return x.shape[0] * calls / dt / 1e9, T, calls, dt
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (CPU oracle port) on this host."""
+    import numpy as np
+    import oracle as o
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    size = args.size if args.size is not None else None
+    t_setup = time.perf_counter()
+    inp = o.config_inputs(2, seed=args.seed, size=size)
+    _, _, A, b_e = o.element_matrices(inp["nodes"], inp["elements"], nu=inp["nu"])
+    indt = np.ascontiguousarray(inp["elements"].T)
+    x = inp["x"]
+    T = cpu_threads()
+    setup = time.perf_counter() - t_setup
+    for _ in range(args.warmup):
+        o.residual(A, b_e, indt, x, threads=T)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.residual(A, b_e, indt, x, threads=T)
+    dt = time.perf_counter() - t0
+    n_n, n_e = x.shape[0], indt.shape[1]
+    value = n_n * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE C2 recipe)",
+        "config": workload_config(n_n, n_e, args, mode="reference order (bincount)"),
+        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": T, "kind": "port",
+                         "sample": f"{args.steps} full C2 residuals (oracle/ebs_oracle.py "
+                                   f"residual, deterministic chunked mode, {T} threads)"},
+        "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "setup_s": setup,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n_n, n_e, args, mode):
+    return {"workload": "C2: 2D P1 unit square, level 11, permuted node numbering, "
+                        "x~U[-1,1], nu=1, f=1; element residual r=b-Ax per step",
+            "n_nodes": n_n, "n_elements": n_e, "seed": args.seed, "mode": mode,
+            "l2": "inputs larger than L2 (slot stream ~1 GB vs 126 MB L2); no flush",
+            "parallelism": f"element slabs x{args.gpus}" if args.gpus > 1 else "single GPU"}
+
+
+# ---------------------------------------------------------------- GPU arm --
+def run_ours(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import _device as D
+    from paper_1911_03973_b200._lib import load
+    from paper_1911_03973_b200.inputs import config_problem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_1911_03973_b200 import dist
+        return dist.bench_rank(args, rank, world, local)
+    torch.cuda.set_device(local)
+    peaks, peak_kind = load_peaks()
+    sampler = ClockSampler(index=local).start()
+
+    t_setup = time.perf_counter()
+    p = config_problem(2, seed=args.seed, size=args.size)
+    batch, m = p["batch"], p["mesh"]
+    n_n, n_e = m.n_nodes, m.n_elements
+    pl = batch.operator(n_n)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t_setup
+    lib = load()
+    h = pl.handle
+    x_np = p["x"]
+    x_dev = torch.from_numpy(x_np).cuda()
+    x_int = D.empty(n_n)
+    r_dev = D.empty(n_n)
+    stream = torch.cuda.current_stream()
+    s = ctypes.c_void_p(stream.cuda_stream)
+    xp, xip, rp = (ctypes.c_void_p(t.data_ptr()) for t in (x_dev, x_int, r_dev))
+
+    def step(op):
+        lib.ebs_to_internal(h, xp, xip, None, s)
+        lib.ebs_plan_apply(h, op, xip, rp, 1, 0, s)
+
+    def timed(op, K):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        n0 = lib.ebs_launch_count()
+        e0.record(stream)
+        for k in range(K):
+            evs[k][0].record(stream)
+            lib.ebs_to_internal(h, xp, xip, None, s)
+            evs[k][1].record(stream)
+            lib.ebs_plan_apply(h, op, xip, rp, 1, 0, s)
+            evs[k][2].record(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        launches = lib.ebs_launch_count() - n0
+        total = e0.elapsed_time(e1) / 1e3
+        gather = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
+        sell = statistics.mean(ev[1].elapsed_time(ev[2]) for ev in evs) / 1e3
+        return total, gather, sell, launches
+
+    # warm-up: W steps, then keep the clocks busy for ~1 s before timing
+    for _ in range(max(3, args.warmup)):
+        step(1)
+    torch.cuda.synchronize()
+    sampler.on()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 1.0:
+        for _ in range(20):
+            step(1)
+        torch.cuda.synchronize()
+    total, gather, sell, launches = timed(1, args.steps)
+    total_ex, gather_ex, sell_ex, _ = timed(2, args.steps)
+    sampler.off()
+    r_fast = r_dev.clone()
+
+    # end to end through the public API: pinned host x in, host r out
+    x_host = torch.from_numpy(x_np).pin_memory()
+    r_host = torch.empty(n_n, dtype=torch.float64).pin_memory()
+    for _ in range(max(3, args.warmup)):
+        r_host.copy_(eb.residual(batch, x_host, deterministic=False), non_blocking=True)
+    torch.cuda.synchronize()
+    sampler.on()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        r_host.copy_(eb.residual(batch, x_host, deterministic=False), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall_e2e = time.perf_counter() - t0
+    sampler.off()
+    sampler.stop()
+    t_e2e = e0.elapsed_time(e1) / 1e3
+    assert torch.equal(r_host, r_fast.cpu()), "public API and C-ABI paths disagree"
+
+    bytes_alg = residual_bytes(n_n, n_e)
+    value = n_n * args.steps / total / 1e9
+    achieved = bytes_alg / sell / 1e9
+    peak = float(peaks["hbm_gbs"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get("k_sell_op<3,1>")
+    except Exception:
+        pass
+
+    cpu = None
+    if not args.no_cpu:
+        import oracle  # noqa: F401  (CPU baseline only)
+        A = batch.A_e.permute(2, 0, 1).contiguous().cpu().numpy().transpose(1, 2, 0)
+        b_e = batch.b_e.cpu().numpy()
+        indt = batch.index.indt.cpu().numpy().astype(np.int64)
+        rate, T, calls, dt = oracle_residual_rate(A, b_e, indt, x_np, budget_s=args.cpu_budget)
+        cpu = {"value": rate, "unit": "GDoF/s", "cores": T, "kind": "port",
+               "sample": f"{calls} full C2 residuals in {dt:.1f} s (oracle/ebs_oracle.py residual, "
+                         f"reference algorithm, {T} threads)"}
+
+    extra = {}
+    if args.extra:
+        extra = solver_extras(args)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 mesh, x~U[-1,1])",
+        "config": workload_config(n_n, n_e, args, mode="fast (pre-assembled b)"),
+        "hbm_gbs_algorithmic": bytes_alg / (total / args.steps) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_sell_op<3,1> (fused gather-product-ordered-sum)",
+                     "bytes_per_launch": bytes_alg, "kernel_ms": sell * 1e3,
+                     "gather_kernel_ms": gather * 1e3, "peak_source": peak_kind},
+        "exact_mode": {"value": n_n * args.steps / total_ex / 1e9, "unit": "GDoF/s",
+                       "kernel_ms": sell_ex * 1e3,
+                       "note": "bit-identical to ebsolve.residual (b_e streamed per slot)"},
+        "e2e": {"value": n_n * args.steps / t_e2e / 1e9, "unit": "GDoF/s",
+                "h2d_bytes_per_step": 8 * n_n, "d2h_bytes_per_step": 8 * n_n,
+                "wall_s": wall_e2e, "api": "paper_1911_03973_b200.residual(batch, x_pinned_host, "
+                                           "deterministic=False) + copy to pinned host"},
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+        "cpu_baseline": cpu,
+        "setup_s": setup,
+    }
+    if extra:
+        line["solvers"] = extra
+    print(json.dumps(line), flush=True)
+
+
+def solver_extras(args):
+    """Solver throughput on the other BASELINE configs (C3 JPCG, C4 Jacobi, C5 JPCG)."""
+    import numpy as np
+    import torch
+
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    out = {}
+    peaks, _ = load_peaks()
+    for cfg, iters, tol in ((3, 20000, 1e-8), (4, 200, None), (5, 500, None)):
+        if cfg not in args.solver_configs:
+            continue
+        try:
+            t0 = time.perf_counter()
+            p = config_problem(cfg, seed=args.seed)
+            batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+            pl = batch.operator(m.n_nodes)
+            pl.ensure_dirichlet(d)
+            torch.cuda.synchronize()
+            setup = time.perf_counter() - t0
+            x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+            solve = (lambda: eb.jacobi(batch, d, x0, iters, omega=0.8)) if cfg == 4 else \
+                (lambda: eb.pcg(batch, d, x0, iters, tol=tol))
+            solve() if cfg != 3 else eb.pcg(batch, d, x0, 5)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            x, h = solve()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            its = h.iterations
+            nb = m.n_b
+            n_n, n_e = m.n_nodes, m.n_elements
+            per_it = n_e * (8 * nb * nb + 4 * nb) + (32 if cfg == 4 else 104) * n_n
+            out[f"C{cfg}"] = {
+                "method": "jacobi" if cfg == 4 else "pcg", "iterations": its,
+                "it_per_s": its / t, "ms_per_it": t / its * 1e3,
+                "hbm_gbs_algorithmic": per_it * its / t / 1e9,
+                "frac_of_peak": per_it * its / t / 1e9 / float(peaks["hbm_gbs"]),
+                "final_rel_residual": float(h.residual_norms[-1] / h.residual_norms[0]),
+                "n_nodes": n_n, "n_elements": n_e, "setup_s": setup}
+            del p, batch, pl, x
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, never kill the headline line
+            out[f"C{cfg}"] = {"error": f"{type(e).__name__}: {e}"}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--size", type=int, default=None, help="override the C2 level")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--extra", action="store_true", help="also time C3/C4/C5 solvers")
+    ap.add_argument("--solver-configs", type=int, nargs="*", default=[3, 4, 5])
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

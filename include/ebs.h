@@ -1,0 +1,208 @@
+/*
+ * ebs.h -- C-ABI of libebs.so, the B200 (sm_100a) element-based P1 solver path.
+ *
+ * The reference (arXiv 1911.03973, package `ebsolve`, /root/reference/pkg/src/ebsolve)
+ * is pure Python/NumPy and has no FFI; its Python functions ARE the operator API
+ * (SURVEY.md 8b).  Each entry point below replaces one of those functions (cited
+ * as `file.py:line`); the Python package `paper_1911_03973_b200` binds this header
+ * with ctypes and maps it back to the reference signatures.
+ *
+ * Conventions
+ *   - Every function returns an int status: EBS_OK (0) or a negative EBS_E* code;
+ *     ebs_last_error() returns the message of the calling thread's last failure.
+ *     No C++ exception crosses this boundary.
+ *   - All array pointers are DEVICE pointers owned by the caller (torch); the library
+ *     never frees caller memory.  `stream` is a cudaStream_t (NULL = legacy default).
+ *     Calls are asynchronous on `stream` unless stated otherwise.
+ *   - Connectivity is int32 structure-of-arrays `conn[j*n_e + e]` (j = local vertex),
+ *     i.e. the reference `indt` (mesh.py:151-154) narrowed to int32.
+ *   - Element matrices are element-major `A[(e*nb + i)*nb + j]`, the memory behind the
+ *     reference's (nb, nb, n_e) views (elements.py:86,93); b_e is SoA `b_e[j*n_e + e]`
+ *     (elements.py:112).  nb = dim + 1 (3 triangles, 4 tetrahedra).
+ *   - Vectors passed to operators are in the caller's node numbering; the plan keeps its
+ *     own locality-ordered internal numbering and converts at the boundary.
+ *   - Arithmetic is IEEE fp64 without FMA contraction (the library is compiled with
+ *     -fmad=false) so results can be bit-identical to the NumPy reference.
+ */
+#ifndef EBS_H
+#define EBS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EBS_OK 0
+#define EBS_EINVAL (-1)      /* invalid argument -> ValueError            */
+#define EBS_ENOMEM (-2)      /* device allocation failed -> MemoryError   */
+#define EBS_ECUDA (-3)       /* CUDA runtime error -> RuntimeError        */
+#define EBS_ENCCL (-4)       /* collective failure -> RuntimeError        */
+#define EBS_ENONFINITE (-5)  /* non-finite input -> ValueError            */
+#define EBS_EDEGENERATE (-6) /* degenerate element -> ValueError          */
+#define EBS_ECALLBACK (-7)   /* user callback asked to stop               */
+
+typedef struct ebs_plan *ebs_plan_t;
+
+/* residual modes (ebs_residual) */
+#define EBS_RES_EXACT 0 /* sum_e C_e^T (b_e - A_e x_e), reference order (operators.py:98) */
+#define EBS_RES_FAST 1  /* b - sum_e C_e^T A_e x_e with pre-assembled b            */
+
+/* solver methods (ebs_solve) */
+#define EBS_RICHARDSON 0 /* solvers.py:163-183                                   */
+#define EBS_JACOBI 1     /* damped Jacobi on the solvers.py:117-160 loop (NEW)   */
+#define EBS_CG 2         /* conjugate gradients (NEW)                            */
+#define EBS_PCG 3        /* Jacobi-preconditioned CG (NEW)                       */
+
+int ebs_version(void);
+int ebs_last_error(char *buf, size_t len);
+/* number of this library's kernels launched so far (process-wide counter) */
+int64_t ebs_launch_count(void);
+
+/* ------------------------------------------------------------------ mesh ---- */
+/* mesh.py:104-128 build_grid_mesh: n nodes per side; nodes (n*n, 2) row-major,
+ * conn SoA (3, 2(n-1)^2) with per cell lower (ll,ll+1,ll+n+1), upper (ll,ll+n+1,ll+n). */
+int ebs_mesh_grid2d(int64_t n, double *nodes, int32_t *conn, void *stream);
+/* NEW (no reference): unit cube, N cells/side, 6 Kuhn tets per cube (oracle/ebs_oracle.py
+ * kuhn_cube_mesh); nodes ((N+1)^3, 3), conn SoA (4, 6N^3). */
+int ebs_mesh_kuhn3d(int64_t N, double *nodes, int32_t *conn, void *stream);
+/* mesh.py:145-148 _detect_boundary (which=0: any coordinate within 1e-12 of 0 or 1)
+ * or the z=0 face (which=1, BASELINE C3/C5).  flags[n] = 1/0. */
+int ebs_mesh_flags(int dim, int64_t n_n, const double *nodes, int which, uint8_t *flags,
+                   void *stream);
+/* mesh.py:39-52 Mesh.__post_init__ checks: counts[0] = #connectivity entries out of
+ * [0, n_n), counts[1] = #elements with signed measure <= 0 (device int64[2], zeroed here). */
+int ebs_mesh_check(int dim, int64_t n_n, int64_t n_e, const double *nodes,
+                   const int32_t *conn, int64_t *counts, void *stream);
+/* signed area (mesh.py:96-101) / volume per element */
+int ebs_mesh_measure(int dim, int64_t n_e, const double *nodes, const int32_t *conn,
+                     double *measure, void *stream);
+/* NEW: relabel nodes, new id of old node i = perm[i] (BASELINE C2/C4 recipe). */
+int ebs_mesh_permute(int dim, int64_t n_n, int64_t n_e, const int64_t *perm,
+                     const double *nodes, const int32_t *conn, double *nodes_out,
+                     int32_t *conn_out, void *stream);
+/* elements.py:107 centroids p.mean(axis=1) = ((p0+p1)+p2)/3 [+p3 ../4]; out (n_e, dim). */
+int ebs_centroids(int dim, int64_t n_e, const double *nodes, const int32_t *conn,
+                  double *out, void *stream);
+
+/* -------------------------------------------------------------- assembly ---- */
+/* elements.py:56-137 local_{stiffness,mass,load}_batch + combine_system, fused:
+ * K_e = meas * G^T G, M_e = meas * pattern, A_e = K_e + nu*M_e,
+ * b_e[j] = (f*meas)/nb with f = f_vals[e] (nullable -> f_const).  Any output may be NULL.
+ * n_degenerate (device int64, zeroed here) counts elements with measure <= EPS
+ * (elements.py:67-71); the caller raises ValueError when it is non-zero. */
+int ebs_assemble_p1(int dim, int64_t n_e, const double *nodes, const int32_t *conn,
+                    double nu, const double *f_vals, double f_const, double *K_e,
+                    double *M_e, double *A_e, double *b_e, int64_t *n_degenerate,
+                    void *stream);
+/* elements.py:115-121 combine_system: A = K + nu*M over count doubles. */
+int ebs_combine(int64_t count, const double *K_e, const double *M_e, double nu, double *A_e,
+                void *stream);
+
+/* ------------------------------------------------------------------ plan ---- */
+/* Build the execution plan of a mesh (synchronous on `stream`): node->(j,e) incidence in
+ * the bincount order j*n_e+e (operators.py:98), a first-appearance internal node
+ * numbering and the SELL-32 slot layout the operator kernels stream.  The plan owns its
+ * device workspace; destroy releases it. */
+int ebs_plan_create(int nb, int64_t n_nodes, int64_t n_elems, const int32_t *conn,
+                    void *stream, ebs_plan_t *out);
+int ebs_plan_destroy(ebs_plan_t plan);
+/* info[0]=n_nodes info[1]=n_elems info[2]=nb info[3]=n_chunks info[4]=n_rows
+ * info[5]=slot bytes resident  info[6]=max valence  info[7]=loaded flags */
+int ebs_plan_info(ebs_plan_t plan, int64_t *info);
+/* copy the internal numbering maps out (device int32 arrays of n_nodes) */
+int ebs_plan_node_maps(ebs_plan_t plan, int32_t *new_of_old, int32_t *old_of_new,
+                       void *stream);
+/* Load an operator: pack A_e (element-major) rows into the slot stream; when b_e is
+ * non-NULL also pack it per slot (exact residual) and pre-assemble b (fast residual). */
+int ebs_plan_load(ebs_plan_t plan, const double *A_e, const double *b_e, void *stream);
+/* operators.py:29-55 DirichletData.nd (caller numbering, any order): the constrained set
+ * used by masked operators and solvers.  n_d = 0 clears it. */
+int ebs_plan_set_dirichlet(ebs_plan_t plan, const int64_t *nd, int64_t n_d, void *stream);
+
+/* ------------------------------------------------------------- operators ---- */
+/* operators.py:72-111 residual: r = b - A x (mode EBS_RES_EXACT reproduces the reference
+ * bit for bit; EBS_RES_FAST uses the pre-assembled b).  masked != 0 also applies
+ * mask_dirichlet (operators.py:114-118).  nonfinite (device int32, nullable) is set to
+ * 1 when x has a non-finite entry (operators.py:90-91). */
+int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int masked,
+                 int32_t *nonfinite, void *stream);
+/* spectrum.py:54-61 _apply_masked: y = A x in (j,e) order; masked != 0 zeroes y[nd]. */
+int ebs_matvec(ebs_plan_t plan, const double *x, double *y, int masked, void *stream);
+/* NEW diag(A) = assemble_rhs(stack_j A_e[j,j,:]), caller numbering. */
+int ebs_diagonal(ebs_plan_t plan, double *d, void *stream);
+/* operators.py:58-63 assemble_rhs: b = bincount(indt, b_e) in (j,e) order; needs only
+ * the plan's structure (no load). */
+int ebs_assemble_rhs(ebs_plan_t plan, const double *b_e, double *b, void *stream);
+/* operators.py:114-118 mask_dirichlet on a caller-numbered vector: out = v, out[nd] = 0. */
+int ebs_mask(int64_t n, const double *v, int64_t n_d, const int64_t *nd, double *out,
+             void *stream);
+/* Internal-numbering access (bench timing, multi-GPU driver).  The plan's internal node
+ * order is first appearance over (e, j); vectors in that order are "internal".
+ * ebs_to_internal: x_int[m] = x[old_of_new[m]] (+ non-finite flag, nullable);
+ * ebs_to_user: v[old_of_new[m]] = v_int[m]. */
+int ebs_to_internal(ebs_plan_t plan, const double *x, double *x_int, int32_t *nonfinite,
+                    void *stream);
+int ebs_to_user(ebs_plan_t plan, const double *v_int, double *v, void *stream);
+/* One SELL pass on internal vectors: op = 0 matvec, 1 fast residual, 2 exact residual;
+ * out_user != 0 scatters the result to caller numbering, else writes internal order;
+ * masked != 0 zeroes constrained rows. */
+int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, int out_user,
+                   int masked, void *stream);
+/* all-finite check (operators.py:90): *flag (device int32) = 1 if any non-finite. */
+int ebs_check_finite(int64_t n, const double *v, int32_t *flag, void *stream);
+
+/* ----------------------------------------------------------- vector work ---- */
+/* deterministic (fixed-order, launch-size independent of the device) reductions */
+int ebs_dot(int64_t n, const double *x, const double *y, double *out, void *stream);
+int ebs_nrm2(int64_t n, const double *x, double *out, void *stream);
+/* y = a*x + b*y */
+int ebs_axpby(int64_t n, double a, const double *x, double b, double *y, void *stream);
+
+/* --------------------------------------------------------------- solvers ---- */
+/* The solvers.py:117-160 loop (_iterate) run on the device: per iteration one fused
+ * element-operator pass plus vector work, norms kept on the device and read once at
+ * the end.  Richardson: x += omega*r (solvers.py:179-180), omega = 2/(l1+l2) given by the
+ * caller.  Jacobi: x += omega*(dinv*r).  CG / PCG: see oracle/ebs_oracle.py pcg().
+ * Iterates, history and divergence semantics follow _iterate (history length
+ * n_norms <= iters+1, tol relative to ||r_0||, divergence is a flag, never an error). */
+typedef int (*ebs_callback_t)(void *user, int k);
+
+typedef struct {
+    int method;              /* EBS_RICHARDSON / EBS_JACOBI / EBS_CG / EBS_PCG           */
+    int iters;               /* >= 0                                                     */
+    int exact;               /* residual mode for Richardson/Jacobi (1 = EBS_RES_EXACT)  */
+    int has_tol;             /* tol is not None                                          */
+    double tol;              /* stop when ||r_k|| <= tol*||r_0|| (solvers.py:135)        */
+    double omega;            /* Richardson / Jacobi step                                 */
+    const double *x0;        /* device, caller numbering (copied, never written)          */
+    double *x;               /* device out, caller numbering                             */
+    const double *reference; /* device, nullable: error norms ||x_k - reference||         */
+    double *norms;           /* HOST out, iters+1 entries                                 */
+    double *errors;          /* HOST out, iters+1 entries (when reference != NULL)        */
+    int *n_norms;            /* HOST out: recorded history length                         */
+    int *diverged;           /* HOST out                                                  */
+    ebs_callback_t callback; /* nullable: called as callback(user, k) after x_k and r_k   */
+    void *user;              /*   were copied into cb_x / cb_r (device, caller numbering); */
+    double *cb_x;            /*   a non-zero return stops the solve with EBS_ECALLBACK     */
+    double *cb_r;
+    double *r_out;           /* device, nullable: final residual (caller numbering)       */
+} ebs_solve_params;
+
+/* synchronous on `stream` (one host read of the history at the end) */
+int ebs_solve(ebs_plan_t plan, const ebs_solve_params *params, void *stream);
+
+/* ------------------------------------------------------------ multi-GPU ---- */
+/* Element-slab partition helpers.  A rank's plan is built on its element
+ * slab with its local node numbering; interface partial sums are exchanged by the host
+ * (torch.distributed / NCCL over NVLink) through these pack/unpack kernels.
+ * buf[i] = v[idx[i]]                                                          */
+int ebs_gather(int64_t n, const int64_t *idx, const double *v, double *buf, void *stream);
+/* v[idx[i]] += buf[i]  (idx entries unique)                                   */
+int ebs_scatter_add(int64_t n, const int64_t *idx, const double *buf, double *v, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EBS_H */

@@ -1,0 +1,139 @@
+"""ctypes binding of libebs.so (include/ebs.h).
+
+The library is built in-tree (``paper_1911_03973_b200/libebs.so``, see
+``csrc/Makefile`` / ``__graft_entry__.build``).  Loading it needs no GPU; every
+compute entry point does.  There is no CPU fallback: when the library or the
+device is missing, the first call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int, c_int64, c_size_t, c_void_p, c_char_p
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libebs.so")
+
+EBS_OK = 0
+EBS_EINVAL = -1
+EBS_ENOMEM = -2
+EBS_ECUDA = -3
+EBS_ENCCL = -4
+EBS_ENONFINITE = -5
+EBS_EDEGENERATE = -6
+EBS_ECALLBACK = -7
+
+EBS_RES_EXACT = 0
+EBS_RES_FAST = 1
+
+EBS_RICHARDSON = 0
+EBS_JACOBI = 1
+EBS_CG = 2
+EBS_PCG = 3
+
+CALLBACK = ctypes.CFUNCTYPE(c_int, c_void_p, c_int)
+
+
+class SolveParams(ctypes.Structure):
+    """Mirror of ebs_solve_params (include/ebs.h)."""
+    _fields_ = [
+        ("method", c_int), ("iters", c_int), ("exact", c_int), ("has_tol", c_int),
+        ("tol", c_double), ("omega", c_double),
+        ("x0", c_void_p), ("x", c_void_p), ("reference", c_void_p),
+        ("norms", POINTER(c_double)), ("errors", POINTER(c_double)),
+        ("n_norms", POINTER(c_int)), ("diverged", POINTER(c_int)),
+        ("callback", CALLBACK), ("user", c_void_p), ("cb_x", c_void_p), ("cb_r", c_void_p),
+        ("r_out", c_void_p),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/ebs.h
+SIGNATURES = {
+    "ebs_version": (c_int, []),
+    "ebs_last_error": (c_int, [c_char_p, c_size_t]),
+    "ebs_launch_count": (c_int64, []),
+    "ebs_mesh_grid2d": (c_int, [c_int64, c_void_p, c_void_p, c_void_p]),
+    "ebs_mesh_kuhn3d": (c_int, [c_int64, c_void_p, c_void_p, c_void_p]),
+    "ebs_mesh_flags": (c_int, [c_int, c_int64, c_void_p, c_int, c_void_p, c_void_p]),
+    "ebs_mesh_check": (c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_mesh_measure": (c_int, [c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_mesh_permute": (c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p, c_void_p]),
+    "ebs_centroids": (c_int, [c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_assemble_p1": (c_int, [c_int, c_int64, c_void_p, c_void_p, c_double, c_void_p,
+                                c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p]),
+    "ebs_combine": (c_int, [c_int64, c_void_p, c_void_p, c_double, c_void_p, c_void_p]),
+    "ebs_plan_create": (c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, POINTER(c_void_p)]),
+    "ebs_plan_destroy": (c_int, [c_void_p]),
+    "ebs_plan_info": (c_int, [c_void_p, POINTER(c_int64)]),
+    "ebs_plan_node_maps": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_plan_load": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_plan_set_dirichlet": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "ebs_residual": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "ebs_matvec": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+    "ebs_diagonal": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ebs_assemble_rhs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_mask": (c_int, [c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ebs_check_finite": (c_int, [c_int64, c_void_p, c_void_p, c_void_p]),
+    "ebs_to_internal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_to_user": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_plan_apply": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p]),
+    "ebs_dot": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_nrm2": (c_int, [c_int64, c_void_p, c_void_p, c_void_p]),
+    "ebs_axpby": (c_int, [c_int64, c_double, c_void_p, c_double, c_void_p, c_void_p]),
+    "ebs_solve": (c_int, [c_void_p, POINTER(SolveParams), c_void_p]),
+    "ebs_gather": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_scatter_add": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+}
+
+_lib = None
+
+
+class EbsError(RuntimeError):
+    pass
+
+
+def load():
+    """Load libebs.so (no GPU needed); raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (or `make -C paper_1911_03973_b200/csrc`). There is no CPU fallback.")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(1024)
+    load().ebs_last_error(buf, 1024)
+    return buf.value.decode(errors="replace")
+
+
+def check(code: int, what: str = ""):
+    if code == EBS_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if code in (EBS_EINVAL, EBS_ENONFINITE, EBS_EDEGENERATE):
+        raise ValueError(msg)
+    if code == EBS_ENOMEM:
+        raise MemoryError(msg)
+    raise EbsError(f"[{code}] {msg}")
+
+
+def call(name: str, *args):
+    """Call an ebs_* entry point and map its status to a Python exception."""
+    check(getattr(load(), name)(*args), name)
+
+
+def launch_count() -> int:
+    return int(load().ebs_launch_count())

@@ -1,0 +1,186 @@
+// common.cu -- error reporting, launch counter and small vector kernels of libebs.so.
+#include <atomic>
+#include <cstdarg>
+
+#include "ebs_internal.cuh"
+
+namespace ebs {
+
+static thread_local char g_err[1024] = {0};
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int64_t bump_launches(int64_t n) { return g_launches.fetch_add(n) + n; }
+
+// ------------------------------------------------------------- kernels ------
+__global__ void k_dot(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
+                      double *partials, unsigned int *counter, double *out, int sqrt_it) {
+    double v[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[0] += x[i] * y[i];
+    double tot[1];
+    if (grid_sum_last<1>(v, partials, counter, tot) && threadIdx.x == 0)
+        *out = sqrt_it ? sqrt(tot[0]) : tot[0];
+}
+
+__global__ void k_axpby(int64_t n, double a, const double *__restrict__ x, double b,
+                        double *__restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = a * x[i] + b * y[i];
+}
+
+__global__ void k_mask(int64_t n, const double *__restrict__ v, int64_t n_d,
+                       const int64_t *__restrict__ nd, double *__restrict__ out, int pass) {
+    if (pass == 0) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x)
+            out[i] = v[i];
+    } else {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_d;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            int64_t k = nd[i];
+            if (k >= 0 && k < n) out[k] = 0.0;
+        }
+    }
+}
+
+__global__ void k_check_finite(int64_t n, const double *__restrict__ v, int32_t *flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(v[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_gather(int64_t n, const int64_t *__restrict__ idx,
+                         const double *__restrict__ v, double *__restrict__ buf) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = v[idx[i]];
+}
+
+__global__ void k_scatter_add(int64_t n, const int64_t *__restrict__ idx,
+                              const double *__restrict__ buf, double *__restrict__ v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[idx[i]] += buf[i];
+}
+
+// scratch for the standalone reductions (one per device is enough: stream-ordered use)
+static double *g_partials = nullptr;
+static unsigned int *g_counter = nullptr;
+
+void reduce_scratch(double **partials, unsigned int **counter) {
+    if (!g_partials) {
+        CU(cudaMalloc(&g_partials, sizeof(double) * 4 * RED_MAX_BLOCKS));
+        CU(cudaMalloc(&g_counter, sizeof(unsigned int) * 4));
+        CU(cudaMemset(g_counter, 0, sizeof(unsigned int) * 4));
+    }
+    *partials = g_partials;
+    *counter = g_counter;
+}
+
+}  // namespace ebs
+
+using namespace ebs;
+
+extern "C" {
+
+int ebs_version(void) { return 100; }
+
+int ebs_last_error(char *buf, size_t len) {
+    if (!buf || len == 0) return EBS_EINVAL;
+    strncpy(buf, g_err, len - 1);
+    buf[len - 1] = 0;
+    return EBS_OK;
+}
+
+int64_t ebs_launch_count(void) { return g_launches.load(); }
+
+int ebs_dot(int64_t n, const double *x, const double *y, double *out, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && out, "ebs_dot: bad arguments");
+    double *partials;
+    unsigned int *counter;
+    reduce_scratch(&partials, &counter);
+    k_dot<<<grid_for(n, RED_BLOCK, RED_MAX_BLOCKS), RED_BLOCK, 0, S(stream)>>>(
+        n, x, y, partials, counter, out, 0);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_nrm2(int64_t n, const double *x, double *out, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && out, "ebs_nrm2: bad arguments");
+    double *partials;
+    unsigned int *counter;
+    reduce_scratch(&partials, &counter);
+    k_dot<<<grid_for(n, RED_BLOCK, RED_MAX_BLOCKS), RED_BLOCK, 0, S(stream)>>>(
+        n, x, x, partials, counter, out, 1);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_axpby(int64_t n, double a, const double *x, double b, double *y, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0, "ebs_axpby: bad n");
+    if (n == 0) return EBS_OK;
+    k_axpby<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, a, x, b, y);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_mask(int64_t n, const double *v, int64_t n_d, const int64_t *nd, double *out,
+             void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && n_d >= 0, "ebs_mask: bad sizes");
+    if (n > 0 && v != out) {
+        k_mask<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, v, n_d, nd, out, 0);
+        LAUNCHED();
+    }
+    if (n_d > 0) {
+        k_mask<<<grid_for(n_d, 256), 256, 0, S(stream)>>>(n, v, n_d, nd, out, 1);
+        LAUNCHED();
+    }
+    EBS_CATCH
+}
+
+int ebs_check_finite(int64_t n, const double *v, int32_t *flag, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && flag, "ebs_check_finite: bad arguments");
+    CU(cudaMemsetAsync(flag, 0, sizeof(int32_t), S(stream)));
+    if (n > 0) {
+        k_check_finite<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, v, flag);
+        LAUNCHED();
+    }
+    EBS_CATCH
+}
+
+int ebs_gather(int64_t n, const int64_t *idx, const double *v, double *buf, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0, "ebs_gather: bad n");
+    if (n == 0) return EBS_OK;
+    k_gather<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, idx, v, buf);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_scatter_add(int64_t n, const int64_t *idx, const double *buf, double *v,
+                    void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0, "ebs_scatter_add: bad n");
+    if (n == 0) return EBS_OK;
+    k_scatter_add<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, idx, buf, v);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+}  // extern "C"

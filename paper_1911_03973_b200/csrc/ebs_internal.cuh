@@ -1,0 +1,207 @@
+// ebs_internal.cuh -- shared device/host helpers of libebs.so (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/ebs.h"
+
+namespace ebs {
+
+// ---------------------------------------------------------------- errors ----
+void set_error(const char *fmt, ...);
+int64_t bump_launches(int64_t n);
+
+struct Fail {
+    int code;
+};
+
+#define EBS_TRY try {
+#define EBS_CATCH                                                                 \
+    }                                                                             \
+    catch (const ebs::Fail &f) {                                                  \
+        return f.code;                                                            \
+    }                                                                             \
+    catch (...) {                                                                 \
+        ebs::set_error("unexpected C++ exception");                               \
+        return EBS_ECUDA;                                                         \
+    }                                                                             \
+    return EBS_OK;
+
+#define EBS_REQUIRE(cond, ...)                                                    \
+    do {                                                                          \
+        if (!(cond)) {                                                            \
+            ebs::set_error(__VA_ARGS__);                                          \
+            throw ebs::Fail{EBS_EINVAL};                                          \
+        }                                                                         \
+    } while (0)
+
+#define CU(call)                                                                  \
+    do {                                                                          \
+        cudaError_t err_ = (call);                                                \
+        if (err_ != cudaSuccess) {                                                \
+            ebs::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                           cudaGetErrorString(err_));                             \
+            throw ebs::Fail{err_ == cudaErrorMemoryAllocation ? EBS_ENOMEM       \
+                                                               : EBS_ECUDA};      \
+        }                                                                         \
+    } while (0)
+
+// launch check: counts one launch of our own kernels
+#define LAUNCHED()                                                                \
+    do {                                                                          \
+        CU(cudaGetLastError());                                                   \
+        ebs::bump_launches(1);                                                    \
+    } while (0)
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <class T>
+T *dmalloc(size_t count) {
+    T *p = nullptr;
+    if (count == 0) count = 1;
+    CU(cudaMalloc(&p, count * sizeof(T)));
+    return p;
+}
+template <class T>
+void dfree(T *&p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+// grid for a 1-D elementwise launch: enough CTAs to fill the 148 SMs several
+// times over, grid-stride beyond that
+inline int grid_for(int64_t n, int block, int max_blocks = 148 * 16) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (int)g;
+}
+
+// ----------------------------------------------------- SELL-32 plan layout ----
+constexpr int LANES = 32;                 // nodes per chunk (one warp)
+constexpr int J_SHIFT = 30;               // local vertex j packed in the top 2 bits
+constexpr int32_t ID_MASK = (1 << J_SHIFT) - 1;
+
+// device-side control block of the solver loop (solve.cu)
+struct Ctl {
+    int k;              // iteration whose residual was recorded last
+    int done;           // 1: later launches are no-ops
+    int diverged;
+    int n_norms;
+    int final_buf;      // ping-pong buffer that holds the returned iterate
+    int nonfinite;      // set by any thread writing a non-finite iterate
+    int cb_ok;          // r_k of the last step was recorded normally (callback due)
+    int pad_;
+    unsigned int counter;  // last-block-done counter of the fused reductions
+    unsigned int pad2_;
+    double norm0;
+    double rz, pq, alpha, beta;
+};
+
+struct Plan {
+    int nb;
+    int64_t n_n, n_e;
+    int64_t n_chunks, n_rows;
+    int max_valence;
+    // structure
+    int32_t *new_of_old = nullptr;  // caller id -> internal id
+    int32_t *old_of_new = nullptr;  // internal id -> caller id
+    int32_t *cnt = nullptr;         // valence per internal node
+    int32_t *rowbase = nullptr;     // first slot row of each chunk
+    int32_t *width = nullptr;       // slot rows of each chunk
+    int32_t *slot_ej = nullptr;     // [row][lane]: e | j<<30, -1 for padding
+    int32_t *slot_nb = nullptr;     // [row][t][lane]: t-th cyclic neighbour (t=0 carries j)
+    // loaded operator
+    double *slot_A = nullptr;   // [row][i][lane]: A_e[j, i, e]
+    double *slot_be = nullptr;  // [row][lane]: b_e[j, e] (exact residual)
+    double *b_int = nullptr;    // pre-assembled b, internal numbering
+    int has_A = 0, has_be = 0;
+    // Dirichlet set
+    uint8_t *free_int = nullptr;  // 1 free, 0 constrained (internal numbering)
+    int64_t n_dirichlet = 0;
+    // workspace (lazily grown)
+    double *wvec[8] = {nullptr};
+    double *partials = nullptr;  // reduction partials
+    Ctl *ctl = nullptr;          // device control block
+    Ctl *ctl_host = nullptr;     // pinned mirror
+    double *hist_dev = nullptr;  // device history (norms, errors)
+    int64_t hist_cap = 0;
+    int32_t *flag = nullptr;     // device scratch flag
+};
+
+double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)
+
+// ------------------------------------------------------ reductions ----------
+constexpr int RED_BLOCK = 256;
+constexpr int RED_MAX_BLOCKS = 1184;  // 148 SMs x 8: fixed -> deterministic order
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum of NV values (fixed tree).  Result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *smem /*[NV*32]*/) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) smem[q * 32 + wid] = v[q];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            double t = lane < nw ? smem[q * 32 + lane] : 0.0;
+            v[q] = warp_sum(t);
+        }
+    }
+}
+
+// Last-block-done pattern: every block writes its NV partial sums; the last block
+// to arrive sums all partials in block order and returns true in ALL its threads
+// with the totals in tot[] (valid in thread 0).  Deterministic for a fixed grid.
+template <int NV>
+__device__ __forceinline__ bool grid_sum_last(double (&v)[NV], double *partials,
+                                              unsigned int *counter, double (&tot)[NV]) {
+    __shared__ double smem[NV * 32];
+    __shared__ bool am_last;
+    block_sum<NV>(v, smem);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) partials[(size_t)q * gridDim.x + blockIdx.x] = v[q];
+        __threadfence();
+        unsigned int prev = atomicAdd(counter, 1u);
+        am_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return false;
+    __threadfence();
+    double w[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+            s += __ldcg(&partials[(size_t)q * gridDim.x + b]);
+        w[q] = s;
+    }
+    block_sum<NV>(w, smem);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) tot[q] = w[q];
+        *counter = 0u;  // re-arm for the next launch (stream order)
+    }
+    return true;
+}
+
+}  // namespace ebs

@@ -1,0 +1,161 @@
+// operators.cu -- residual / matvec entry points (caller numbering in and out).
+//
+//   ebs_residual  <- operators.py:72-111 residual (+ operators.py:114-118 mask)
+//   ebs_matvec    <- spectrum.py:54-61 _apply_masked
+//
+// Each call is two launches: a gather of x into the plan's internal numbering (with the
+// finiteness check of operators.py:90 fused in), then the SELL kernel, whose epilogue
+// scatters straight into the caller's numbering.
+#include "sell.cuh"
+
+namespace ebs {
+
+__global__ void k_to_internal(int64_t n, const int32_t *__restrict__ old_of_new,
+                              const double *__restrict__ x_user, double *__restrict__ x_int,
+                              int32_t *nonfinite) {
+    bool bad = false;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double v = x_user[old_of_new[m]];
+        bad |= !isfinite(v);
+        x_int[m] = v;
+    }
+    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(nonfinite, 1);
+}
+
+__global__ void k_to_user(int64_t n, const int32_t *__restrict__ old_of_new,
+                          const double *__restrict__ v_int, double *__restrict__ v_user) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        v_user[old_of_new[m]] = v_int[m];
+}
+
+// MODE 0: y = A x   1: r = b - A x (pre-assembled b)   2: r = sum(b_e - A_e x_e) exact
+template <int NB, int MODE>
+__global__ void __launch_bounds__(256)
+    k_sell_op(SellView v, const double *__restrict__ x, const double *__restrict__ b_int,
+              const uint8_t *__restrict__ free_int, const int32_t *__restrict__ old_of_new,
+              double *__restrict__ out) {
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
+    const int lane = threadIdx.x & (LANES - 1);
+    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
+    if (chunk >= n_chunks) return;
+    const int64_t m = chunk * LANES + lane;
+    const bool valid = m < v.n_n;
+    const int c_m = valid ? v.cnt[m] : 0;
+    const double xo = valid ? x[m] : 0.0;
+    double s = sell_node_sum<NB, MODE == 2>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, x, xo);
+    if (!valid) return;
+    if (MODE == 1) s = b_int[m] - s;
+    if (free_int && !free_int[m]) s = 0.0;
+    if (old_of_new) out[old_of_new[m]] = s;
+    else out[m] = s;
+}
+
+template <int MODE>
+void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
+                    const int32_t *old_of_new, double *out, cudaStream_t s) {
+    if (p->n_n == 0) return;
+    const int block = 256;
+    const int64_t grid = (p->n_chunks * LANES + block - 1) / block;
+    SellView v = sell_view(p);
+    if (p->nb == 3)
+        k_sell_op<3, MODE><<<(unsigned)grid, block, 0, s>>>(v, x_int, p->b_int, free_int,
+                                                          old_of_new, out);
+    else
+        k_sell_op<4, MODE><<<(unsigned)grid, block, 0, s>>>(v, x_int, p->b_int, free_int,
+                                                          old_of_new, out);
+    LAUNCHED();
+}
+
+void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
+                 cudaStream_t s) {
+    if (p->n_n == 0) return;
+    k_to_internal<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(p->n_n, p->old_of_new, x_user,
+                                                                  x_int, nonfinite);
+    LAUNCHED();
+}
+
+void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s) {
+    if (p->n_n == 0) return;
+    k_to_user<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(p->n_n, p->old_of_new, v_int,
+                                                              v_user);
+    LAUNCHED();
+}
+
+void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *free_int,
+                const int32_t *old_of_new, double *out, cudaStream_t s) {
+    if (mode == 0) launch_sell_op<0>(p, x_int, free_int, old_of_new, out, s);
+    else if (mode == 1) launch_sell_op<1>(p, x_int, free_int, old_of_new, out, s);
+    else launch_sell_op<2>(p, x_int, free_int, old_of_new, out, s);
+}
+
+}  // namespace ebs
+
+using namespace ebs;
+
+extern "C" {
+
+int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int masked,
+                 int32_t *nonfinite, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && x && r, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A && p->has_be, "residual needs an operator loaded with b_e");
+    EBS_REQUIRE(mode == EBS_RES_EXACT || mode == EBS_RES_FAST, "bad residual mode %d", mode);
+    EBS_REQUIRE(x != r, "x and r must not alias");
+    cudaStream_t s = S(stream);
+    double *x_int = plan_vec(p, 0);
+    if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
+    to_internal(p, x, x_int, nonfinite, s);
+    sell_apply(p, mode == EBS_RES_EXACT ? 2 : 1, x_int, masked ? p->free_int : nullptr,
+               p->old_of_new, r, s);
+    EBS_CATCH
+}
+
+int ebs_matvec(ebs_plan_t plan, const double *x, double *y, int masked, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && x && y, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(x != y, "x and y must not alias");
+    cudaStream_t s = S(stream);
+    double *x_int = plan_vec(p, 0);
+    to_internal(p, x, x_int, nullptr, s);
+    sell_apply(p, 0, x_int, masked ? p->free_int : nullptr, p->old_of_new, y, s);
+    EBS_CATCH
+}
+
+int ebs_to_internal(ebs_plan_t plan, const double *x, double *x_int, int32_t *nonfinite,
+                    void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && x && x_int, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), S(stream)));
+    to_internal(p, x, x_int, nonfinite, S(stream));
+    EBS_CATCH
+}
+
+int ebs_to_user(ebs_plan_t plan, const double *v_int, double *v, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && v_int && v, "null argument");
+    to_user(reinterpret_cast<Plan *>(plan), v_int, v, S(stream));
+    EBS_CATCH
+}
+
+int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, int out_user,
+                   int masked, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && x_int && out, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(op >= 0 && op <= 2, "bad op %d", op);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(op == 0 || p->has_be, "residual needs an operator loaded with b_e");
+    EBS_REQUIRE(x_int != out, "x and out must not alias");
+    sell_apply(p, op, x_int, masked ? p->free_int : nullptr, out_user ? p->old_of_new : nullptr,
+               out, S(stream));
+    EBS_CATCH
+}
+
+}  // extern "C"

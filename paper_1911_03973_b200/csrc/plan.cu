@@ -1,0 +1,542 @@
+// plan.cu -- execution plan of a mesh: node->(j,e) incidence in bincount order, a
+// locality-preserving internal node numbering and the SELL-32 slot stream.
+//
+// Why: the reference scatter is np.bincount(indt.ravel(), w) (operators.py:98): per node a
+// sequential sum from 0.0 over its contributions ordered by key j*n_e + e.  A node-centric
+// gather that walks each node's slots in that key order reproduces it bit for bit without
+// float atomics.  Slots are stored SELL-32: 32 consecutive internal nodes form a chunk
+// (one warp), slot k of lane l lives in row rowbase[c]+k, so every load of the hot loop
+// is a coalesced 256 B (doubles) / 128 B (ids) warp transaction.
+//
+// Internal numbering = first appearance when scanning elements e ascending, j ascending
+// (oracle/ebs_oracle.py first_appearance_order).  On structured meshes this recovers the
+// geometric row/plane order even when the caller's numbering is a random permutation
+// (BASELINE C2/C4), so the x gathers of a warp hit a few cache lines.
+#include <cub/cub.cuh>
+
+#include "ebs_internal.cuh"
+
+namespace ebs {
+
+// ------------------------------------------------------------- build kernels --
+__global__ void k_incidence(int nb, int64_t n_n, int64_t n_e, const int32_t *__restrict__ conn,
+                            int32_t *__restrict__ cnt, unsigned long long *__restrict__ first,
+                            int32_t *bad) {
+    const int64_t total = (int64_t)nb * n_e;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t j = t / n_e, e = t - j * n_e;
+        int32_t n = conn[t];
+        if (n < 0 || n >= n_n) { atomicOr(bad, 1); continue; }
+        atomicAdd(&cnt[n], 1);
+        atomicMin(&first[n], (unsigned long long)(e * nb + j));
+    }
+}
+
+// flag[e*nb + j] = 1 iff (e, j) is the first appearance of its node
+__global__ void k_first_flags(int nb, int64_t n_e, const int32_t *__restrict__ conn,
+                              const unsigned long long *__restrict__ first,
+                              int32_t *__restrict__ flag) {
+    const int64_t total = (int64_t)nb * n_e;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t e = t / nb, j = t - e * nb;
+        int32_t n = conn[j * n_e + e];
+        flag[t] = (first[n] == (unsigned long long)t) ? 1 : 0;
+    }
+}
+
+__global__ void k_isolated_flags(int64_t n_n, const int32_t *__restrict__ cnt,
+                                 int32_t *__restrict__ flag) {
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_n;
+         n += (int64_t)gridDim.x * blockDim.x)
+        flag[n] = cnt[n] == 0 ? 1 : 0;
+}
+
+__global__ void k_numbering(int64_t n_n, int64_t n_conn, const int32_t *__restrict__ cnt,
+                            const unsigned long long *__restrict__ first,
+                            const int32_t *__restrict__ pos_first,
+                            const int32_t *__restrict__ pos_iso, int32_t *__restrict__ new_of_old,
+                            int32_t *__restrict__ old_of_new) {
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_n;
+         n += (int64_t)gridDim.x * blockDim.x) {
+        int32_t m = cnt[n] > 0 ? pos_first[first[n]] : (int32_t)(n_conn + pos_iso[n]);
+        new_of_old[n] = m;
+        old_of_new[m] = (int32_t)n;
+    }
+}
+
+__global__ void k_permute_cnt(int64_t n_n, const int32_t *__restrict__ old_of_new,
+                              const int32_t *__restrict__ cnt_old, int32_t *__restrict__ cnt_new) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        cnt_new[m] = cnt_old[old_of_new[m]];
+}
+
+__global__ void k_fill_keys(int nb, int64_t n_e, const int32_t *__restrict__ conn,
+                            const int32_t *__restrict__ new_of_old,
+                            const int32_t *__restrict__ rowptr, int32_t *__restrict__ fill,
+                            int64_t *__restrict__ keys) {
+    const int64_t total = (int64_t)nb * n_e;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int32_t m = new_of_old[conn[t]];
+        int32_t p = rowptr[m] + atomicAdd(&fill[m], 1);
+        keys[p] = t;  // t = j*n_e + e: the bincount order key
+    }
+}
+
+// sort each node's keys ascending (atomics above filled them in arbitrary order)
+__global__ void k_sort_segments(int64_t n_n, const int32_t *__restrict__ rowptr,
+                                const int32_t *__restrict__ cnt, int64_t *__restrict__ keys) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        int64_t *k = keys + rowptr[m];
+        int c = cnt[m];
+        for (int a = 1; a < c; ++a) {
+            int64_t v = k[a];
+            int b = a - 1;
+            while (b >= 0 && k[b] > v) { k[b + 1] = k[b]; --b; }
+            k[b + 1] = v;
+        }
+    }
+}
+
+__global__ void k_chunk_width(int64_t n_n, int64_t n_chunks, const int32_t *__restrict__ cnt,
+                              int32_t *__restrict__ width) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        int w = 0;
+        for (int l = 0; l < LANES; ++l) {
+            int64_t m = c * LANES + l;
+            if (m < n_n && cnt[m] > w) w = cnt[m];
+        }
+        width[c] = w;
+    }
+}
+
+__global__ void k_fill_slots(int nb, int64_t n_n, int64_t n_e, const int32_t *__restrict__ conn,
+                             const int32_t *__restrict__ new_of_old,
+                             const int32_t *__restrict__ rowptr, const int32_t *__restrict__ cnt,
+                             const int64_t *__restrict__ keys, const int32_t *__restrict__ rowbase,
+                             const int32_t *__restrict__ width, int32_t *__restrict__ slot_ej,
+                             int32_t *__restrict__ slot_nb) {
+    const int64_t n_pad = ((n_n + LANES - 1) / LANES) * LANES;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_pad;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = m / LANES;
+        const int lane = (int)(m - c * LANES);
+        const int c_m = m < n_n ? cnt[m] : 0;
+        const int w = width[c];
+        for (int k = 0; k < w; ++k) {
+            const int64_t row = (int64_t)rowbase[c] + k;
+            if (k < c_m) {
+                int64_t key = keys[rowptr[m] + k];
+                int64_t j = key / n_e, e = key - j * n_e;
+                slot_ej[row * LANES + lane] = (int32_t)e | (int32_t)(j << J_SHIFT);
+                for (int t = 1; t < nb; ++t) {
+                    int64_t jj = (j + t) % nb;
+                    int32_t id = new_of_old[conn[jj * n_e + e]];
+                    if (t == 1) id |= (int32_t)(j << J_SHIFT);
+                    slot_nb[(row * (nb - 1) + (t - 1)) * LANES + lane] = id;
+                }
+            } else {
+                slot_ej[row * LANES + lane] = -1;
+                int32_t self = m < n_n ? (int32_t)m : 0;
+                for (int t = 1; t < nb; ++t)
+                    slot_nb[(row * (nb - 1) + (t - 1)) * LANES + lane] = self;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- load kernels --
+__global__ void k_pack(int nb, int64_t n_e, int64_t n_slots, const int32_t *__restrict__ slot_ej,
+                       const double *__restrict__ A_e, const double *__restrict__ b_e,
+                       double *__restrict__ slot_A, double *__restrict__ slot_be) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_slots;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = s / LANES;
+        const int lane = (int)(s - row * LANES);
+        const int32_t ej = slot_ej[s];
+        if (ej >= 0) {
+            const int64_t e = ej & ID_MASK, j = (uint32_t)ej >> J_SHIFT;
+            const double *src = A_e + (e * nb + j) * nb;  // row j of element e
+            for (int i = 0; i < nb; ++i) slot_A[(row * nb + i) * LANES + lane] = src[i];
+            if (slot_be) slot_be[s] = b_e[j * n_e + e];
+        } else {
+            for (int i = 0; i < nb; ++i) slot_A[(row * nb + i) * LANES + lane] = 0.0;
+            if (slot_be) slot_be[s] = 0.0;
+        }
+    }
+}
+
+// Ordered per-node sums over slots of a value fetched per slot:
+//   what = 0: b_e[j, e] (assemble_rhs, operators.py:58-63)
+//   what = 1: slot_A[row][j][lane] = A_e[j, j, e] (diag)
+//   what = 2: slot_be (pre-assembled b from the packed stream)
+// out_user != nullptr writes caller numbering, else internal numbering.
+__global__ void k_slot_sum(int nb, int64_t n_n, int64_t n_e, const int32_t *__restrict__ rowbase,
+                           const int32_t *__restrict__ width, const int32_t *__restrict__ cnt,
+                           const int32_t *__restrict__ slot_ej, const double *__restrict__ slot_A,
+                           const double *__restrict__ slot_be, const double *__restrict__ b_e,
+                           int what, const int32_t *__restrict__ old_of_new,
+                           double *__restrict__ out) {
+    const int64_t n_pad = ((n_n + LANES - 1) / LANES) * LANES;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_pad;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        if (m >= n_n) continue;
+        const int64_t c = m / LANES;
+        const int lane = (int)(m - c * LANES);
+        const int c_m = cnt[m];
+        double s = 0.0;
+        for (int k = 0; k < c_m; ++k) {
+            const int64_t row = (int64_t)rowbase[c] + k;
+            const int64_t sidx = row * LANES + lane;
+            double v;
+            if (what == 2) {
+                v = slot_be[sidx];
+            } else {
+                const int32_t ej = slot_ej[sidx];
+                const int64_t e = ej & ID_MASK, j = (uint32_t)ej >> J_SHIFT;
+                v = what == 0 ? b_e[j * n_e + e] : slot_A[(row * nb + j) * LANES + lane];
+            }
+            s = s + v;
+        }
+        if (old_of_new) out[old_of_new[m]] = s;
+        else out[m] = s;
+    }
+}
+
+__global__ void k_set_free(int64_t n_n, uint8_t *__restrict__ free_int) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        free_int[m] = 1;
+}
+
+__global__ void k_clear_free(int64_t n_d, const int64_t *__restrict__ nd, int64_t n_n,
+                             const int32_t *__restrict__ new_of_old, uint8_t *__restrict__ free_int,
+                             int32_t *bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t n = nd[i];
+        if (n < 0 || n >= n_n) { atomicOr(bad, 1); continue; }
+        free_int[new_of_old[n]] = 0;
+    }
+}
+
+void slot_sum(const Plan *p, int what, const double *b_e, const int32_t *old_of_new, double *out,
+              cudaStream_t s) {
+    if (p->n_n == 0) return;
+    k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, s>>>(
+        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot_A, p->slot_be,
+        b_e, what, old_of_new, out);
+    LAUNCHED();
+}
+
+// -------------------------------------------------------------- host helpers --
+template <class T>
+T read1(const T *dptr, cudaStream_t s) {
+    T v;
+    CU(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    return v;
+}
+
+// exclusive scan of n int32 values; returns the total
+static int64_t scan_i32(const int32_t *in, int32_t *out, int64_t n, cudaStream_t s) {
+    if (n == 0) return 0;
+    size_t bytes = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    void *tmp = dmalloc<char>(bytes);
+    cudaError_t err = cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n, s);
+    cudaFree(tmp);
+    CU(err);
+    bump_launches(1);
+    int32_t last_in = read1(in + n - 1, s), last_out = read1(out + n - 1, s);
+    return (int64_t)last_in + last_out;
+}
+
+double *plan_vec(Plan *p, int i) {
+    if (!p->wvec[i]) p->wvec[i] = dmalloc<double>(p->n_n + 1);
+    return p->wvec[i];
+}
+
+static void plan_free(Plan *p) {
+    dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->rowbase);
+    dfree(p->width); dfree(p->slot_ej); dfree(p->slot_nb); dfree(p->slot_A);
+    dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
+    dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag);
+    for (auto &v : p->wvec) dfree(v);
+    if (p->ctl_host) cudaFreeHost(p->ctl_host);
+    p->ctl_host = nullptr;
+}
+
+}  // namespace ebs
+
+using namespace ebs;
+
+extern "C" {
+
+int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void *stream,
+                    ebs_plan_t *out) {
+    Plan *p = nullptr;
+    int32_t *cnt_old = nullptr, *flag = nullptr, *pos = nullptr, *iso = nullptr,
+            *rowptr = nullptr, *fill = nullptr, *bad = nullptr;
+    unsigned long long *first = nullptr;
+    int64_t *keys = nullptr;
+    EBS_TRY
+    EBS_REQUIRE(out, "out must not be NULL");
+    *out = nullptr;
+    EBS_REQUIRE(nb == 3 || nb == 4, "nb must be 3 (triangles) or 4 (tetrahedra), got %d", nb);
+    EBS_REQUIRE(n_n >= 0 && n_e >= 0, "negative sizes");
+    EBS_REQUIRE(n_n < (int64_t)ID_MASK && n_e < (int64_t)ID_MASK,
+                "mesh too large: need n_nodes, n_elems < 2^30");
+    EBS_REQUIRE((int64_t)nb * n_e < (1ll << 31) - 1, "too many element slots (nb*n_e >= 2^31)");
+    cudaStream_t s = S(stream);
+    p = new Plan();
+    p->nb = nb;
+    p->n_n = n_n;
+    p->n_e = n_e;
+    p->n_chunks = (n_n + LANES - 1) / LANES;
+    const int64_t total = (int64_t)nb * n_e;
+
+    // 1. valence + first appearance
+    cnt_old = dmalloc<int32_t>(n_n);
+    first = dmalloc<unsigned long long>(n_n);
+    bad = dmalloc<int32_t>(1);
+    CU(cudaMemsetAsync(cnt_old, 0, sizeof(int32_t) * (n_n ? n_n : 1), s));
+    CU(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long) * (n_n ? n_n : 1), s));
+    CU(cudaMemsetAsync(bad, 0, sizeof(int32_t), s));
+    if (total) {
+        k_incidence<<<grid_for(total, 256), 256, 0, s>>>(nb, n_n, n_e, conn, cnt_old, first, bad);
+        LAUNCHED();
+    }
+    EBS_REQUIRE(read1(bad, s) == 0, "element connectivity references nonexistent nodes");
+
+    // 2. internal numbering
+    p->new_of_old = dmalloc<int32_t>(n_n);
+    p->old_of_new = dmalloc<int32_t>(n_n);
+    flag = dmalloc<int32_t>(total);
+    pos = dmalloc<int32_t>(total);
+    int64_t n_conn = 0;
+    if (total) {
+        k_first_flags<<<grid_for(total, 256), 256, 0, s>>>(nb, n_e, conn, first, flag);
+        LAUNCHED();
+        n_conn = scan_i32(flag, pos, total, s);
+    }
+    iso = dmalloc<int32_t>(n_n);
+    int32_t *iso_pos = dmalloc<int32_t>(n_n);
+    if (n_n) {
+        k_isolated_flags<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, cnt_old, iso);
+        LAUNCHED();
+        scan_i32(iso, iso_pos, n_n, s);
+        k_numbering<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, n_conn, cnt_old, first, pos, iso_pos,
+                                                      p->new_of_old, p->old_of_new);
+        LAUNCHED();
+    }
+    cudaFree(iso_pos);
+    dfree(flag);
+    dfree(pos);
+    dfree(iso);
+
+    // 3. incidence CSR in internal numbering, keys sorted per node
+    p->cnt = dmalloc<int32_t>(n_n);
+    rowptr = dmalloc<int32_t>(n_n);
+    if (n_n) {
+        k_permute_cnt<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, p->old_of_new, cnt_old, p->cnt);
+        LAUNCHED();
+        scan_i32(p->cnt, rowptr, n_n, s);
+    }
+    keys = dmalloc<int64_t>(total);
+    fill = dmalloc<int32_t>(n_n);
+    CU(cudaMemsetAsync(fill, 0, sizeof(int32_t) * (n_n ? n_n : 1), s));
+    if (total) {
+        k_fill_keys<<<grid_for(total, 256), 256, 0, s>>>(nb, n_e, conn, p->new_of_old, rowptr,
+                                                        fill, keys);
+        LAUNCHED();
+        k_sort_segments<<<grid_for(n_n, 128), 128, 0, s>>>(n_n, rowptr, p->cnt, keys);
+        LAUNCHED();
+    }
+    dfree(fill);
+
+    // 4. SELL-32 chunks
+    p->width = dmalloc<int32_t>(p->n_chunks);
+    p->rowbase = dmalloc<int32_t>(p->n_chunks);
+    p->n_rows = 0;
+    if (p->n_chunks) {
+        k_chunk_width<<<grid_for(p->n_chunks, 256), 256, 0, s>>>(n_n, p->n_chunks, p->cnt,
+                                                                p->width);
+        LAUNCHED();
+        p->n_rows = scan_i32(p->width, p->rowbase, p->n_chunks, s);
+    }
+    EBS_REQUIRE(p->n_rows * LANES * (int64_t)nb < (1ll << 40), "slot stream too large");
+    p->slot_ej = dmalloc<int32_t>(p->n_rows * LANES);
+    p->slot_nb = dmalloc<int32_t>(p->n_rows * LANES * (nb - 1));
+    if (p->n_chunks) {
+        k_fill_slots<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
+            nb, n_n, n_e, conn, p->new_of_old, rowptr, p->cnt, keys, p->rowbase, p->width,
+            p->slot_ej, p->slot_nb);
+        LAUNCHED();
+    }
+    // max valence (for info)
+    {
+        int32_t mv = 0;
+        if (p->n_chunks) {
+            int32_t *w = new int32_t[p->n_chunks];
+            cudaError_t e1 = cudaMemcpyAsync(w, p->width, sizeof(int32_t) * p->n_chunks,
+                                             cudaMemcpyDeviceToHost, s);
+            cudaError_t e2 = cudaStreamSynchronize(s);
+            for (int64_t c = 0; c < p->n_chunks; ++c) mv = w[c] > mv ? w[c] : mv;
+            delete[] w;
+            CU(e1);
+            CU(e2);
+        }
+        p->max_valence = mv;
+    }
+    dfree(keys);
+    dfree(rowptr);
+    dfree(cnt_old);
+    dfree(first);
+    dfree(bad);
+
+    // control block + reduction scratch
+    p->ctl = dmalloc<Ctl>(1);
+    CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
+    CU(cudaMallocHost(&p->ctl_host, sizeof(Ctl)));
+    p->partials = dmalloc<double>(4 * (p->n_chunks / 8 + RED_MAX_BLOCKS + 8));
+    p->flag = dmalloc<int32_t>(4);
+    p->free_int = dmalloc<uint8_t>(n_n);
+    if (n_n) {
+        k_set_free<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, p->free_int);
+        LAUNCHED();
+    }
+    CU(cudaStreamSynchronize(s));
+    *out = reinterpret_cast<ebs_plan_t>(p);
+    p = nullptr;
+    }
+    catch (const ebs::Fail &f) {
+        cudaFree(cnt_old); cudaFree(flag); cudaFree(pos); cudaFree(iso); cudaFree(rowptr);
+        cudaFree(fill); cudaFree(bad); cudaFree(first); cudaFree(keys);
+        if (p) { plan_free(p); delete p; }
+        return f.code;
+    }
+    catch (...) {
+        if (p) { plan_free(p); delete p; }
+        set_error("unexpected C++ exception in ebs_plan_create");
+        return EBS_ECUDA;
+    }
+    return EBS_OK;
+}
+
+int ebs_plan_destroy(ebs_plan_t plan) {
+    if (!plan) return EBS_OK;
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    plan_free(p);
+    delete p;
+    return EBS_OK;
+}
+
+int ebs_plan_info(ebs_plan_t plan, int64_t *info) {
+    EBS_TRY
+    EBS_REQUIRE(plan && info, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    info[0] = p->n_n;
+    info[1] = p->n_e;
+    info[2] = p->nb;
+    info[3] = p->n_chunks;
+    info[4] = p->n_rows;
+    int64_t slots = p->n_rows * LANES;
+    info[5] = slots * (int64_t)(4 * (p->nb - 1) + (p->has_A ? 8 * p->nb : 0) +
+                                (p->has_be ? 8 : 0));
+    info[6] = p->max_valence;
+    info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0);
+    EBS_CATCH
+}
+
+int ebs_plan_node_maps(ebs_plan_t plan, int32_t *new_of_old, int32_t *old_of_new,
+                       void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan, "null plan");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (p->n_n == 0) return EBS_OK;
+    if (new_of_old)
+        CU(cudaMemcpyAsync(new_of_old, p->new_of_old, sizeof(int32_t) * p->n_n,
+                           cudaMemcpyDeviceToDevice, S(stream)));
+    if (old_of_new)
+        CU(cudaMemcpyAsync(old_of_new, p->old_of_new, sizeof(int32_t) * p->n_n,
+                           cudaMemcpyDeviceToDevice, S(stream)));
+    EBS_CATCH
+}
+
+int ebs_plan_load(ebs_plan_t plan, const double *A_e, const double *b_e, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && A_e, "null plan or A_e");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    cudaStream_t s = S(stream);
+    const int64_t n_slots = p->n_rows * LANES;
+    if (!p->slot_A) p->slot_A = dmalloc<double>(n_slots * p->nb);
+    if (b_e && !p->slot_be) p->slot_be = dmalloc<double>(n_slots);
+    if (b_e && !p->b_int) p->b_int = dmalloc<double>(p->n_n);
+    if (n_slots) {
+        k_pack<<<grid_for(n_slots, 256, 148 * 64), 256, 0, s>>>(
+            p->nb, p->n_e, n_slots, p->slot_ej, A_e, b_e, p->slot_A, b_e ? p->slot_be : nullptr);
+        LAUNCHED();
+    }
+    p->has_A = 1;
+    p->has_be = b_e ? 1 : 0;
+    if (b_e && p->n_n) {
+        k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, s>>>(
+            p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot_A,
+            p->slot_be, nullptr, 2, nullptr, p->b_int);
+        LAUNCHED();
+    }
+    EBS_CATCH
+}
+
+int ebs_plan_set_dirichlet(ebs_plan_t plan, const int64_t *nd, int64_t n_d, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && n_d >= 0, "bad arguments");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    cudaStream_t s = S(stream);
+    if (p->n_n) {
+        k_set_free<<<grid_for(p->n_n, 256), 256, 0, s>>>(p->n_n, p->free_int);
+        LAUNCHED();
+    }
+    p->n_dirichlet = n_d;
+    if (n_d) {
+        CU(cudaMemsetAsync(p->flag, 0, sizeof(int32_t), s));
+        k_clear_free<<<grid_for(n_d, 256), 256, 0, s>>>(n_d, nd, p->n_n, p->new_of_old,
+                                                       p->free_int, p->flag);
+        LAUNCHED();
+        EBS_REQUIRE(read1(p->flag, s) == 0, "Dirichlet node index out of range");
+    }
+    EBS_CATCH
+}
+
+int ebs_assemble_rhs(ebs_plan_t plan, const double *b_e, double *b, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && b_e && b, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (p->n_n == 0) return EBS_OK;
+    k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, S(stream)>>>(
+        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, nullptr, nullptr, b_e, 0,
+        p->old_of_new, b);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_diagonal(ebs_plan_t plan, double *d, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && d, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    if (p->n_n == 0) return EBS_OK;
+    k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, S(stream)>>>(
+        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot_A, nullptr,
+        nullptr, 1, p->old_of_new, d);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+}  // extern "C"

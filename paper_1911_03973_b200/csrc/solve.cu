@@ -1,0 +1,444 @@
+// solve.cu -- the solvers.py:117-160 `_iterate` loop run on the device.
+//
+// Richardson / damped Jacobi (one fused launch per iteration):
+//   L(k): r_k = mask(b - A x_k) [SELL]; ||r_k||^2 (+ ||x_k - ref||^2) reduced in-kernel;
+//         x_{k+1} = x_k + omega*r_k   (Richardson, solvers.py:179-180)
+//         x_{k+1} = x_k + omega*(dinv*r_k)   (Jacobi)
+//         into the other ping-pong buffer.  The last CTA applies the loop rules:
+//         record norms[k]; k>0 and non-finite -> diverged (solvers.py:150-152);
+//         ||r_k|| <= tol*||r_0|| -> stop with x_k (solvers.py:135);
+//         x_{k+1} non-finite -> norms[k+1] = inf, diverged (solvers.py:138-143).
+//   R   : the residual of the last iterate (history entry `iters`).
+// CG / Jacobi-PCG (oracle/ebs_oracle.py pcg): init I, then per iteration
+//   M(k): q = mask(A p) [SELL] + p.q  -> alpha
+//   U(k): x += alpha p, r -= alpha q, ||r||^2, r.(dinv r) -> norms[k+1], beta
+//   P(k): p = dinv*r + beta*p
+// Kernels read the iteration index and the stop flag from the device control block, so
+// the host only enqueues launches; it synchronises once per batch of iterations to stop
+// enqueuing after convergence (and every iteration when a callback is attached).
+// Reductions are fixed-order (deterministic run to run).
+#include "sell.cuh"
+
+namespace ebs {
+
+void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
+                 cudaStream_t s);
+void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s);
+
+struct LoopArgs {
+    Ctl *ctl;
+    double *norms;   // device history
+    double *errors;  // device history (nullable)
+    double *partials;
+    int has_tol;
+    double tol;
+    double omega;
+};
+
+__device__ __forceinline__ void flag_nonfinite(Ctl *ctl, bool bad) {
+    if (bad) {
+        atomicOr(&ctl->nonfinite, 1);
+        __threadfence();
+    }
+}
+
+// ---------------------------------------------------------- Richardson/Jacobi --
+template <int NB, bool EXACT>
+__global__ void __launch_bounds__(256)
+    k_jacobi_step(SellView v, LoopArgs L, double *__restrict__ xa, double *__restrict__ xb,
+                  const double *__restrict__ b_int, const uint8_t *__restrict__ free_int,
+                  const double *__restrict__ dinv, const double *__restrict__ ref,
+                  double *__restrict__ r_out, int final_step) {
+    Ctl *ctl = L.ctl;
+    if (ctl->done) return;
+    const int k = ctl->k;
+    const double *x = (k & 1) ? xb : xa;
+    double *xn_buf = (k & 1) ? xa : xb;
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
+    const int lane = threadIdx.x & (LANES - 1);
+    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
+    double part[2] = {0.0, 0.0};
+    bool bad = false;
+    if (chunk < n_chunks) {
+        const int64_t m = chunk * LANES + lane;
+        const bool valid = m < v.n_n;
+        const int c_m = valid ? v.cnt[m] : 0;
+        const double xo = valid ? x[m] : 0.0;
+        double s = sell_node_sum<NB, EXACT>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, x, xo);
+        if (valid) {
+            double r = EXACT ? s : b_int[m] - s;
+            if (!free_int[m]) r = 0.0;
+            part[0] = r * r;
+            if (ref) {
+                double d = xo - ref[m];
+                part[1] = d * d;
+            }
+            if (r_out) r_out[m] = r;
+            if (!final_step) {
+                double xn = dinv ? xo + L.omega * (dinv[m] * r) : xo + L.omega * r;
+                xn_buf[m] = xn;
+                bad = !isfinite(xn);
+            }
+        }
+    }
+    flag_nonfinite(ctl, bad);
+    double tot[2];
+    if (!grid_sum_last<2>(part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    // ---- loop rules (single thread) ----
+    const double nr = sqrt(tot[0]);
+    L.norms[k] = nr;
+    if (L.errors) L.errors[k] = sqrt(tot[1]);
+    if (k == 0) ctl->norm0 = nr;
+    ctl->n_norms = k + 1;
+    ctl->cb_ok = 1;
+    ctl->final_buf = k & 1;
+    if (k > 0 && !isfinite(nr)) {
+        ctl->diverged = 1;
+        ctl->done = 1;
+        return;
+    }
+    if (final_step) {
+        ctl->done = 1;
+        return;
+    }
+    if (L.has_tol && nr <= L.tol * ctl->norm0) {
+        ctl->done = 1;
+        return;
+    }
+    if (ctl->nonfinite) {
+        L.norms[k + 1] = INFINITY;
+        if (L.errors) L.errors[k + 1] = INFINITY;
+        ctl->n_norms = k + 2;
+        ctl->diverged = 1;
+        ctl->done = 1;
+        ctl->final_buf = (k + 1) & 1;
+        ctl->k = k + 1;
+        return;
+    }
+    ctl->k = k + 1;
+    ctl->final_buf = (k + 1) & 1;
+}
+
+// ------------------------------------------------------------------ CG / PCG --
+template <int NB>
+__global__ void __launch_bounds__(256)
+    k_pcg_init(SellView v, LoopArgs L, const double *__restrict__ x, const double *__restrict__ b_int,
+               const uint8_t *__restrict__ free_int, const double *__restrict__ dinv,
+               const double *__restrict__ ref, double *__restrict__ r_int,
+               double *__restrict__ p_int) {
+    Ctl *ctl = L.ctl;
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
+    const int lane = threadIdx.x & (LANES - 1);
+    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
+    double part[3] = {0.0, 0.0, 0.0};
+    if (chunk < n_chunks) {
+        const int64_t m = chunk * LANES + lane;
+        const bool valid = m < v.n_n;
+        const int c_m = valid ? v.cnt[m] : 0;
+        const double xo = valid ? x[m] : 0.0;
+        double s = sell_node_sum<NB, false>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, x, xo);
+        if (valid) {
+            double r = free_int[m] ? b_int[m] - s : 0.0;
+            double z = dinv[m] * r;
+            r_int[m] = r;
+            p_int[m] = z;
+            part[0] = r * r;
+            part[1] = r * z;
+            if (ref) {
+                double d = xo - ref[m];
+                part[2] = d * d;
+            }
+        }
+    }
+    double tot[3];
+    if (!grid_sum_last<3>(part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    const double nr = sqrt(tot[0]);
+    L.norms[0] = nr;
+    if (L.errors) L.errors[0] = sqrt(tot[2]);
+    ctl->norm0 = nr;
+    ctl->rz = tot[1];
+    ctl->n_norms = 1;
+    ctl->k = 0;
+    ctl->cb_ok = 1;
+    if (L.has_tol && nr <= L.tol * nr) ctl->done = 1;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256)
+    k_pcg_matvec(SellView v, LoopArgs L, const double *__restrict__ p_int,
+                 const uint8_t *__restrict__ free_int, double *__restrict__ q_int) {
+    Ctl *ctl = L.ctl;
+    if (ctl->done) return;
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
+    const int lane = threadIdx.x & (LANES - 1);
+    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
+    double part[1] = {0.0};
+    if (chunk < n_chunks) {
+        const int64_t m = chunk * LANES + lane;
+        const bool valid = m < v.n_n;
+        const int c_m = valid ? v.cnt[m] : 0;
+        const double po = valid ? p_int[m] : 0.0;
+        double s =
+            sell_node_sum<NB, false>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, p_int, po);
+        if (valid) {
+            double q = free_int[m] ? s : 0.0;  // spectrum.py:60 out[nd] = 0
+            q_int[m] = q;
+            part[0] = po * q;
+        }
+    }
+    double tot[1];
+    if (!grid_sum_last<1>(part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    ctl->pq = tot[0];
+    ctl->alpha = tot[0] != 0.0 ? ctl->rz / tot[0] : 0.0;
+}
+
+__global__ void __launch_bounds__(256)
+    k_pcg_update(int64_t n, LoopArgs L, double *__restrict__ x, double *__restrict__ r,
+                 const double *__restrict__ p, const double *__restrict__ q,
+                 const double *__restrict__ dinv, const double *__restrict__ ref) {
+    Ctl *ctl = L.ctl;
+    if (ctl->done) return;
+    const double alpha = ctl->alpha;
+    double part[3] = {0.0, 0.0, 0.0};
+    bool bad = false;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double xn = x[m] + alpha * p[m];
+        double rn = r[m] - alpha * q[m];
+        x[m] = xn;
+        r[m] = rn;
+        bad |= !isfinite(xn);
+        part[0] += rn * rn;
+        part[1] += rn * (dinv[m] * rn);
+        if (ref) {
+            double d = xn - ref[m];
+            part[2] += d * d;
+        }
+    }
+    flag_nonfinite(ctl, bad);
+    double tot[3];
+    if (!grid_sum_last<3>(part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    const int k = ctl->k;
+    ctl->k = k + 1;
+    ctl->n_norms = k + 2;
+    if (ctl->nonfinite) {
+        L.norms[k + 1] = INFINITY;
+        if (L.errors) L.errors[k + 1] = INFINITY;
+        ctl->diverged = 1;
+        ctl->done = 1;
+        ctl->cb_ok = 0;
+        return;
+    }
+    const double nr = sqrt(tot[0]);
+    L.norms[k + 1] = nr;
+    if (L.errors) L.errors[k + 1] = sqrt(tot[2]);
+    ctl->cb_ok = 1;
+    if (!isfinite(nr)) {
+        ctl->diverged = 1;
+        ctl->done = 1;
+        return;
+    }
+    if (L.has_tol && nr <= L.tol * ctl->norm0) {
+        ctl->done = 1;
+        return;
+    }
+    const double rz_new = tot[1];
+    ctl->beta = ctl->rz != 0.0 ? rz_new / ctl->rz : 0.0;
+    ctl->rz = rz_new;
+}
+
+__global__ void __launch_bounds__(256)
+    k_pcg_direction(int64_t n, Ctl *ctl, double *__restrict__ p, const double *__restrict__ r,
+                    const double *__restrict__ dinv) {
+    if (ctl->done) return;
+    const double beta = ctl->beta;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        p[m] = dinv[m] * r[m] + beta * p[m];
+}
+
+// dinv = 1/diag on free nodes (Jacobi, PCG), 1 on free nodes (CG), 0 on constrained ones
+__global__ void k_dinv(int64_t n, const double *__restrict__ diag,
+                       const uint8_t *__restrict__ free_int, double *__restrict__ dinv) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        dinv[m] = free_int[m] ? (diag ? 1.0 / diag[m] : 1.0) : 0.0;
+}
+
+// ordered per-node sums over slots (plan.cu); what = 1: diag(A)
+void slot_sum(const Plan *p, int what, const double *b_e, const int32_t *old_of_new, double *out,
+              cudaStream_t s);
+
+static void ensure_hist(Plan *p, int64_t n) {
+    if (p->hist_cap < n) {
+        dfree(p->hist_dev);
+        p->hist_dev = dmalloc<double>(2 * n);
+        p->hist_cap = n;
+    }
+}
+
+}  // namespace ebs
+
+using namespace ebs;
+
+extern "C" {
+
+int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && P, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(P->iters >= 0, "iteration count must be nonnegative, got %d", P->iters);
+    EBS_REQUIRE(P->method >= EBS_RICHARDSON && P->method <= EBS_PCG, "bad method %d", P->method);
+    EBS_REQUIRE(p->has_A && p->has_be, "solver needs an operator loaded with b_e");
+    EBS_REQUIRE(P->x0 && P->x && P->norms && P->n_norms && P->diverged, "null argument");
+    EBS_REQUIRE(!P->reference || P->errors, "errors buffer required with reference");
+    EBS_REQUIRE(!P->callback || (P->cb_x && P->cb_r), "callback needs cb_x and cb_r");
+    cudaStream_t s = S(stream);
+    const int64_t n = p->n_n;
+    const int iters = P->iters;
+    const int nb = p->nb;
+    ensure_hist(p, (int64_t)iters + 2);
+    double *xa = plan_vec(p, 1), *xb = plan_vec(p, 2), *r_int = plan_vec(p, 3);
+    double *dinv = plan_vec(p, 4), *ref_int = nullptr;
+    CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
+    CU(cudaMemsetAsync(p->hist_dev, 0, sizeof(double) * 2 * ((int64_t)iters + 2), s));
+    to_internal(p, P->x0, xa, nullptr, s);
+    if (P->reference) {
+        ref_int = plan_vec(p, 7);
+        to_internal(p, P->reference, ref_int, nullptr, s);
+    }
+    LoopArgs L{p->ctl, p->hist_dev, P->reference ? p->hist_dev + iters + 2 : nullptr,
+               p->partials, P->has_tol, P->tol, P->omega};
+    SellView v = sell_view(p);
+    const int block = 256;
+    const unsigned sgrid = (unsigned)((p->n_chunks * LANES + block - 1) / block);
+    const int vgrid = grid_for(n, 256, RED_MAX_BLOCKS);
+    const bool cb = P->callback != nullptr;
+    const int batch = cb ? 1 : 32;
+    bool aborted = false;
+
+    auto read_ctl = [&]() {
+        CU(cudaMemcpyAsync(p->ctl_host, p->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    };
+    auto do_callback = [&](const double *x_int_k, int k) {
+        to_user(p, x_int_k, P->cb_x, s);
+        to_user(p, r_int, P->cb_r, s);
+        CU(cudaStreamSynchronize(s));
+        if (P->callback(P->user, k) != 0) aborted = true;
+    };
+
+    if (n > 0 && (P->method == EBS_RICHARDSON || P->method == EBS_JACOBI)) {
+        const double *dv = nullptr;
+        if (P->method == EBS_JACOBI) {
+            double *diag = plan_vec(p, 5);
+            slot_sum(p, 1, nullptr, nullptr, diag, s);
+            k_dinv<<<grid_for(n, 256), 256, 0, s>>>(n, diag, p->free_int, dinv);
+            LAUNCHED();
+            dv = dinv;
+        }
+        const bool exact = P->exact != 0;
+        double *rcb = (cb || P->r_out) ? r_int : nullptr;
+        auto step = [&](int final_step) {
+            if (nb == 3) {
+                if (exact)
+                    k_jacobi_step<3, true><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
+                                                                  dv, ref_int, rcb, final_step);
+                else
+                    k_jacobi_step<3, false><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
+                                                                   dv, ref_int, rcb, final_step);
+            } else {
+                if (exact)
+                    k_jacobi_step<4, true><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
+                                                                  dv, ref_int, rcb, final_step);
+                else
+                    k_jacobi_step<4, false><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
+                                                                   dv, ref_int, rcb, final_step);
+            }
+            LAUNCHED();
+        };
+        int k = 0;
+        bool done = false;
+        while (k < iters && !done && !aborted) {
+            int kend = k + batch < iters ? k + batch : iters;
+            for (; k < kend; ++k) step(0);
+            read_ctl();
+            done = p->ctl_host->done != 0;
+            if (cb && p->ctl_host->cb_ok) {
+                int kk = p->ctl_host->n_norms - 1;
+                if (p->ctl_host->nonfinite) kk = p->ctl_host->n_norms - 2;
+                do_callback(((kk & 1) ? xb : xa), kk);
+            }
+        }
+        if (!done && !aborted) {
+            step(1);
+            read_ctl();
+            if (cb) do_callback(((iters & 1) ? xb : xa), iters);
+        }
+        const double *xf = (p->ctl_host->final_buf & 1) ? xb : xa;
+        to_user(p, xf, P->x, s);
+    } else if (n > 0) {
+        // CG / PCG
+        double *pv = plan_vec(p, 5), *qv = plan_vec(p, 6);
+        double *diag = nullptr;
+        if (P->method == EBS_PCG) {
+            diag = qv;  // scratch before the loop
+            slot_sum(p, 1, nullptr, nullptr, diag, s);
+        }
+        k_dinv<<<grid_for(n, 256), 256, 0, s>>>(n, diag, p->free_int, dinv);
+        LAUNCHED();
+        if (nb == 3)
+            k_pcg_init<3><<<sgrid, block, 0, s>>>(v, L, xa, p->b_int, p->free_int, dinv, ref_int,
+                                                 r_int, pv);
+        else
+            k_pcg_init<4><<<sgrid, block, 0, s>>>(v, L, xa, p->b_int, p->free_int, dinv, ref_int,
+                                                 r_int, pv);
+        LAUNCHED();
+        if (cb) {
+            read_ctl();
+            do_callback(xa, 0);
+        }
+        int k = 0;
+        bool done = false;
+        while (k < iters && !done && !aborted) {
+            int kend = k + batch < iters ? k + batch : iters;
+            for (; k < kend; ++k) {
+                if (nb == 3)
+                    k_pcg_matvec<3><<<sgrid, block, 0, s>>>(v, L, pv, p->free_int, qv);
+                else
+                    k_pcg_matvec<4><<<sgrid, block, 0, s>>>(v, L, pv, p->free_int, qv);
+                LAUNCHED();
+                k_pcg_update<<<vgrid, 256, 0, s>>>(n, L, xa, r_int, pv, qv, dinv, ref_int);
+                LAUNCHED();
+                k_pcg_direction<<<grid_for(n, 256), 256, 0, s>>>(n, p->ctl, pv, r_int, dinv);
+                LAUNCHED();
+            }
+            read_ctl();
+            done = p->ctl_host->done != 0;
+            if (cb && p->ctl_host->cb_ok) do_callback(xa, p->ctl_host->n_norms - 1);
+        }
+        read_ctl();
+        to_user(p, xa, P->x, s);
+    } else {
+        read_ctl();
+    }
+    if (P->r_out && n > 0) to_user(p, r_int, P->r_out, s);
+    read_ctl();
+    const int nn = n > 0 ? p->ctl_host->n_norms : 0;
+    *P->n_norms = nn;
+    *P->diverged = p->ctl_host->diverged;
+    if (nn > 0) {
+        CU(cudaMemcpyAsync(P->norms, p->hist_dev, sizeof(double) * nn, cudaMemcpyDeviceToHost, s));
+        if (P->reference)
+            CU(cudaMemcpyAsync(P->errors, p->hist_dev + iters + 2, sizeof(double) * nn,
+                               cudaMemcpyDeviceToHost, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    if (aborted) {
+        set_error("solve stopped by callback");
+        return EBS_ECALLBACK;
+    }
+    EBS_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+"""Iterative solvers on the device (solvers.py of the reference, plus Jacobi/CG/PCG).
+
+All methods run the reference's shared loop (`_iterate`, solvers.py:117-160) inside
+libebs.so (``ebs_solve``): the residual norms stay on the device and are read once
+at the end; the iteration stops on ``tol`` relative to ||r_0||; divergence sets a
+flag and is never raised; ``callback(k, x, r)`` is called for k = 0..iters with
+device tensors in the caller's numbering (reused buffers -- clone to keep them).
+
+  richardson  x += omega r, omega = 2/(l1+l2)          solvers.py:163-183
+  jacobi      x += omega D^-1 r                        NEW (north star)
+  cg / pcg    (Jacobi-preconditioned) CG on the masked operator  NEW (north star)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import (CALLBACK, EBS_CG, EBS_ECALLBACK, EBS_JACOBI, EBS_PCG, EBS_RICHARDSON,
+                   SolveParams, check, load)
+from .elements import ElementBatch
+from .operators import DirichletData
+
+
+@dataclass(frozen=True)
+class SpectralBounds:
+    """solvers.py:30-56: an interval [lambda1, lambda2] enclosing the spectrum."""
+
+    lambda1: float
+    lambda2: float
+
+    def __post_init__(self):
+        if not (np.isfinite(self.lambda1) and np.isfinite(self.lambda2)):
+            raise ValueError("spectral bounds must be finite")
+        if self.lambda1 < 0 or self.lambda2 < self.lambda1 or self.lambda2 <= 0:
+            raise ValueError(
+                f"need 0 <= lambda1 <= lambda2, lambda2 > 0; got [{self.lambda1}, {self.lambda2}]")
+
+    @property
+    def center(self) -> float:
+        return (self.lambda2 + self.lambda1) / 2.0
+
+    @property
+    def half_width(self) -> float:
+        return (self.lambda2 - self.lambda1) / 2.0
+
+
+@dataclass(frozen=True)
+class ConvergenceHistory:
+    """solvers.py:69-82: residual_norms[k] = ||r^k||_2 for k = 0..iters (host arrays)."""
+
+    residual_norms: np.ndarray
+    error_norms: np.ndarray | None
+    wall_time: float
+    diverged: bool = False
+
+    @property
+    def iterations(self) -> int:
+        return len(self.residual_norms) - 1
+
+
+def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.0, exact=False,
+           tol=None, reference=None, callback=None):
+    if iters < 0:
+        raise ValueError(f"iteration count must be nonnegative, got {iters}")
+    x0 = D.f64(x0)
+    if x0.ndim != 1:
+        raise ValueError(f"x0 must be a flat global vector, got shape {tuple(x0.shape)}")
+    n = x0.shape[0]
+    pl = batch.operator(n)
+    pl.ensure_dirichlet(d)
+    x = D.empty(n)
+    ref = D.f64(reference) if reference is not None else None
+    norms = (ctypes.c_double * (iters + 2))()
+    errors = (ctypes.c_double * (iters + 2))()
+    n_norms = ctypes.c_int(0)
+    diverged = ctypes.c_int(0)
+    state = {"exc": None}
+    cb_x = cb_r = None
+    cb_fn = CALLBACK()
+    if callback is not None:
+        cb_x = D.empty(n)
+        cb_r = D.empty(n)
+
+        def _cb(user, k):
+            try:
+                callback(int(k), cb_x, cb_r)
+                return 0
+            except BaseException as e:  # re-raised after the C call returns
+                state["exc"] = e
+                return 1
+
+        cb_fn = CALLBACK(_cb)
+    P = SolveParams()
+    P.method = method
+    P.iters = int(iters)
+    P.exact = 1 if exact else 0
+    P.has_tol = 0 if tol is None else 1
+    P.tol = 0.0 if tol is None else float(tol)
+    P.omega = float(omega)
+    P.x0 = x0.data_ptr()
+    P.x = x.data_ptr()
+    P.reference = ref.data_ptr() if ref is not None else None
+    P.norms = ctypes.cast(norms, ctypes.POINTER(ctypes.c_double))
+    P.errors = ctypes.cast(errors, ctypes.POINTER(ctypes.c_double))
+    P.n_norms = ctypes.pointer(n_norms)
+    P.diverged = ctypes.pointer(diverged)
+    P.callback = cb_fn
+    P.user = None
+    P.cb_x = cb_x.data_ptr() if cb_x is not None else None
+    P.cb_r = cb_r.data_ptr() if cb_r is not None else None
+    P.r_out = None
+    t0 = time.perf_counter()
+    code = load().ebs_solve(pl.handle, ctypes.byref(P), D.stream())
+    wall = time.perf_counter() - t0
+    if code == EBS_ECALLBACK and state["exc"] is not None:
+        raise state["exc"]
+    check(code, "ebs_solve")
+    k = n_norms.value
+    hist = ConvergenceHistory(
+        residual_norms=np.array(norms[:k]),
+        error_norms=np.array(errors[:k]) if ref is not None else None,
+        wall_time=wall, diverged=bool(diverged.value))
+    return x, hist
+
+
+def richardson(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds, iters: int, *,
+               tol=None, reference=None, callback=None, threads: int = 1,
+               deterministic: bool = True):
+    """solvers.py:163-183: damped Richardson with the step 2/(lambda1+lambda2).
+
+    With ``deterministic=True`` the residual is the reference-order exact one, so
+    the iterates are bit-identical to ebsolve.richardson."""
+    omega = 2.0 / (bounds.lambda1 + bounds.lambda2)
+    return _solve(EBS_RICHARDSON, batch, d, x0, iters, omega=omega, exact=deterministic, tol=tol,
+                  reference=reference, callback=callback)
+
+
+def jacobi(batch: ElementBatch, d: DirichletData, x0, iters: int, *, omega: float = 0.8,
+           tol=None, reference=None, callback=None, deterministic: bool = False):
+    """NEW: damped Jacobi x += omega * (D^-1 mask(b - A x)), D = diagonal(batch),
+    on the _iterate loop (oracle/ebs_oracle.py jacobi)."""
+    return _solve(EBS_JACOBI, batch, d, x0, iters, omega=omega, exact=deterministic, tol=tol,
+                  reference=reference, callback=callback)
+
+
+def cg(batch: ElementBatch, d: DirichletData, x0, iters: int, *, tol=None, reference=None,
+       callback=None):
+    """NEW: conjugate gradients on the Dirichlet-masked operator (oracle pcg with
+    dinv = 1); history holds the recursive residual norms."""
+    return _solve(EBS_CG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback)
+
+
+def pcg(batch: ElementBatch, d: DirichletData, x0, iters: int, *, tol=None, reference=None,
+        callback=None):
+    """NEW: Jacobi (diagonal) preconditioned CG (oracle/ebs_oracle.py pcg)."""
+    return _solve(EBS_PCG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback)

@@ -1,0 +1,186 @@
+"""GPU parity: the element residual / matvec / rhs / diag through the C-ABI against the
+reference's own outputs (golden) and the oracle -- bitwise in reference order, within
+1e-12 (north-star tolerance) for the pre-assembled-b fast mode."""
+
+import numpy as np
+import numpy.testing as npt
+import pytest
+import torch
+
+from conftest import golden, to_np
+
+import oracle as o
+
+pytestmark = pytest.mark.gpu
+
+TOL_FAST = 1e-12  # north_star: fp64 residual within relative max-norm 1e-12
+
+
+def rel_max(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+@pytest.mark.parametrize("tag", ["l1_nu0.0", "l2_nu1.0", "l5_nu0.0", "l5_nu1.0"])
+def test_residual_family_matches_reference(gpu, tag):
+    import paper_1911_03973_b200 as eb
+    g = golden("residual2d")
+    level, nu = int(tag[1]), float(tag.split("nu")[1])
+    m = eb.build_unit_square_mesh(level)
+    batch = eb.build_element_batch(m, nu=nu)
+    d = eb.constant_dirichlet(m, 1.0)
+    x = g[f"x_{tag}"]
+    npt.assert_array_equal(to_np(eb.residual(batch, x)), g[f"r_{tag}"])
+    npt.assert_array_equal(to_np(eb.residual(batch, x, threads=8)), g[f"r_{tag}"])
+    assert rel_max(to_np(eb.residual(batch, x, deterministic=False)), g[f"r_{tag}"]) <= TOL_FAST
+    npt.assert_array_equal(to_np(eb.residual(batch, np.ones(m.n_nodes))), g[f"r1_{tag}"])
+    npt.assert_array_equal(to_np(eb.assemble_rhs(batch.b_e, batch.index)), g[f"rhs_{tag}"])
+    npt.assert_array_equal(to_np(eb.assemble_rhs(batch.b_e, batch.index.indt)), g[f"rhs_{tag}"])
+    npt.assert_array_equal(to_np(eb.matvec(batch, x, d)), g[f"av_{tag}"])
+    npt.assert_array_equal(to_np(eb.diagonal(batch)), g[f"diag_{tag}"])
+    masked = eb.mask_dirichlet(eb.residual(batch, x), d)
+    npt.assert_array_equal(to_np(masked), g[f"masked_{tag}"])
+
+
+def test_residual_known_answers(gpu):
+    import paper_1911_03973_b200 as eb
+    # test_operators.py:33-45: residual(0) == b, residual(1) == b (nu = 0) bitwise
+    for level in range(1, 5):
+        m = eb.build_unit_square_mesh(level)
+        batch = eb.build_element_batch(m)
+        b = to_np(eb.assemble_rhs(batch.b_e, batch.index))
+        npt.assert_array_equal(to_np(eb.residual(batch, np.zeros(m.n_nodes))), b)
+        npt.assert_array_equal(to_np(eb.residual(batch, np.ones(m.n_nodes))), b)
+    m = eb.build_unit_square_mesh(1)
+    b = to_np(eb.assemble_rhs(eb.build_element_batch(m).b_e, eb.build_element_batch(m).index))
+    assert abs(b[4] - 0.25) <= 1e-15
+
+
+def test_residual_input_validation(gpu):
+    import paper_1911_03973_b200 as eb
+    m = eb.build_unit_square_mesh(1)
+    batch = eb.build_element_batch(m)
+    with pytest.raises(ValueError):
+        eb.residual(batch, np.zeros((m.n_nodes, 1)))
+    bad = np.zeros(m.n_nodes)
+    bad[3] = np.nan
+    with pytest.raises(ValueError):
+        eb.residual(batch, bad)
+    bad[3] = np.inf
+    with pytest.raises(ValueError):
+        eb.residual(batch, torch.from_numpy(bad).cuda())
+
+
+def test_mask_and_dirichlet_semantics(gpu):
+    import paper_1911_03973_b200 as eb
+    m = eb.build_unit_square_mesh(2)
+    batch = eb.build_element_batch(m)
+    d = eb.constant_dirichlet(m, 1.0)
+    r = eb.residual(batch, np.zeros(m.n_nodes))
+    r_before = r.clone()
+    masked = eb.mask_dirichlet(r, d)
+    assert masked.data_ptr() != r.data_ptr()
+    assert bool((masked[d.nd] == 0).all())
+    assert torch.equal(r, r_before)
+    x0 = eb.apply_initial_guess(eb.build_unit_square_mesh(1), eb.constant_dirichlet(
+        eb.build_unit_square_mesh(1), 1.0))
+    assert int(torch.count_nonzero(x0)) == 8 and float(x0[4]) == 0.0
+    dd = eb.DirichletData(np.array([5, 2]), np.array([50.0, 20.0]))
+    npt.assert_array_equal(to_np(dd.nd), [2, 5])
+    npt.assert_array_equal(to_np(dd.values), [20.0, 50.0])
+    with pytest.raises(ValueError):
+        eb.DirichletData(np.array([1, 1]), np.array([0.0, 0.0]))
+    with pytest.raises(ValueError):
+        eb.DirichletData(np.array([1, 2]), np.array([0.0]))
+
+
+@pytest.mark.parametrize("name", ["c4_l4_seed0", "c2_l3_seed0"])
+def test_permuted_meshes_bitwise(gpu, name):
+    import paper_1911_03973_b200 as eb
+    g = golden(name)
+    m = eb.Mesh(g["nodes"], g["elements"], g["dirichlet"])
+    batch = eb.ElementBatch(K_e=g["K_e"], M_e=g["M_e"], A_e=g["A_e"], b_e=g["b_e"], nu=1.0,
+                            index=eb.build_index_arrays(m))
+    npt.assert_array_equal(to_np(eb.residual(batch, g["x"])), g["r"])
+    assert rel_max(to_np(eb.residual(batch, g["x"], deterministic=False)), g["r"]) <= TOL_FAST
+    if "av" in g:
+        d = eb.DirichletData(g["dirichlet"], np.zeros(len(g["dirichlet"])))
+        npt.assert_array_equal(to_np(eb.matvec(batch, g["x"], d)), g["av"])
+
+
+def test_plan_numbering_matches_oracle(gpu):
+    import paper_1911_03973_b200 as eb
+    inp = o.config_inputs(2, seed=0, size=5)
+    m = eb.Mesh(inp["nodes"], inp["elements"], inp["dirichlet"])
+    pl = eb.build_index_arrays(m).plan()
+    new_of_old, old_of_new = (to_np(t) for t in pl.node_maps())
+    ref = o.first_appearance_order(np.ascontiguousarray(inp["elements"].T), m.n_nodes)
+    npt.assert_array_equal(new_of_old, ref)
+    npt.assert_array_equal(old_of_new[new_of_old], np.arange(m.n_nodes))
+    info = pl.info()
+    assert info["max_valence"] == 6 and info["n_chunks"] == (m.n_nodes + 31) // 32
+
+
+@pytest.mark.parametrize("N", [2, 3])
+def test_tet_operator_matches_reference_code(gpu, N):
+    import paper_1911_03973_b200 as eb
+    g = golden("kuhn3d")
+    m = eb.build_unit_cube_mesh(N)
+    batch = eb.build_element_batch(m, nu=1.0)
+    x = g[f"x_N{N}"]
+    face = eb.face_z0_nodes(m)
+    d = eb.DirichletData(face, torch.zeros(face.numel(), dtype=torch.float64, device=face.device))
+    npt.assert_array_equal(to_np(eb.residual(batch, x)), g[f"r_N{N}"])
+    assert rel_max(to_np(eb.residual(batch, x, deterministic=False)), g[f"r_N{N}"]) <= TOL_FAST
+    npt.assert_array_equal(to_np(eb.matvec(batch, x, d)), g[f"av_N{N}"])
+    npt.assert_array_equal(to_np(eb.assemble_rhs(batch.b_e, batch.index)), g[f"rhs_N{N}"])
+
+
+def test_isolated_nodes_and_user_batches(gpu):
+    """A hand-built batch (conftest.diagonal_batch of the reference) with x longer than
+    the mesh: trailing nodes no element touches get residual 0 (np.bincount minlength)."""
+    import paper_1911_03973_b200 as eb
+    A = np.diag([2.0, 3.0, 4.0]).reshape(3, 3, 1)
+    indt = np.array([[0], [1], [2]])
+    batch = eb.ElementBatch(K_e=A, M_e=np.zeros_like(A), A_e=A, b_e=np.array([[1.0], [0.0], [0.0]]),
+                            nu=0.0, index=eb.IndexArrays(indt.reshape(3, 1, 1), indt))
+    r = to_np(eb.residual(batch, np.array([1.0, 1.0, 1.0, 5.0])))
+    npt.assert_array_equal(r, [1.0 - 2.0, -3.0, -4.0, 0.0])
+
+
+@pytest.mark.parametrize("level", [7, 9])
+def test_random_inputs_bitwise_vs_oracle(gpu, level):
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    for config in (2, 4):
+        p = config_problem(config, seed=level, size=level)
+        inp = o.config_inputs(config, seed=level, size=level)
+        _, _, A, b_e = o.element_matrices(inp["nodes"], inp["elements"], nu=p["nu"],
+                                          f_vals=inp["f_vals"])
+        indt = np.ascontiguousarray(inp["elements"].T)
+        x = inp["x"] if config == 2 else np.random.default_rng(1).uniform(-1, 1, len(inp["nodes"]))
+        ref = o.residual(A, b_e, indt, x)
+        npt.assert_array_equal(to_np(eb.residual(p["batch"], x)), ref)
+        assert rel_max(to_np(eb.residual(p["batch"], x, deterministic=False)), ref) <= TOL_FAST
+        nd = inp["dirichlet"]
+        d = p["dirichlet"]
+        npt.assert_array_equal(to_np(eb.matvec(p["batch"], x, d)), o.matvec_masked(A, indt, x, nd))
+
+
+@pytest.mark.slow
+def test_c2_full_size_vs_oracle(gpu):
+    """BASELINE C2 at full size (level 11, 8.4M triangles, permuted): bitwise vs the oracle,
+    plus run-to-run determinism of both modes."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(2, seed=0)
+    batch, x = p["batch"], p["x"]
+    r_exact = eb.residual(batch, x)
+    r_fast = eb.residual(batch, x, deterministic=False)
+    assert torch.equal(r_exact, eb.residual(batch, x))
+    assert torch.equal(r_fast, eb.residual(batch, x, deterministic=False))
+    A = batch.A_e.permute(2, 0, 1).contiguous().cpu().numpy().transpose(1, 2, 0)
+    b_e = to_np(batch.b_e)
+    indt = to_np(batch.index.indt).astype(np.int64)
+    ref = o.residual(A, b_e, indt, x, threads=8)
+    npt.assert_array_equal(to_np(r_exact), ref)
+    assert rel_max(to_np(r_fast), ref) <= TOL_FAST

@@ -1,0 +1,192 @@
+"""GPU parity of the solver loop (solvers.py:117-183 semantics) and of the north-star
+solvers: Richardson iterates bit-identical to the reference; Jacobi / CG / PCG against the
+oracle restatement (same iteration count, solution within 1e-8) and the reference's direct
+solution."""
+
+import numpy as np
+import numpy.testing as npt
+import pytest
+import torch
+
+from conftest import golden, to_np
+
+import oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(level, nu=0.0, value=1.0):
+    import paper_1911_03973_b200 as eb
+    m = eb.build_unit_square_mesh(level)
+    batch = eb.build_element_batch(m, nu=nu)
+    return m, batch, eb.constant_dirichlet(m, value)
+
+
+def test_richardson_bitwise_vs_reference(gpu):
+    import paper_1911_03973_b200 as eb
+    g = golden("richardson_l3")
+    m, batch, d = problem(3)
+    bounds = eb.model_eigen_bounds(9)
+    assert bounds.lambda1 == float(g["lambda1"]) and bounds.lambda2 == float(g["lambda2"])
+    xs = []
+    x, hist = eb.richardson(batch, d, np.ones(m.n_nodes), bounds, 20,
+                            callback=lambda k, x, r: xs.append(to_np(x).copy()))
+    npt.assert_array_equal(to_np(x), g["x"])
+    npt.assert_array_equal(np.stack(xs), g["iterates"])
+    npt.assert_allclose(hist.residual_norms, g["norms"], rtol=1e-12)
+    # same without a callback (device-resident loop)
+    x2, hist2 = eb.richardson(batch, d, np.ones(m.n_nodes), bounds, 20)
+    npt.assert_array_equal(to_np(x2), g["x"])
+    npt.assert_array_equal(hist2.residual_norms, hist.residual_norms)
+    # tol early stop (solvers.py:135)
+    x3, hist3 = eb.richardson(batch, d, np.ones(m.n_nodes), bounds, 500, tol=1e-3)
+    npt.assert_array_equal(to_np(x3), g["x_tol"])
+    assert len(hist3.residual_norms) == len(g["norms_tol"])
+    # error norms against a reference solution
+    _, hist4 = eb.richardson(batch, d, np.ones(m.n_nodes), bounds, 7, reference=g["u"])
+    npt.assert_allclose(hist4.error_norms, g["errors"], rtol=1e-12)
+    npt.assert_allclose(hist4.residual_norms, g["norms_err"], rtol=1e-12)
+
+
+def test_loop_mechanics(gpu):
+    import paper_1911_03973_b200 as eb
+    m, batch, d = problem(2)
+    bounds = eb.model_eigen_bounds(5)
+    x0 = torch.ones(m.n_nodes, dtype=torch.float64, device="cuda")
+    x, hist = eb.richardson(batch, d, x0, bounds, 7)
+    assert len(hist.residual_norms) == 8 and hist.wall_time >= 0 and not hist.diverged
+    x, hist = eb.richardson(batch, d, x0, bounds, 0)
+    assert len(hist.residual_norms) == 1
+    assert torch.equal(x, x0) and x.data_ptr() != x0.data_ptr()
+    with pytest.raises(ValueError):
+        eb.richardson(batch, d, x0, bounds, -1)
+    ks = []
+    eb.richardson(batch, d, x0, bounds, 5, callback=lambda k, x, r: ks.append(k))
+    assert ks == [0, 1, 2, 3, 4, 5]
+    for solver in (eb.pcg, eb.cg, eb.jacobi):
+        ks = []
+        solver(batch, d, x0, 5, callback=lambda k, x, r: ks.append(k))
+        assert ks == [0, 1, 2, 3, 4, 5], solver.__name__
+
+    def boom(k, x, r):
+        if k == 2:
+            raise KeyError("stop")
+    with pytest.raises(KeyError):
+        eb.richardson(batch, d, x0, bounds, 5, callback=boom)
+
+
+def test_divergence_sets_flag(gpu):
+    import paper_1911_03973_b200 as eb
+    m, batch, d = problem(2)
+    bad = eb.SpectralBounds(1e-4, 2e-4)
+    x, hist = eb.richardson(batch, d, np.ones(m.n_nodes), bad, 300)
+    assert hist.diverged
+    assert not np.isfinite(hist.residual_norms[-1])
+    assert len(hist.residual_norms) <= 301
+    # oracle takes the same number of steps before blowing up
+    nodes, elements, nd = o.unit_square_mesh(2)
+    _, _, A, b_e = o.element_matrices(nodes, elements)
+    _, ho = o.richardson(A, b_e, np.ascontiguousarray(elements.T), nd, np.ones(len(nodes)),
+                         1e-4, 2e-4, 300)
+    assert len(ho["residual_norms"]) == len(hist.residual_norms)
+
+
+def test_constrained_entries_never_move(gpu):
+    import paper_1911_03973_b200 as eb
+    m, batch, d = problem(3)
+    bounds = eb.model_eigen_bounds(9)
+
+    def pinned(k, x, r):
+        assert bool((x[d.nd] == 1.0).all())
+        assert bool((r[d.nd] == 0.0).all())
+    x, _ = eb.richardson(batch, d, np.ones(m.n_nodes), bounds, 20, callback=pinned)
+    assert bool((x[d.nd] == 1.0).all())
+    for solver in (eb.jacobi, eb.cg, eb.pcg):
+        x, _ = solver(batch, d, np.ones(m.n_nodes), 20, callback=pinned)
+        assert bool((x[d.nd] == 1.0).all())
+
+
+def oracle_problem(level, nu):
+    nodes, elements, nd = o.unit_square_mesh(level)
+    _, _, A, b_e = o.element_matrices(nodes, elements, nu=nu)
+    return nodes, np.ascontiguousarray(elements.T), nd, A, b_e
+
+
+@pytest.mark.parametrize("method", ["jacobi", "cg", "pcg"])
+def test_solvers_match_oracle(gpu, method):
+    import paper_1911_03973_b200 as eb
+    m, batch, d = problem(5, nu=1.0, value=0.0)
+    nodes, indt, nd, A, b_e = oracle_problem(5, 1.0)
+    x0 = np.zeros(m.n_nodes)
+    if method == "jacobi":
+        x, h = eb.jacobi(batch, d, x0, 60, omega=0.8)
+        xo, ho = o.jacobi(A, b_e, indt, nd, x0, 0.8, 60)
+    else:
+        x, h = getattr(eb, method)(batch, d, x0, 1000, tol=1e-8)
+        xo, ho = getattr(o, method)(A, b_e, indt, nd, x0, 1000, tol=1e-8)
+    assert len(h.residual_norms) == len(ho["residual_norms"])
+    npt.assert_allclose(h.residual_norms, ho["residual_norms"], rtol=1e-8, atol=1e-14)
+    assert np.linalg.norm(to_np(x) - xo) <= 1e-8 * np.linalg.norm(xo)
+    assert not h.diverged
+
+
+def test_pcg_c1_against_reference_direct_solve(gpu):
+    """BASELINE C1: level 6, nu=1, f=1, Dirichlet 0, JPCG to 1e-8 relative residual."""
+    import paper_1911_03973_b200 as eb
+    g = golden("c1_solution")
+    m, batch, d = problem(6, nu=1.0, value=0.0)
+    nodes, indt, nd, A, b_e = oracle_problem(6, 1.0)
+    x, h = eb.pcg(batch, d, np.zeros(m.n_nodes), 10_000, tol=1e-8)
+    xo, ho = o.pcg(A, b_e, indt, nd, np.zeros(m.n_nodes), 10_000, tol=1e-8)
+    assert len(h.residual_norms) == len(ho["residual_norms"])
+    assert np.linalg.norm(to_np(x) - xo) <= 1e-8 * np.linalg.norm(xo)
+    u = g["u_direct"]
+    assert np.linalg.norm(to_np(x) - u) <= 1e-7 * np.linalg.norm(u)
+    assert abs(h.iterations - int(g["scipy_pcg_iters"])) <= 2
+
+
+def test_pcg_3d_against_reference_direct_solve(gpu):
+    import paper_1911_03973_b200 as eb
+    g = golden("kuhn3d")
+    for N in (2, 3):
+        m = eb.build_unit_cube_mesh(N)
+        batch = eb.build_element_batch(m, nu=1.0)
+        face = eb.face_z0_nodes(m)
+        d = eb.DirichletData(face, torch.zeros(face.numel(), dtype=torch.float64, device="cuda"))
+        x, h = eb.pcg(batch, d, np.zeros(m.n_nodes), 1000, tol=1e-13)
+        u = g[f"u_N{N}"]
+        assert np.linalg.norm(to_np(x) - u) <= 1e-10 * np.linalg.norm(u)
+
+
+def test_pcg_3d_c3_recipe_reduced(gpu):
+    """BASELINE C3 recipe (nu=0, Dirichlet on z=0 only, Neumann elsewhere) at N=8:
+    same iteration count and solution as the oracle."""
+    from paper_1911_03973_b200.inputs import config_problem
+    import paper_1911_03973_b200 as eb
+    p = config_problem(3, size=8)
+    nodes, elements, face = o.kuhn_cube_mesh(8)
+    _, _, A, b_e = o.element_matrices(nodes, elements, nu=0.0)
+    indt = np.ascontiguousarray(elements.T)
+    x, h = eb.pcg(p["batch"], p["dirichlet"], np.zeros(p["mesh"].n_nodes), 2000, tol=1e-8)
+    xo, ho = o.pcg(A, b_e, indt, face, np.zeros(len(nodes)), 2000, tol=1e-8)
+    assert len(h.residual_norms) == len(ho["residual_norms"])
+    assert np.linalg.norm(to_np(x) - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_jacobi_c4_recipe_reduced(gpu):
+    """BASELINE C4 recipe (jittered, permuted, nu=10, f=sin sin) at level 6, 200 damped
+    Jacobi iterations: history and iterate vs the oracle."""
+    from paper_1911_03973_b200.inputs import config_problem
+    import paper_1911_03973_b200 as eb
+    p = config_problem(4, size=6)
+    inp = o.config_inputs(4, size=6)
+    _, _, A, b_e = o.element_matrices(inp["nodes"], inp["elements"], nu=10.0, f_vals=inp["f_vals"])
+    indt = np.ascontiguousarray(inp["elements"].T)
+    x0 = np.zeros(len(inp["nodes"]))
+    x, h = eb.jacobi(p["batch"], p["dirichlet"], x0, 200, omega=0.8)
+    xo, ho = o.jacobi(A, b_e, indt, inp["dirichlet"], x0, 0.8, 200)
+    npt.assert_allclose(h.residual_norms, ho["residual_norms"], rtol=1e-10)
+    assert np.linalg.norm(to_np(x) - xo) <= 1e-10 * np.linalg.norm(xo)
+    # exact-residual Jacobi reproduces the oracle iterate bit for bit
+    x_ex, _ = eb.jacobi(p["batch"], p["dirichlet"], x0, 200, omega=0.8, deterministic=True)
+    npt.assert_array_equal(to_np(x_ex), xo)
