@@ -159,7 +159,7 @@ __global__ void k_pack(int nb, int64_t n_e, int64_t n_slots, const int32_t *__re
         const int64_t row = s / LANES;
         const int lane = (int)(s - row * LANES);
         const int32_t ej = slot_ej[s];
-        if (ej >= 0) {
+        if (ej != -1) {  // j >= 2 sets the sign bit: only -1 marks padding
             const int64_t e = ej & ID_MASK, j = (uint32_t)ej >> J_SHIFT;
             const double *src = A_e + (e * nb + j) * nb;  // row j of element e
             for (int i = 0; i < nb; ++i) slot_A[(row * nb + i) * LANES + lane] = src[i];
