@@ -12,7 +12,7 @@ import ctypes
 import os
 from ctypes import POINTER, c_double, c_int, c_int64, c_size_t, c_void_p, c_char_p
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libebs.so")
+LIB_PATH = os.environ.get("EBS_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libebs.so")
 
 EBS_OK = 0
 EBS_EINVAL = -1

@@ -74,6 +74,28 @@ __global__ void k_scatter_add(int64_t n, const int64_t *__restrict__ idx,
         v[idx[i]] += buf[i];
 }
 
+// occupancy-sized persistent grid, cached per (kernel, device)
+int persistent_grid(const void *kernel, int block, int64_t work_blocks) {
+    struct Ent { const void *k; int dev; int block; int grid; };
+    static Ent cache[64];
+    static int n_cache = 0;
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    int grid = -1;
+    for (int i = 0; i < n_cache; ++i)
+        if (cache[i].k == kernel && cache[i].dev == dev && cache[i].block == block) grid = cache[i].grid;
+    if (grid < 0) {
+        int per_sm = 0, sms = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        grid = (per_sm > 0 ? per_sm : 1) * sms;
+        if (grid > 8192) grid = 8192;
+        if (n_cache < 64) cache[n_cache++] = Ent{kernel, dev, block, grid};
+    }
+    if (work_blocks < 1) work_blocks = 1;
+    return (int)(work_blocks < grid ? work_blocks : grid);
+}
+
 // scratch for the standalone reductions (one per device is enough: stream-ordered use)
 static double *g_partials = nullptr;
 static unsigned int *g_counter = nullptr;

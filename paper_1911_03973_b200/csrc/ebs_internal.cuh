@@ -115,9 +115,11 @@ struct Plan {
     int32_t *rowbase = nullptr;     // first slot row of each chunk
     int32_t *width = nullptr;       // slot rows of each chunk
     int32_t *slot_ej = nullptr;     // [row][lane]: e | j<<30, -1 for padding
-    int32_t *slot_nb = nullptr;     // [row][t][lane]: t-th cyclic neighbour (t=0 carries j)
+    // slot blob: per row NB planes of 32 doubles (A rows) + the id plane (sell.cuh)
+    uint8_t *slot = nullptr;
+    int rowb = 0;                   // bytes per slot row
+    int packed = 0;                 // 1: delta-packed ids, 0: absolute int32 ids
     // loaded operator
-    double *slot_A = nullptr;   // [row][i][lane]: A_e[j, i, e]
     double *slot_be = nullptr;  // [row][lane]: b_e[j, e] (exact residual)
     double *b_int = nullptr;    // pre-assembled b, internal numbering
     int has_A = 0, has_be = 0;

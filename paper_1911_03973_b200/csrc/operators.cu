@@ -32,48 +32,77 @@ __global__ void k_to_user(int64_t n, const int32_t *__restrict__ old_of_new,
 }
 
 // MODE 0: y = A x   1: r = b - A x (pre-assembled b)   2: r = sum(b_e - A_e x_e) exact
-template <int NB, int MODE>
-__global__ void __launch_bounds__(256)
-    k_sell_op(SellView v, const double *__restrict__ x, const double *__restrict__ b_int,
-              const uint8_t *__restrict__ free_int, const int32_t *__restrict__ old_of_new,
-              double *__restrict__ out) {
-    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-    const int lane = threadIdx.x & (LANES - 1);
-    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
-    if (chunk >= n_chunks) return;
-    const int64_t m = chunk * LANES + lane;
-    const bool valid = m < v.n_n;
-    const int c_m = valid ? v.cnt[m] : 0;
-    const double xo = valid ? x[m] : 0.0;
-    double s = sell_node_sum<NB, MODE == 2>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, x, xo);
-    if (!valid) return;
-    if (MODE == 1) s = b_int[m] - s;
-    if (free_int && !free_int[m]) s = 0.0;
-    if (old_of_new) out[old_of_new[m]] = s;
-    else out[m] = s;
+struct OpEpi {
+    int mode;
+    const double *__restrict__ b_int;
+    const uint8_t *__restrict__ free_int;
+    const int32_t *__restrict__ old_of_new;
+    double *__restrict__ out;
+    __device__ __forceinline__ void operator()(int64_t m, double s, double) {
+        if (mode == 1) s = b_int[m] - s;
+        if (free_int && !free_int[m]) s = 0.0;
+        if (old_of_new) out[old_of_new[m]] = s;
+        else out[m] = s;
+    }
+};
+
+template <int NB, bool PACKED, int MODE>
+__global__ void EBS_SELL_BOUNDS(NB)
+    k_sell_op(SellView v, const double *__restrict__ x, OpEpi epi) {
+    sell_sweep<NB, PACKED, MODE == 2>(v, x, epi);
+}
+
+template <int NB, bool PACKED, int MODE>
+void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cudaStream_t s) {
+    auto kern = k_sell_op<NB, PACKED, MODE>;
+    const int grid = persistent_grid((const void *)kern, 256, (p->n_chunks * LANES + 255) / 256);
+    kern<<<grid, 256, 0, s>>>(sell_view(p), x_int, epi);
+    LAUNCHED();
 }
 
 template <int MODE>
 void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
                     const int32_t *old_of_new, double *out, cudaStream_t s) {
     if (p->n_n == 0) return;
-    const int block = 256;
-    const int64_t grid = (p->n_chunks * LANES + block - 1) / block;
-    SellView v = sell_view(p);
-    if (p->nb == 3)
-        k_sell_op<3, MODE><<<(unsigned)grid, block, 0, s>>>(v, x_int, p->b_int, free_int,
-                                                          old_of_new, out);
-    else
-        k_sell_op<4, MODE><<<(unsigned)grid, block, 0, s>>>(v, x_int, p->b_int, free_int,
-                                                          old_of_new, out);
-    LAUNCHED();
+    OpEpi epi{MODE, p->b_int, free_int, old_of_new, out};
+    if (p->nb == 3) {
+        if (p->packed) launch_sell_op_t<3, true, MODE>(p, x_int, epi, s);
+        else launch_sell_op_t<3, false, MODE>(p, x_int, epi, s);
+    } else {
+        if (p->packed) launch_sell_op_t<4, true, MODE>(p, x_int, epi, s);
+        else launch_sell_op_t<4, false, MODE>(p, x_int, epi, s);
+    }
 }
+
+// scatter orientation: coalesced read of x in caller order, 8 B writes into the
+// L2-resident internal vector (writes do not stall the issuing warp)
+__global__ void k_to_internal_scatter(int64_t n, const int32_t *__restrict__ new_of_old,
+                                      const double *__restrict__ x_user,
+                                      double *__restrict__ x_int, int32_t *nonfinite) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double v = x_user[i];
+        bad |= !isfinite(v);
+        x_int[new_of_old[i]] = v;
+    }
+    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(nonfinite, 1);
+}
+
+#ifndef EBS_TO_INTERNAL_SCATTER
+#define EBS_TO_INTERNAL_SCATTER 1
+#endif
 
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
                  cudaStream_t s) {
     if (p->n_n == 0) return;
-    k_to_internal<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(p->n_n, p->old_of_new, x_user,
-                                                                  x_int, nonfinite);
+    if (EBS_TO_INTERNAL_SCATTER)
+        k_to_internal_scatter<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(
+            p->n_n, p->new_of_old, x_user, x_int, nonfinite);
+    else
+        k_to_internal<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(p->n_n, p->old_of_new,
+                                                                      x_user, x_int, nonfinite);
     LAUNCHED();
 }
 

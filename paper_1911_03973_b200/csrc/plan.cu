@@ -120,8 +120,9 @@ __global__ void k_fill_slots(int nb, int64_t n_n, int64_t n_e, const int32_t *__
                              const int32_t *__restrict__ rowptr, const int32_t *__restrict__ cnt,
                              const int64_t *__restrict__ keys, const int32_t *__restrict__ rowbase,
                              const int32_t *__restrict__ width, int32_t *__restrict__ slot_ej,
-                             int32_t *__restrict__ slot_nb) {
+                             int32_t *__restrict__ ids_abs, unsigned long long *max_delta) {
     const int64_t n_pad = ((n_n + LANES - 1) / LANES) * LANES;
+    unsigned long long md = 0;
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_pad;
          m += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = m / LANES;
@@ -137,35 +138,85 @@ __global__ void k_fill_slots(int nb, int64_t n_n, int64_t n_e, const int32_t *__
                 for (int t = 1; t < nb; ++t) {
                     int64_t jj = (j + t) % nb;
                     int32_t id = new_of_old[conn[jj * n_e + e]];
+                    int64_t d = (int64_t)id - m;
+                    unsigned long long ad = (unsigned long long)(d < 0 ? -d : d);
+                    md = ad > md ? ad : md;
                     if (t == 1) id |= (int32_t)(j << J_SHIFT);
-                    slot_nb[(row * (nb - 1) + (t - 1)) * LANES + lane] = id;
+                    ids_abs[(row * (nb - 1) + (t - 1)) * LANES + lane] = id;
                 }
             } else {
                 slot_ej[row * LANES + lane] = -1;
                 int32_t self = m < n_n ? (int32_t)m : 0;
                 for (int t = 1; t < nb; ++t)
-                    slot_nb[(row * (nb - 1) + (t - 1)) * LANES + lane] = self;
+                    ids_abs[(row * (nb - 1) + (t - 1)) * LANES + lane] = self;
+            }
+        }
+    }
+    if (md) atomicMax(max_delta, md);
+}
+
+// id plane of every slot row (sell.cuh layout): delta-packed or absolute
+__global__ void k_write_ids(int nb, int64_t n_n, int64_t n_chunks, int rowb, int packed,
+                            const int32_t *__restrict__ rowbase, const int32_t *__restrict__ width,
+                            const int32_t *__restrict__ ids_abs, uint8_t *__restrict__ slot) {
+    const int64_t n_pad = n_chunks * LANES;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_pad;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = m / LANES;
+        const int lane = (int)(m - c * LANES);
+        const int w = width[c];
+        const int64_t self = m < n_n ? m : 0;
+        for (int k = 0; k < w; ++k) {
+            const int64_t row = (int64_t)rowbase[c] + k;
+            const int32_t *src = ids_abs + row * (nb - 1) * LANES + lane;
+            uint8_t *dst = slot + row * rowb + nb * 256;
+            if (packed) {
+                const int32_t id0 = src[0];
+                const uint64_t j = (uint32_t)id0 >> J_SHIFT;
+                if (nb == 3) {
+                    uint32_t wd = (uint32_t)j << 30;
+                    for (int t = 0; t < 2; ++t) {
+                        int64_t id = (int64_t)(src[t * LANES] & ID_MASK);
+                        uint32_t f = (uint32_t)(id - self + (1 << 14)) & 0x7FFFu;
+                        wd |= f << (15 * (1 - t));
+                    }
+                    reinterpret_cast<uint32_t *>(dst)[lane] = wd;
+                } else {
+                    unsigned long long wd = (unsigned long long)j << 62;
+                    for (int t = 0; t < 3; ++t) {
+                        int64_t id = (int64_t)(src[t * LANES] & ID_MASK);
+                        unsigned long long f =
+                            (unsigned long long)(id - self + (1 << 19)) & 0xFFFFFull;
+                        wd |= f << (20 * (2 - t));
+                    }
+                    reinterpret_cast<unsigned long long *>(dst)[lane] = wd;
+                }
+            } else {
+                for (int t = 0; t < nb - 1; ++t)
+                    reinterpret_cast<int32_t *>(dst)[t * LANES + lane] = src[t * LANES];
             }
         }
     }
 }
 
 // ------------------------------------------------------------- load kernels --
-__global__ void k_pack(int nb, int64_t n_e, int64_t n_slots, const int32_t *__restrict__ slot_ej,
-                       const double *__restrict__ A_e, const double *__restrict__ b_e,
-                       double *__restrict__ slot_A, double *__restrict__ slot_be) {
+__global__ void k_pack(int nb, int64_t n_e, int64_t n_slots, int rowb,
+                       const int32_t *__restrict__ slot_ej, const double *__restrict__ A_e,
+                       const double *__restrict__ b_e, uint8_t *__restrict__ slot,
+                       double *__restrict__ slot_be) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = s / LANES;
         const int lane = (int)(s - row * LANES);
         const int32_t ej = slot_ej[s];
+        double *dst = reinterpret_cast<double *>(slot + row * rowb) + lane;
         if (ej != -1) {  // j >= 2 sets the sign bit: only -1 marks padding
             const int64_t e = ej & ID_MASK, j = (uint32_t)ej >> J_SHIFT;
             const double *src = A_e + (e * nb + j) * nb;  // row j of element e
-            for (int i = 0; i < nb; ++i) slot_A[(row * nb + i) * LANES + lane] = src[i];
+            for (int i = 0; i < nb; ++i) dst[i * LANES] = src[i];
             if (slot_be) slot_be[s] = b_e[j * n_e + e];
         } else {
-            for (int i = 0; i < nb; ++i) slot_A[(row * nb + i) * LANES + lane] = 0.0;
+            for (int i = 0; i < nb; ++i) dst[i * LANES] = 0.0;
             if (slot_be) slot_be[s] = 0.0;
         }
     }
@@ -173,12 +224,13 @@ __global__ void k_pack(int nb, int64_t n_e, int64_t n_slots, const int32_t *__re
 
 // Ordered per-node sums over slots of a value fetched per slot:
 //   what = 0: b_e[j, e] (assemble_rhs, operators.py:58-63)
-//   what = 1: slot_A[row][j][lane] = A_e[j, j, e] (diag)
+//   what = 1: A plane j of the slot row = A_e[j, j, e] (diag)
 //   what = 2: slot_be (pre-assembled b from the packed stream)
 // out_user != nullptr writes caller numbering, else internal numbering.
 __global__ void k_slot_sum(int nb, int64_t n_n, int64_t n_e, const int32_t *__restrict__ rowbase,
                            const int32_t *__restrict__ width, const int32_t *__restrict__ cnt,
-                           const int32_t *__restrict__ slot_ej, const double *__restrict__ slot_A,
+                           const int32_t *__restrict__ slot_ej, const uint8_t *__restrict__ slot,
+                           int rowb,
                            const double *__restrict__ slot_be, const double *__restrict__ b_e,
                            int what, const int32_t *__restrict__ old_of_new,
                            double *__restrict__ out) {
@@ -199,7 +251,8 @@ __global__ void k_slot_sum(int nb, int64_t n_n, int64_t n_e, const int32_t *__re
             } else {
                 const int32_t ej = slot_ej[sidx];
                 const int64_t e = ej & ID_MASK, j = (uint32_t)ej >> J_SHIFT;
-                v = what == 0 ? b_e[j * n_e + e] : slot_A[(row * nb + j) * LANES + lane];
+                v = what == 0 ? b_e[j * n_e + e]
+                              : reinterpret_cast<const double *>(slot + row * rowb)[j * LANES + lane];
             }
             s = s + v;
         }
@@ -229,7 +282,7 @@ void slot_sum(const Plan *p, int what, const double *b_e, const int32_t *old_of_
               cudaStream_t s) {
     if (p->n_n == 0) return;
     k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, s>>>(
-        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot_A, p->slot_be,
+        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot, p->rowb, p->slot_be,
         b_e, what, old_of_new, out);
     LAUNCHED();
 }
@@ -264,7 +317,7 @@ double *plan_vec(Plan *p, int i) {
 
 static void plan_free(Plan *p) {
     dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->rowbase);
-    dfree(p->width); dfree(p->slot_ej); dfree(p->slot_nb); dfree(p->slot_A);
+    dfree(p->width); dfree(p->slot_ej); dfree(p->slot);
     dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
     dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag);
     for (auto &v : p->wvec) dfree(v);
@@ -372,12 +425,32 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     }
     EBS_REQUIRE(p->n_rows * LANES * (int64_t)nb < (1ll << 40), "slot stream too large");
     p->slot_ej = dmalloc<int32_t>(p->n_rows * LANES);
-    p->slot_nb = dmalloc<int32_t>(p->n_rows * LANES * (nb - 1));
-    if (p->n_chunks) {
-        k_fill_slots<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
-            nb, n_n, n_e, conn, p->new_of_old, rowptr, p->cnt, keys, p->rowbase, p->width,
-            p->slot_ej, p->slot_nb);
-        LAUNCHED();
+    {
+        int32_t *ids_abs = dmalloc<int32_t>(p->n_rows * LANES * (nb - 1));
+        unsigned long long *md = dmalloc<unsigned long long>(1);
+        CU(cudaMemsetAsync(md, 0, sizeof(unsigned long long), s));
+        if (p->n_chunks) {
+            k_fill_slots<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
+                nb, n_n, n_e, conn, p->new_of_old, rowptr, p->cnt, keys, p->rowbase, p->width,
+                p->slot_ej, ids_abs, md);
+            LAUNCHED();
+        }
+        unsigned long long max_delta = read1(md, s);
+        cudaFree(md);
+        // packed deltas: 2 x 15 bit (2D) / 3 x 20 bit (3D), biased; else absolute ids
+        const unsigned long long limit = nb == 3 ? (1ull << 14) - 1 : (1ull << 19) - 1;
+        p->packed = max_delta <= limit ? 1 : 0;
+        const int id_bytes = p->packed ? (nb == 3 ? 4 : 8) * LANES : 4 * (nb - 1) * LANES;
+        p->rowb = nb * 8 * LANES + id_bytes;
+        p->slot = dmalloc<uint8_t>((size_t)p->n_rows * p->rowb);
+        CU(cudaMemsetAsync(p->slot, 0, (size_t)p->n_rows * p->rowb, s));
+        if (p->n_chunks) {
+            k_write_ids<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
+                nb, n_n, p->n_chunks, p->rowb, p->packed, p->rowbase, p->width, ids_abs, p->slot);
+            LAUNCHED();
+        }
+        CU(cudaStreamSynchronize(s));
+        cudaFree(ids_abs);
     }
     // max valence (for info)
     {
@@ -404,7 +477,7 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     p->ctl = dmalloc<Ctl>(1);
     CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
     CU(cudaMallocHost(&p->ctl_host, sizeof(Ctl)));
-    p->partials = dmalloc<double>(4 * (p->n_chunks / 8 + RED_MAX_BLOCKS + 8));
+    p->partials = dmalloc<double>(4 * 8192);
     p->flag = dmalloc<int32_t>(4);
     p->free_int = dmalloc<uint8_t>(n_n);
     if (n_n) {
@@ -447,10 +520,9 @@ int ebs_plan_info(ebs_plan_t plan, int64_t *info) {
     info[3] = p->n_chunks;
     info[4] = p->n_rows;
     int64_t slots = p->n_rows * LANES;
-    info[5] = slots * (int64_t)(4 * (p->nb - 1) + (p->has_A ? 8 * p->nb : 0) +
-                                (p->has_be ? 8 : 0));
+    info[5] = p->n_rows * (int64_t)p->rowb + (p->has_be ? slots * 8 : 0);
     info[6] = p->max_valence;
-    info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0);
+    info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0) | (p->packed ? 4 : 0);
     EBS_CATCH
 }
 
@@ -475,19 +547,19 @@ int ebs_plan_load(ebs_plan_t plan, const double *A_e, const double *b_e, void *s
     Plan *p = reinterpret_cast<Plan *>(plan);
     cudaStream_t s = S(stream);
     const int64_t n_slots = p->n_rows * LANES;
-    if (!p->slot_A) p->slot_A = dmalloc<double>(n_slots * p->nb);
     if (b_e && !p->slot_be) p->slot_be = dmalloc<double>(n_slots);
     if (b_e && !p->b_int) p->b_int = dmalloc<double>(p->n_n);
     if (n_slots) {
         k_pack<<<grid_for(n_slots, 256, 148 * 64), 256, 0, s>>>(
-            p->nb, p->n_e, n_slots, p->slot_ej, A_e, b_e, p->slot_A, b_e ? p->slot_be : nullptr);
+            p->nb, p->n_e, n_slots, p->rowb, p->slot_ej, A_e, b_e, p->slot,
+            b_e ? p->slot_be : nullptr);
         LAUNCHED();
     }
     p->has_A = 1;
     p->has_be = b_e ? 1 : 0;
     if (b_e && p->n_n) {
         k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, s>>>(
-            p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot_A,
+            p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot, p->rowb,
             p->slot_be, nullptr, 2, nullptr, p->b_int);
         LAUNCHED();
     }
@@ -520,8 +592,8 @@ int ebs_assemble_rhs(ebs_plan_t plan, const double *b_e, double *b, void *stream
     Plan *p = reinterpret_cast<Plan *>(plan);
     if (p->n_n == 0) return EBS_OK;
     k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, S(stream)>>>(
-        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, nullptr, nullptr, b_e, 0,
-        p->old_of_new, b);
+        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, nullptr, 0, nullptr, b_e,
+        0, p->old_of_new, b);
     LAUNCHED();
     EBS_CATCH
 }
@@ -533,7 +605,7 @@ int ebs_diagonal(ebs_plan_t plan, double *d, void *stream) {
     EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
     if (p->n_n == 0) return EBS_OK;
     k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, S(stream)>>>(
-        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot_A, nullptr,
+        p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot, p->rowb, nullptr,
         nullptr, 1, p->old_of_new, d);
     LAUNCHED();
     EBS_CATCH

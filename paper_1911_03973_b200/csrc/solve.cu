@@ -43,8 +43,36 @@ __device__ __forceinline__ void flag_nonfinite(Ctl *ctl, bool bad) {
 }
 
 // ---------------------------------------------------------- Richardson/Jacobi --
-template <int NB, bool EXACT>
-__global__ void __launch_bounds__(256)
+struct JacobiEpi {
+    const double *__restrict__ b_int;
+    const uint8_t *__restrict__ free_int;
+    const double *__restrict__ dinv;
+    const double *__restrict__ ref;
+    double *__restrict__ r_out;
+    double *__restrict__ xn_buf;
+    double omega;
+    int exact, final_step;
+    double part[2];
+    bool bad;
+    __device__ __forceinline__ void operator()(int64_t m, double s, double xo) {
+        double r = exact ? s : b_int[m] - s;
+        if (!free_int[m]) r = 0.0;
+        part[0] += r * r;
+        if (ref) {
+            double d = xo - ref[m];
+            part[1] += d * d;
+        }
+        if (r_out) r_out[m] = r;
+        if (!final_step) {
+            double xn = dinv ? xo + omega * (dinv[m] * r) : xo + omega * r;
+            xn_buf[m] = xn;
+            bad |= !isfinite(xn);
+        }
+    }
+};
+
+template <int NB, bool PACKED, bool EXACT>
+__global__ void EBS_SELL_BOUNDS(NB)
     k_jacobi_step(SellView v, LoopArgs L, double *__restrict__ xa, double *__restrict__ xb,
                   const double *__restrict__ b_int, const uint8_t *__restrict__ free_int,
                   const double *__restrict__ dinv, const double *__restrict__ ref,
@@ -53,37 +81,12 @@ __global__ void __launch_bounds__(256)
     if (ctl->done) return;
     const int k = ctl->k;
     const double *x = (k & 1) ? xb : xa;
-    double *xn_buf = (k & 1) ? xa : xb;
-    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-    const int lane = threadIdx.x & (LANES - 1);
-    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
-    double part[2] = {0.0, 0.0};
-    bool bad = false;
-    if (chunk < n_chunks) {
-        const int64_t m = chunk * LANES + lane;
-        const bool valid = m < v.n_n;
-        const int c_m = valid ? v.cnt[m] : 0;
-        const double xo = valid ? x[m] : 0.0;
-        double s = sell_node_sum<NB, EXACT>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, x, xo);
-        if (valid) {
-            double r = EXACT ? s : b_int[m] - s;
-            if (!free_int[m]) r = 0.0;
-            part[0] = r * r;
-            if (ref) {
-                double d = xo - ref[m];
-                part[1] = d * d;
-            }
-            if (r_out) r_out[m] = r;
-            if (!final_step) {
-                double xn = dinv ? xo + L.omega * (dinv[m] * r) : xo + L.omega * r;
-                xn_buf[m] = xn;
-                bad = !isfinite(xn);
-            }
-        }
-    }
-    flag_nonfinite(ctl, bad);
+    JacobiEpi epi{b_int, free_int, dinv, ref, r_out, (k & 1) ? xa : xb, L.omega, EXACT ? 1 : 0,
+                  final_step, {0.0, 0.0}, false};
+    sell_sweep<NB, PACKED, EXACT>(v, x, epi);
+    flag_nonfinite(ctl, epi.bad);
     double tot[2];
-    if (!grid_sum_last<2>(part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    if (!grid_sum_last<2>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
     // ---- loop rules (single thread) ----
     const double nr = sqrt(tot[0]);
     L.norms[k] = nr;
@@ -120,38 +123,35 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------ CG / PCG --
-template <int NB>
-__global__ void __launch_bounds__(256)
-    k_pcg_init(SellView v, LoopArgs L, const double *__restrict__ x, const double *__restrict__ b_int,
-               const uint8_t *__restrict__ free_int, const double *__restrict__ dinv,
-               const double *__restrict__ ref, double *__restrict__ r_int,
-               double *__restrict__ p_int) {
-    Ctl *ctl = L.ctl;
-    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-    const int lane = threadIdx.x & (LANES - 1);
-    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
-    double part[3] = {0.0, 0.0, 0.0};
-    if (chunk < n_chunks) {
-        const int64_t m = chunk * LANES + lane;
-        const bool valid = m < v.n_n;
-        const int c_m = valid ? v.cnt[m] : 0;
-        const double xo = valid ? x[m] : 0.0;
-        double s = sell_node_sum<NB, false>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, x, xo);
-        if (valid) {
-            double r = free_int[m] ? b_int[m] - s : 0.0;
-            double z = dinv[m] * r;
-            r_int[m] = r;
-            p_int[m] = z;
-            part[0] = r * r;
-            part[1] = r * z;
-            if (ref) {
-                double d = xo - ref[m];
-                part[2] = d * d;
-            }
+struct PcgInitEpi {
+    const double *__restrict__ b_int;
+    const uint8_t *__restrict__ free_int;
+    const double *__restrict__ dinv;
+    const double *__restrict__ ref;
+    double *__restrict__ r_int;
+    double *__restrict__ p_int;
+    double part[3];
+    __device__ __forceinline__ void operator()(int64_t m, double s, double xo) {
+        double r = free_int[m] ? b_int[m] - s : 0.0;
+        double z = dinv[m] * r;
+        r_int[m] = r;
+        p_int[m] = z;
+        part[0] += r * r;
+        part[1] += r * z;
+        if (ref) {
+            double d = xo - ref[m];
+            part[2] += d * d;
         }
     }
+};
+
+template <int NB, bool PACKED>
+__global__ void EBS_SELL_BOUNDS(NB)
+    k_pcg_init(SellView v, LoopArgs L, const double *__restrict__ x, PcgInitEpi epi) {
+    Ctl *ctl = L.ctl;
+    sell_sweep<NB, PACKED, false>(v, x, epi);
     double tot[3];
-    if (!grid_sum_last<3>(part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    if (!grid_sum_last<3>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
     const double nr = sqrt(tot[0]);
     L.norms[0] = nr;
     if (L.errors) L.errors[0] = sqrt(tot[2]);
@@ -163,31 +163,25 @@ __global__ void __launch_bounds__(256)
     if (L.has_tol && nr <= L.tol * nr) ctl->done = 1;
 }
 
-template <int NB>
-__global__ void __launch_bounds__(256)
-    k_pcg_matvec(SellView v, LoopArgs L, const double *__restrict__ p_int,
-                 const uint8_t *__restrict__ free_int, double *__restrict__ q_int) {
+struct PcgMatvecEpi {
+    const uint8_t *__restrict__ free_int;
+    double *__restrict__ q_int;
+    double part[1];
+    __device__ __forceinline__ void operator()(int64_t m, double s, double po) {
+        double q = free_int[m] ? s : 0.0;  // spectrum.py:60 out[nd] = 0
+        q_int[m] = q;
+        part[0] += po * q;
+    }
+};
+
+template <int NB, bool PACKED>
+__global__ void EBS_SELL_BOUNDS(NB)
+    k_pcg_matvec(SellView v, LoopArgs L, const double *__restrict__ p_int, PcgMatvecEpi epi) {
     Ctl *ctl = L.ctl;
     if (ctl->done) return;
-    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-    const int lane = threadIdx.x & (LANES - 1);
-    const int64_t n_chunks = (v.n_n + LANES - 1) / LANES;
-    double part[1] = {0.0};
-    if (chunk < n_chunks) {
-        const int64_t m = chunk * LANES + lane;
-        const bool valid = m < v.n_n;
-        const int c_m = valid ? v.cnt[m] : 0;
-        const double po = valid ? p_int[m] : 0.0;
-        double s =
-            sell_node_sum<NB, false>(v, v.rowbase[chunk], v.width[chunk], lane, c_m, p_int, po);
-        if (valid) {
-            double q = free_int[m] ? s : 0.0;  // spectrum.py:60 out[nd] = 0
-            q_int[m] = q;
-            part[0] = po * q;
-        }
-    }
+    sell_sweep<NB, PACKED, false>(v, p_int, epi);
     double tot[1];
-    if (!grid_sum_last<1>(part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    if (!grid_sum_last<1>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
     ctl->pq = tot[0];
     ctl->alpha = tot[0] != 0.0 ? ctl->rz / tot[0] : 0.0;
 }
@@ -311,7 +305,7 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
                p->partials, P->has_tol, P->tol, P->omega};
     SellView v = sell_view(p);
     const int block = 256;
-    const unsigned sgrid = (unsigned)((p->n_chunks * LANES + block - 1) / block);
+    const int64_t sgrid = (p->n_chunks * LANES + block - 1) / block;
     const int vgrid = grid_for(n, 256, RED_MAX_BLOCKS);
     const bool cb = P->callback != nullptr;
     const int batch = cb ? 1 : 32;
@@ -340,21 +334,27 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         const bool exact = P->exact != 0;
         double *rcb = (cb || P->r_out) ? r_int : nullptr;
         auto step = [&](int final_step) {
+#define EBS_JAC(NB_, PK_, EX_)                                                              \
+    {                                                                                       \
+        auto kern = k_jacobi_step<NB_, PK_, EX_>;                                           \
+        const int g = persistent_grid((const void *)kern, block, sgrid);                    \
+        kern<<<g, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int, dv, ref_int, rcb,     \
+                                 final_step);                                               \
+    }
             if (nb == 3) {
-                if (exact)
-                    k_jacobi_step<3, true><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
-                                                                  dv, ref_int, rcb, final_step);
-                else
-                    k_jacobi_step<3, false><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
-                                                                   dv, ref_int, rcb, final_step);
+                if (p->packed) {
+                    if (exact) EBS_JAC(3, true, true) else EBS_JAC(3, true, false)
+                } else {
+                    if (exact) EBS_JAC(3, false, true) else EBS_JAC(3, false, false)
+                }
             } else {
-                if (exact)
-                    k_jacobi_step<4, true><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
-                                                                  dv, ref_int, rcb, final_step);
-                else
-                    k_jacobi_step<4, false><<<sgrid, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int,
-                                                                   dv, ref_int, rcb, final_step);
+                if (p->packed) {
+                    if (exact) EBS_JAC(4, true, true) else EBS_JAC(4, true, false)
+                } else {
+                    if (exact) EBS_JAC(4, false, true) else EBS_JAC(4, false, false)
+                }
             }
+#undef EBS_JAC
             LAUNCHED();
         };
         int k = 0;
@@ -387,13 +387,21 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         }
         k_dinv<<<grid_for(n, 256), 256, 0, s>>>(n, diag, p->free_int, dinv);
         LAUNCHED();
-        if (nb == 3)
-            k_pcg_init<3><<<sgrid, block, 0, s>>>(v, L, xa, p->b_int, p->free_int, dinv, ref_int,
-                                                 r_int, pv);
-        else
-            k_pcg_init<4><<<sgrid, block, 0, s>>>(v, L, xa, p->b_int, p->free_int, dinv, ref_int,
-                                                 r_int, pv);
-        LAUNCHED();
+        {
+            PcgInitEpi ie{p->b_int, p->free_int, dinv, ref_int, r_int, pv, {0.0, 0.0, 0.0}};
+#define EBS_INIT(NB_, PK_)                                                                  \
+    {                                                                                       \
+        auto kern = k_pcg_init<NB_, PK_>;                                                   \
+        kern<<<persistent_grid((const void *)kern, block, sgrid), block, 0, s>>>(v, L, xa, ie); \
+    }
+            if (nb == 3) {
+                if (p->packed) EBS_INIT(3, true) else EBS_INIT(3, false)
+            } else {
+                if (p->packed) EBS_INIT(4, true) else EBS_INIT(4, false)
+            }
+#undef EBS_INIT
+            LAUNCHED();
+        }
         if (cb) {
             read_ctl();
             do_callback(xa, 0);
@@ -403,10 +411,20 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         while (k < iters && !done && !aborted) {
             int kend = k + batch < iters ? k + batch : iters;
             for (; k < kend; ++k) {
-                if (nb == 3)
-                    k_pcg_matvec<3><<<sgrid, block, 0, s>>>(v, L, pv, p->free_int, qv);
-                else
-                    k_pcg_matvec<4><<<sgrid, block, 0, s>>>(v, L, pv, p->free_int, qv);
+                {
+                    PcgMatvecEpi me{p->free_int, qv, {0.0}};
+#define EBS_MV(NB_, PK_)                                                                    \
+    {                                                                                       \
+        auto kern = k_pcg_matvec<NB_, PK_>;                                                 \
+        kern<<<persistent_grid((const void *)kern, block, sgrid), block, 0, s>>>(v, L, pv, me); \
+    }
+                    if (nb == 3) {
+                        if (p->packed) EBS_MV(3, true) else EBS_MV(3, false)
+                    } else {
+                        if (p->packed) EBS_MV(4, true) else EBS_MV(4, false)
+                    }
+#undef EBS_MV
+                }
                 LAUNCHED();
                 k_pcg_update<<<vgrid, 256, 0, s>>>(n, L, xa, r_int, pv, qv, dinv, ref_int);
                 LAUNCHED();
