@@ -201,6 +201,37 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *params, void *stream);
 int ebs_gather(int64_t n, const int64_t *idx, const double *v, double *buf, void *stream);
 /* v[idx[i]] += buf[i]  (idx entries unique)                                   */
 int ebs_scatter_add(int64_t n, const int64_t *idx, const double *buf, double *v, void *stream);
+/* v[idx[i]] = value;  dst[idx[i]] = src[idx[i]]  (interface combine in rank order)    */
+int ebs_index_fill(int64_t n, const int64_t *idx, double value, double *v, void *stream);
+int ebs_index_copy(int64_t n, const int64_t *idx, const double *src, double *dst, void *stream);
+/* Per-rank vector steps on internal-numbered vectors.  `owned` (uint8, 1 = this rank owns
+ * the node) restricts every reduction to owned nodes; the host all-reduces `red`.
+ * `ws` is a device workspace of ebs_vec_workspace_bytes() bytes (zero-initialised once,
+ * one per concurrent stream).  Damped Jacobi / Richardson (dinv NULL) step:
+ *   r = free ? b - s : 0;  x_out = x + omega*(dinv*r);  red[0] = sum_owned r^2          */
+size_t ebs_vec_workspace_bytes(void);
+int ebs_vec_jacobi(int64_t n, double omega, const double *b, const double *s, const double *dinv,
+                   const uint8_t *free_m, const uint8_t *owned, const double *x, double *x_out,
+                   double *r_out, double *red, int32_t *nonfinite, void *ws, void *stream);
+/* CG / PCG steps (oracle/ebs_oracle.py pcg):  q = free ? q : 0, red[0] = sum_owned p.q;
+ * update with scal = [rz, pq]: alpha = rz/pq, x += alpha p, r -= alpha q,
+ * red = [sum_owned r.r, sum_owned r.(dinv r)];  direction: p = dinv r + (rz_new/rz_old) p */
+int ebs_vec_pcg_q(int64_t n, const uint8_t *free_m, const uint8_t *owned, const double *p,
+                  double *q, double *red, void *ws, void *stream);
+int ebs_vec_pcg_update(int64_t n, const double *scal, const uint8_t *owned, const double *dinv,
+                       double *x, double *r, const double *p, const double *q, double *red,
+                       int32_t *nonfinite, void *ws, void *stream);
+int ebs_vec_pcg_direction(int64_t n, const double *rz_old, const double *rz_new,
+                          const double *dinv, const double *r, double *p, void *stream);
+int ebs_vec_dot_owned(int64_t n, const double *x, const double *y, const uint8_t *owned,
+                      double *red, void *ws, void *stream);
+/* dinv = free ? (diag ? 1/diag : 1) : 0 */
+int ebs_vec_dinv(int64_t n, const double *diag, const uint8_t *free_m, double *dinv,
+                 void *stream);
+/* plan internals in internal numbering: Dirichlet free flags, pre-assembled b, diag(A) */
+int ebs_plan_free_mask(ebs_plan_t plan, uint8_t *free_int, void *stream);
+int ebs_plan_internal_rhs(ebs_plan_t plan, double *b_int, void *stream);
+int ebs_plan_internal_diag(ebs_plan_t plan, double *d_int, void *stream);
 
 #ifdef __cplusplus
 }

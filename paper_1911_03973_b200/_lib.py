@@ -85,6 +85,24 @@ SIGNATURES = {
     "ebs_solve": (c_int, [c_void_p, POINTER(SolveParams), c_void_p]),
     "ebs_gather": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_scatter_add": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_index_fill": (c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p]),
+    "ebs_index_copy": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_vec_workspace_bytes": (c_size_t, []),
+    "ebs_vec_jacobi": (c_int, [c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_void_p]),
+    "ebs_vec_pcg_q": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                              c_void_p, c_void_p]),
+    "ebs_vec_pcg_update": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_vec_pcg_direction": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p]),
+    "ebs_vec_dot_owned": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                  c_void_p]),
+    "ebs_vec_dinv": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_plan_free_mask": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ebs_plan_internal_rhs": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ebs_plan_internal_diag": (c_int, [c_void_p, c_void_p, c_void_p]),
 }
 
 _lib = None

@@ -1,0 +1,262 @@
+// dist.cu -- vector kernels of the element-slab multi-GPU path.
+//
+// A rank owns the elements [lo, hi) of np.linspace(0, n_e, P+1) (operators.py:100) and a
+// plan over the nodes they touch.  Its SELL pass yields partial node sums; interface
+// partials are exchanged with the slab neighbours by the host (NCCL P2P) and combined in
+// ascending rank order with ebs_index_fill / ebs_scatter_add / ebs_index_copy, so every
+// rank holds identical values on shared nodes.  Dots and norms sum OWNED nodes only
+// (owner = lowest rank touching the node) and are then all-reduced.  All reductions here
+// are fixed-order (deterministic for a fixed launch configuration).
+#include "ebs_internal.cuh"
+
+namespace ebs {
+
+__global__ void k_index_fill(int64_t n, const int64_t *__restrict__ idx, double value,
+                             double *__restrict__ v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[idx[i]] = value;
+}
+
+__global__ void k_index_copy(int64_t n, const int64_t *__restrict__ idx,
+                             const double *__restrict__ src, double *__restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[idx[i]] = src[idx[i]];
+}
+
+// r = free ? b - s : 0;  x_out = x + omega*(dinv*r) (or x + omega*r);  red[0] = sum_owned r^2
+__global__ void __launch_bounds__(256)
+    k_vec_jacobi(int64_t n, double omega, const double *__restrict__ b,
+                 const double *__restrict__ s, const double *__restrict__ dinv,
+                 const uint8_t *__restrict__ free_m, const uint8_t *__restrict__ owned,
+                 const double *__restrict__ x, double *__restrict__ x_out,
+                 double *__restrict__ r_out, double *partials, unsigned int *counter,
+                 double *red, int32_t *nonfinite) {
+    double part[1] = {0.0};
+    bool bad = false;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double r = free_m[m] ? b[m] - s[m] : 0.0;
+        if (owned[m]) part[0] += r * r;
+        if (r_out) r_out[m] = r;
+        if (x_out) {
+            double xn = dinv ? x[m] + omega * (dinv[m] * r) : x[m] + omega * r;
+            x_out[m] = xn;
+            bad |= !isfinite(xn);
+        }
+    }
+    if (bad) atomicOr(nonfinite, 1);
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+// q = free ? q : 0;  red[0] = sum_owned p*q
+__global__ void __launch_bounds__(256)
+    k_vec_pcg_q(int64_t n, const uint8_t *__restrict__ free_m, const uint8_t *__restrict__ owned,
+                const double *__restrict__ p, double *__restrict__ q, double *partials,
+                unsigned int *counter, double *red) {
+    double part[1] = {0.0};
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double qm = free_m[m] ? q[m] : 0.0;
+        q[m] = qm;
+        if (owned[m]) part[0] += p[m] * qm;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+// alpha = pq != 0 ? rz/pq : 0 (scal = [rz, pq]);  x += alpha p;  r -= alpha q;
+// red = [sum_owned r^2, sum_owned r*(dinv*r)]
+__global__ void __launch_bounds__(256)
+    k_vec_pcg_update(int64_t n, const double *__restrict__ scal, const uint8_t *__restrict__ owned,
+                     const double *__restrict__ dinv, double *__restrict__ x,
+                     double *__restrict__ r, const double *__restrict__ p,
+                     const double *__restrict__ q, double *partials, unsigned int *counter,
+                     double *red, int32_t *nonfinite) {
+    const double rz = scal[0], pq = scal[1];
+    const double alpha = pq != 0.0 ? rz / pq : 0.0;
+    double part[2] = {0.0, 0.0};
+    bool bad = false;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double xn = x[m] + alpha * p[m];
+        double rn = r[m] - alpha * q[m];
+        x[m] = xn;
+        r[m] = rn;
+        bad |= !isfinite(xn);
+        if (owned[m]) {
+            part[0] += rn * rn;
+            part[1] += rn * (dinv[m] * rn);
+        }
+    }
+    if (bad) atomicOr(nonfinite, 1);
+    double tot[2];
+    if (grid_sum_last<2>(part, partials, counter, tot) && threadIdx.x == 0) {
+        red[0] = tot[0];
+        red[1] = tot[1];
+    }
+}
+
+// beta = rz_old != 0 ? rz_new/rz_old : 0;  p = dinv*r + beta*p
+__global__ void __launch_bounds__(256)
+    k_vec_pcg_direction(int64_t n, const double *__restrict__ rz_old,
+                        const double *__restrict__ rz_new, const double *__restrict__ dinv,
+                        const double *__restrict__ r, double *__restrict__ p) {
+    const double beta = rz_old[0] != 0.0 ? rz_new[0] / rz_old[0] : 0.0;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        p[m] = dinv[m] * r[m] + beta * p[m];
+}
+
+// red[0] = sum_owned x*y (owned nullable: all)
+__global__ void __launch_bounds__(256)
+    k_vec_dot_owned(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
+                    const uint8_t *__restrict__ owned, double *partials, unsigned int *counter,
+                    double *red) {
+    double part[1] = {0.0};
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        if (!owned || owned[m]) part[0] += x[m] * y[m];
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+// dinv = free ? (diag ? 1/diag : 1) : 0
+__global__ void k_vec_dinv(int64_t n, const double *__restrict__ diag,
+                           const uint8_t *__restrict__ free_m, double *__restrict__ dinv) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        dinv[m] = free_m[m] ? (diag ? 1.0 / diag[m] : 1.0) : 0.0;
+}
+
+struct Scratch {
+    double *partials;
+    unsigned int *counter;
+};
+
+static Scratch scratch(void *ws) {
+    // ws: caller-provided device workspace of ebs_vec_workspace_bytes() bytes
+    Scratch s;
+    s.counter = reinterpret_cast<unsigned int *>(ws);
+    s.partials = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256);
+    return s;
+}
+
+}  // namespace ebs
+
+using namespace ebs;
+
+extern "C" {
+
+size_t ebs_vec_workspace_bytes(void) { return 256 + sizeof(double) * 2 * RED_MAX_BLOCKS; }
+
+int ebs_index_fill(int64_t n, const int64_t *idx, double value, double *v, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0, "bad n");
+    if (n == 0) return EBS_OK;
+    k_index_fill<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, idx, value, v);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_index_copy(int64_t n, const int64_t *idx, const double *src, double *dst, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0, "bad n");
+    if (n == 0) return EBS_OK;
+    k_index_copy<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, idx, src, dst);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_vec_jacobi(int64_t n, double omega, const double *b, const double *s, const double *dinv,
+                   const uint8_t *free_m, const uint8_t *owned, const double *x, double *x_out,
+                   double *r_out, double *red, int32_t *nonfinite, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && b && s && free_m && owned && red && nonfinite && ws, "null argument");
+    EBS_REQUIRE(!x_out || x, "x_out needs x");
+    Scratch sc = scratch(ws);
+    k_vec_jacobi<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+        n, omega, b, s, dinv, free_m, owned, x, x_out, r_out, sc.partials, sc.counter, red,
+        nonfinite);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_vec_pcg_q(int64_t n, const uint8_t *free_m, const uint8_t *owned, const double *p,
+                  double *q, double *red, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && free_m && owned && p && q && red && ws, "null argument");
+    Scratch sc = scratch(ws);
+    k_vec_pcg_q<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+        n, free_m, owned, p, q, sc.partials, sc.counter, red);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_vec_pcg_update(int64_t n, const double *scal, const uint8_t *owned, const double *dinv,
+                       double *x, double *r, const double *p, const double *q, double *red,
+                       int32_t *nonfinite, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && scal && owned && dinv && x && r && p && q && red && nonfinite && ws,
+                "null argument");
+    Scratch sc = scratch(ws);
+    k_vec_pcg_update<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+        n, scal, owned, dinv, x, r, p, q, sc.partials, sc.counter, red, nonfinite);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_vec_pcg_direction(int64_t n, const double *rz_old, const double *rz_new,
+                          const double *dinv, const double *r, double *p, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && rz_old && rz_new && dinv && r && p, "null argument");
+    if (n == 0) return EBS_OK;
+    k_vec_pcg_direction<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, rz_old, rz_new, dinv, r, p);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_vec_dot_owned(int64_t n, const double *x, const double *y, const uint8_t *owned,
+                      double *red, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && x && y && red && ws, "null argument");
+    Scratch sc = scratch(ws);
+    k_vec_dot_owned<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+        n, x, y, owned, sc.partials, sc.counter, red);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_vec_dinv(int64_t n, const double *diag, const uint8_t *free_m, double *dinv,
+                 void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && free_m && dinv, "null argument");
+    if (n == 0) return EBS_OK;
+    k_vec_dinv<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, diag, free_m, dinv);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_plan_free_mask(ebs_plan_t plan, uint8_t *free_int, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && free_int, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (p->n_n)
+        CU(cudaMemcpyAsync(free_int, p->free_int, p->n_n, cudaMemcpyDeviceToDevice, S(stream)));
+    EBS_CATCH
+}
+
+int ebs_plan_internal_rhs(ebs_plan_t plan, double *b_int, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && b_int, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_be, "no b_e loaded");
+    if (p->n_n)
+        CU(cudaMemcpyAsync(b_int, p->b_int, sizeof(double) * p->n_n, cudaMemcpyDeviceToDevice,
+                           S(stream)));
+    EBS_CATCH
+}
+
+}  // extern "C"

@@ -611,4 +611,13 @@ int ebs_diagonal(ebs_plan_t plan, double *d, void *stream) {
     EBS_CATCH
 }
 
+int ebs_plan_internal_diag(ebs_plan_t plan, double *d_int, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && d_int, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    slot_sum(p, 1, nullptr, nullptr, d_int, S(stream));
+    EBS_CATCH
+}
+
 }  // extern "C"

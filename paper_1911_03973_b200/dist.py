@@ -1,0 +1,418 @@
+"""Element-slab multi-GPU path: one process per GPU, NCCL over NVLink.
+
+Partition: rank p owns the elements [lo, hi) of ``np.linspace(0, n_e, P+1)`` -- the
+reference's own chunk rule (operators.py:100).  The generators order cells row-major
+(2D) / z-outer (3D), so slabs are geometric and meet along one node row / plane.
+
+Per rank: a plan over the slab's local nodes (sorted global ids), the SELL kernel
+producing PARTIAL node sums, then a halo step: interface partials go to / come from the
+slab neighbours (NCCL send/recv) and every shared node is summed in ascending rank order,
+so all ranks hold the same value for it.  Dots and norms sum owned nodes (owner = lowest
+rank touching the node) and are all-reduced.  Maps (local node sets, interfaces, owners)
+match oracle/ebs_oracle.py halo_maps bit for bit.
+
+The solver loops are written against two small protocols so the same code runs
+  * distributed: one ``GpuRankOperator`` per process, ``TorchTransport`` (NCCL / gloo);
+  * emulated:    P ``GpuRankOperator``s in one process on one GPU, ``LocalTransport``
+                 (device copies; used by the GPU tests -- nothing waits on anything);
+  * CPU tests:   a torch-CPU rank operator (tests/) over gloo, world size 2.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import call, load
+
+
+# ------------------------------------------------------------------------ maps --
+def element_slabs(n_e: int, P: int) -> np.ndarray:
+    """operators.py:100 chunk rule reused for ranks."""
+    return np.linspace(0, n_e, P + 1, dtype=int)
+
+
+def partition_maps(indt: torch.Tensor, n_nodes: int, P: int) -> dict:
+    """Local node sets (sorted global ids), pairwise interfaces and owners for P slabs.
+
+    Works on any torch device; identical to oracle.halo_maps (tests)."""
+    bounds = element_slabs(indt.shape[1], P)
+    local = [torch.unique(indt[:, lo:hi].reshape(-1).to(torch.int64))
+             for lo, hi in zip(bounds[:-1], bounds[1:])]
+    interface = []
+    for p in range(P):
+        row = {}
+        for q in range(P):
+            if q != p:
+                common = local[p][torch.isin(local[p], local[q])]
+                if common.numel():
+                    row[q] = common
+        interface.append(row)
+    owner = torch.full((n_nodes,), -1, dtype=torch.int64, device=indt.device)
+    for p in reversed(range(P)):
+        owner[local[p]] = p
+    return dict(bounds=bounds, local=local, interface=interface, owner=owner)
+
+
+# ------------------------------------------------------------------ transports --
+class TorchTransport:
+    """torch.distributed (NCCL on GPUs, gloo on CPU): one rank per process."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def exchange(self, ops: list, sends: list) -> list:
+        """sends[i] = {q: tensor} for local rank ops[i] (len 1 here) -> recvs {q: tensor}."""
+        (op,), (snd,) = ops, sends
+        p2p = []
+        recvs = {}
+        for q in sorted(snd):
+            recvs[q] = torch.empty_like(snd[q])
+            p2p.append(self.dist.P2POp(self.dist.isend, snd[q].contiguous(), q, self.group))
+            p2p.append(self.dist.P2POp(self.dist.irecv, recvs[q], q, self.group))
+        if p2p:
+            for w in self.dist.batch_isend_irecv(p2p):
+                w.wait()
+        return [recvs]
+
+    def allreduce(self, tensors: list):
+        (t,) = tensors
+        self.dist.all_reduce(t, group=self.group)
+
+
+class LocalTransport:
+    """All P ranks in this process (one GPU): the exchange is a device copy."""
+
+    def exchange(self, ops: list, sends: list) -> list:
+        ranks = {op.rank: i for i, op in enumerate(ops)}
+        recvs = [dict() for _ in ops]
+        for i, op in enumerate(ops):
+            for q, buf in sends[i].items():
+                recvs[ranks[q]][op.rank] = buf.clone()
+        return recvs
+
+    def allreduce(self, tensors: list):
+        total = tensors[0].clone()
+        for t in tensors[1:]:
+            total += t
+        for t in tensors:
+            t.copy_(total)
+
+
+# ---------------------------------------------------------------- rank operator --
+class GpuRankOperator:
+    """Rank p's slab of a global ElementBatch on the current CUDA device.
+
+    Vectors are in this rank's plan-internal numbering ("internal")."""
+
+    def __init__(self, batch, n_nodes: int, d, maps: dict, p: int):
+        from .elements import ElementBatch
+        from .mesh import IndexArrays
+        from .operators import DirichletData
+        self.rank = p
+        self.P = len(maps["local"])
+        lo, hi = int(maps["bounds"][p]), int(maps["bounds"][p + 1])
+        gl = maps["local"][p].to(D.device())
+        self.global_ids = gl
+        n = gl.numel()
+        self.n = n
+        indt = batch.index.indt
+        conn = torch.searchsorted(gl, indt[:, lo:hi].to(torch.int64)).to(torch.int32).contiguous()
+        A_store = batch._A_store()[lo:hi]
+        b_e = batch.b_e[:, lo:hi].contiguous()
+        self.batch = ElementBatch(K_e=A_store.permute(1, 2, 0), M_e=A_store.permute(1, 2, 0),
+                                  A_e=A_store.permute(1, 2, 0), b_e=b_e, nu=batch.nu,
+                                  index=IndexArrays(None, conn, n_nodes=n))
+        self.plan = self.batch.operator(n)
+        # Dirichlet nodes of this slab (local ids)
+        if d is not None and d.nd.numel():
+            nd = d.nd.to(gl.device)
+            mine = nd[torch.isin(nd, gl)]
+            self.d_local = DirichletData(torch.searchsorted(gl, mine),
+                                         torch.zeros(mine.numel(), dtype=torch.float64,
+                                                     device=gl.device))
+        else:
+            self.d_local = None
+        self.plan.ensure_dirichlet(self.d_local)
+        new_of_old, old_of_new = self.plan.node_maps()
+        self.new_of_old = new_of_old.to(torch.int64)
+        self.old_of_new = old_of_new.to(torch.int64)
+        self.global_of_int = gl[self.old_of_new]
+        self.if_idx = {q: self.new_of_old[torch.searchsorted(gl, ids.to(gl.device))].contiguous()
+                       for q, ids in maps["interface"][p].items()}
+        self.all_if = (torch.unique(torch.cat(list(self.if_idx.values())))
+                       if self.if_idx else torch.empty(0, dtype=torch.int64, device=gl.device))
+        owner = maps["owner"].to(gl.device)
+        self.owned = (owner[self.global_of_int] == p).to(torch.uint8).contiguous()
+        self.free = D.empty(n, torch.uint8)
+        call("ebs_plan_free_mask", self.plan.handle, D.ptr(self.free), D.stream())
+        self._ws = D.zeros(int(load().ebs_vec_workspace_bytes()), torch.uint8)
+        self._acc = D.zeros(n)
+        self._flag = D.zeros(1, torch.int32)
+
+    # ---- primitives used by the generic loops ----
+    def to_internal(self, x_global: torch.Tensor) -> torch.Tensor:
+        return x_global.to(D.device())[self.global_of_int].contiguous()
+
+    def scatter_owned(self, v_int: torch.Tensor, out_global: torch.Tensor):
+        m = self.owned.bool()
+        out_global[self.global_of_int[m]] = v_int[m]
+
+    def matvec_partial(self, x: torch.Tensor, out: torch.Tensor):
+        call("ebs_plan_apply", self.plan.handle, 0, D.ptr(x), D.ptr(out), 0, 0, D.stream())
+
+    def rhs_partial(self) -> torch.Tensor:
+        b = D.empty(self.n)
+        call("ebs_plan_internal_rhs", self.plan.handle, D.ptr(b), D.stream())
+        return b
+
+    def diag_partial(self) -> torch.Tensor:
+        dg = D.empty(self.n)
+        call("ebs_plan_internal_diag", self.plan.handle, D.ptr(dg), D.stream())
+        return dg
+
+    def gather(self, idx, v):
+        buf = D.empty(idx.numel())
+        call("ebs_gather", idx.numel(), D.ptr(idx), D.ptr(v), D.ptr(buf), D.stream())
+        return buf
+
+    def combine(self, v: torch.Tensor, recvs: dict):
+        """v[shared] = sum over touching ranks in ascending rank order (own partial at p)."""
+        if not self.if_idx:
+            return
+        s = D.stream()
+        acc = self._acc
+        call("ebs_index_fill", self.all_if.numel(), D.ptr(self.all_if), 0.0, D.ptr(acc), s)
+        own = self.gather(self.all_if, v)
+        for r in sorted(set(recvs) | {self.rank}):
+            if r == self.rank:
+                call("ebs_scatter_add", self.all_if.numel(), D.ptr(self.all_if), D.ptr(own),
+                     D.ptr(acc), s)
+            else:
+                idx = self.if_idx[r]
+                call("ebs_scatter_add", idx.numel(), D.ptr(idx), D.ptr(recvs[r]), D.ptr(acc), s)
+        call("ebs_index_copy", self.all_if.numel(), D.ptr(self.all_if), D.ptr(acc), D.ptr(v), s)
+
+    def vec_dinv(self, diag):
+        dinv = D.empty(self.n)
+        call("ebs_vec_dinv", self.n, D.ptr(diag), D.ptr(self.free), D.ptr(dinv), D.stream())
+        return dinv
+
+    def vec_jacobi(self, omega, b, s_, dinv, x, x_out, r_out, red):
+        call("ebs_vec_jacobi", self.n, float(omega), D.ptr(b), D.ptr(s_), D.ptr(dinv),
+             D.ptr(self.free), D.ptr(self.owned), D.ptr(x), D.ptr(x_out), D.ptr(r_out),
+             D.ptr(red), D.ptr(self._flag), D.ptr(self._ws), D.stream())
+
+    def vec_pcg_q(self, p, q, red):
+        call("ebs_vec_pcg_q", self.n, D.ptr(self.free), D.ptr(self.owned), D.ptr(p), D.ptr(q),
+             D.ptr(red), D.ptr(self._ws), D.stream())
+
+    def vec_pcg_update(self, scal, dinv, x, r, p, q, red):
+        call("ebs_vec_pcg_update", self.n, D.ptr(scal), D.ptr(self.owned), D.ptr(dinv), D.ptr(x),
+             D.ptr(r), D.ptr(p), D.ptr(q), D.ptr(red), D.ptr(self._flag), D.ptr(self._ws),
+             D.stream())
+
+    def vec_pcg_direction(self, rz_old, rz_new, dinv, r, p):
+        call("ebs_vec_pcg_direction", self.n, D.ptr(rz_old), D.ptr(rz_new), D.ptr(dinv), D.ptr(r),
+             D.ptr(p), D.stream())
+
+    def dot_owned(self, x, y, red):
+        call("ebs_vec_dot_owned", self.n, D.ptr(x), D.ptr(y), D.ptr(self.owned), D.ptr(red),
+             D.ptr(self._ws), D.stream())
+
+    def zeros(self, n=None):
+        return D.zeros(self.n if n is None else n)
+
+
+# ------------------------------------------------------------------- loops --
+def halo(ops, comm, vs):
+    """Exchange interface partials of vs[i] (rank ops[i]) and combine in rank order."""
+    sends = [{q: op.gather(idx, v) for q, idx in op.if_idx.items()} for op, v in zip(ops, vs)]
+    recvs = comm.exchange(ops, sends)
+    for op, v, rc in zip(ops, vs, recvs):
+        op.combine(v, rc)
+
+
+@dataclass
+class DistProblem:
+    ops: list
+    comm: object
+    b: list       # full (combined) b per rank, internal numbering
+    dinv: list    # Jacobi 1/diag (0 at constrained nodes)
+
+
+def setup(ops, comm, precondition=True) -> DistProblem:
+    bs = [op.rhs_partial() for op in ops]
+    halo(ops, comm, bs)
+    dgs = [op.diag_partial() for op in ops]
+    halo(ops, comm, dgs)
+    dinv = [op.vec_dinv(dg if precondition else None) for op, dg in zip(ops, dgs)]
+    return DistProblem(ops, comm, bs, dinv)
+
+
+def residual(prob: DistProblem, xs, out=None):
+    """r = mask? no: b - A x (unmasked, operators.py:72) on every rank's local nodes."""
+    ops, comm = prob.ops, prob.comm
+    ss = [op.zeros() for op in ops]
+    for op, x, s in zip(ops, xs, ss):
+        op.matvec_partial(x, s)
+    halo(ops, comm, ss)
+    return [b - s for b, s in zip(prob.b, ss)]
+
+
+def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: bool = False):
+    """Damped Jacobi on P ranks (oracle/ebs_oracle.py jacobi semantics, fixed count).
+
+    Returns (xs, norms) with norms[k] = ||mask(b - A x_k)||, k = 0..iters."""
+    ops, comm = prob.ops, prob.comm
+    xa = [x.clone() for x in xs0]
+    xb = [op.zeros() for op in ops]
+    ss = [op.zeros() for op in ops]
+    red = [torch.zeros(iters + 1, dtype=torch.float64, device=x.device) for x in xa]
+    for k in range(iters + 1):
+        final = k == iters
+        for op, x, s in zip(ops, xa, ss):
+            op.matvec_partial(x, s)
+        halo(ops, comm, ss)
+        for i, op in enumerate(ops):
+            op.vec_jacobi(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i], xa[i],
+                          None if final else xb[i], None, red[i][k:k + 1])
+        if not final:
+            xa, xb = xb, xa
+    comm.allreduce(red)
+    return xa, torch.sqrt(red[0]).cpu().numpy()
+
+
+def pcg(prob: DistProblem, xs0, iters: int, tol=None):
+    """Jacobi-PCG on P ranks (oracle/ebs_oracle.py pcg; with prob from setup(..,
+    precondition=False) plain CG).  Two scalar all-reduces per iteration."""
+    ops, comm = prob.ops, prob.comm
+    dev = xs0[0].device
+    xs = [x.clone() for x in xs0]
+    rs = [op.zeros() for op in ops]
+    ps = [op.zeros() for op in ops]
+    qs = [op.zeros() for op in ops]
+    ss = [op.zeros() for op in ops]
+    zero = torch.zeros(1, dtype=torch.float64, device=dev)
+    for op, x, s in zip(ops, xs, ss):
+        op.matvec_partial(x, s)
+    halo(ops, comm, ss)
+    hist = [torch.zeros(iters + 1, dtype=torch.float64, device=dev) for _ in ops]
+    red = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in ops]
+    scal = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in ops]
+    for i, op in enumerate(ops):
+        op.vec_jacobi(0.0, prob.b[i], ss[i], None, xs[i], None, rs[i], red[i][0:1])
+        op.vec_pcg_direction(zero, zero, prob.dinv[i], rs[i], ps[i])  # p = dinv r
+        op.dot_owned(rs[i], ps[i], red[i][1:2])
+    comm.allreduce(red)
+    for i in range(len(ops)):
+        hist[i][0:1].copy_(red[i][0:1])
+        scal[i][0:1].copy_(red[i][1:2])
+    n0 = None
+    k_done = iters
+    for k in range(iters):
+        if tol is not None:
+            nk = float(torch.sqrt(hist[0][k]))
+            n0 = nk if n0 is None else n0
+            if nk <= tol * n0:
+                k_done = k
+                break
+        for op, p, q in zip(ops, ps, qs):
+            op.matvec_partial(p, q)
+        halo(ops, comm, qs)
+        pq = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in ops]
+        for i, op in enumerate(ops):
+            op.vec_pcg_q(ps[i], qs[i], pq[i])
+        comm.allreduce(pq)
+        for i, op in enumerate(ops):
+            scal[i][1:2].copy_(pq[i])
+            op.vec_pcg_update(scal[i], prob.dinv[i], xs[i], rs[i], ps[i], qs[i], red[i])
+        comm.allreduce(red)
+        for i, op in enumerate(ops):
+            hist[i][k + 1:k + 2].copy_(red[i][0:1])
+            op.vec_pcg_direction(scal[i][0:1], red[i][1:2], prob.dinv[i], rs[i], ps[i])
+            scal[i][0:1].copy_(red[i][1:2])
+    n = k_done + 1
+    return xs, torch.sqrt(hist[0][:n]).cpu().numpy()
+
+
+def gather_global(ops, vs, n_nodes, comm=None):
+    """Assemble a global vector (caller numbering) from owned entries (emulated ranks or
+    rank-local with an all-reduce of the disjoint owned parts)."""
+    out = torch.zeros(n_nodes, dtype=torch.float64, device=vs[0].device)
+    for op, v in zip(ops, vs):
+        op.scatter_owned(v, out)
+    if comm is not None and isinstance(comm, TorchTransport):
+        comm.allreduce([out])
+    return out
+
+
+def emulate(batch, n_nodes, d, P, precondition=True):
+    """P ranks in this process on the current GPU (tests; nothing waits on anything)."""
+    maps = partition_maps(batch.index.indt, n_nodes, P)
+    ops = [GpuRankOperator(batch, n_nodes, d, maps, p) for p in range(P)]
+    comm = LocalTransport()
+    return setup(ops, comm, precondition=precondition), maps
+
+
+# ------------------------------------------------------------------- bench --
+def bench_rank(args, rank, world, local_rank):
+    """bench.py --gpus N under torchrun: C2 residual strong-scaled over N element slabs,
+    NCCL halo exchange, device-timed max over ranks; rank 0 prints the JSON line."""
+    import json
+    import os
+    import torch.distributed as dist
+
+    from .inputs import config_problem
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    p = config_problem(2, seed=args.seed, size=args.size)
+    m, batch = p["mesh"], p["batch"]
+    maps = partition_maps(batch.index.indt, m.n_nodes, world)
+    op = GpuRankOperator(batch, m.n_nodes, None, maps, rank)
+    comm = TorchTransport()
+    prob = setup([op], comm)
+    x_int = op.to_internal(torch.from_numpy(p["x"]).cuda())
+    s, r = op.zeros(), op.zeros()
+    red = torch.zeros(1, dtype=torch.float64, device="cuda")
+    n0 = load().ebs_launch_count()
+
+    def step():  # r = b - A x on this slab's nodes: SELL partials, halo, b - s
+        op.matvec_partial(x_int, s)
+        halo([op], comm, [s])
+        op.vec_jacobi(0.0, prob.b[0], s, None, x_int, None, r, red)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    launches = load().ebs_launch_count() - n0
+    if rank == 0:
+        T = float(t)
+        line = {"metric": "element matvec GDoF/s & HBM GB/s (fraction of peak); PCG iterations/sec",
+                "value": m.n_nodes * args.steps / T / 1e9, "unit": "GDoF/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": T / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded BASELINE C2 recipe)",
+                "config": {"workload": "C2 residual, element slabs + NCCL halo exchange",
+                           "n_nodes": m.n_nodes, "n_elements": m.n_elements,
+                           "parallelism": f"element slabs x{world}"},
+                "gpu_launches": launches}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
