@@ -278,7 +278,7 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get("k_sell_op<3,1>")
+            traffic = json.load(f).get("k_sell_op<3,1,1>@C2")
     except Exception:
         pass
 
@@ -306,7 +306,7 @@ def run_ours(args):
         "hbm_gbs_algorithmic": bytes_alg / (total / args.steps) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_sell_op<3,1> (fused gather-product-ordered-sum)",
+                     "kernel": "k_sell_op<3,1,1> (fused gather-product-ordered-sum, packed ids)",
                      "bytes_per_launch": bytes_alg, "kernel_ms": sell * 1e3,
                      "gather_kernel_ms": gather * 1e3, "peak_source": peak_kind},
         "exact_mode": {"value": n_n * args.steps / total_ex / 1e9, "unit": "GDoF/s",

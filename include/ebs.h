@@ -54,6 +54,8 @@ typedef struct ebs_plan *ebs_plan_t;
 #define EBS_JACOBI 1     /* damped Jacobi on the solvers.py:117-160 loop (NEW)   */
 #define EBS_CG 2         /* conjugate gradients (NEW)                            */
 #define EBS_PCG 3        /* Jacobi-preconditioned CG (NEW)                       */
+#define EBS_CHEB2 4      /* cyclic two-level Chebyshev, solvers.py:186-213       */
+#define EBS_CHEB3 5      /* three-level Chebyshev recurrence, solvers.py:216-261 */
 
 int ebs_version(void);
 int ebs_last_error(char *buf, size_t len);
@@ -188,10 +190,19 @@ typedef struct {
     double *cb_x;            /*   a non-zero return stops the solve with EBS_ECALLBACK     */
     double *cb_r;
     double *r_out;           /* device, nullable: final residual (caller numbering)       */
+    const double *coef_a;    /* HOST, iters entries: CHEB2 step 1/alpha_{k mod N};         */
+    const double *coef_b;    /*   CHEB3 alpha_k and beta_k (solvers.py:247-258)             */
 } ebs_solve_params;
 
 /* synchronous on `stream` (one host read of the history at the end) */
 int ebs_solve(ebs_plan_t plan, const ebs_solve_params *params, void *stream);
+
+/* spectrum.py:64-99 power_iteration_lambda_max on the masked operator (loaded Dirichlet
+ * set): v = v0 masked and normalised, then v <- A v / ||A v|| until the Rayleigh quotient
+ * changes by <= tol*max(1,|lam|) or iters steps; *lam (HOST) receives the estimate, *its
+ * (HOST) the steps taken.  Returns EBS_EINVAL when v0 vanishes after masking. */
+int ebs_power_iteration(ebs_plan_t plan, const double *v0, int iters, double tol, double *lam,
+                        int *its, void *stream);
 
 /* ------------------------------------------------------------ multi-GPU ---- */
 /* Element-slab partition helpers.  A rank's plan is built on its element

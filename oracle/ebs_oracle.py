@@ -33,6 +33,8 @@ __all__ = [
     "residual", "matvec_masked", "diagonal", "mask", "initial_guess",
     "richardson", "jacobi", "pcg", "cg", "element_slabs", "halo_maps",
     "first_appearance_order", "node_slots", "config_inputs",
+    "chebyshev_roots", "chebyshev2", "chebyshev3", "chebyshev3_coefficients",
+    "model_eigen_bounds", "power_iteration_lambda_max", "mass_gershgorin", "operator_bounds",
 ]
 
 MAX_LEVEL = 12                       # mesh.py:20
@@ -479,6 +481,126 @@ def pcg(A_e, b_e, indt, nd, x0, iters, tol=None, reference=None, callback=None,
 def cg(A_e, b_e, indt, nd, x0, iters, **kw):
     """RESTATEMENT: unpreconditioned CG (pcg with dinv = 1 on free nodes)."""
     return pcg(A_e, b_e, indt, nd, x0, iters, precondition=False, **kw)
+
+
+def chebyshev_roots(lambda1, lambda2, N):
+    """solvers.py:85-99: alphas[k] = d + c cos(pi (k + 1/2)/N)."""
+    if N < 1:
+        raise ValueError(f"cycle length must be positive, got N={N}")
+    d = (lambda2 + lambda1) / 2.0
+    c = (lambda2 - lambda1) / 2.0
+    k = np.arange(N)
+    return d + c * np.cos(np.pi * (k + 0.5) / N)
+
+
+def chebyshev2(A_e, b_e, indt, nd, x0, lambda1, lambda2, N, iters, **kw):
+    """solvers.py:186-213: x += (1/alpha_{k mod N}) r."""
+    alphas = chebyshev_roots(lambda1, lambda2, N)
+    return _iterate(A_e, b_e, indt, nd, x0, iters,
+                    lambda k, x, r: x + (1.0 / alphas[k % N]) * r, **kw)
+
+
+def chebyshev3_coefficients(lambda1, lambda2, iters):
+    """The scalar recurrence of solvers.py:247-258 (data independent):
+    alpha_0 = 1/d; beta_k = 0.5 (c alpha_{k-1})^2 (x 0.5 for k > 1);
+    alpha_k = 1/(d - beta_k/alpha_{k-1})."""
+    if not lambda1 < lambda2:
+        raise ValueError("chebyshev3 needs lambda1 < lambda2")
+    dd = (lambda2 + lambda1) / 2.0
+    cc = (lambda2 - lambda1) / 2.0
+    alphas, betas = [], []
+    alpha = 0.0
+    for k in range(iters):
+        if k == 0:
+            alpha = 1.0 / dd
+            beta = 0.0
+        else:
+            beta = 0.5 * (cc * alpha) ** 2
+            if k > 1:
+                beta *= 0.5
+            alpha = 1.0 / (dd - beta / alpha)
+        alphas.append(alpha)
+        betas.append(beta)
+    return np.array(alphas), np.array(betas)
+
+
+def chebyshev3(A_e, b_e, indt, nd, x0, lambda1, lambda2, iters, **kw):
+    """solvers.py:216-261: p = r (k=0) or r + beta_k p;  x += alpha_k p."""
+    alphas, betas = chebyshev3_coefficients(lambda1, lambda2, iters)
+    state = {"p": None}
+
+    def advance(k, x, r):
+        state["p"] = r.copy() if k == 0 else r + betas[k] * state["p"]
+        return x + alphas[k] * state["p"]
+
+    return _iterate(A_e, b_e, indt, nd, x0, iters, advance, **kw)
+
+
+def model_eigen_bounds(n):
+    """spectrum.py:41-51."""
+    if n < 3:
+        raise ValueError(f"need n >= 3 for an interior node, got n={n}")
+    lam1 = 8.0 * np.sin(np.pi / (2 * (n - 1))) ** 2
+    return float(lam1), float(8.0 - lam1)
+
+
+def power_iteration_lambda_max(A_e, indt, nd, n, iters=1000, seed=0, tol=1e-10):
+    """spectrum.py:64-99 (Rayleigh quotient of the masked operator)."""
+    if iters < 1:
+        raise ValueError(f"need at least one iteration, got {iters}")
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(n)
+    v[nd] = 0.0
+    nv = np.linalg.norm(v)
+    if nv == 0.0:
+        raise ValueError("start vector vanished after masking (no free nodes?)")
+    v /= nv
+    lam = 0.0
+    for _ in range(iters):
+        av = matvec_masked(A_e, indt, v, nd)
+        lam_new = float(v @ av)
+        nav = np.linalg.norm(av)
+        if nav == 0.0:
+            return 0.0
+        v = av / nav
+        if abs(lam_new - lam) <= tol * max(1.0, abs(lam_new)):
+            return lam_new
+        lam = lam_new
+    return lam
+
+
+def mass_gershgorin(M_e, indt, nd, n):
+    """spectrum.py:102-126 (diag summed per j, then j = 0, 1, 2)."""
+    is_free = np.ones(n, dtype=bool)
+    is_free[nd] = False
+    free_cols = is_free[indt].astype(np.float64)
+    nb = indt.shape[0]
+    rows = np.empty((nb, indt.shape[1]))
+    for i in range(nb):
+        acc = M_e[i, 0] * free_cols[0]
+        for c in range(1, nb):
+            acc = acc + M_e[i, c] * free_cols[c]
+        rows[i] = acc
+    row_sums = np.bincount(indt.ravel(), weights=rows.ravel(), minlength=n)
+    diags = np.zeros(n)
+    for j in range(nb):
+        diags += np.bincount(indt[j], weights=M_e[j, j, :], minlength=n)
+    lo = (2.0 * diags - row_sums)[is_free]
+    hi = row_sums[is_free]
+    if lo.size == 0:
+        raise ValueError("no free nodes")
+    return max(float(lo.min()), 0.0), float(hi.max())
+
+
+def operator_bounds(A_e, M_e, indt, nd, n_side, nu, n, seed=0):
+    """spectrum.py:129-149."""
+    l1, l2 = model_eigen_bounds(n_side)
+    if nu == 0.0:
+        return l1, l2
+    m_lo, _ = mass_gershgorin(M_e, indt, nd, n)
+    lam1 = l1 + nu * m_lo
+    lam2 = 1.05 * power_iteration_lambda_max(A_e, indt, nd, n, seed=seed)
+    return lam1, float(max(lam2, lam1))
 
 
 # ------------------------------------------------ partition / halo maps

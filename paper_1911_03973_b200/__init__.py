@@ -17,10 +17,15 @@ from .mesh import (MAX_LEVEL, IndexArrays, Mesh, boundary_nodes, build_grid_mesh
                    face_z0_nodes, jitter_interior, permute_nodes, signed_areas)
 from .operators import (DirichletData, apply_initial_guess, assemble_rhs, constant_dirichlet,
                         diagonal, mask_dirichlet, matvec, residual)
-from .solvers import ConvergenceHistory, SpectralBounds, cg, jacobi, pcg, richardson
-from .spectrum import model_eigen_bounds, model_eigenvalues_all
+from .solvers import (ChebyshevCycle, ConvergenceHistory, SpectralBounds, cg, chebyshev2,
+                      chebyshev3, chebyshev_roots, chebyshev_scaling_factor, jacobi, pcg,
+                      richardson)
+from .spectrum import (mass_gershgorin, model_eigen_bounds, model_eigenvalues_all,
+                       operator_bounds, power_iteration_lambda_max)
 
 __all__ = [
+    "ChebyshevCycle", "chebyshev2", "chebyshev3", "chebyshev_roots", "chebyshev_scaling_factor",
+    "mass_gershgorin", "operator_bounds", "power_iteration_lambda_max",
     "ConvergenceHistory", "DirichletData", "ElementBatch", "IndexArrays", "MAX_LEVEL", "Mesh",
     "SpectralBounds", "apply_initial_guess", "assemble_rhs", "boundary_nodes",
     "build_element_batch", "build_grid_mesh", "build_index_arrays", "build_unit_cube_mesh",

@@ -30,6 +30,8 @@ EBS_RICHARDSON = 0
 EBS_JACOBI = 1
 EBS_CG = 2
 EBS_PCG = 3
+EBS_CHEB2 = 4
+EBS_CHEB3 = 5
 
 CALLBACK = ctypes.CFUNCTYPE(c_int, c_void_p, c_int)
 
@@ -44,6 +46,7 @@ class SolveParams(ctypes.Structure):
         ("n_norms", POINTER(c_int)), ("diverged", POINTER(c_int)),
         ("callback", CALLBACK), ("user", c_void_p), ("cb_x", c_void_p), ("cb_r", c_void_p),
         ("r_out", c_void_p),
+        ("coef_a", POINTER(c_double)), ("coef_b", POINTER(c_double)),
     ]
 
 
@@ -83,6 +86,8 @@ SIGNATURES = {
     "ebs_nrm2": (c_int, [c_int64, c_void_p, c_void_p, c_void_p]),
     "ebs_axpby": (c_int, [c_int64, c_double, c_void_p, c_double, c_void_p, c_void_p]),
     "ebs_solve": (c_int, [c_void_p, POINTER(SolveParams), c_void_p]),
+    "ebs_power_iteration": (c_int, [c_void_p, c_void_p, c_int, c_double, POINTER(c_double),
+                                    POINTER(c_int), c_void_p]),
     "ebs_gather": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_scatter_add": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_index_fill": (c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p]),

@@ -43,6 +43,9 @@ __device__ __forceinline__ void flag_nonfinite(Ctl *ctl, bool bad) {
 }
 
 // ---------------------------------------------------------- Richardson/Jacobi --
+// stationary steps on the _iterate loop:
+//   0 Richardson x + omega*r            1 Jacobi x + omega*(dinv*r)
+//   4 Chebyshev-2 x + a_k*r             5 Chebyshev-3 p = k ? r + b_k*p : r;  x + a_k*p
 struct JacobiEpi {
     const double *__restrict__ b_int;
     const uint8_t *__restrict__ free_int;
@@ -50,8 +53,9 @@ struct JacobiEpi {
     const double *__restrict__ ref;
     double *__restrict__ r_out;
     double *__restrict__ xn_buf;
-    double omega;
-    int exact, final_step;
+    double *__restrict__ p;
+    double omega, coef_b;
+    int method, k, exact, final_step;
     double part[2];
     bool bad;
     __device__ __forceinline__ void operator()(int64_t m, double s, double xo) {
@@ -64,7 +68,16 @@ struct JacobiEpi {
         }
         if (r_out) r_out[m] = r;
         if (!final_step) {
-            double xn = dinv ? xo + omega * (dinv[m] * r) : xo + omega * r;
+            double xn;
+            if (method == EBS_JACOBI) {
+                xn = xo + omega * (dinv[m] * r);
+            } else if (method == EBS_CHEB3) {
+                double pm = k == 0 ? r : r + coef_b * p[m];
+                p[m] = pm;
+                xn = xo + omega * pm;
+            } else {
+                xn = xo + omega * r;  // Richardson (omega) and Chebyshev-2 (omega = a_k)
+            }
             xn_buf[m] = xn;
             bad |= !isfinite(xn);
         }
@@ -76,13 +89,18 @@ __global__ void EBS_SELL_BOUNDS(NB)
     k_jacobi_step(SellView v, LoopArgs L, double *__restrict__ xa, double *__restrict__ xb,
                   const double *__restrict__ b_int, const uint8_t *__restrict__ free_int,
                   const double *__restrict__ dinv, const double *__restrict__ ref,
-                  double *__restrict__ r_out, int final_step) {
+                  double *__restrict__ r_out, int final_step, int method,
+                  const double *__restrict__ ca, const double *__restrict__ cb,
+                  double *__restrict__ pbuf) {
     Ctl *ctl = L.ctl;
     if (ctl->done) return;
     const int k = ctl->k;
     const double *x = (k & 1) ? xb : xa;
-    JacobiEpi epi{b_int, free_int, dinv, ref, r_out, (k & 1) ? xa : xb, L.omega, EXACT ? 1 : 0,
-                  final_step, {0.0, 0.0}, false};
+    const bool cheb = method == EBS_CHEB2 || method == EBS_CHEB3;
+    const double om = (cheb && !final_step) ? ca[k] : L.omega;
+    const double cbk = (method == EBS_CHEB3 && !final_step) ? cb[k] : 0.0;
+    JacobiEpi epi{b_int, free_int, dinv, ref, r_out, (k & 1) ? xa : xb, pbuf, om, cbk, method, k,
+                  EXACT ? 1 : 0, final_step, {0.0, 0.0}, false};
     sell_sweep<NB, PACKED, EXACT>(v, x, epi);
     flag_nonfinite(ctl, epi.bad);
     double tot[2];
@@ -263,6 +281,72 @@ __global__ void k_dinv(int64_t n, const double *__restrict__ diag,
 void slot_sum(const Plan *p, int what, const double *b_e, const int32_t *old_of_new, double *out,
               cudaStream_t s);
 
+// ------------------------------------------------------------ power iteration --
+// spectrum.py:64-99.  Ctl reuse: rz = lam (previous quotient), alpha = nav, pq = result,
+// k = step, done.
+struct PowerEpi {
+    const uint8_t *__restrict__ free_int;
+    double *__restrict__ av;
+    double part[2];
+    __device__ __forceinline__ void operator()(int64_t m, double s, double vo) {
+        double a = free_int[m] ? s : 0.0;  // spectrum.py:60 out[nd] = 0
+        av[m] = a;
+        part[0] += vo * a;
+        part[1] += a * a;
+    }
+};
+
+template <int NB, bool PACKED>
+__global__ void EBS_SELL_BOUNDS(NB)
+    k_power_matvec(SellView v, Ctl *ctl, double *partials, const double *__restrict__ vin,
+                   PowerEpi epi, double tol) {
+    if (ctl->done) return;
+    sell_sweep<NB, PACKED, false>(v, vin, epi);
+    double tot[2];
+    if (!grid_sum_last<2>(epi.part, partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    const double lam_new = tot[0];
+    const double nav = sqrt(tot[1]);
+    ctl->k += 1;
+    ctl->alpha = nav;
+    if (nav == 0.0) {
+        ctl->pq = 0.0;
+        ctl->done = 1;
+        return;
+    }
+    if (fabs(lam_new - ctl->rz) <= tol * fmax(1.0, fabs(lam_new))) {
+        ctl->pq = lam_new;
+        ctl->done = 1;
+        return;
+    }
+    ctl->rz = lam_new;
+    ctl->pq = lam_new;
+}
+
+// v = av / nav (spectrum.py:94)
+__global__ void k_power_scale(int64_t n, const Ctl *ctl, const double *__restrict__ av,
+                              double *__restrict__ v) {
+    if (ctl->done && ctl->alpha == 0.0) return;
+    const double nav = ctl->alpha;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        v[m] = av[m] / nav;
+}
+
+// v = free ? v : 0 and ||v||^2 (start vector, spectrum.py:81-86)
+__global__ void k_power_start(int64_t n, const uint8_t *__restrict__ free_int,
+                              double *__restrict__ v, double *partials, unsigned int *counter,
+                              Ctl *ctl) {
+    double part[1] = {0.0};
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double x = free_int[m] ? v[m] : 0.0;
+        v[m] = x;
+        part[0] += x * x;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) ctl->alpha = sqrt(tot[0]);
+}
+
 static void ensure_hist(Plan *p, int64_t n) {
     if (p->hist_cap < n) {
         dfree(p->hist_dev);
@@ -282,7 +366,10 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
     EBS_REQUIRE(plan && P, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
     EBS_REQUIRE(P->iters >= 0, "iteration count must be nonnegative, got %d", P->iters);
-    EBS_REQUIRE(P->method >= EBS_RICHARDSON && P->method <= EBS_PCG, "bad method %d", P->method);
+    EBS_REQUIRE(P->method >= EBS_RICHARDSON && P->method <= EBS_CHEB3, "bad method %d", P->method);
+    EBS_REQUIRE(P->method != EBS_CHEB2 || P->coef_a || P->iters == 0, "CHEB2 needs coef_a");
+    EBS_REQUIRE(P->method != EBS_CHEB3 || ((P->coef_a && P->coef_b) || P->iters == 0),
+                "CHEB3 needs coef_a and coef_b");
     EBS_REQUIRE(p->has_A && p->has_be, "solver needs an operator loaded with b_e");
     EBS_REQUIRE(P->x0 && P->x && P->norms && P->n_norms && P->diverged, "null argument");
     EBS_REQUIRE(!P->reference || P->errors, "errors buffer required with reference");
@@ -291,7 +378,8 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
     const int64_t n = p->n_n;
     const int iters = P->iters;
     const int nb = p->nb;
-    ensure_hist(p, (int64_t)iters + 2);
+    // history: norms [0, iters+2), errors [iters+2, 2(iters+2)), then 2*iters coefficients
+    ensure_hist(p, 2 * ((int64_t)iters + 2) + (int64_t)iters);
     double *xa = plan_vec(p, 1), *xb = plan_vec(p, 2), *r_int = plan_vec(p, 3);
     double *dinv = plan_vec(p, 4), *ref_int = nullptr;
     CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
@@ -322,8 +410,22 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         if (P->callback(P->user, k) != 0) aborted = true;
     };
 
-    if (n > 0 && (P->method == EBS_RICHARDSON || P->method == EBS_JACOBI)) {
+    const bool stationary = P->method == EBS_RICHARDSON || P->method == EBS_JACOBI ||
+                            P->method == EBS_CHEB2 || P->method == EBS_CHEB3;
+    if (n > 0 && stationary) {
         const double *dv = nullptr;
+        double *coef_a = nullptr, *coef_b = nullptr, *pbuf = nullptr;
+        if ((P->method == EBS_CHEB2 || P->method == EBS_CHEB3) && iters > 0) {
+            // coefficient tables live behind the history on the device
+            coef_a = p->hist_dev + 2 * ((int64_t)iters + 2);
+            coef_b = coef_a + iters;
+            CU(cudaMemcpyAsync(coef_a, P->coef_a, sizeof(double) * iters, cudaMemcpyHostToDevice, s));
+            if (P->method == EBS_CHEB3) {
+                CU(cudaMemcpyAsync(coef_b, P->coef_b, sizeof(double) * iters,
+                                   cudaMemcpyHostToDevice, s));
+                pbuf = plan_vec(p, 6);
+            }
+        }
         if (P->method == EBS_JACOBI) {
             double *diag = plan_vec(p, 5);
             slot_sum(p, 1, nullptr, nullptr, diag, s);
@@ -339,7 +441,7 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         auto kern = k_jacobi_step<NB_, PK_, EX_>;                                           \
         const int g = persistent_grid((const void *)kern, block, sgrid);                    \
         kern<<<g, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int, dv, ref_int, rcb,     \
-                                 final_step);                                               \
+                                 final_step, P->method, coef_a, coef_b, pbuf);              \
     }
             if (nb == 3) {
                 if (p->packed) {
@@ -456,6 +558,67 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         set_error("solve stopped by callback");
         return EBS_ECALLBACK;
     }
+    EBS_CATCH
+}
+
+int ebs_power_iteration(ebs_plan_t plan, const double *v0, int iters, double tol, double *lam,
+                        int *its, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && v0 && lam && its, "null argument");
+    EBS_REQUIRE(iters >= 1, "need at least one iteration, got %d", iters);
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    cudaStream_t s = S(stream);
+    const int64_t n = p->n_n;
+    double *v = plan_vec(p, 1), *av = plan_vec(p, 2);
+    CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
+    to_internal(p, v0, v, nullptr, s);
+    k_power_start<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, s>>>(n, p->free_int, v, p->partials,
+                                                                  &p->ctl->counter, p->ctl);
+    LAUNCHED();
+    CU(cudaMemcpyAsync(p->ctl_host, p->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const double nv = p->ctl_host->alpha;
+    if (nv == 0.0) {
+        set_error("start vector vanished after masking (no free nodes?)");
+        return EBS_EINVAL;
+    }
+    // v /= ||v||: reuse the scale kernel with ctl->alpha = ||v||, done = 0
+    k_power_scale<<<grid_for(n, 256), 256, 0, s>>>(n, p->ctl, v, v);
+    LAUNCHED();
+    CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
+    SellView sv = sell_view(p);
+    const int block = 256;
+    const int64_t sgrid = (p->n_chunks * LANES + block - 1) / block;
+    int k = 0;
+    while (k < iters) {
+        int kend = k + 32 < iters ? k + 32 : iters;
+        for (; k < kend; ++k) {
+            PowerEpi epi{p->free_int, av, {0.0, 0.0}};
+#define EBS_PW(NB_, PK_)                                                                    \
+    {                                                                                       \
+        auto kern = k_power_matvec<NB_, PK_>;                                               \
+        kern<<<persistent_grid((const void *)kern, block, sgrid), block, 0, s>>>(           \
+            sv, p->ctl, p->partials, v, epi, tol);                                          \
+    }
+            if (p->nb == 3) {
+                if (p->packed) EBS_PW(3, true) else EBS_PW(3, false)
+            } else {
+                if (p->packed) EBS_PW(4, true) else EBS_PW(4, false)
+            }
+#undef EBS_PW
+            LAUNCHED();
+            k_power_scale<<<grid_for(n, 256), 256, 0, s>>>(n, p->ctl, av, v);
+            LAUNCHED();
+        }
+        CU(cudaMemcpyAsync(p->ctl_host, p->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (p->ctl_host->done) break;
+    }
+    CU(cudaMemcpyAsync(p->ctl_host, p->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *lam = p->ctl_host->pq;
+    *its = p->ctl_host->k;
     EBS_CATCH
 }
 

@@ -7,8 +7,14 @@ flag and is never raised; ``callback(k, x, r)`` is called for k = 0..iters with
 device tensors in the caller's numbering (reused buffers -- clone to keep them).
 
   richardson  x += omega r, omega = 2/(l1+l2)          solvers.py:163-183
+  chebyshev2  x += (1/alpha_{k mod N}) r               solvers.py:186-213
+  chebyshev3  p = r + beta_k p; x += alpha_k p         solvers.py:216-261
   jacobi      x += omega D^-1 r                        NEW (north star)
   cg / pcg    (Jacobi-preconditioned) CG on the masked operator  NEW (north star)
+
+The Chebyshev step scalars are data independent; they are computed on the host with the
+reference's exact expressions and streamed to the fused step kernel, so the iterates are
+bit-identical to ebsolve's.
 """
 
 from __future__ import annotations
@@ -21,8 +27,8 @@ import numpy as np
 import torch
 
 from . import _device as D
-from ._lib import (CALLBACK, EBS_CG, EBS_ECALLBACK, EBS_JACOBI, EBS_PCG, EBS_RICHARDSON,
-                   SolveParams, check, load)
+from ._lib import (CALLBACK, EBS_CG, EBS_CHEB2, EBS_CHEB3, EBS_ECALLBACK, EBS_JACOBI, EBS_PCG,
+                   EBS_RICHARDSON, SolveParams, check, load)
 from .elements import ElementBatch
 from .operators import DirichletData
 
@@ -51,6 +57,43 @@ class SpectralBounds:
 
 
 @dataclass(frozen=True)
+class ChebyshevCycle:
+    """solvers.py:59-66: precomputed cycle of step denominators."""
+
+    N: int
+    alphas: np.ndarray
+    d: float
+    c: float
+
+
+def chebyshev_roots(bounds: SpectralBounds, N: int) -> ChebyshevCycle:
+    """solvers.py:85-99: alphas[k] = d + c cos(pi (k+1/2)/N), natural order."""
+    if N < 1:
+        raise ValueError(f"cycle length must be positive, got N={N}")
+    d = bounds.center
+    c = bounds.half_width
+    k = np.arange(N)
+    alphas = d + c * np.cos(np.pi * (k + 0.5) / N)
+    alphas.setflags(write=False)
+    return ChebyshevCycle(N=N, alphas=alphas, d=d, c=c)
+
+
+def chebyshev_scaling_factor(bounds: SpectralBounds, k: int) -> float:
+    """solvers.py:102-114: C_k = T_k((l1+l2)/(l2-l1)) by the three-term recurrence."""
+    if k < 0:
+        raise ValueError(f"k must be nonnegative, got {k}")
+    if bounds.lambda1 >= bounds.lambda2:
+        raise ValueError("scaling factors need lambda1 < lambda2")
+    t = (bounds.lambda1 + bounds.lambda2) / (bounds.lambda2 - bounds.lambda1)
+    c_prev, c_cur = 1.0, t
+    if k == 0:
+        return c_prev
+    for _ in range(k - 1):
+        c_prev, c_cur = c_cur, 2.0 * t * c_cur - c_prev
+    return c_cur
+
+
+@dataclass(frozen=True)
 class ConvergenceHistory:
     """solvers.py:69-82: residual_norms[k] = ||r^k||_2 for k = 0..iters (host arrays)."""
 
@@ -65,7 +108,7 @@ class ConvergenceHistory:
 
 
 def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.0, exact=False,
-           tol=None, reference=None, callback=None):
+           tol=None, reference=None, callback=None, coef_a=None, coef_b=None):
     if iters < 0:
         raise ValueError(f"iteration count must be nonnegative, got {iters}")
     x0 = D.f64(x0)
@@ -115,6 +158,13 @@ def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.
     P.cb_x = cb_x.data_ptr() if cb_x is not None else None
     P.cb_r = cb_r.data_ptr() if cb_r is not None else None
     P.r_out = None
+    ca = cb = None
+    if coef_a is not None:
+        ca = (ctypes.c_double * max(1, len(coef_a)))(*coef_a)
+        P.coef_a = ctypes.cast(ca, ctypes.POINTER(ctypes.c_double))
+    if coef_b is not None:
+        cb = (ctypes.c_double * max(1, len(coef_b)))(*coef_b)
+        P.coef_b = ctypes.cast(cb, ctypes.POINTER(ctypes.c_double))
     t0 = time.perf_counter()
     code = load().ebs_solve(pl.handle, ctypes.byref(P), D.stream())
     wall = time.perf_counter() - t0
@@ -139,6 +189,51 @@ def richardson(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds
     omega = 2.0 / (bounds.lambda1 + bounds.lambda2)
     return _solve(EBS_RICHARDSON, batch, d, x0, iters, omega=omega, exact=deterministic, tol=tol,
                   reference=reference, callback=callback)
+
+
+def chebyshev2(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds, N: int,
+               iters: int, *, tol=None, reference=None, callback=None, threads: int = 1,
+               deterministic: bool = True):
+    """solvers.py:186-213: cyclic two-level Chebyshev, roots in natural order."""
+    cycle = chebyshev_roots(bounds, N)
+    if iters < 0:
+        raise ValueError(f"iteration count must be nonnegative, got {iters}")
+    coef = [1.0 / cycle.alphas[k % cycle.N] for k in range(iters)]
+    return _solve(EBS_CHEB2, batch, d, x0, iters, exact=deterministic, tol=tol,
+                  reference=reference, callback=callback, coef_a=coef)
+
+
+def _chebyshev3_coefficients(bounds: SpectralBounds, iters: int):
+    """The scalar recurrence of solvers.py:247-258, same expressions."""
+    dd = bounds.center
+    cc = bounds.half_width
+    alphas, betas = [], []
+    alpha = 0.0
+    for k in range(iters):
+        if k == 0:
+            alpha = 1.0 / dd
+            beta = 0.0
+        else:
+            beta = 0.5 * (cc * alpha) ** 2
+            if k > 1:
+                beta *= 0.5
+            alpha = 1.0 / (dd - beta / alpha)
+        alphas.append(alpha)
+        betas.append(beta)
+    return alphas, betas
+
+
+def chebyshev3(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds, iters: int, *,
+               tol=None, reference=None, callback=None, threads: int = 1,
+               deterministic: bool = True):
+    """solvers.py:216-261: three-level Chebyshev via the stable two-term recurrence."""
+    if not bounds.lambda1 < bounds.lambda2:
+        raise ValueError("chebyshev3 needs lambda1 < lambda2")
+    if iters < 0:
+        raise ValueError(f"iteration count must be nonnegative, got {iters}")
+    a, b = _chebyshev3_coefficients(bounds, iters)
+    return _solve(EBS_CHEB3, batch, d, x0, iters, exact=deterministic, tol=tol,
+                  reference=reference, callback=callback, coef_a=a, coef_b=b)
 
 
 def jacobi(batch: ElementBatch, d: DirichletData, x0, iters: int, *, omega: float = 0.8,

@@ -123,6 +123,48 @@ def main():
          norms_tol=hist_tol.residual_norms, u=u, errors=hist_err.error_norms,
          norms_err=hist_err.residual_norms)
 
+    # --- Chebyshev two-/three-level (solvers.py:186-261) ----------------
+    from ebsolve import spectrum as sp
+    arrs = {}
+    for level in (2, 3):
+        m = eb.build_unit_square_mesh(level)
+        batch = eb.build_element_batch(m, nu=0.0)
+        d = eb.constant_dirichlet(m, 1.0)
+        bounds = model_eigen_bounds(2**level + 1)
+        x0 = np.ones(m.n_nodes)
+        for N in (1, 4, 8):
+            xs = []
+            x, h = eb.chebyshev2(batch, d, x0, bounds, N, 20,
+                                 callback=lambda k, x, r: xs.append(x.copy()))
+            arrs[f"cheb2_l{level}_N{N}_iterates"] = np.stack(xs)
+            arrs[f"cheb2_l{level}_N{N}_norms"] = h.residual_norms
+        xs = []
+        x, h = eb.chebyshev3(batch, d, x0, bounds, 16,
+                             callback=lambda k, x, r: xs.append(x.copy()))
+        arrs[f"cheb3_l{level}_iterates"] = np.stack(xs)
+        arrs[f"cheb3_l{level}_norms"] = h.residual_norms
+        x, h = eb.chebyshev3(batch, d, x0, bounds, 500, tol=1e-6)
+        arrs[f"cheb3_l{level}_tol_x"] = x
+        arrs[f"cheb3_l{level}_tol_norms"] = h.residual_norms
+    save("chebyshev", **arrs)
+
+    # --- spectral bounds (spectrum.py:64-149) ---------------------------
+    arrs = {}
+    for level, nu in ((3, 1.0), (4, 2.5)):
+        m = eb.build_unit_square_mesh(level)
+        batch = eb.build_element_batch(m, nu=nu)
+        d = eb.constant_dirichlet(m, 1.0)
+        tag = f"l{level}_nu{nu}"
+        arrs[f"power_{tag}"] = sp.power_iteration_lambda_max(batch, d)
+        arrs[f"power10_{tag}"] = sp.power_iteration_lambda_max(batch, d, iters=10, seed=3)
+        lo, hi = sp.mass_gershgorin(batch, d)
+        arrs[f"gersh_{tag}"] = np.array([lo, hi])
+        b = sp.operator_bounds(batch, d, 2**level + 1, nu)
+        arrs[f"bounds_{tag}"] = np.array([b.lambda1, b.lambda2])
+        A = eb.assemble_sparse(batch.A_e, batch.index.indt)
+        arrs[f"dense_{tag}"] = eb.dense_interior_eigenvalues(A, d)
+    save("spectrum", **arrs)
+
     # --- C1: direct solution + SciPy Jacobi-PCG (reference.py:42-81) ------
     m = eb.build_unit_square_mesh(6)
     batch = eb.build_element_batch(m, nu=1.0)

@@ -105,3 +105,22 @@ def test_host_validation_matches_reference():
     lam = eb.model_eigenvalues_all(9)
     bnd = eb.model_eigen_bounds(9)
     assert abs(lam[0] - bnd.lambda1) <= 1e-12 and abs(lam[-1] - bnd.lambda2) <= 1e-12
+
+
+def test_chebyshev_host_scalars_match_reference_rules():
+    import numpy as np
+    import paper_1911_03973_b200 as eb
+    cyc = eb.chebyshev_roots(eb.SpectralBounds(0.0, 8.0), 2)
+    np.testing.assert_allclose(cyc.alphas, [4 + 2 * np.sqrt(2), 4 - 2 * np.sqrt(2)], rtol=1e-14)
+    b = eb.SpectralBounds(1.0, 3.0)
+    assert [eb.chebyshev_scaling_factor(b, k) for k in range(5)] == [1, 2, 7, 26, 97]
+    c8 = eb.chebyshev_roots(b, 8)
+    assert np.all(np.diff(c8.alphas) < 0)
+    for bb in (b, eb.model_eigen_bounds(33)):
+        assert eb.chebyshev_roots(bb, 1).alphas[0] == bb.center
+    with pytest.raises(ValueError):
+        eb.chebyshev_roots(b, 0)
+    with pytest.raises(ValueError):
+        eb.chebyshev_scaling_factor(b, -1)
+    with pytest.raises(ValueError):
+        eb.chebyshev_scaling_factor(eb.SpectralBounds(2.0, 2.0), 3)
