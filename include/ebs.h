@@ -134,6 +134,9 @@ int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int mask
 int ebs_matvec(ebs_plan_t plan, const double *x, double *y, int masked, void *stream);
 /* NEW diag(A) = assemble_rhs(stack_j A_e[j,j,:]), caller numbering. */
 int ebs_diagonal(ebs_plan_t plan, double *d, void *stream);
+/* spectrum.py:118-120 order: per local vertex j a bincount of A_e[j,j,:], then the
+ * per-j sums added j = 0, 1, ... (mass_gershgorin), caller numbering. */
+int ebs_diagonal_grouped(ebs_plan_t plan, double *d, void *stream);
 /* operators.py:58-63 assemble_rhs: b = bincount(indt, b_e) in (j,e) order; needs only
  * the plan's structure (no load). */
 int ebs_assemble_rhs(ebs_plan_t plan, const double *b_e, double *b, void *stream);

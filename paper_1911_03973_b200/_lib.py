@@ -76,6 +76,7 @@ SIGNATURES = {
     "ebs_residual": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "ebs_matvec": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "ebs_diagonal": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ebs_diagonal_grouped": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ebs_assemble_rhs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_mask": (c_int, [c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "ebs_check_finite": (c_int, [c_int64, c_void_p, c_void_p, c_void_p]),

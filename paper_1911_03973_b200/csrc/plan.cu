@@ -226,6 +226,7 @@ __global__ void k_pack(int nb, int64_t n_e, int64_t n_slots, int rowb,
 //   what = 0: b_e[j, e] (assemble_rhs, operators.py:58-63)
 //   what = 1: A plane j of the slot row = A_e[j, j, e] (diag)
 //   what = 2: slot_be (pre-assembled b from the packed stream)
+//   what = 3: diag summed per local vertex j first (mass_gershgorin order)
 // out_user != nullptr writes caller numbering, else internal numbering.
 __global__ void k_slot_sum(int nb, int64_t n_n, int64_t n_e, const int32_t *__restrict__ rowbase,
                            const int32_t *__restrict__ width, const int32_t *__restrict__ cnt,
@@ -241,21 +242,34 @@ __global__ void k_slot_sum(int nb, int64_t n_n, int64_t n_e, const int32_t *__re
         const int64_t c = m / LANES;
         const int lane = (int)(m - c * LANES);
         const int c_m = cnt[m];
-        double s = 0.0;
+        double s = 0.0, grp = 0.0;
+        int cur_j = -1;
         for (int k = 0; k < c_m; ++k) {
             const int64_t row = (int64_t)rowbase[c] + k;
             const int64_t sidx = row * LANES + lane;
             double v;
+            int j_slot = 0;
             if (what == 2) {
                 v = slot_be[sidx];
             } else {
                 const int32_t ej = slot_ej[sidx];
                 const int64_t e = ej & ID_MASK, j = (uint32_t)ej >> J_SHIFT;
+                j_slot = (int)j;
                 v = what == 0 ? b_e[j * n_e + e]
                               : reinterpret_cast<const double *>(slot + row * rowb)[j * LANES + lane];
             }
-            s = s + v;
+            if (what == 3) {  // spectrum.py:118-120: per-j bincounts, then added j = 0, 1, ..
+                if (j_slot != cur_j) {
+                    if (cur_j >= 0) s = s + grp;
+                    grp = 0.0;
+                    cur_j = j_slot;
+                }
+                grp = grp + v;
+            } else {
+                s = s + v;
+            }
         }
+        if (what == 3 && cur_j >= 0) s = s + grp;
         if (old_of_new) out[old_of_new[m]] = s;
         else out[m] = s;
     }
@@ -617,6 +631,15 @@ int ebs_plan_internal_diag(ebs_plan_t plan, double *d_int, void *stream) {
     Plan *p = reinterpret_cast<Plan *>(plan);
     EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
     slot_sum(p, 1, nullptr, nullptr, d_int, S(stream));
+    EBS_CATCH
+}
+
+int ebs_diagonal_grouped(ebs_plan_t plan, double *d, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && d, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    slot_sum(p, 3, nullptr, p->old_of_new, d, S(stream));
     EBS_CATCH
 }
 

@@ -17,7 +17,7 @@ import torch
 from . import _device as D
 from ._lib import call
 from .elements import ElementBatch
-from .operators import DirichletData, diagonal, matvec
+from .operators import DirichletData, matvec
 from .solvers import SpectralBounds
 
 POWER_ITERS = 1000     # spectrum.py:26
@@ -82,14 +82,17 @@ class _MassBatch:
 def mass_gershgorin(batch: ElementBatch, d: DirichletData) -> tuple[float, float]:
     """spectrum.py:102-126: Gershgorin enclosure of the free-node mass spectrum.
     Row sums over free columns = M times the free indicator (device matvec, the
-    reference's einsum + bincount order); diagonal by (j, e)-ordered slot sums."""
+    reference's einsum + bincount order); diagonal summed per j then over j, as the
+    reference does -- both bit-identical."""
     n_n = batch.index.node_count()
     mb = _MassBatch(batch.M_e, batch.index)
     is_free = torch.ones(n_n, dtype=torch.bool, device=D.device())
     if d.nd.numel():
         is_free[d.nd] = False
     row_sums = matvec(mb, is_free.to(torch.float64))
-    diags = diagonal(mb, n_n)
+    pl = mb.operator(n_n)
+    diags = D.empty(n_n)
+    call("ebs_diagonal_grouped", pl.handle, D.ptr(diags), D.stream())
     if not bool(is_free.any()):
         raise ValueError("no free nodes")
     lo = (2.0 * diags - row_sums)[is_free]
