@@ -75,25 +75,51 @@ __global__ void k_scatter_add(int64_t n, const int64_t *__restrict__ idx,
 }
 
 // occupancy-sized persistent grid, cached per (kernel, device)
-int persistent_grid(const void *kernel, int block, int64_t work_blocks) {
-    struct Ent { const void *k; int dev; int block; int grid; };
+int persistent_grid(const void *kernel, int block, int64_t work_blocks, size_t smem) {
+    struct Ent { const void *k; int dev; int block; size_t smem; int grid; };
     static Ent cache[64];
     static int n_cache = 0;
     int dev = 0;
     CU(cudaGetDevice(&dev));
     int grid = -1;
     for (int i = 0; i < n_cache; ++i)
-        if (cache[i].k == kernel && cache[i].dev == dev && cache[i].block == block) grid = cache[i].grid;
+        if (cache[i].k == kernel && cache[i].dev == dev && cache[i].block == block &&
+            cache[i].smem == smem)
+            grid = cache[i].grid;
     if (grid < 0) {
         int per_sm = 0, sms = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
+        if (smem > 48 * 1024)
+            CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         grid = (per_sm > 0 ? per_sm : 1) * sms;
         if (grid > 8192) grid = 8192;
-        if (n_cache < 64) cache[n_cache++] = Ent{kernel, dev, block, grid};
+        if (n_cache < 64) cache[n_cache++] = Ent{kernel, dev, block, smem, grid};
     }
     if (work_blocks < 1) work_blocks = 1;
     return (int)(work_blocks < grid ? work_blocks : grid);
+}
+
+}  // namespace ebs
+#include "sell.cuh"
+namespace ebs {
+
+SellLaunch sell_launch(const void *kernel, int nb, int rowb, int64_t n_chunks) {
+    SellLaunch L;
+#if EBS_TMA
+    const int W = nb == 3 ? TmaCfg<3>::W : TmaCfg<4>::W;
+    const int R = nb == 3 ? TmaCfg<3>::R : TmaCfg<4>::R;
+    const int S = nb == 3 ? TmaCfg<3>::S : TmaCfg<4>::S;
+    L.block = W * LANES;
+    L.smem = (size_t)W * S * R * rowb;
+    L.grid = persistent_grid(kernel, L.block, (n_chunks + W - 1) / W, L.smem);
+#else
+    (void)rowb;
+    L.block = 256;
+    L.smem = 0;
+    L.grid = persistent_grid(kernel, 256, (n_chunks * LANES + 255) / 256, 0);
+#endif
+    return L;
 }
 
 // scratch for the standalone reductions (one per device is enough: stream-ordered use)

@@ -55,8 +55,8 @@ __global__ void EBS_SELL_BOUNDS(NB)
 template <int NB, bool PACKED, int MODE>
 void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cudaStream_t s) {
     auto kern = k_sell_op<NB, PACKED, MODE>;
-    const int grid = persistent_grid((const void *)kern, 256, (p->n_chunks * LANES + 255) / 256);
-    kern<<<grid, 256, 0, s>>>(sell_view(p), x_int, epi);
+    const SellLaunch SL = sell_launch((const void *)kern, NB, p->rowb, p->n_chunks);
+    kern<<<SL.grid, SL.block, SL.smem, s>>>(sell_view(p), x_int, epi);
     LAUNCHED();
 }
 

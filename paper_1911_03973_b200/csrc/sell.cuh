@@ -88,7 +88,6 @@ __device__ __forceinline__ double pick(int t, double xo, const double (&g)[NB - 
 #ifndef EBS_MINB3
 #define EBS_MINB3 6  // min resident 256-thread CTAs per SM, 3D SELL kernels
 #endif
-#define EBS_SELL_BOUNDS(NB) __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
 
 template <int NB, bool PACKED, bool EXACT>
 __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0, int w, int lane,
@@ -157,10 +156,10 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
     return s;
 }
 
-// Grid-stride sweep over chunks: epi(m, s, xo) for every valid node.
+// Grid-stride sweep over chunks: epi(m, s, xo) for every valid node (direct loads).
 template <int NB, bool PACKED, bool EXACT, class Epi>
-__device__ __forceinline__ void sell_sweep(const SellView &v, const double *__restrict__ x,
-                                           Epi &epi) {
+__device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *__restrict__ x,
+                                               Epi &epi) {
     const int lane = threadIdx.x & (LANES - 1);
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / LANES;
@@ -175,7 +174,203 @@ __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__re
     }
 }
 
+// ---------------------------------------------------------------- TMA bulk path --
+// Each warp owns a ring of S shared-memory stages of R slot rows.  Lane 0 arms a stage's
+// mbarrier with the byte count and issues one cp.async.bulk (TMA, 1-D) of the piece's
+// contiguous rows; the warp consumes stage i while the next S-1 pieces are in flight.
+// A piece is up to R rows of one chunk (chunks are `width` rows, contiguous in the blob).
+#ifndef EBS_TMA
+#define EBS_TMA 0
+#endif
+#ifndef EBS_TMA_W2
+#define EBS_TMA_W2 8  // warps per CTA, 2D
+#endif
+#ifndef EBS_TMA_R2
+#define EBS_TMA_R2 6  // rows per stage, 2D (structured 2D chunks are 6 rows)
+#endif
+#ifndef EBS_TMA_S2
+#define EBS_TMA_S2 3  // stages per warp, 2D
+#endif
+#ifndef EBS_TMA_W3
+#define EBS_TMA_W3 4
+#endif
+#ifndef EBS_TMA_R3
+#define EBS_TMA_R3 8
+#endif
+#ifndef EBS_TMA_S3
+#define EBS_TMA_S3 4
+#endif
+
+template <int NB>
+struct TmaCfg {
+    static constexpr int W = NB == 3 ? EBS_TMA_W2 : EBS_TMA_W3;
+    static constexpr int R = NB == 3 ? EBS_TMA_R2 : EBS_TMA_R3;
+    static constexpr int S = NB == 3 ? EBS_TMA_S2 : EBS_TMA_S3;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+template <int NB, bool PACKED, bool EXACT, class Epi>
+__device__ __forceinline__ void sell_sweep_tma(const SellView &v, const double *__restrict__ x,
+                                               Epi &epi) {
+    constexpr int R = TmaCfg<NB>::R, S = TmaCfg<NB>::S, W = TmaCfg<NB>::W;
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ uint64_t bars[W][S];
+    const int lane = threadIdx.x & (LANES - 1);
+    const int wib = threadIdx.x / LANES;
+    const int64_t warp = (int64_t)blockIdx.x * W + wib;
+    const int64_t nwarps = (int64_t)gridDim.x * W;
+    const int rowb = v.rowb;
+    uint8_t *ring = dsm + (size_t)wib * S * R * rowb;
+    uint64_t *bar = bars[wib];
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // producer cursor (lane 0 state, kept uniform)
+    int64_t pc = warp;
+    int pk0 = 0;
+    int pstage = 0;
+    auto produce = [&]() {
+        if (pc >= v.n_chunks) return;
+        const int w = v.width[pc];
+        int nr = w - pk0;
+        nr = nr > R ? R : nr;
+        if (nr > 0 && lane == 0) {
+            const uint32_t bytes = (uint32_t)nr * rowb;
+            mbar_expect_tx(&bar[pstage], bytes);
+            bulk_g2s(ring + (size_t)pstage * R * rowb,
+                     v.slot + ((int64_t)v.rowbase[pc] + pk0) * rowb, bytes, &bar[pstage]);
+        }
+        pstage = pstage + 1 == S ? 0 : pstage + 1;
+        pk0 += R;
+        if (pk0 >= w) {
+            pc += nwarps;
+            pk0 = 0;
+        }
+    };
+    for (int s = 0; s < S; ++s) produce();
+    uint32_t phases = 0;
+    int cstage = 0;
+    for (int64_t c = warp; c < v.n_chunks; c += nwarps) {
+        const int64_t m = c * LANES + lane;
+        const bool valid = m < v.n_n;
+        const int c_m = valid ? v.cnt[m] : 0;
+        const double xo = valid ? x[m] : 0.0;
+        const int w = v.width[c];
+        const int64_t row0 = v.rowbase[c];
+        double sum = 0.0;
+        for (int k0 = 0; k0 < w || (k0 == 0 && w == 0); k0 += R) {
+            int nr = w - k0;
+            nr = nr > R ? R : nr;
+            if (nr > 0) {
+                mbar_wait(&bar[cstage], (phases >> cstage) & 1u);
+                phases ^= 1u << cstage;
+                const uint8_t *base = ring + (size_t)cstage * R * rowb;
+#pragma unroll 2
+                for (int r = 0; r < nr; ++r) {
+                    const int k = k0 + r;
+                    if (k < c_m) {
+                        const uint8_t *rp = base + r * rowb;
+                        const double *ap = reinterpret_cast<const double *>(rp) + lane;
+                        double a[NB];
+#pragma unroll
+                        for (int i = 0; i < NB; ++i) a[i] = ap[i * LANES];
+                        int32_t nid[NB - 1];
+                        int j;
+                        if constexpr (PACKED) {
+                            using Wd = typename Pack<NB>::W;
+                            const Wd wd = reinterpret_cast<const Wd *>(rp + NB * 256)[lane];
+                            j = Pack<NB>::j(wd);
+#pragma unroll
+                            for (int t = 0; t < NB - 1; ++t)
+                                nid[t] = (int32_t)(m + Pack<NB>::d(wd, t));
+                        } else {
+                            const int32_t *ip = reinterpret_cast<const int32_t *>(rp + NB * 256) + lane;
+                            int32_t id0 = ip[0];
+                            j = (int)((uint32_t)id0 >> J_SHIFT);
+#pragma unroll
+                            for (int t = 0; t < NB - 1; ++t) nid[t] = ip[t * LANES] & ID_MASK;
+                        }
+                        double g[NB - 1];
+#pragma unroll
+                        for (int t = 0; t < NB - 1; ++t) g[t] = __ldg(x + nid[t]);
+                        double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
+#pragma unroll
+                        for (int i = 1; i < NB; ++i)
+                            loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
+                        if constexpr (EXACT)
+                            sum = sum + (__ldcs(v.be + (row0 + k) * LANES + lane) - loc);
+                        else
+                            sum = sum + loc;
+                    }
+                }
+                __syncwarp();
+            }
+            cstage = cstage + 1 == S ? 0 : cstage + 1;
+            produce();  // refill the stage just released with the piece S ahead
+            if (w == 0) break;
+        }
+        if (valid) epi(m, sum, xo);
+    }
+}
+
+#if EBS_TMA
+#define EBS_SELL_THREADS(NB) (TmaCfg<NB>::W * LANES)
+#define EBS_SELL_BOUNDS(NB) __launch_bounds__(EBS_SELL_THREADS(NB), 1)
+#else
+#define EBS_SELL_THREADS(NB) 256
+#define EBS_SELL_BOUNDS(NB) __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
+#endif
+
+template <int NB, bool PACKED, bool EXACT, class Epi>
+__device__ __forceinline__ void sell_sweep(const SellView &v, const double *__restrict__ x,
+                                           Epi &epi) {
+#if EBS_TMA
+    sell_sweep_tma<NB, PACKED, EXACT>(v, x, epi);
+#else
+    sell_sweep_ldg<NB, PACKED, EXACT>(v, x, epi);
+#endif
+}
+
+// launch configuration of a SELL kernel (threads, dynamic smem, persistent grid)
+struct SellLaunch {
+    int grid, block;
+    size_t smem;
+};
+SellLaunch sell_launch(const void *kernel, int nb, int rowb, int64_t n_chunks);
+
 // Occupancy-sized persistent grid (cached per kernel and device).
-int persistent_grid(const void *kernel, int block, int64_t work_blocks);
+int persistent_grid(const void *kernel, int block, int64_t work_blocks, size_t smem = 0);
 
 }  // namespace ebs

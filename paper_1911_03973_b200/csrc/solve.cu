@@ -439,8 +439,9 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
 #define EBS_JAC(NB_, PK_, EX_)                                                              \
     {                                                                                       \
         auto kern = k_jacobi_step<NB_, PK_, EX_>;                                           \
-        const int g = persistent_grid((const void *)kern, block, sgrid);                    \
-        kern<<<g, block, 0, s>>>(v, L, xa, xb, p->b_int, p->free_int, dv, ref_int, rcb,     \
+        const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
+        kern<<<SL.grid, SL.block, SL.smem, s>>>(v, L, xa, xb, p->b_int, p->free_int, dv,    \
+                                                 ref_int, rcb,                              \
                                  final_step, P->method, coef_a, coef_b, pbuf);              \
     }
             if (nb == 3) {
@@ -494,7 +495,8 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
 #define EBS_INIT(NB_, PK_)                                                                  \
     {                                                                                       \
         auto kern = k_pcg_init<NB_, PK_>;                                                   \
-        kern<<<persistent_grid((const void *)kern, block, sgrid), block, 0, s>>>(v, L, xa, ie); \
+        const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
+        kern<<<SL.grid, SL.block, SL.smem, s>>>(v, L, xa, ie);                              \
     }
             if (nb == 3) {
                 if (p->packed) EBS_INIT(3, true) else EBS_INIT(3, false)
@@ -518,7 +520,8 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
 #define EBS_MV(NB_, PK_)                                                                    \
     {                                                                                       \
         auto kern = k_pcg_matvec<NB_, PK_>;                                                 \
-        kern<<<persistent_grid((const void *)kern, block, sgrid), block, 0, s>>>(v, L, pv, me); \
+        const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
+        kern<<<SL.grid, SL.block, SL.smem, s>>>(v, L, pv, me);                              \
     }
                     if (nb == 3) {
                         if (p->packed) EBS_MV(3, true) else EBS_MV(3, false)
@@ -598,8 +601,8 @@ int ebs_power_iteration(ebs_plan_t plan, const double *v0, int iters, double tol
 #define EBS_PW(NB_, PK_)                                                                    \
     {                                                                                       \
         auto kern = k_power_matvec<NB_, PK_>;                                               \
-        kern<<<persistent_grid((const void *)kern, block, sgrid), block, 0, s>>>(           \
-            sv, p->ctl, p->partials, v, epi, tol);                                          \
+        const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
+        kern<<<SL.grid, SL.block, SL.smem, s>>>(sv, p->ctl, p->partials, v, epi, tol);      \
     }
             if (p->nb == 3) {
                 if (p->packed) EBS_PW(3, true) else EBS_PW(3, false)

@@ -165,6 +165,22 @@ def main():
         arrs[f"dense_{tag}"] = eb.dense_interior_eigenvalues(A, d)
     save("spectrum", **arrs)
 
+    # --- experiment driver exports (cli.py:110-233) -------------------------
+    import tempfile
+    from ebsolve.cli import ExperimentConfig, run_experiment
+    arrs = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        rep = run_experiment(ExperimentConfig(level=3, iters=20, solver="all", out_dir=tmp))
+        for f in sorted(Path(tmp).iterdir()):
+            arrs[f.name] = np.frombuffer(f.read_bytes(), dtype=np.uint8)
+        arrs["bounds"] = np.array(rep.bounds)
+    with tempfile.TemporaryDirectory() as tmp:
+        run_experiment(ExperimentConfig(level=2, iters=5, solver="cheb3", out_dir=tmp,
+                                        export_vtk=True))
+        for f in sorted(Path(tmp).iterdir()):
+            arrs["vtk_" + f.name] = np.frombuffer(f.read_bytes(), dtype=np.uint8)
+    save("cli_exports", **arrs)
+
     # --- C1: direct solution + SciPy Jacobi-PCG (reference.py:42-81) ------
     m = eb.build_unit_square_mesh(6)
     batch = eb.build_element_batch(m, nu=1.0)

@@ -124,3 +124,12 @@ def test_chebyshev_host_scalars_match_reference_rules():
         eb.chebyshev_scaling_factor(b, -1)
     with pytest.raises(ValueError):
         eb.chebyshev_scaling_factor(eb.SpectralBounds(2.0, 2.0), 3)
+
+
+def test_cli_validation_without_gpu(capsys):
+    from paper_1911_03973_b200.cli import main
+    assert main(["--level", "0"]) == 2
+    assert main(["--level", "1", "--solver", "cheb3"]) == 2
+    assert main(["--level", "3", "--iters", "-1"]) == 2
+    err = capsys.readouterr().err
+    assert "--level" in err and "cheb3" in err and "--iters" in err
