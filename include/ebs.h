@@ -158,6 +158,14 @@ int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, in
 /* all-finite check (operators.py:90): *flag (device int32) = 1 if any non-finite. */
 int ebs_check_finite(int64_t n, const double *v, int32_t *flag, void *stream);
 
+/* reference.py:25-39 assemble_sparse, on the device (cross-check path, never used by the
+ * solvers): CSR of the loaded operator in caller numbering, columns sorted, duplicates
+ * summed in (j, e) order.  ebs_csr_nnz fills crow (n+1 entries, int64); ebs_csr_fill
+ * writes col (int32) / val.  conn is the plan's connectivity (int32 SoA). */
+int ebs_csr_nnz(ebs_plan_t plan, const int32_t *conn, int64_t *crow, void *stream);
+int ebs_csr_fill(ebs_plan_t plan, const int32_t *conn, const int64_t *crow, int32_t *col,
+                 double *val, void *stream);
+
 /* ----------------------------------------------------------- vector work ---- */
 /* deterministic (fixed-order, launch-size independent of the device) reductions */
 int ebs_dot(int64_t n, const double *x, const double *y, double *out, void *stream);

@@ -20,12 +20,13 @@ from .operators import (DirichletData, apply_initial_guess, assemble_rhs, consta
 from .solvers import (ChebyshevCycle, ConvergenceHistory, SpectralBounds, cg, chebyshev2,
                       chebyshev3, chebyshev_roots, chebyshev_scaling_factor, jacobi, pcg,
                       richardson)
+from .sparse import assemble_sparse
 from .spectrum import (mass_gershgorin, model_eigen_bounds, model_eigenvalues_all,
                        operator_bounds, power_iteration_lambda_max)
 
 __all__ = [
     "ChebyshevCycle", "chebyshev2", "chebyshev3", "chebyshev_roots", "chebyshev_scaling_factor",
-    "mass_gershgorin", "operator_bounds", "power_iteration_lambda_max",
+    "mass_gershgorin", "operator_bounds", "power_iteration_lambda_max", "assemble_sparse",
     "ConvergenceHistory", "DirichletData", "ElementBatch", "IndexArrays", "MAX_LEVEL", "Mesh",
     "SpectralBounds", "apply_initial_guess", "assemble_rhs", "boundary_nodes",
     "build_element_batch", "build_grid_mesh", "build_index_arrays", "build_unit_cube_mesh",

@@ -83,6 +83,8 @@ SIGNATURES = {
     "ebs_to_internal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_to_user": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_plan_apply": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p]),
+    "ebs_csr_nnz": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_csr_fill": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_dot": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_nrm2": (c_int, [c_int64, c_void_p, c_void_p, c_void_p]),
     "ebs_axpby": (c_int, [c_int64, c_double, c_void_p, c_double, c_void_p, c_void_p]),

@@ -165,6 +165,17 @@ def main():
         arrs[f"dense_{tag}"] = eb.dense_interior_eigenvalues(A, d)
     save("spectrum", **arrs)
 
+    # --- assembled CSR (reference.py:25-39) ------------------------------
+    arrs = {}
+    m = eb.build_unit_square_mesh(3)
+    batch = eb.build_element_batch(m, nu=1.0)
+    for name in ("K_e", "A_e"):
+        S = eb.assemble_sparse(getattr(batch, name), batch.index.indt)
+        S.sort_indices()
+        arrs[f"{name}_indptr"], arrs[f"{name}_indices"], arrs[f"{name}_data"] = \
+            S.indptr, S.indices, S.data
+    save("sparse_l3", **arrs)
+
     # --- experiment driver exports (cli.py:110-233) -------------------------
     import tempfile
     from ebsolve.cli import ExperimentConfig, run_experiment
