@@ -14,7 +14,8 @@ from .elements import (ElementBatch, build_element_batch, combine_system, local_
                        local_mass_batch, local_stiffness_batch)
 from .mesh import (MAX_LEVEL, IndexArrays, Mesh, boundary_nodes, build_grid_mesh,
                    build_index_arrays, build_unit_cube_mesh, build_unit_square_mesh,
-                   face_z0_nodes, jitter_interior, permute_nodes, signed_areas)
+                   export_mesh, face_z0_nodes, jitter_interior, permute_nodes, signed_areas,
+                   uniform_refine)
 from .operators import (DirichletData, apply_initial_guess, assemble_rhs, constant_dirichlet,
                         diagonal, mask_dirichlet, matvec, residual)
 from .solvers import (ChebyshevCycle, ConvergenceHistory, SpectralBounds, cg, chebyshev2,
@@ -27,6 +28,7 @@ from .spectrum import (mass_gershgorin, model_eigen_bounds, model_eigenvalues_al
 __all__ = [
     "ChebyshevCycle", "chebyshev2", "chebyshev3", "chebyshev_roots", "chebyshev_scaling_factor",
     "mass_gershgorin", "operator_bounds", "power_iteration_lambda_max", "assemble_sparse",
+    "uniform_refine", "export_mesh",
     "ConvergenceHistory", "DirichletData", "ElementBatch", "IndexArrays", "MAX_LEVEL", "Mesh",
     "SpectralBounds", "apply_initial_guess", "assemble_rhs", "boundary_nodes",
     "build_element_batch", "build_grid_mesh", "build_index_arrays", "build_unit_cube_mesh",

@@ -112,7 +112,7 @@ def _assemble(m: Mesh, nu=0.0, f=None, want=("K", "M", "A", "b"), check_degenera
          D.ptr(f_vals), float(f_const), D.ptr(out["K"]), D.ptr(out["M"]), D.ptr(out["A"]),
          D.ptr(out["b"]), D.ptr(ndeg), D.stream())
     if check_degenerate and int(ndeg.item()):
-        meas = signed_areas(m.nodes, m.conn)
+        meas = signed_areas(m.nodes, conn=m.conn)
         worst = int(torch.argmin(meas))
         what, eps = ("area", EPS_AREA) if m.dim == 2 else ("volume", EPS_VOLUME)
         raise ValueError(

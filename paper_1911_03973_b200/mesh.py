@@ -28,8 +28,8 @@ class Mesh:
 
     mesh.py:25-65.  ``elements`` accepts (n_e, n_b) node-index rows (any integer
     array); validation (shape, index range, positive measure, boundary range,
-    mesh.py:39-52) runs on the device.  ``dirichlet_face`` optionally records the
-    3D z=0 face used by the BASELINE 3D configs.
+    mesh.py:39-52) runs on the device.  ``conn`` (keyword) passes the int32 SoA
+    connectivity directly.
     """
 
     nodes: torch.Tensor
@@ -167,15 +167,15 @@ def face_z0_nodes(m: Mesh) -> torch.Tensor:
     return _boundary_from_flags(m.nodes, 1)
 
 
-def signed_areas(nodes, elements) -> torch.Tensor:
-    """mesh.py:96-101 (2D signed area; 3D signed volume) for every element."""
+def signed_areas(nodes, elements=None, *, conn=None) -> torch.Tensor:
+    """mesh.py:96-101 (2D signed area; 3D signed volume) for every element.
+    ``elements`` is (n_e, n_b) as in the reference; ``conn`` the (n_b, n_e) SoA."""
     nodes = D.f64(nodes)
-    if isinstance(elements, torch.Tensor) and elements.ndim == 2 and elements.shape[0] == nodes.shape[1] + 1 \
-            and elements.dtype == torch.int32 and elements.is_contiguous():
-        conn = elements
-    else:
-        el = elements if isinstance(elements, torch.Tensor) else torch.from_numpy(np.asarray(elements))
-        conn = D.i32(el.t())
+    if conn is None:
+        el = elements if isinstance(elements, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(np.asarray(elements, dtype=np.int64)))
+        conn = el.t()
+    conn = D.i32(conn)
     out = D.empty(conn.shape[1])
     call("ebs_mesh_measure", nodes.shape[1], conn.shape[1], D.ptr(nodes), D.ptr(conn), D.ptr(out),
          D.stream())
@@ -256,3 +256,52 @@ def jitter_interior(m: Mesh, delta) -> Mesh:
     nodes = m.nodes.clone()
     nodes[interior] += delta_t
     return Mesh(nodes, None, m.boundary_nodes, level=None, conn=m.conn)
+
+
+def uniform_refine(m: Mesh) -> Mesh:
+    """mesh.py:157-208 on the device: split every triangle into 4 via edge midpoints and
+    renumber canonically (nodes by (y, x), triples rotated to their smallest index, rows
+    sorted), so refining a structured mesh equals build_unit_square_mesh(level + 1)."""
+    if m.dim != 2:
+        raise ValueError("uniform_refine is defined for triangle meshes")
+    if m.level is not None and m.level + 1 > MAX_LEVEL:
+        raise ValueError(f"refining level {m.level} exceeds the size guard (max {MAX_LEVEL})")
+    if 4 * m.n_elements > 2 * 4**MAX_LEVEL:
+        raise ValueError("refinement exceeds the size guard")
+    tri = m.conn.t().to(torch.int64)                       # (n_e, 3)
+    edges = torch.cat([tri[:, [0, 1]], tri[:, [1, 2]], tri[:, [2, 0]]])
+    edges = torch.sort(edges, dim=1).values
+    uniq, inv = torch.unique(edges, dim=0, return_inverse=True)
+    mid = m.n_nodes + inv.reshape(3, -1)                   # rows ab, bc, ca per element
+    mid_coords = 0.5 * (m.nodes[uniq[:, 0]] + m.nodes[uniq[:, 1]])
+    all_nodes = torch.cat([m.nodes, mid_coords])
+    a, b, c = tri[:, 0], tri[:, 1], tri[:, 2]
+    ab, bc, ca = mid[0], mid[1], mid[2]
+    children = torch.cat([torch.stack([a, ab, ca], 1), torch.stack([ab, b, bc], 1),
+                          torch.stack([ca, bc, c], 1), torch.stack([ab, bc, ca], 1)])
+    # np.lexsort((x, y)): stable sort by x, then stable by y
+    order = torch.argsort(all_nodes[:, 0], stable=True)
+    order = order[torch.argsort(all_nodes[order, 1], stable=True)]
+    rank = torch.empty_like(order)
+    rank[order] = torch.arange(order.numel(), device=order.device)
+    new_nodes = all_nodes[order].contiguous()
+    children = rank[children]
+    shift = torch.argmin(children, dim=1)
+    cols = (shift[:, None] + torch.arange(3, device=shift.device)) % 3
+    children = torch.gather(children, 1, cols)
+    # np.lexsort((c2, c1, c0)): stable sorts by c2, c1, c0
+    idx = torch.argsort(children[:, 2], stable=True)
+    idx = idx[torch.argsort(children[idx, 1], stable=True)]
+    idx = idx[torch.argsort(children[idx, 0], stable=True)]
+    children = children[idx]
+    level = None if m.level is None else m.level + 1
+    return Mesh(new_nodes, children, _boundary_from_flags(new_nodes, 0), level=level)
+
+
+def export_mesh(m: Mesh, directory) -> None:
+    """mesh.py:211-218 debug dump: nodes.txt (%.17g) and elements.txt (%d)."""
+    from pathlib import Path
+    directory = Path(directory)
+    directory.mkdir(parents=True, exist_ok=True)
+    np.savetxt(directory / "nodes.txt", m.nodes.cpu().numpy(), fmt="%.17g")
+    np.savetxt(directory / "elements.txt", m.elements.cpu().numpy(), fmt="%d")

@@ -165,6 +165,13 @@ def main():
         arrs[f"dense_{tag}"] = eb.dense_interior_eigenvalues(A, d)
     save("spectrum", **arrs)
 
+    # --- uniform_refine (mesh.py:157-208) on an unstructured (jittered) mesh --
+    g4 = oracle.config_inputs(4, seed=0, size=3)
+    m = eb.Mesh(g4["nodes"], g4["elements"], g4["dirichlet"])
+    fine = eb.uniform_refine(m)
+    save("refine", nodes=g4["nodes"], elements=g4["elements"], boundary=g4["dirichlet"],
+         fine_nodes=fine.nodes, fine_elements=fine.elements, fine_boundary=fine.boundary_nodes)
+
     # --- assembled CSR (reference.py:25-39) ------------------------------
     arrs = {}
     m = eb.build_unit_square_mesh(3)

@@ -60,7 +60,7 @@ def test_kuhn_mesh_matches_oracle(gpu, N):
     npt.assert_array_equal(to_np(m.elements), elements)
     npt.assert_array_equal(to_np(eb.face_z0_nodes(m)), face)
     npt.assert_array_equal(to_np(m.boundary_nodes), o.detect_boundary(nodes))
-    vol = to_np(eb.signed_areas(m.nodes, m.conn))
+    vol = to_np(eb.signed_areas(m.nodes, conn=m.conn))
     npt.assert_array_equal(vol, o.signed_measure(nodes, elements))
 
 
