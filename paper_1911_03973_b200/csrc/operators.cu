@@ -90,14 +90,53 @@ __global__ void k_to_internal_scatter(int64_t n, const int32_t *__restrict__ new
         atomicOr(nonfinite, 1);
 }
 
+// gather orientation with 8 independent index->value chains per thread (memory-level
+// parallelism for the random 8 B reads)
+constexpr int PERM_ILP = 8;
+__global__ void __launch_bounds__(256)
+    k_to_internal_ilp(int64_t n, const int32_t *__restrict__ old_of_new,
+                      const double *__restrict__ x_user, double *__restrict__ x_int,
+                      int32_t *nonfinite) {
+    bool bad = false;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+         base += stride * PERM_ILP) {
+        int32_t idx[PERM_ILP];
+        double v[PERM_ILP];
+#pragma unroll
+        for (int u = 0; u < PERM_ILP; ++u) {
+            const int64_t m = base + u * stride;
+            idx[u] = m < n ? __ldcs(old_of_new + m) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < PERM_ILP; ++u) {
+            const int64_t m = base + u * stride;
+            v[u] = m < n ? __ldg(x_user + idx[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PERM_ILP; ++u) {
+            const int64_t m = base + u * stride;
+            if (m < n) {
+                bad |= !isfinite(v[u]);
+                x_int[m] = v[u];
+            }
+        }
+    }
+    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(nonfinite, 1);
+}
+
 #ifndef EBS_TO_INTERNAL_SCATTER
-#define EBS_TO_INTERNAL_SCATTER 1
+#define EBS_TO_INTERNAL_SCATTER 2  // 0 gather, 1 scatter, 2 gather with ILP
 #endif
 
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
                  cudaStream_t s) {
     if (p->n_n == 0) return;
-    if (EBS_TO_INTERNAL_SCATTER)
+    if (EBS_TO_INTERNAL_SCATTER == 2)
+        k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
+                            s>>>(p->n_n, p->old_of_new, x_user, x_int, nonfinite);
+    else if (EBS_TO_INTERNAL_SCATTER == 1)
         k_to_internal_scatter<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(
             p->n_n, p->new_of_old, x_user, x_int, nonfinite);
     else

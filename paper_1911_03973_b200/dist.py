@@ -364,55 +364,108 @@ def emulate(batch, n_nodes, d, P, precondition=True):
 
 # ------------------------------------------------------------------- bench --
 def bench_rank(args, rank, world, local_rank):
-    """bench.py --gpus N under torchrun: C2 residual strong-scaled over N element slabs,
-    NCCL halo exchange, device-timed max over ranks; rank 0 prints the JSON line."""
+    """bench.py --gpus N under torchrun: the C2 residual strong-scaled over N element
+    slabs with the NCCL halo exchange; device-timed, max over ranks; rank 0 prints the
+    JSON line.  `value` = n_n * K / T_max (whole job); `e2e` adds each rank's host->device
+    copy of its x slab and device->host copy of its r slab inside the timed loop."""
     import json
     import os
+    import statistics
+    import sys
     import torch.distributed as dist
 
     from .inputs import config_problem
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench as B
+
     torch.cuda.set_device(local_rank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    peaks, peak_kind = B.load_peaks()
+    sampler = B.ClockSampler(index=local_rank).start()
     p = config_problem(2, seed=args.seed, size=args.size)
     m, batch = p["mesh"], p["batch"]
     maps = partition_maps(batch.index.indt, m.n_nodes, world)
     op = GpuRankOperator(batch, m.n_nodes, None, maps, rank)
     comm = TorchTransport()
     prob = setup([op], comm)
-    x_int = op.to_internal(torch.from_numpy(p["x"]).cuda())
+    x_glob = torch.from_numpy(p["x"]).cuda()
+    x_int = op.to_internal(x_glob)
     s, r = op.zeros(), op.zeros()
     red = torch.zeros(1, dtype=torch.float64, device="cuda")
-    n0 = load().ebs_launch_count()
+    stream = torch.cuda.current_stream()
+    lo, hi = int(maps["bounds"][rank]), int(maps["bounds"][rank + 1])
 
-    def step():  # r = b - A x on this slab's nodes: SELL partials, halo, b - s
+    def step(ev=None):  # r = b - A x on this slab's nodes: SELL partials, halo, b - s
+        if ev is not None:
+            ev[0].record(stream)
         op.matvec_partial(x_int, s)
+        if ev is not None:
+            ev[1].record(stream)
         halo([op], comm, [s])
         op.vec_jacobi(0.0, prob.b[0], s, None, x_int, None, r, red)
 
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    sampler.on()
     dist.barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    n0 = load().ebs_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        step()
-    e1.record()
+    e0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = load().ebs_launch_count() - n0
+    dist.barrier()
+    kern = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3, kern], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # end to end: this rank's x slab in from pinned host memory, its r slab out
+    x_host = x_int.cpu().pin_memory()
+    r_host = torch.empty(op.n, dtype=torch.float64).pin_memory()
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1) / 1e3], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    launches = load().ebs_launch_count() - n0
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        x_int.copy_(x_host, non_blocking=True)
+        step()
+        r_host.copy_(r, non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    sampler.off()
+    sampler.stop()
+    te = torch.tensor([e2.elapsed_time(e3) / 1e3, 8.0 * op.n], device="cuda")
+    dist.all_reduce(te[0:1], op=dist.ReduceOp.MAX)
+    dist.all_reduce(te[1:2], op=dist.ReduceOp.SUM)
+    T, K_max = float(t[0]), float(t[1])
+    n_loc_e = hi - lo
+    bytes_rank = B.residual_bytes(op.n, n_loc_e)
     if rank == 0:
-        T = float(t)
-        line = {"metric": "element matvec GDoF/s & HBM GB/s (fraction of peak); PCG iterations/sec",
-                "value": m.n_nodes * args.steps / T / 1e9, "unit": "GDoF/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": T / args.steps * 1e3,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic (seeded BASELINE C2 recipe)",
-                "config": {"workload": "C2 residual, element slabs + NCCL halo exchange",
-                           "n_nodes": m.n_nodes, "n_elements": m.n_elements,
+        peak = float(peaks["hbm_gbs"])
+        line = {"metric": B.METRIC, "value": m.n_nodes * args.steps / T / 1e9, "unit": "GDoF/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 mesh)",
+                "config": {"workload": "C2: 2D P1 unit square, level 11, permuted; element "
+                                       "residual r=b-Ax per step, element slabs + NCCL halo",
+                           "n_nodes": m.n_nodes, "n_elements": m.n_elements, "seed": args.seed,
+                           "mode": "fast (pre-assembled b), internal numbering per rank",
+                           "l2": "inputs larger than L2 per rank at N<=8 (~1/N GB slot stream)",
                            "parallelism": f"element slabs x{world}"},
-                "gpu_launches": launches}
+                "roofline": {"bound": "hbm", "achieved": bytes_rank / K_max / 1e9, "peak": peak,
+                             "unit": "GB/s", "frac": bytes_rank / K_max / 1e9 / peak,
+                             "traffic": None, "kernel": "k_sell_op<3,1,0> (rank 0 slab)",
+                             "bytes_per_launch": bytes_rank, "kernel_ms": K_max * 1e3,
+                             "peak_source": peak_kind},
+                "e2e": {"value": m.n_nodes * args.steps / float(te[0]) / 1e9, "unit": "GDoF/s",
+                        "h2d_bytes_per_step": int(te[1]), "d2h_bytes_per_step": int(te[1]),
+                        "api": "dist.residual step per rank with its x/r slab via pinned host"},
+                "gpu_launches": launches, "clocks": sampler.summary(), "cpu_baseline": None}
         print(json.dumps(line), flush=True)
+    dist.barrier()
     dist.destroy_process_group()
