@@ -1,0 +1,123 @@
+"""Parity at the full BASELINE sizes through size-independent properties (the CPU oracle
+cannot run these sizes in seconds):
+
+* C2 (8.4M triangles): relabelling invariance -- the residual on the permuted mesh is the
+  permuted residual of the unpermuted mesh, BIT FOR BIT (the reference's (j, e) summation
+  order does not depend on node labels); linearity r(x)+r(y)-r(x+y) = b; symmetry
+  x.Ay = y.Ax; run-to-run determinism.
+* C3 (12.6M tets): Jacobi-PCG to 1e-8 with the recursive residual matching the true one.
+* C4 (33.5M triangles, jittered + permuted, nu=10, sin*sin): 200 damped-Jacobi iterations
+  single-GPU vs 2 emulated element slabs.
+* C5 (100.7M tets): residual(0) == assembled b bitwise; 50 PCG iterations consistent."""
+
+import gc
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import to_np
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _free():
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def test_c2_relabelling_invariance_bitwise(gpu):
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(2, seed=0)
+    perm = torch.from_numpy(p["perm"]).cuda()
+    x_perm = torch.from_numpy(p["x"]).cuda()            # caller (permuted) numbering
+    m0 = eb.build_unit_square_mesh(11)
+    b0 = eb.build_element_batch(m0, nu=1.0)
+    x0 = x_perm[perm]                                    # same field, original numbering
+    for det in (True, False):
+        r = eb.residual(p["batch"], x_perm, deterministic=det)
+        r0 = eb.residual(b0, x0, deterministic=det)
+        assert torch.equal(r[perm], r0), f"deterministic={det}"
+        assert torch.equal(r, eb.residual(p["batch"], x_perm, deterministic=det))
+    del b0, m0
+    _free()
+
+
+def test_c2_linearity_and_symmetry(gpu):
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(2, seed=1)
+    batch = p["batch"]
+    n = p["mesh"].n_nodes
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    y = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    b = eb.assemble_rhs(batch.b_e, batch.index)
+    rx, ry, rxy = (eb.residual(batch, v) for v in (x, y, x + y))
+    scale = float(torch.maximum(rx.abs().max(), ry.abs().max()))
+    assert float((rx + ry - rxy - b).abs().max()) <= 1e-12 * scale
+    ax, ay = eb.matvec(batch, x), eb.matvec(batch, y)
+    assert abs(float(x @ ay) - float(y @ ax)) <= 1e-12 * abs(float(x @ ay))
+    del batch, p
+    _free()
+
+
+def test_c3_pcg_full_size(gpu):
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(3)
+    batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+    x, h = eb.pcg(batch, d, torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda"), 20000,
+                  tol=1e-8)
+    assert not h.diverged and h.residual_norms[-1] <= 1e-8 * h.residual_norms[0]
+    assert 300 < h.iterations < 2000
+    r_true = eb.mask_dirichlet(eb.residual(batch, x, deterministic=False), d)
+    rel_true = float(torch.linalg.vector_norm(r_true)) / h.residual_norms[0]
+    assert rel_true <= 2e-8, rel_true
+    assert bool((x[d.nd] == 0).all())
+    del batch, p, x
+    _free()
+
+
+def test_c4_jacobi_full_size_vs_two_slabs(gpu):
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(4, seed=0)
+    batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+    x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+    x1, h1 = eb.jacobi(batch, d, x0, 200, omega=0.8)
+    assert len(h1.residual_norms) == 201 and not h1.diverged
+    # damped Jacobi is a smoother: at 16.8M unknowns 200 sweeps barely move the 2-norm
+    assert h1.residual_norms.max() <= 1.01 * h1.residual_norms[0]
+    prob, _ = dist.emulate(batch, m.n_nodes, d, 2)
+    xs, norms = dist.jacobi(prob, [op.to_internal(x0) for op in prob.ops], 200, 0.8)
+    np.testing.assert_allclose(norms, h1.residual_norms, rtol=1e-10)
+    xg = dist.gather_global(prob.ops, xs, m.n_nodes)
+    assert float(torch.linalg.vector_norm(xg - x1)) <= 1e-10 * float(torch.linalg.vector_norm(x1))
+    del prob, xs, batch, p
+    _free()
+
+
+def test_c5_full_size(gpu):
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(5)
+    batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+    assert m.n_elements == 100_663_296 and m.n_nodes == 16_974_593
+    pl = batch.operator(m.n_nodes)
+    assert pl.info()["max_valence"] == 24 and pl.info()["loaded"] & 4  # delta-packed ids
+    b = eb.assemble_rhs(batch.b_e, batch.index)
+    zero = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+    assert torch.equal(eb.residual(batch, zero), b)
+    assert abs(float(b.sum()) - 1.0) <= 1e-10
+    x, h = eb.pcg(batch, d, zero, 50)
+    assert len(h.residual_norms) == 51 and not h.diverged
+    assert np.all(np.isfinite(h.residual_norms))
+    r_true = eb.mask_dirichlet(eb.residual(batch, x, deterministic=False), d)
+    # recursive (CG) residual == true residual to rounding (no drift after 50 steps)
+    assert abs(float(torch.linalg.vector_norm(r_true)) - h.residual_norms[-1]) <= \
+        1e-9 * h.residual_norms[-1]
+    del batch, p, x, b
+    _free()
