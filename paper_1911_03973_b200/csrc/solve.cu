@@ -204,7 +204,7 @@ __global__ void EBS_SELL_BOUNDS(NB)
     ctl->alpha = tot[0] != 0.0 ? ctl->rz / tot[0] : 0.0;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     k_pcg_update(int64_t n, LoopArgs L, double *__restrict__ x, double *__restrict__ r,
                  const double *__restrict__ p, const double *__restrict__ q,
                  const double *__restrict__ dinv, const double *__restrict__ ref) {
@@ -213,18 +213,38 @@ __global__ void __launch_bounds__(256)
     const double alpha = ctl->alpha;
     double part[3] = {0.0, 0.0, 0.0};
     bool bad = false;
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
-         m += (int64_t)gridDim.x * blockDim.x) {
-        double xn = x[m] + alpha * p[m];
-        double rn = r[m] - alpha * q[m];
-        x[m] = xn;
-        r[m] = rn;
-        bad |= !isfinite(xn);
-        part[0] += rn * rn;
-        part[1] += rn * (dinv[m] * rn);
-        if (ref) {
-            double d = xn - ref[m];
-            part[2] += d * d;
+    constexpr int ILP = 4;  // independent node updates in flight per thread
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+         base += stride * ILP) {
+        double xv[ILP], rv[ILP], pv[ILP], qv[ILP], dv[ILP], fv[ILP];
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+            const int64_t m = base + u * stride;
+            const bool ok = m < n;
+            xv[u] = ok ? x[m] : 0.0;
+            rv[u] = ok ? r[m] : 0.0;
+            pv[u] = ok ? p[m] : 0.0;
+            qv[u] = ok ? q[m] : 0.0;
+            dv[u] = ok ? dinv[m] : 0.0;
+            fv[u] = (ok && ref) ? ref[m] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+            const int64_t m = base + u * stride;
+            if (m < n) {
+                double xn = xv[u] + alpha * pv[u];
+                double rn = rv[u] - alpha * qv[u];
+                x[m] = xn;
+                r[m] = rn;
+                bad |= !isfinite(xn);
+                part[0] += rn * rn;
+                part[1] += rn * (dv[u] * rn);
+                if (ref) {
+                    double d = xn - fv[u];
+                    part[2] += d * d;
+                }
+            }
         }
     }
     flag_nonfinite(ctl, bad);
@@ -264,9 +284,25 @@ __global__ void __launch_bounds__(256)
                     const double *__restrict__ dinv) {
     if (ctl->done) return;
     const double beta = ctl->beta;
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
-         m += (int64_t)gridDim.x * blockDim.x)
-        p[m] = dinv[m] * r[m] + beta * p[m];
+    constexpr int ILP = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+         base += stride * ILP) {
+        double rv[ILP], pv[ILP], dv[ILP];
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+            const int64_t m = base + u * stride;
+            const bool ok = m < n;
+            rv[u] = ok ? r[m] : 0.0;
+            pv[u] = ok ? p[m] : 0.0;
+            dv[u] = ok ? dinv[m] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+            const int64_t m = base + u * stride;
+            if (m < n) p[m] = dv[u] * rv[u] + beta * pv[u];
+        }
+    }
 }
 
 // dinv = 1/diag on free nodes (Jacobi, PCG), 1 on free nodes (CG), 0 on constrained ones
