@@ -404,7 +404,8 @@ def main():
     ap.add_argument("--size", type=int, default=None, help="override the C2 level")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
-    ap.add_argument("--extra", action="store_true", help="also time C3/C4/C5 solvers")
+    ap.add_argument("--extra", action=argparse.BooleanOptionalAction, default=True,
+                    help="also time the C3/C4/C5 solvers (default on; --no-extra to skip)")
     ap.add_argument("--solver-configs", type=int, nargs="*", default=[3, 4, 5])
     args = ap.parse_args()
     if args.warmup < 3:
