@@ -403,9 +403,11 @@ def jacobi(A_e, b_e, indt, nd, x0, omega, iters, **kw):
 
 
 def _dinv(A_e, indt, n, nd):
+    """1/diag(A) on free nodes; 0 on nd and on nodes no element touches (diag == 0)."""
     d = diagonal(A_e, indt, n)
     free = np.ones(n, dtype=bool)
     free[nd] = False
+    free &= d != 0.0
     out = np.zeros(n)
     out[free] = 1.0 / d[free]
     return out

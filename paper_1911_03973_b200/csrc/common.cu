@@ -1,6 +1,7 @@
 // common.cu -- error reporting, launch counter and small vector kernels of libebs.so.
 #include <atomic>
 #include <cstdarg>
+#include <mutex>
 
 #include "ebs_internal.cuh"
 
@@ -79,6 +80,8 @@ int persistent_grid(const void *kernel, int block, int64_t work_blocks, size_t s
     struct Ent { const void *k; int dev; int block; size_t smem; int grid; };
     static Ent cache[64];
     static int n_cache = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     int dev = 0;
     CU(cudaGetDevice(&dev));
     int grid = -1;

@@ -123,12 +123,12 @@ __global__ void __launch_bounds__(256)
     if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
 }
 
-// dinv = free ? (diag ? 1/diag : 1) : 0
+// dinv = free ? (diag ? (diag != 0 ? 1/diag : 0) : 1) : 0
 __global__ void k_vec_dinv(int64_t n, const double *__restrict__ diag,
                            const uint8_t *__restrict__ free_m, double *__restrict__ dinv) {
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
          m += (int64_t)gridDim.x * blockDim.x)
-        dinv[m] = free_m[m] ? (diag ? 1.0 / diag[m] : 1.0) : 0.0;
+        dinv[m] = free_m[m] ? (diag ? (diag[m] != 0.0 ? 1.0 / diag[m] : 0.0) : 1.0) : 0.0;
 }
 
 struct Scratch {

@@ -557,12 +557,14 @@ int ebs_plan_node_maps(ebs_plan_t plan, int32_t *new_of_old, int32_t *old_of_new
 
 int ebs_plan_load(ebs_plan_t plan, const double *A_e, const double *b_e, void *stream) {
     EBS_TRY
-    EBS_REQUIRE(plan && A_e, "null plan or A_e");
+    EBS_REQUIRE(plan, "null plan");
     Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(A_e || p->n_e == 0, "null A_e");
     cudaStream_t s = S(stream);
     const int64_t n_slots = p->n_rows * LANES;
-    if (b_e && !p->slot_be) p->slot_be = dmalloc<double>(n_slots);
-    if (b_e && !p->b_int) p->b_int = dmalloc<double>(p->n_n);
+    const bool want_be = b_e != nullptr || p->n_e == 0;  // an empty mesh has an (empty) b_e
+    if (want_be && !p->slot_be) p->slot_be = dmalloc<double>(n_slots);
+    if (want_be && !p->b_int) p->b_int = dmalloc<double>(p->n_n);
     if (n_slots) {
         k_pack<<<grid_for(n_slots, 256, 148 * 64), 256, 0, s>>>(
             p->nb, p->n_e, n_slots, p->rowb, p->slot_ej, A_e, b_e, p->slot,
@@ -570,8 +572,8 @@ int ebs_plan_load(ebs_plan_t plan, const double *A_e, const double *b_e, void *s
         LAUNCHED();
     }
     p->has_A = 1;
-    p->has_be = b_e ? 1 : 0;
-    if (b_e && p->n_n) {
+    p->has_be = want_be ? 1 : 0;
+    if (want_be && p->n_n) {
         k_slot_sum<<<grid_for(p->n_chunks * LANES, 256), 256, 0, s>>>(
             p->nb, p->n_n, p->n_e, p->rowbase, p->width, p->cnt, p->slot_ej, p->slot, p->rowb,
             p->slot_be, nullptr, 2, nullptr, p->b_int);

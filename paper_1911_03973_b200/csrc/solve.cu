@@ -305,12 +305,13 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// dinv = 1/diag on free nodes (Jacobi, PCG), 1 on free nodes (CG), 0 on constrained ones
+// dinv = 1/diag on free nodes (Jacobi, PCG), 1 on free nodes (CG), 0 on constrained
+// nodes and on nodes no element touches (diag == 0: no equation, the iterate stays put)
 __global__ void k_dinv(int64_t n, const double *__restrict__ diag,
                        const uint8_t *__restrict__ free_int, double *__restrict__ dinv) {
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
          m += (int64_t)gridDim.x * blockDim.x)
-        dinv[m] = free_int[m] ? (diag ? 1.0 / diag[m] : 1.0) : 0.0;
+        dinv[m] = free_int[m] ? (diag ? (diag[m] != 0.0 ? 1.0 / diag[m] : 0.0) : 1.0) : 0.0;
 }
 
 // ordered per-node sums over slots (plan.cu); what = 1: diag(A)

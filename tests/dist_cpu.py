@@ -73,6 +73,8 @@ class CpuRankOperator:
 
     def vec_dinv(self, diag):
         f = self.free.bool()
+        if diag is not None:
+            f = f & (diag != 0)
         d = torch.zeros(self.n, dtype=torch.float64)
         d[f] = 1.0 / diag[f] if diag is not None else 1.0
         return d
