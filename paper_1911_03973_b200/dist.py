@@ -466,6 +466,66 @@ def bench_rank(args, rank, world, local_rank):
                         "h2d_bytes_per_step": int(te[1]), "d2h_bytes_per_step": int(te[1]),
                         "api": "dist.residual step per rank with its x/r slab via pinned host"},
                 "gpu_launches": launches, "clocks": sampler.summary(), "cpu_baseline": None}
+    del op, prob, batch, p, x_int, s, r
+    torch.cuda.empty_cache()
+    solvers = {}
+    if getattr(args, "extra", False):
+        solvers = _bench_solvers(args, rank, world)
+    if rank == 0:
+        if solvers:
+            line["solvers"] = solvers
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _bench_solvers(args, rank, world):
+    """C4 damped Jacobi x200 and C5 Jacobi-PCG x500 on `world` element slabs (strong
+    scaling; device time, max over ranks).  Errors are reported, never raised."""
+    import gc
+    import torch.distributed as dist
+    from .inputs import config_problem
+    peaks = __import__("bench").load_peaks()[0]
+    out = {}
+    for cfg, iters in ((4, 200), (5, 500)):
+        if cfg not in getattr(args, "solver_configs", (4, 5)):
+            continue
+        try:
+            p = config_problem(cfg, seed=args.seed)
+            batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+            maps = partition_maps(batch.index.indt, m.n_nodes, world)
+            op = GpuRankOperator(batch, m.n_nodes, d, maps, rank)
+            del p, batch
+            gc.collect()
+            torch.cuda.empty_cache()
+            comm = TorchTransport()
+            prob = setup([op], comm)
+            x0 = op.zeros()
+            run = (lambda: jacobi(prob, [x0], iters, 0.8)) if cfg == 4 else \
+                (lambda: pcg(prob, [x0], iters))
+            run()  # warm-up (creates the NCCL P2P communicators)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, norms = run()
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / 1e3], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            T = float(t)
+            nb = m.n_b
+            per_it = m.n_elements * (8 * nb * nb + 4 * nb) + (32 if cfg == 4 else 104) * m.n_nodes
+            out[f"C{cfg}"] = {"method": "jacobi" if cfg == 4 else "pcg", "iterations": iters,
+                              "ranks": world, "it_per_s": iters / T, "ms_per_it": T / iters * 1e3,
+                              "hbm_gbs_algorithmic_total": per_it * iters / T / 1e9,
+                              "frac_of_peak_per_gpu": per_it * iters / T / 1e9 / world /
+                              float(peaks["hbm_gbs"]),
+                              "final_norm": float(norms[-1]), "n_nodes": m.n_nodes,
+                              "n_elements": m.n_elements}
+            del op, prob
+        except Exception as e:  # noqa: BLE001
+            out[f"C{cfg}"] = {"error": f"{type(e).__name__}: {e}"}
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
