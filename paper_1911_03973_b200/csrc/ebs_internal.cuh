@@ -118,7 +118,9 @@ struct Plan {
     // slot blob: per row NB planes of 32 doubles (A rows) + the id plane (sell.cuh)
     uint8_t *slot = nullptr;
     int rowb = 0;                   // bytes per slot row
-    int packed = 0;                 // 1: delta-packed ids, 0: absolute int32 ids
+    int packed = 0;                 // id layout: 0 absolute, 1 packed deltas, 2 per-chunk table
+    int32_t *tab = nullptr;         // per-chunk delta tables (layout 2)
+    int32_t *taboff = nullptr;      // n_chunks + 1
     // loaded operator
     double *slot_be = nullptr;  // [row][lane]: b_e[j, e] (exact residual)
     double *b_int = nullptr;    // pre-assembled b, internal numbering

@@ -46,15 +46,15 @@ struct OpEpi {
     }
 };
 
-template <int NB, bool PACKED, int MODE>
+template <int NB, int IDS, int MODE>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_sell_op(SellView v, const double *__restrict__ x, OpEpi epi) {
-    sell_sweep<NB, PACKED, MODE == 2>(v, x, epi);
+    sell_sweep<NB, IDS, MODE == 2>(v, x, epi);
 }
 
-template <int NB, bool PACKED, int MODE>
+template <int NB, int IDS, int MODE>
 void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cudaStream_t s) {
-    auto kern = k_sell_op<NB, PACKED, MODE>;
+    auto kern = k_sell_op<NB, IDS, MODE>;
     const SellLaunch SL = sell_launch((const void *)kern, NB, p->rowb, p->n_chunks);
     kern<<<SL.grid, SL.block, SL.smem, s>>>(sell_view(p), x_int, epi);
     LAUNCHED();
@@ -65,13 +65,9 @@ void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
                     const int32_t *old_of_new, double *out, cudaStream_t s) {
     if (p->n_n == 0) return;
     OpEpi epi{MODE, p->b_int, free_int, old_of_new, out};
-    if (p->nb == 3) {
-        if (p->packed) launch_sell_op_t<3, true, MODE>(p, x_int, epi, s);
-        else launch_sell_op_t<3, false, MODE>(p, x_int, epi, s);
-    } else {
-        if (p->packed) launch_sell_op_t<4, true, MODE>(p, x_int, epi, s);
-        else launch_sell_op_t<4, false, MODE>(p, x_int, epi, s);
-    }
+#define EBS_OP(NB_, IDS_) { launch_sell_op_t<NB_, IDS_, MODE>(p, x_int, epi, s); }
+    EBS_SELL_DISPATCH(p, EBS_OP);
+#undef EBS_OP
 }
 
 // scatter orientation: coalesced read of x in caller order, 8 B writes into the

@@ -16,6 +16,10 @@
 
 #include "ebs_internal.cuh"
 
+#ifndef EBS_IDS_TABLE
+#define EBS_IDS_TABLE 0  // per-chunk delta-table id layout (opt-in: measured slower, profiles/README.md)
+#endif
+
 namespace ebs {
 
 // ------------------------------------------------------------- build kernels --
@@ -153,6 +157,96 @@ __global__ void k_fill_slots(int nb, int64_t n_n, int64_t n_e, const int32_t *__
         }
     }
     if (md) atomicMax(max_delta, md);
+}
+
+// Per-chunk delta tables (id layout 2): every distinct (neighbour - node) delta of a
+// chunk's slots, sorted ascending; slots store 7-bit (2D) / 8-bit (3D) indices into it.
+// Warp per chunk, open-addressing hash in shared memory; pass 1 counts, pass 2 (with
+// the scanned offsets) writes the table and the id plane.  Deterministic: the table is
+// the sorted set, independent of the insertion order.
+constexpr int TAB_HASH = 1024;
+constexpr int32_t TAB_EMPTY = (int32_t)0x80000000;
+
+__device__ __forceinline__ int tab_hash(int32_t d) {
+    return (int)(((uint32_t)d * 2654435761u) >> 22) & (TAB_HASH - 1);
+}
+
+__global__ void __launch_bounds__(128)
+    k_chunk_tables(int nb, int64_t n_n, int64_t n_chunks, int cap, const int32_t *__restrict__ rowbase,
+                   const int32_t *__restrict__ width, const int32_t *__restrict__ cnt,
+                   const int32_t *__restrict__ ids_abs, int32_t *__restrict__ counts,
+                   const int32_t *__restrict__ taboff, int32_t *__restrict__ tab,
+                   uint8_t *__restrict__ slot, int rowb, int32_t *overflow) {
+    __shared__ int32_t hkey[4][TAB_HASH];
+    __shared__ int16_t hrank[4][TAB_HASH];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t *key = hkey[w];
+    int16_t *rnk = hrank[w];
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < n_chunks; c += nwarps) {
+        for (int h = lane; h < TAB_HASH; h += 32) key[h] = TAB_EMPTY;
+        __syncwarp();
+        const int64_t m = c * 32 + lane;
+        const int c_m = m < n_n ? cnt[m] : 0;
+        const int wd = width[c];
+        const int64_t row0 = rowbase[c];
+        for (int k = 0; k < c_m; ++k)
+            for (int t = 0; t < nb - 1; ++t) {
+                const int32_t d = (ids_abs[((row0 + k) * (nb - 1) + t) * 32 + lane] & ID_MASK) - (int32_t)m;
+                int h = tab_hash(d);
+                while (true) {
+                    int32_t old = atomicCAS(&key[h], TAB_EMPTY, d);
+                    if (old == TAB_EMPTY || old == d) break;
+                    h = (h + 1) & (TAB_HASH - 1);
+                }
+            }
+        __syncwarp();
+        int K = 0;
+        for (int h = lane; h < TAB_HASH; h += 32) K += key[h] != TAB_EMPTY;
+        for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
+        if (K > cap) {
+            if (lane == 0) atomicOr(overflow, 1);
+            continue;
+        }
+        if (!taboff) {
+            if (lane == 0) counts[c] = K;
+            continue;
+        }
+        // rank = number of smaller keys (sorted, deterministic)
+        for (int h = lane; h < TAB_HASH; h += 32) {
+            const int32_t v = key[h];
+            if (v == TAB_EMPTY) continue;
+            int r = 0;
+            for (int g = 0; g < TAB_HASH; ++g) {
+                const int32_t u = key[g];
+                r += (u != TAB_EMPTY) & (u < v);
+            }
+            rnk[h] = (int16_t)r;
+            tab[taboff[c] + r] = v;
+        }
+        __syncwarp();
+        for (int k = 0; k < wd; ++k) {
+            const int64_t row = row0 + k;
+            uint32_t word = 0;
+            if (k < c_m) {
+                const int32_t id0 = ids_abs[(row * (nb - 1)) * 32 + lane];
+                const uint32_t j = (uint32_t)id0 >> J_SHIFT;
+                word = nb == 3 ? (j << 14) : (j << 30);
+                for (int t = 0; t < nb - 1; ++t) {
+                    const int32_t d = (ids_abs[(row * (nb - 1) + t) * 32 + lane] & ID_MASK) - (int32_t)m;
+                    int h = tab_hash(d);
+                    while (key[h] != d) h = (h + 1) & (TAB_HASH - 1);
+                    const uint32_t r = (uint32_t)rnk[h];
+                    word |= nb == 3 ? (r << (7 * (1 - t))) : (r << (8 * (2 - t)));
+                }
+            }
+            uint8_t *dst = slot + row * rowb + nb * 256;
+            if (nb == 3) reinterpret_cast<uint16_t *>(dst)[lane] = (uint16_t)word;
+            else reinterpret_cast<uint32_t *>(dst)[lane] = word;
+        }
+        __syncwarp();
+    }
 }
 
 // id plane of every slot row (sell.cuh layout): delta-packed or absolute
@@ -331,7 +425,7 @@ double *plan_vec(Plan *p, int i) {
 
 static void plan_free(Plan *p) {
     dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->rowbase);
-    dfree(p->width); dfree(p->slot_ej); dfree(p->slot);
+    dfree(p->width); dfree(p->slot_ej); dfree(p->slot); dfree(p->tab); dfree(p->taboff);
     dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
     dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag);
     for (auto &v : p->wvec) dfree(v);
@@ -366,6 +460,7 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     p->n_n = n_n;
     p->n_e = n_e;
     p->n_chunks = (n_n + LANES - 1) / LANES;
+    p->flag = dmalloc<int32_t>(4);
     const int64_t total = (int64_t)nb * n_e;
 
     // 1. valence + first appearance
@@ -451,18 +546,48 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
         }
         unsigned long long max_delta = read1(md, s);
         cudaFree(md);
-        // packed deltas: 2 x 15 bit (2D) / 3 x 20 bit (3D), biased; else absolute ids
+        // id layout: per-chunk delta tables when every chunk has few distinct deltas,
+        // else packed deltas (2 x 15 bit 2D / 3 x 20 bit 3D, biased), else absolute ids
+        const int cap = nb == 3 ? 128 : 256;
+        int layout = -1;
+        int32_t *counts = nullptr;
+        if (EBS_IDS_TABLE && p->n_chunks) {
+            counts = dmalloc<int32_t>(p->n_chunks);
+            CU(cudaMemsetAsync(p->flag, 0, sizeof(int32_t), s));
+            k_chunk_tables<<<grid_for(p->n_chunks * 32, 128, 148 * 16), 128, 0, s>>>(
+                nb, n_n, p->n_chunks, cap, p->rowbase, p->width, p->cnt, ids_abs, counts, nullptr,
+                nullptr, nullptr, 0, p->flag);
+            LAUNCHED();
+            if (read1(p->flag, s) == 0) layout = 2;
+        }
         const unsigned long long limit = nb == 3 ? (1ull << 14) - 1 : (1ull << 19) - 1;
-        p->packed = max_delta <= limit ? 1 : 0;
-        const int id_bytes = p->packed ? (nb == 3 ? 4 : 8) * LANES : 4 * (nb - 1) * LANES;
+        if (layout < 0) layout = max_delta <= limit ? 1 : 0;
+        p->packed = layout;
+        const int id_bytes = layout == 2 ? (nb == 3 ? 2 : 4) * LANES
+                                         : (layout == 1 ? (nb == 3 ? 4 : 8) * LANES
+                                                        : 4 * (nb - 1) * LANES);
         p->rowb = nb * 8 * LANES + id_bytes;
         p->slot = dmalloc<uint8_t>((size_t)p->n_rows * p->rowb);
         CU(cudaMemsetAsync(p->slot, 0, (size_t)p->n_rows * p->rowb, s));
-        if (p->n_chunks) {
+        p->taboff = dmalloc<int32_t>(p->n_chunks + 1);
+        CU(cudaMemsetAsync(p->taboff, 0, sizeof(int32_t) * (p->n_chunks + 1), s));
+        if (layout == 2) {
+            const int32_t ntab = (int32_t)scan_i32(counts, p->taboff, p->n_chunks, s);
+            CU(cudaMemcpyAsync(p->taboff + p->n_chunks, &ntab, sizeof(int32_t),
+                               cudaMemcpyHostToDevice, s));
+            CU(cudaStreamSynchronize(s));
+            p->tab = dmalloc<int32_t>(ntab);
+            k_chunk_tables<<<grid_for(p->n_chunks * 32, 128, 148 * 16), 128, 0, s>>>(
+                nb, n_n, p->n_chunks, cap, p->rowbase, p->width, p->cnt, ids_abs, nullptr,
+                p->taboff, p->tab, p->slot, p->rowb, p->flag);
+            LAUNCHED();
+        } else if (p->n_chunks) {
+            p->tab = dmalloc<int32_t>(1);
             k_write_ids<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
                 nb, n_n, p->n_chunks, p->rowb, p->packed, p->rowbase, p->width, ids_abs, p->slot);
             LAUNCHED();
         }
+        if (counts) cudaFree(counts);
         CU(cudaStreamSynchronize(s));
         cudaFree(ids_abs);
     }
@@ -492,7 +617,6 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
     CU(cudaMallocHost(&p->ctl_host, sizeof(Ctl)));
     p->partials = dmalloc<double>(4 * 8192);
-    p->flag = dmalloc<int32_t>(4);
     p->free_int = dmalloc<uint8_t>(n_n);
     if (n_n) {
         k_set_free<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, p->free_int);
@@ -536,7 +660,7 @@ int ebs_plan_info(ebs_plan_t plan, int64_t *info) {
     int64_t slots = p->n_rows * LANES;
     info[5] = p->n_rows * (int64_t)p->rowb + (p->has_be ? slots * 8 : 0);
     info[6] = p->max_valence;
-    info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0) | (p->packed ? 4 : 0);
+    info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0) | (p->packed ? 4 : 0) | (p->packed == 2 ? 8 : 0);
     EBS_CATCH
 }
 

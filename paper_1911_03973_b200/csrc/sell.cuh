@@ -31,11 +31,41 @@ struct SellView {
     const int32_t *__restrict__ cnt;
     const uint8_t *__restrict__ slot;
     const double *__restrict__ be;
+    const int32_t *__restrict__ tab;     // per-chunk offset tables (IDS_TABLE)
+    const int32_t *__restrict__ taboff;  // n_chunks + 1 offsets into tab
 };
 
 inline SellView sell_view(const Plan *p) {
     return SellView{p->n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, p->slot,
-                    p->slot_be};
+                    p->slot_be, p->tab, p->taboff};
+}
+
+// id-plane layouts (Plan::packed)
+constexpr int IDS_ABS = 0;    // NB-1 planes of int32 absolute ids, j in the top bits of plane 0
+constexpr int IDS_DELTA = 1;  // deltas to the node packed in 32 (2D) / 64 (3D) bits
+constexpr int IDS_TABLE = 2;  // indices into a per-chunk table of deltas: 16 (2D) / 32 (3D) bits
+
+template <int NB>
+struct Tab;
+template <>
+struct Tab<3> {  // uint16: j (2 bits) | i0 (7) | i1 (7)
+    using W = uint16_t;
+    static constexpr int CAP = 128;
+    __device__ __forceinline__ static int j(W w) { return (int)(w >> 14); }
+    __device__ __forceinline__ static int idx(W w, int t) { return (w >> (7 * (1 - t))) & 127; }
+};
+template <>
+struct Tab<4> {  // uint32: j (2 bits) | 6 spare | i0 (8) | i1 (8) | i2 (8)
+    using W = uint32_t;
+    static constexpr int CAP = 256;
+    __device__ __forceinline__ static int j(W w) { return (int)(w >> 30); }
+    __device__ __forceinline__ static int idx(W w, int t) { return (w >> (8 * (2 - t))) & 255; }
+};
+
+template <int NB, int IDS>
+constexpr int id_plane_bytes() {
+    return IDS == IDS_ABS ? 4 * (NB - 1) * 32
+                          : (IDS == IDS_DELTA ? (NB == 3 ? 4 : 8) * 32 : (NB == 3 ? 2 : 4) * 32);
 }
 
 // packed id plane geometry
@@ -89,10 +119,10 @@ __device__ __forceinline__ double pick(int t, double xo, const double (&g)[NB - 
 #define EBS_MINB3 6  // min resident 256-thread CTAs per SM, 3D SELL kernels
 #endif
 
-template <int NB, bool PACKED, bool EXACT>
+template <int NB, int IDS, bool EXACT>
 __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0, int w, int lane,
                                                 int64_t m, int c_m, const double *__restrict__ x,
-                                                double xo) {
+                                                double xo, const int32_t *stab) {
     constexpr int U = NB == 3 ? EBS_U2 : EBS_U3;
     double s = 0.0;
     for (int k0 = 0; k0 < w; k0 += U) {
@@ -111,7 +141,14 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
                 const double *ap = reinterpret_cast<const double *>(rp) + lane;
 #pragma unroll
                 for (int i = 0; i < NB; ++i) a[u][i] = __ldcs(ap + i * LANES);
-                if constexpr (PACKED) {
+                if constexpr (IDS == IDS_TABLE) {
+                    using W = typename Tab<NB>::W;
+                    const W wd = __ldcs(reinterpret_cast<const W *>(rp + NB * 256) + lane);
+                    jj[u] = Tab<NB>::j(wd);
+#pragma unroll
+                    for (int t = 0; t < NB - 1; ++t)
+                        nid[u][t] = (int32_t)m + stab[Tab<NB>::idx(wd, t)];
+                } else if constexpr (IDS == IDS_DELTA) {
                     using W = typename Pack<NB>::W;
                     const W wd = __ldcs(reinterpret_cast<const W *>(rp + NB * 256) + lane);
                     jj[u] = Pack<NB>::j(wd);
@@ -157,19 +194,28 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
 }
 
 // Grid-stride sweep over chunks: epi(m, s, xo) for every valid node (direct loads).
-template <int NB, bool PACKED, bool EXACT, class Epi>
+template <int NB, int IDS, bool EXACT, class Epi>
 __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *__restrict__ x,
                                                Epi &epi) {
+    constexpr int CAP = IDS == IDS_TABLE ? Tab<NB>::CAP : 1;
+    __shared__ int32_t stab_all[256 / LANES][CAP];  // 256-thread CTAs: one table per warp
     const int lane = threadIdx.x & (LANES - 1);
+    int32_t *stab = stab_all[threadIdx.x / LANES];
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / LANES;
     for (int64_t c = warp; c < v.n_chunks; c += nwarps) {
+        if constexpr (IDS == IDS_TABLE) {
+            const int t0 = v.taboff[c], t1 = v.taboff[c + 1];
+            __syncwarp();
+            for (int i = lane; i < t1 - t0; i += LANES) stab[i] = v.tab[t0 + i];
+            __syncwarp();
+        }
         const int64_t m = c * LANES + lane;
         const bool valid = m < v.n_n;
         const int c_m = valid ? v.cnt[m] : 0;
         const double xo = valid ? x[m] : 0.0;
-        const double s = sell_node_sum<NB, PACKED, EXACT>(v, v.rowbase[c], v.width[c], lane, m,
-                                                          c_m, x, xo);
+        const double s = sell_node_sum<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m,
+                                                       c_m, x, xo, stab);
         if (valid) epi(m, s, xo);
     }
 }
@@ -239,9 +285,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         : "memory");
 }
 
-template <int NB, bool PACKED, bool EXACT, class Epi>
+template <int NB, int IDS, bool EXACT, class Epi>
 __device__ __forceinline__ void sell_sweep_tma(const SellView &v, const double *__restrict__ x,
                                                Epi &epi) {
+    constexpr bool PACKED = IDS == IDS_DELTA;
     constexpr int R = TmaCfg<NB>::R, S = TmaCfg<NB>::S, W = TmaCfg<NB>::W;
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ uint64_t bars[W][S];
@@ -353,15 +400,31 @@ __device__ __forceinline__ void sell_sweep_tma(const SellView &v, const double *
 #define EBS_SELL_BOUNDS(NB) __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
 #endif
 
-template <int NB, bool PACKED, bool EXACT, class Epi>
+template <int NB, int IDS, bool EXACT, class Epi>
 __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__restrict__ x,
                                            Epi &epi) {
 #if EBS_TMA
-    sell_sweep_tma<NB, PACKED, EXACT>(v, x, epi);
-#else
-    sell_sweep_ldg<NB, PACKED, EXACT>(v, x, epi);
+    if constexpr (IDS != IDS_TABLE) {
+        sell_sweep_tma<NB, IDS, EXACT>(v, x, epi);
+        return;
+    }
 #endif
+    sell_sweep_ldg<NB, IDS, EXACT>(v, x, epi);
 }
+
+// dispatch a macro M(NB, IDS) on the plan's geometry
+#define EBS_SELL_DISPATCH(p, M)                                                          \
+    do {                                                                                 \
+        if ((p)->nb == 3) {                                                              \
+            if ((p)->packed == IDS_TABLE) M(3, IDS_TABLE)                                \
+            else if ((p)->packed == IDS_DELTA) M(3, IDS_DELTA)                           \
+            else M(3, IDS_ABS)                                                           \
+        } else {                                                                         \
+            if ((p)->packed == IDS_TABLE) M(4, IDS_TABLE)                                \
+            else if ((p)->packed == IDS_DELTA) M(4, IDS_DELTA)                           \
+            else M(4, IDS_ABS)                                                           \
+        }                                                                                \
+    } while (0)
 
 // launch configuration of a SELL kernel (threads, dynamic smem, persistent grid)
 struct SellLaunch {

@@ -84,7 +84,7 @@ struct JacobiEpi {
     }
 };
 
-template <int NB, bool PACKED, bool EXACT>
+template <int NB, int IDS, bool EXACT>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_jacobi_step(SellView v, LoopArgs L, double *__restrict__ xa, double *__restrict__ xb,
                   const double *__restrict__ b_int, const uint8_t *__restrict__ free_int,
@@ -101,7 +101,7 @@ __global__ void EBS_SELL_BOUNDS(NB)
     const double cbk = (method == EBS_CHEB3 && !final_step) ? cb[k] : 0.0;
     JacobiEpi epi{b_int, free_int, dinv, ref, r_out, (k & 1) ? xa : xb, pbuf, om, cbk, method, k,
                   EXACT ? 1 : 0, final_step, {0.0, 0.0}, false};
-    sell_sweep<NB, PACKED, EXACT>(v, x, epi);
+    sell_sweep<NB, IDS, EXACT>(v, x, epi);
     flag_nonfinite(ctl, epi.bad);
     double tot[2];
     if (!grid_sum_last<2>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
@@ -163,11 +163,11 @@ struct PcgInitEpi {
     }
 };
 
-template <int NB, bool PACKED>
+template <int NB, int IDS>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_pcg_init(SellView v, LoopArgs L, const double *__restrict__ x, PcgInitEpi epi) {
     Ctl *ctl = L.ctl;
-    sell_sweep<NB, PACKED, false>(v, x, epi);
+    sell_sweep<NB, IDS, false>(v, x, epi);
     double tot[3];
     if (!grid_sum_last<3>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
     const double nr = sqrt(tot[0]);
@@ -192,12 +192,12 @@ struct PcgMatvecEpi {
     }
 };
 
-template <int NB, bool PACKED>
+template <int NB, int IDS>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_pcg_matvec(SellView v, LoopArgs L, const double *__restrict__ p_int, PcgMatvecEpi epi) {
     Ctl *ctl = L.ctl;
     if (ctl->done) return;
-    sell_sweep<NB, PACKED, false>(v, p_int, epi);
+    sell_sweep<NB, IDS, false>(v, p_int, epi);
     double tot[1];
     if (!grid_sum_last<1>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
     ctl->pq = tot[0];
@@ -333,12 +333,12 @@ struct PowerEpi {
     }
 };
 
-template <int NB, bool PACKED>
+template <int NB, int IDS>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_power_matvec(SellView v, Ctl *ctl, double *partials, const double *__restrict__ vin,
                    PowerEpi epi, double tol) {
     if (ctl->done) return;
-    sell_sweep<NB, PACKED, false>(v, vin, epi);
+    sell_sweep<NB, IDS, false>(v, vin, epi);
     double tot[2];
     if (!grid_sum_last<2>(epi.part, partials, &ctl->counter, tot) || threadIdx.x != 0) return;
     const double lam_new = tot[0];
@@ -481,19 +481,9 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
                                                  ref_int, rcb,                              \
                                  final_step, P->method, coef_a, coef_b, pbuf);              \
     }
-            if (nb == 3) {
-                if (p->packed) {
-                    if (exact) EBS_JAC(3, true, true) else EBS_JAC(3, true, false)
-                } else {
-                    if (exact) EBS_JAC(3, false, true) else EBS_JAC(3, false, false)
-                }
-            } else {
-                if (p->packed) {
-                    if (exact) EBS_JAC(4, true, true) else EBS_JAC(4, true, false)
-                } else {
-                    if (exact) EBS_JAC(4, false, true) else EBS_JAC(4, false, false)
-                }
-            }
+#define EBS_JAC_T(NB_, IDS_) { if (exact) EBS_JAC(NB_, IDS_, true) else EBS_JAC(NB_, IDS_, false) }
+            EBS_SELL_DISPATCH(p, EBS_JAC_T);
+#undef EBS_JAC_T
 #undef EBS_JAC
             LAUNCHED();
         };
@@ -535,11 +525,7 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
         kern<<<SL.grid, SL.block, SL.smem, s>>>(v, L, xa, ie);                              \
     }
-            if (nb == 3) {
-                if (p->packed) EBS_INIT(3, true) else EBS_INIT(3, false)
-            } else {
-                if (p->packed) EBS_INIT(4, true) else EBS_INIT(4, false)
-            }
+            EBS_SELL_DISPATCH(p, EBS_INIT);
 #undef EBS_INIT
             LAUNCHED();
         }
@@ -560,11 +546,7 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
         kern<<<SL.grid, SL.block, SL.smem, s>>>(v, L, pv, me);                              \
     }
-                    if (nb == 3) {
-                        if (p->packed) EBS_MV(3, true) else EBS_MV(3, false)
-                    } else {
-                        if (p->packed) EBS_MV(4, true) else EBS_MV(4, false)
-                    }
+                    EBS_SELL_DISPATCH(p, EBS_MV);
 #undef EBS_MV
                 }
                 LAUNCHED();
@@ -641,11 +623,7 @@ int ebs_power_iteration(ebs_plan_t plan, const double *v0, int iters, double tol
         const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
         kern<<<SL.grid, SL.block, SL.smem, s>>>(sv, p->ctl, p->partials, v, epi, tol);      \
     }
-            if (p->nb == 3) {
-                if (p->packed) EBS_PW(3, true) else EBS_PW(3, false)
-            } else {
-                if (p->packed) EBS_PW(4, true) else EBS_PW(4, false)
-            }
+            EBS_SELL_DISPATCH(p, EBS_PW);
 #undef EBS_PW
             LAUNCHED();
             k_power_scale<<<grid_for(n, 256), 256, 0, s>>>(n, p->ctl, av, v);
