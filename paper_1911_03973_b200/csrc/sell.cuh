@@ -193,8 +193,73 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
     return s;
 }
 
+// Raw id word(s) of one slot and their decoding (IDS_DELTA / IDS_ABS).
+template <int NB, int IDS>
+struct IdWord {
+    using W = typename Pack<NB>::W;
+    W w;
+    int32_t a[NB - 1];
+    __device__ __forceinline__ void load(const uint8_t *rp, int lane) {
+        if constexpr (IDS == IDS_DELTA) {
+            w = __ldcs(reinterpret_cast<const W *>(rp + NB * 256) + lane);
+        } else {
+            const int32_t *ip = reinterpret_cast<const int32_t *>(rp + NB * 256) + lane;
+#pragma unroll
+            for (int t = 0; t < NB - 1; ++t) a[t] = __ldcs(ip + t * LANES);
+        }
+    }
+    __device__ __forceinline__ int decode(int64_t m, int32_t (&nid)[NB - 1]) const {
+        if constexpr (IDS == IDS_DELTA) {
+#pragma unroll
+            for (int t = 0; t < NB - 1; ++t) nid[t] = (int32_t)(m + Pack<NB>::d(w, t));
+            return Pack<NB>::j(w);
+        } else {
+#pragma unroll
+            for (int t = 0; t < NB - 1; ++t) nid[t] = a[t] & ID_MASK;
+            return (int)((uint32_t)a[0] >> J_SHIFT);
+        }
+    }
+};
+
+// One slot in flight, with the id word of slot k+1 loaded while slot k is processed, so
+// the x gathers of a slot issue at the start of its iteration (overlapping the A-row
+// loads) instead of waiting a DRAM round trip for the ids.
+template <int NB, int IDS, bool EXACT>
+__device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t row0, int w,
+                                                     int lane, int64_t m, int c_m,
+                                                     const double *__restrict__ x, double xo) {
+    double s = 0.0;
+    IdWord<NB, IDS> nxt;
+    if (0 < c_m) nxt.load(v.slot + row0 * v.rowb, lane);
+    for (int k = 0; k < w; ++k) {
+        if (k < c_m) {
+            const IdWord<NB, IDS> cur = nxt;
+            const uint8_t *rp = v.slot + (row0 + k) * v.rowb;
+            int32_t nid[NB - 1];
+            const int j = cur.decode(m, nid);
+            double g[NB - 1];
+#pragma unroll
+            for (int t = 0; t < NB - 1; ++t) g[t] = __ldg(x + nid[t]);
+            const double *ap = reinterpret_cast<const double *>(rp) + lane;
+            double a[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) a[i] = __ldcs(ap + i * LANES);
+            double be = 0.0;
+            if constexpr (EXACT) be = __ldcs(v.be + (row0 + k) * LANES + lane);
+            if (k + 1 < c_m) nxt.load(rp + v.rowb, lane);
+            double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
+#pragma unroll
+            for (int i = 1; i < NB; ++i) loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
+            if constexpr (EXACT) s = s + (be - loc);
+            else s = s + loc;
+        }
+    }
+    return s;
+}
+
+
 // Grid-stride sweep over chunks: epi(m, s, xo) for every valid node (direct loads).
-template <int NB, int IDS, bool EXACT, class Epi>
+template <int NB, int IDS, bool EXACT, bool PIPE, class Epi>
 __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *__restrict__ x,
                                                Epi &epi) {
     constexpr int CAP = IDS == IDS_TABLE ? Tab<NB>::CAP : 1;
@@ -214,8 +279,13 @@ __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *
         const bool valid = m < v.n_n;
         const int c_m = valid ? v.cnt[m] : 0;
         const double xo = valid ? x[m] : 0.0;
-        const double s = sell_node_sum<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m,
-                                                       c_m, x, xo, stab);
+        double s;
+        if constexpr (PIPE && IDS != IDS_TABLE && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
+            s = sell_node_sum_pipe<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m, c_m, x,
+                                                   xo);
+        else
+            s = sell_node_sum<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m, c_m, x, xo,
+                                              stab);
         if (valid) epi(m, s, xo);
     }
 }
@@ -400,7 +470,9 @@ __device__ __forceinline__ void sell_sweep_tma(const SellView &v, const double *
 #define EBS_SELL_BOUNDS(NB) __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
 #endif
 
-template <int NB, int IDS, bool EXACT, class Epi>
+// PIPE: load the id plane one slot ahead (sell_node_sum_pipe) -- measured faster only
+// for the 2D Jacobi step, slower for the other kernels (profiles/README.md)
+template <int NB, int IDS, bool EXACT, bool PIPE = false, class Epi>
 __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__restrict__ x,
                                            Epi &epi) {
 #if EBS_TMA
@@ -409,7 +481,7 @@ __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__re
         return;
     }
 #endif
-    sell_sweep_ldg<NB, IDS, EXACT>(v, x, epi);
+    sell_sweep_ldg<NB, IDS, EXACT, PIPE>(v, x, epi);
 }
 
 // dispatch a macro M(NB, IDS) on the plan's geometry

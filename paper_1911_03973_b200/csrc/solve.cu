@@ -101,7 +101,7 @@ __global__ void EBS_SELL_BOUNDS(NB)
     const double cbk = (method == EBS_CHEB3 && !final_step) ? cb[k] : 0.0;
     JacobiEpi epi{b_int, free_int, dinv, ref, r_out, (k & 1) ? xa : xb, pbuf, om, cbk, method, k,
                   EXACT ? 1 : 0, final_step, {0.0, 0.0}, false};
-    sell_sweep<NB, IDS, EXACT>(v, x, epi);
+    sell_sweep<NB, IDS, EXACT, NB == 3>(v, x, epi);
     flag_nonfinite(ctl, epi.bad);
     double tot[2];
     if (!grid_sum_last<2>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
