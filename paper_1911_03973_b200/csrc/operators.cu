@@ -148,11 +148,54 @@ void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s)
     LAUNCHED();
 }
 
+// out_user[n] = v_int[new_of_old[n]]: coalesced writes, random reads of an L2-resident
+// internal vector (ILP-8)
+__global__ void __launch_bounds__(256)
+    k_from_internal_ilp(int64_t n, const int32_t *__restrict__ new_of_old,
+                        const double *__restrict__ v_int, double *__restrict__ v_user) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+         base += stride * PERM_ILP) {
+        int32_t idx[PERM_ILP];
+        double v[PERM_ILP];
+#pragma unroll
+        for (int u = 0; u < PERM_ILP; ++u) {
+            const int64_t i = base + u * stride;
+            idx[u] = i < n ? __ldcs(new_of_old + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < PERM_ILP; ++u) {
+            const int64_t i = base + u * stride;
+            v[u] = i < n ? v_int[idx[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PERM_ILP; ++u) {
+            const int64_t i = base + u * stride;
+            if (i < n) v_user[i] = v[u];
+        }
+    }
+}
+
+#ifndef EBS_OUT_PERM
+#define EBS_OUT_PERM 0  // 1: SELL writes internal order, then a gather pass to caller order
+#endif
+
 void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *free_int,
                 const int32_t *old_of_new, double *out, cudaStream_t s) {
-    if (mode == 0) launch_sell_op<0>(p, x_int, free_int, old_of_new, out, s);
-    else if (mode == 1) launch_sell_op<1>(p, x_int, free_int, old_of_new, out, s);
-    else launch_sell_op<2>(p, x_int, free_int, old_of_new, out, s);
+    double *dst = out;
+    const int32_t *o2n = old_of_new;
+    if (EBS_OUT_PERM && old_of_new) {
+        dst = plan_vec(const_cast<Plan *>(p), 7);
+        o2n = nullptr;
+    }
+    if (mode == 0) launch_sell_op<0>(p, x_int, free_int, o2n, dst, s);
+    else if (mode == 1) launch_sell_op<1>(p, x_int, free_int, o2n, dst, s);
+    else launch_sell_op<2>(p, x_int, free_int, o2n, dst, s);
+    if (EBS_OUT_PERM && old_of_new && p->n_n) {
+        k_from_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
+                              s>>>(p->n_n, p->new_of_old, dst, out);
+        LAUNCHED();
+    }
 }
 
 }  // namespace ebs
