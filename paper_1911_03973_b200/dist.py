@@ -61,30 +61,47 @@ def partition_maps(indt: torch.Tensor, n_nodes: int, P: int) -> dict:
 
 # ------------------------------------------------------------------ transports --
 class TorchTransport:
-    """torch.distributed (NCCL on GPUs, gloo on CPU): one rank per process."""
+    """torch.distributed (NCCL on GPUs, gloo on CPU): one rank per process.
 
-    def __init__(self, group=None):
+    ``stage_host=True`` moves device buffers through host memory around each collective
+    (gloo with GPU ranks -- used to run several GPU rank processes on one device in tests,
+    where nothing may wait on another process's kernels)."""
+
+    def __init__(self, group=None, stage_host: bool = False):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        self.stage_host = stage_host
 
     def exchange(self, ops: list, sends: list) -> list:
         """sends[i] = {q: tensor} for local rank ops[i] (len 1 here) -> recvs {q: tensor}."""
         (op,), (snd,) = ops, sends
         p2p = []
         recvs = {}
+        dev = None
         for q in sorted(snd):
-            recvs[q] = torch.empty_like(snd[q])
-            p2p.append(self.dist.P2POp(self.dist.isend, snd[q].contiguous(), q, self.group))
+            buf = snd[q].contiguous()
+            if self.stage_host and buf.is_cuda:
+                dev = buf.device
+                buf = buf.cpu()
+            recvs[q] = torch.empty_like(buf)
+            p2p.append(self.dist.P2POp(self.dist.isend, buf, q, self.group))
             p2p.append(self.dist.P2POp(self.dist.irecv, recvs[q], q, self.group))
         if p2p:
             for w in self.dist.batch_isend_irecv(p2p):
                 w.wait()
+        if dev is not None:
+            recvs = {q: t.to(dev) for q, t in recvs.items()}
         return [recvs]
 
     def allreduce(self, tensors: list):
         (t,) = tensors
-        self.dist.all_reduce(t, group=self.group)
+        if self.stage_host and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
 
 
 class LocalTransport:

@@ -1,0 +1,74 @@
+"""Real multi-process run of the GPU rank operators: 2 processes on the one GPU of the
+box, gloo transport with the halo buffers staged through host memory (no kernel waits
+on another process).  Jacobi and PCG against the single-GPU solvers."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_1911_03973_b200 import dist as D
+    from paper_1911_03973_b200.inputs import config_problem
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        for cfg, size in ((4, 6), (3, 6)):
+            p = config_problem(cfg, seed=3, size=size)
+            batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+            maps = D.partition_maps(batch.index.indt, m.n_nodes, world)
+            op = D.GpuRankOperator(batch, m.n_nodes, d, maps, rank)
+            comm = D.TorchTransport(stage_host=True)
+            prob = D.setup([op], comm)
+            x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+            if cfg == 4:
+                xs, norms = D.jacobi(prob, [op.to_internal(x0)], 30, 0.8)
+            else:
+                xs, norms = D.pcg(prob, [op.to_internal(x0)], 500, tol=1e-8)
+            xg = D.gather_global([op], xs, m.n_nodes, comm)
+            res[cfg] = (xg.cpu().numpy(), norms)
+        if rank == 0:
+            out.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_gpu_rank_processes_match_single_gpu(gpu):
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for cfg, size in ((4, 6), (3, 6)):
+        pr = config_problem(cfg, seed=3, size=size)
+        x0 = torch.zeros(pr["mesh"].n_nodes, dtype=torch.float64, device="cuda")
+        if cfg == 4:
+            x1, h1 = eb.jacobi(pr["batch"], pr["dirichlet"], x0, 30, omega=0.8)
+            np.testing.assert_allclose(res[cfg][1], h1.residual_norms, rtol=1e-10)
+        else:
+            x1, h1 = eb.pcg(pr["batch"], pr["dirichlet"], x0, 500, tol=1e-8)
+            assert len(res[cfg][1]) == len(h1.residual_norms)
+        x1 = x1.cpu().numpy()
+        assert np.linalg.norm(res[cfg][0] - x1) <= 1e-8 * np.linalg.norm(x1)
