@@ -150,6 +150,11 @@ int ebs_mask(int64_t n, const double *v, int64_t n_d, const int64_t *nd, double 
 int ebs_to_internal(ebs_plan_t plan, const double *x, double *x_int, int32_t *nonfinite,
                     void *stream);
 int ebs_to_user(ebs_plan_t plan, const double *v_int, double *v, void *stream);
+/* SELL pass (op 0 matvec, 1 fast residual) writing out[out_map[m]] (any int32 map, e.g. a
+ * rank's internal -> global ids) and, when s_raw != NULL, the same values in internal
+ * order (an element slab's partial sums / partial residuals for the halo). */
+int ebs_plan_apply_map(ebs_plan_t plan, int op, const double *x_int, double *out,
+                       const int32_t *out_map, double *s_raw, int masked, void *stream);
 /* One SELL pass on internal vectors: op = 0 matvec, 1 fast residual, 2 exact residual;
  * out_user != 0 scatters the result to caller numbering, else writes internal order;
  * masked != 0 zeroes constrained rows. */
@@ -226,6 +231,12 @@ int ebs_scatter_add(int64_t n, const int64_t *idx, const double *buf, double *v,
 /* v[idx[i]] = value;  dst[idx[i]] = src[idx[i]]  (interface combine in rank order)    */
 int ebs_index_fill(int64_t n, const int64_t *idx, double value, double *v, void *stream);
 int ebs_index_copy(int64_t n, const int64_t *idx, const double *src, double *dst, void *stream);
+/* dst[dst_idx[i]] += src[src_idx[i]]  (neighbour partial residuals onto owned entries) */
+int ebs_index_add(int64_t n, const int64_t *src_idx, const double *src, const int64_t *dst_idx,
+                  double *dst, void *stream);
+/* dst[dst_idx[i]] = src[src_idx[i]]  (owned rank results to the caller's numbering)     */
+int ebs_index_move(int64_t n, const int64_t *src_idx, const double *src, const int64_t *dst_idx,
+                   double *dst, void *stream);
 /* Per-rank vector steps on internal-numbered vectors.  `owned` (uint8, 1 = this rank owns
  * the node) restricts every reduction to owned nodes; the host all-reduces `red`.
  * `ws` is a device workspace of ebs_vec_workspace_bytes() bytes (zero-initialised once,

@@ -95,6 +95,10 @@ SIGNATURES = {
     "ebs_scatter_add": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_index_fill": (c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p]),
     "ebs_index_copy": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_index_move": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_index_add": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_plan_apply_map": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                   c_void_p]),
     "ebs_vec_workspace_bytes": (c_size_t, []),
     "ebs_vec_jacobi": (c_int, [c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

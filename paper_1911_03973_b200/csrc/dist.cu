@@ -25,6 +25,24 @@ __global__ void k_index_copy(int64_t n, const int64_t *__restrict__ idx,
         dst[idx[i]] = src[idx[i]];
 }
 
+// dst[dst_idx[i]] = src[src_idx[i]]  (owned results back to the caller's numbering)
+__global__ void k_index_move(int64_t n, const int64_t *__restrict__ src_idx,
+                             const double *__restrict__ src, const int64_t *__restrict__ dst_idx,
+                             double *__restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[dst_idx[i]] = src[src_idx[i]];
+}
+
+// dst[dst_idx[i]] += src[src_idx[i]]  (neighbour partials onto an owned entry)
+__global__ void k_index_add(int64_t n, const int64_t *__restrict__ src_idx,
+                            const double *__restrict__ src, const int64_t *__restrict__ dst_idx,
+                            double *__restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[dst_idx[i]] += src[src_idx[i]];
+}
+
 // r = free ? b - s : 0;  x_out = x + omega*(dinv*r) (or x + omega*r);  red[0] = sum_owned r^2
 __global__ void __launch_bounds__(256)
     k_vec_jacobi(int64_t n, double omega, const double *__restrict__ b,
@@ -166,6 +184,26 @@ int ebs_index_copy(int64_t n, const int64_t *idx, const double *src, double *dst
     EBS_REQUIRE(n >= 0, "bad n");
     if (n == 0) return EBS_OK;
     k_index_copy<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, idx, src, dst);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_index_move(int64_t n, const int64_t *src_idx, const double *src, const int64_t *dst_idx,
+                   double *dst, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0, "bad n");
+    if (n == 0) return EBS_OK;
+    k_index_move<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, src_idx, src, dst_idx, dst);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_index_add(int64_t n, const int64_t *src_idx, const double *src, const int64_t *dst_idx,
+                  double *dst, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0, "bad n");
+    if (n == 0) return EBS_OK;
+    k_index_add<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, src_idx, src, dst_idx, dst);
     LAUNCHED();
     EBS_CATCH
 }

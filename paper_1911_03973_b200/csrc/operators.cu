@@ -38,9 +38,11 @@ struct OpEpi {
     const uint8_t *__restrict__ free_int;
     const int32_t *__restrict__ old_of_new;
     double *__restrict__ out;
+    double *__restrict__ s_raw;  // nullable: the node values again, internal order (halo)
     __device__ __forceinline__ void operator()(int64_t m, double s, double) {
         if (mode == 1) s = b_int[m] - s;
         if (free_int && !free_int[m]) s = 0.0;
+        if (s_raw) s_raw[m] = s;
         if (old_of_new) out[old_of_new[m]] = s;
         else out[m] = s;
     }
@@ -62,9 +64,10 @@ void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cuda
 
 template <int MODE>
 void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
-                    const int32_t *old_of_new, double *out, cudaStream_t s) {
+                    const int32_t *old_of_new, double *out, cudaStream_t s,
+                    double *s_raw = nullptr) {
     if (p->n_n == 0) return;
-    OpEpi epi{MODE, p->b_int, free_int, old_of_new, out};
+    OpEpi epi{MODE, p->b_int, free_int, old_of_new, out, s_raw};
 #define EBS_OP(NB_, IDS_) { launch_sell_op_t<NB_, IDS_, MODE>(p, x_int, epi, s); }
     EBS_SELL_DISPATCH(p, EBS_OP);
 #undef EBS_OP
@@ -262,6 +265,20 @@ int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, in
     EBS_REQUIRE(x_int != out, "x and out must not alias");
     sell_apply(p, op, x_int, masked ? p->free_int : nullptr, out_user ? p->old_of_new : nullptr,
                out, S(stream));
+    EBS_CATCH
+}
+
+int ebs_plan_apply_map(ebs_plan_t plan, int op, const double *x_int, double *out,
+                       const int32_t *out_map, double *s_raw, int masked, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && x_int && out && out_map, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(op == 0 || op == 1, "bad op %d (matvec or fast residual)", op);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(op == 0 || p->has_be, "residual needs an operator loaded with b_e");
+    const uint8_t *fm = masked ? p->free_int : nullptr;
+    if (op == 0) launch_sell_op<0>(p, x_int, fm, out_map, out, S(stream), s_raw);
+    else launch_sell_op<1>(p, x_int, fm, out_map, out, S(stream), s_raw);
     EBS_CATCH
 }
 

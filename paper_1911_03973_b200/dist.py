@@ -170,6 +170,16 @@ class GpuRankOperator:
         self.owned = (owner[self.global_of_int] == p).to(torch.uint8).contiguous()
         self.free = D.empty(n, torch.uint8)
         call("ebs_plan_free_mask", self.plan.handle, D.ptr(self.free), D.stream())
+        m_own = self.owned.bool()
+        self.owned_int = torch.nonzero(m_own).reshape(-1)
+        self.owned_glob = self.global_of_int[self.owned_int].contiguous()
+        self.global_of_int32 = self.global_of_int.to(torch.int32).contiguous()
+        # per neighbour: positions in the interface list whose node this rank owns, and
+        # their global ids (the fused caller-numbering residual corrects only those)
+        self.corr = {}
+        for q, idx in self.if_idx.items():
+            pos = torch.nonzero(m_own[idx]).reshape(-1).contiguous()
+            self.corr[q] = (pos, self.global_of_int[idx[pos]].contiguous())
         self._ws = D.zeros(int(load().ebs_vec_workspace_bytes()), torch.uint8)
         self._acc = D.zeros(n)
         self._flag = D.zeros(1, torch.int32)
@@ -179,8 +189,26 @@ class GpuRankOperator:
         return x_global.to(D.device())[self.global_of_int].contiguous()
 
     def scatter_owned(self, v_int: torch.Tensor, out_global: torch.Tensor):
-        m = self.owned.bool()
-        out_global[self.global_of_int[m]] = v_int[m]
+        call("ebs_index_move", self.owned_int.numel(), D.ptr(self.owned_int), D.ptr(v_int),
+             D.ptr(self.owned_glob), D.ptr(out_global), D.stream())
+
+    def residual_caller_partial(self, x_int, r_global, s_raw):
+        """r_global[g] = b_p - s_p, the slab's partial residual of every node (caller
+        numbering), and the same partials in internal order (s_raw) in one SELL pass."""
+        call("ebs_plan_apply_map", self.plan.handle, 1, D.ptr(x_int), D.ptr(r_global),
+             D.ptr(self.global_of_int32), D.ptr(s_raw), 0, D.stream())
+
+    def correct_owned(self, r_global, recvs: dict):
+        """Owned interface entries: add the neighbours' partial residuals."""
+        for q in sorted(recvs):
+            pos, glob = self.corr[q]
+            call("ebs_index_add", pos.numel(), D.ptr(pos), D.ptr(recvs[q]), D.ptr(glob),
+                 D.ptr(r_global), D.stream())
+
+    def gather_global(self, x_global: torch.Tensor, out_int: torch.Tensor):
+        """out_int[m] = x_global[global id of internal node m] (caller -> rank numbering)."""
+        call("ebs_gather", self.n, D.ptr(self.global_of_int), D.ptr(x_global), D.ptr(out_int),
+             D.stream())
 
     def matvec_partial(self, x: torch.Tensor, out: torch.Tensor):
         call("ebs_plan_apply", self.plan.handle, 0, D.ptr(x), D.ptr(out), 0, 0, D.stream())
@@ -274,6 +302,24 @@ def setup(ops, comm, precondition=True) -> DistProblem:
     return DistProblem(ops, comm, bs, dinv)
 
 
+def residual_caller(prob: DistProblem, x_global: torch.Tensor, r_globals: list, x_ints: list,
+                    s_raws: list):
+    """r = b - A x with x and r in the caller's (global) numbering on P ranks, fused: one
+    SELL pass per rank writes its slab's partial residual b_p - s_p straight into r
+    (caller numbering) and keeps a copy in internal order; after the halo exchange each
+    rank adds its neighbours' partial residuals on the interface nodes it owns (in
+    ascending rank order).  Owned entries of r_globals[i] are the residual (within
+    rounding of the reassociated sum)."""
+    ops, comm = prob.ops, prob.comm
+    for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
+        op.gather_global(x_global, xi)
+        op.residual_caller_partial(xi, rg, sr)
+    sends = [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()} for op, sr in zip(ops, s_raws)]
+    recvs = comm.exchange(ops, sends)
+    for op, rg, rc in zip(ops, r_globals, recvs):
+        op.correct_owned(rg, rc)
+
+
 def residual(prob: DistProblem, xs, out=None):
     """r = mask? no: b - A x (unmasked, operators.py:72) on every rank's local nodes."""
     ops, comm = prob.ops, prob.comm
@@ -284,32 +330,74 @@ def residual(prob: DistProblem, xs, out=None):
     return [b - s for b, s in zip(prob.b, ss)]
 
 
-def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: bool = False):
+GRAPH_BATCH = 8  # iterations per captured CUDA graph (even: Jacobi ping-pong buffers)
+GRAPH_STATS = {"captured": 0, "fallback": 0, "last_error": None}
+
+
+def _graph_ok(ops) -> bool:
+    return all(getattr(op, "n", 0) and torch.cuda.is_available() and
+               isinstance(getattr(op, "free", None), torch.Tensor) and op.free.is_cuda for op in ops)
+
+
+def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: bool = False,
+           graph: bool = False):
     """Damped Jacobi on P ranks (oracle/ebs_oracle.py jacobi semantics, fixed count).
 
-    Returns (xs, norms) with norms[k] = ||mask(b - A x_k)||, k = 0..iters."""
+    Returns (xs, norms) with norms[k] = ||mask(b - A x_k)||, k = 0..iters.  With
+    graph=True the iterations are replayed from a captured CUDA graph of GRAPH_BATCH
+    iterations (same kernels, same results)."""
     ops, comm = prob.ops, prob.comm
     xa = [x.clone() for x in xs0]
     xb = [op.zeros() for op in ops]
     ss = [op.zeros() for op in ops]
     red = [torch.zeros(iters + 1, dtype=torch.float64, device=x.device) for x in xa]
-    for k in range(iters + 1):
-        final = k == iters
-        for op, x, s in zip(ops, xa, ss):
-            op.matvec_partial(x, s)
+
+    def step(src, dst, final, rslot):
+        for op, x, s_ in zip(ops, src, ss):
+            op.matvec_partial(x, s_)
         halo(ops, comm, ss)
         for i, op in enumerate(ops):
-            op.vec_jacobi(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i], xa[i],
-                          None if final else xb[i], None, red[i][k:k + 1])
+            op.vec_jacobi(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i], src[i],
+                          None if final else dst[i], None, rslot[i])
+
+    B = GRAPH_BATCH
+    k = 0
+    if graph and iters >= B and _graph_ok(ops):
+        bred = [torch.zeros(B, dtype=torch.float64, device=x.device) for x in xa]
+        g = None
+        try:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for u in range(B):  # B even: xa/xb roles return to the start
+                    src, dst = (xa, xb) if u % 2 == 0 else (xb, xa)
+                    step(src, dst, False, [r_[u:u + 1] for r_ in bred])
+        except Exception as e:  # capture unsupported here: run eagerly
+            g = None
+            GRAPH_STATS["fallback"] += 1
+            GRAPH_STATS["last_error"] = f"{type(e).__name__}: {e}"
+            torch.cuda.synchronize()
+        else:
+            GRAPH_STATS["captured"] += 1
+        if g is not None:
+            while k + B <= iters:
+                g.replay()
+                for i in range(len(ops)):
+                    red[i][k:k + B].copy_(bred[i])
+                k += B
+    for kk in range(k, iters + 1):
+        final = kk == iters
+        step(xa, xb, final, [r_[kk:kk + 1] for r_ in red])
         if not final:
             xa, xb = xb, xa
     comm.allreduce(red)
     return xa, torch.sqrt(red[0]).cpu().numpy()
 
 
-def pcg(prob: DistProblem, xs0, iters: int, tol=None):
+def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False):
     """Jacobi-PCG on P ranks (oracle/ebs_oracle.py pcg; with prob from setup(..,
-    precondition=False) plain CG).  Two scalar all-reduces per iteration."""
+    precondition=False) plain CG).  Two scalar all-reduces per iteration.  graph=True
+    (fixed iteration count only) replays captured CUDA graphs of GRAPH_BATCH iterations."""
     ops, comm = prob.ops, prob.comm
     dev = xs0[0].device
     xs = [x.clone() for x in xs0]
@@ -324,6 +412,7 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None):
     hist = [torch.zeros(iters + 1, dtype=torch.float64, device=dev) for _ in ops]
     red = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in ops]
     scal = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in ops]
+    pq = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in ops]
     for i, op in enumerate(ops):
         op.vec_jacobi(0.0, prob.b[i], ss[i], None, xs[i], None, rs[i], red[i][0:1])
         op.vec_pcg_direction(zero, zero, prob.dinv[i], rs[i], ps[i])  # p = dinv r
@@ -332,19 +421,11 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None):
     for i in range(len(ops)):
         hist[i][0:1].copy_(red[i][0:1])
         scal[i][0:1].copy_(red[i][1:2])
-    n0 = None
-    k_done = iters
-    for k in range(iters):
-        if tol is not None:
-            nk = float(torch.sqrt(hist[0][k]))
-            n0 = nk if n0 is None else n0
-            if nk <= tol * n0:
-                k_done = k
-                break
-        for op, p, q in zip(ops, ps, qs):
-            op.matvec_partial(p, q)
+
+    def step(hslot):
+        for op, p_, q_ in zip(ops, ps, qs):
+            op.matvec_partial(p_, q_)
         halo(ops, comm, qs)
-        pq = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in ops]
         for i, op in enumerate(ops):
             op.vec_pcg_q(ps[i], qs[i], pq[i])
         comm.allreduce(pq)
@@ -353,9 +434,44 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None):
             op.vec_pcg_update(scal[i], prob.dinv[i], xs[i], rs[i], ps[i], qs[i], red[i])
         comm.allreduce(red)
         for i, op in enumerate(ops):
-            hist[i][k + 1:k + 2].copy_(red[i][0:1])
+            hslot[i].copy_(red[i][0:1])
             op.vec_pcg_direction(scal[i][0:1], red[i][1:2], prob.dinv[i], rs[i], ps[i])
             scal[i][0:1].copy_(red[i][1:2])
+
+    B = GRAPH_BATCH
+    k = 0
+    if graph and tol is None and iters >= B and _graph_ok(ops):
+        bh = [torch.zeros(B, dtype=torch.float64, device=dev) for _ in ops]
+        g = None
+        try:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for u in range(B):
+                    step([h[u:u + 1] for h in bh])
+        except Exception as e:
+            g = None
+            GRAPH_STATS["fallback"] += 1
+            GRAPH_STATS["last_error"] = f"{type(e).__name__}: {e}"
+            torch.cuda.synchronize()
+        else:
+            GRAPH_STATS["captured"] += 1
+        if g is not None:
+            while k + B <= iters:
+                g.replay()
+                for i in range(len(ops)):
+                    hist[i][k + 1:k + 1 + B].copy_(bh[i])
+                k += B
+    n0 = None
+    k_done = iters
+    for kk in range(k, iters):
+        if tol is not None:
+            nk = float(torch.sqrt(hist[0][kk]))
+            n0 = nk if n0 is None else n0
+            if nk <= tol * n0:
+                k_done = kk
+                break
+        step([h[kk + 1:kk + 2] for h in hist])
     n = k_done + 1
     return xs, torch.sqrt(hist[0][:n]).cpu().numpy()
 
@@ -412,32 +528,71 @@ def bench_rank(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     lo, hi = int(maps["bounds"][rank]), int(maps["bounds"][rank + 1])
 
-    def step(ev=None):  # r = b - A x on this slab's nodes: SELL partials, halo, b - s
+    r_glob = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+
+    def step(ev=None):
+        # r = b - A x in the caller's (permuted) numbering, as the 1-GPU residual: gather
+        # the slab's x, one SELL pass writing the partial residual into caller numbering
+        # (+ internal copy), NCCL halo of the partials, owned interface entries completed
+        op.gather_global(x_glob, x_int)
         if ev is not None:
             ev[0].record(stream)
-        op.matvec_partial(x_int, s)
+        op.residual_caller_partial(x_int, r_glob, s)
         if ev is not None:
             ev[1].record(stream)
-        halo([op], comm, [s])
-        op.vec_jacobi(0.0, prob.b[0], s, None, x_int, None, r, red)
+        sends = [{q: op.gather(idx, s) for q, idx in op.if_idx.items()}]
+        recvs = comm.exchange([op], sends)
+        op.correct_owned(r_glob, recvs[0])
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     sampler.on()
+    # per-kernel timing pass (eager, events around the SELL launch)
     dist.barrier()
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-    n0 = load().ebs_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
     for k in range(args.steps):
         step(evs[k])
+    torch.cuda.synchronize()
+    kern = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
+    # timed pass: CUDA-graph replay of GRAPH_BATCH steps (eager fallback)
+    GB = GRAPH_BATCH
+    graph = None
+    try:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(GB):
+                step()
+        graph.replay()
+        torch.cuda.synchronize()
+    except Exception as e:  # noqa: BLE001
+        graph = None
+        GRAPH_STATS["fallback"] += 1
+        GRAPH_STATS["last_error"] = f"{type(e).__name__}: {e}"
+        torch.cuda.synchronize()
+    else:
+        GRAPH_STATS["captured"] += 1
+    launches_per_step = None
+    n0 = load().ebs_launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches_per_step = load().ebs_launch_count() - n0
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    done = 0
+    if graph is not None:
+        while done + GB <= args.steps:
+            graph.replay()
+            done += GB
+    for _ in range(args.steps - done):
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
-    launches = load().ebs_launch_count() - n0
+    launches = launches_per_step * args.steps
     dist.barrier()
-    kern = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
     t = torch.tensor([e0.elapsed_time(e1) / 1e3, kern], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     # end to end: this rank's x slab in from pinned host memory, its r slab out
@@ -471,9 +626,10 @@ def bench_rank(args, rank, world, local_rank):
                 "config": {"workload": "C2: 2D P1 unit square, level 11, permuted; element "
                                        "residual r=b-Ax per step, element slabs + NCCL halo",
                            "n_nodes": m.n_nodes, "n_elements": m.n_elements, "seed": args.seed,
-                           "mode": "fast (pre-assembled b), internal numbering per rank",
+                           "mode": "fast (pre-assembled b); x and r in the caller's numbering",
                            "l2": "inputs larger than L2 per rank at N<=8 (~1/N GB slot stream)",
-                           "parallelism": f"element slabs x{world}"},
+                           "parallelism": f"element slabs x{world}",
+                           "cuda_graph": dict(GRAPH_STATS)},
                 "roofline": {"bound": "hbm", "achieved": bytes_rank / K_max / 1e9, "peak": peak,
                              "unit": "GB/s", "frac": bytes_rank / K_max / 1e9 / peak,
                              "traffic": None, "kernel": "k_sell_op<3,1,0> (rank 0 slab)",
@@ -518,8 +674,8 @@ def _bench_solvers(args, rank, world):
             comm = TorchTransport()
             prob = setup([op], comm)
             x0 = op.zeros()
-            run = (lambda: jacobi(prob, [x0], iters, 0.8)) if cfg == 4 else \
-                (lambda: pcg(prob, [x0], iters))
+            run = (lambda: jacobi(prob, [x0], iters, 0.8, graph=True)) if cfg == 4 else \
+                (lambda: pcg(prob, [x0], iters, graph=True))
             run()  # warm-up (creates the NCCL P2P communicators)
             torch.cuda.synchronize()
             dist.barrier()
@@ -539,6 +695,7 @@ def _bench_solvers(args, rank, world):
                               "frac_of_peak_per_gpu": per_it * iters / T / 1e9 / world /
                               float(peaks["hbm_gbs"]),
                               "final_norm": float(norms[-1]), "n_nodes": m.n_nodes,
+                              "cuda_graph": dict(GRAPH_STATS),
                               "n_elements": m.n_elements}
             del op, prob
         except Exception as e:  # noqa: BLE001
