@@ -33,9 +33,13 @@ def to_device(x, dtype, contiguous=True) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = x
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+        a = np.ascontiguousarray(np.asarray(x))
+        if not a.flags.writeable:  # torch.from_numpy needs a writable buffer
+            a = a.copy()
+        t = torch.from_numpy(a)
     if t.device != dev or t.dtype != dtype:
-        t = t.to(device=dev, dtype=dtype, non_blocking=t.is_pinned() if t.device.type == "cpu" else False)
+        pinned = t.device.type == "cpu" and t.is_pinned()
+        t = t.to(device=dev, dtype=dtype, non_blocking=pinned)
     if contiguous and not t.is_contiguous():
         t = t.contiguous()
     return t

@@ -20,8 +20,6 @@ The solver loops are written against two small protocols so the same code runs
 
 from __future__ import annotations
 
-import ctypes
-import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -124,18 +122,39 @@ class LocalTransport:
 
 
 # ---------------------------------------------------------------- rank operator --
+def rank_operator(mesh, nu: float, f, d, P: int, rank: int, maps: dict | None = None):
+    """Rank `rank` of P: partition maps of the mesh and a GpuRankOperator whose element
+    matrices are assembled for this rank's slab only (memory and setup scale as 1/P)."""
+    from .elements import build_element_batch
+    from .mesh import Mesh
+    if maps is None:
+        maps = partition_maps(mesh.conn, mesh.n_nodes, P)
+    lo, hi = int(maps["bounds"][rank]), int(maps["bounds"][rank + 1])
+    slab = Mesh(mesh.nodes, None, mesh.boundary_nodes, conn=mesh.conn[:, lo:hi].contiguous())
+    batch = build_element_batch(slab, nu=nu, f=f)
+    object.__setattr__(batch.index, "n_nodes", mesh.n_nodes)
+    return GpuRankOperator(batch, mesh.n_nodes, d, maps, rank, slab=True), maps
+
+
+
 class GpuRankOperator:
     """Rank p's slab of a global ElementBatch on the current CUDA device.
 
     Vectors are in this rank's plan-internal numbering ("internal")."""
 
-    def __init__(self, batch, n_nodes: int, d, maps: dict, p: int):
+    def __init__(self, batch, n_nodes: int, d, maps: dict, p: int, slab: bool = False):
+        """`batch` is the global ElementBatch, or (slab=True) a batch holding only this
+        rank's elements [lo, hi) (see rank_operator), in the global node numbering."""
         from .elements import ElementBatch
         from .mesh import IndexArrays
         from .operators import DirichletData
         self.rank = p
         self.P = len(maps["local"])
         lo, hi = int(maps["bounds"][p]), int(maps["bounds"][p + 1])
+        if slab:
+            if batch.n_elements != hi - lo:
+                raise ValueError("slab batch does not match the partition bounds")
+            lo, hi = 0, hi - lo
         gl = maps["local"][p].to(D.device())
         self.global_ids = gl
         n = gl.numel()
@@ -321,7 +340,8 @@ def residual_caller(prob: DistProblem, x_global: torch.Tensor, r_globals: list, 
 
 
 def residual(prob: DistProblem, xs, out=None):
-    """r = mask? no: b - A x (unmasked, operators.py:72) on every rank's local nodes."""
+    """r = b - A x (unmasked, operators.py:72) on every rank's local nodes (internal
+    numbering); shared nodes hold identical values on every rank."""
     ops, comm = prob.ops, prob.comm
     ss = [op.zeros() for op in ops]
     for op, x, s in zip(ops, xs, ss):
@@ -515,10 +535,9 @@ def bench_rank(args, rank, world, local_rank):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     peaks, peak_kind = B.load_peaks()
     sampler = B.ClockSampler(index=local_rank).start()
-    p = config_problem(2, seed=args.seed, size=args.size)
-    m, batch = p["mesh"], p["batch"]
-    maps = partition_maps(batch.index.indt, m.n_nodes, world)
-    op = GpuRankOperator(batch, m.n_nodes, None, maps, rank)
+    p = config_problem(2, seed=args.seed, size=args.size, assemble=False)
+    m = p["mesh"]
+    op, maps = rank_operator(m, p["nu"], p["f"], None, world, rank)
     comm = TorchTransport()
     prob = setup([op], comm)
     x_glob = torch.from_numpy(p["x"]).cuda()
@@ -639,7 +658,7 @@ def bench_rank(args, rank, world, local_rank):
                         "h2d_bytes_per_step": int(te[1]), "d2h_bytes_per_step": int(te[1]),
                         "api": "dist.residual step per rank with its x/r slab via pinned host"},
                 "gpu_launches": launches, "clocks": sampler.summary(), "cpu_baseline": None}
-    del op, prob, batch, p, x_int, s, r
+    del op, prob, p, x_int, s, r
     torch.cuda.empty_cache()
     solvers = {}
     if getattr(args, "extra", False):
@@ -664,11 +683,10 @@ def _bench_solvers(args, rank, world):
         if cfg not in getattr(args, "solver_configs", (4, 5)):
             continue
         try:
-            p = config_problem(cfg, seed=args.seed)
-            batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
-            maps = partition_maps(batch.index.indt, m.n_nodes, world)
-            op = GpuRankOperator(batch, m.n_nodes, d, maps, rank)
-            del p, batch
+            p = config_problem(cfg, seed=args.seed, assemble=False)
+            d, m = p["dirichlet"], p["mesh"]
+            op, maps = rank_operator(m, p["nu"], p["f"], d, world, rank)
+            del p
             gc.collect()
             torch.cuda.empty_cache()
             comm = TorchTransport()

@@ -32,9 +32,9 @@ class DirichletData:
     values: torch.Tensor
 
     def __post_init__(self):
-        nd = D.i64(self.nd).reshape(-1) if not _is_1d_mismatch(self.nd) else None
-        if nd is None:
+        if len(np.shape(self.nd)) != 1:
             raise ValueError("nd and values must be 1-D arrays of equal length")
+        nd = D.i64(self.nd)
         values = D.f64(self.values)
         if values.ndim != 1 or tuple(values.shape) != tuple(nd.shape):
             raise ValueError("nd and values must be 1-D arrays of equal length")
@@ -45,11 +45,6 @@ class DirichletData:
             raise ValueError("duplicate constrained node indices")
         object.__setattr__(self, "nd", nd)
         object.__setattr__(self, "values", values)
-
-
-def _is_1d_mismatch(nd) -> bool:
-    shape = tuple(nd.shape) if hasattr(nd, "shape") else np.asarray(nd).shape
-    return len(shape) != 1
 
 
 def constant_dirichlet(m: Mesh, value: float = 1.0) -> DirichletData:
@@ -88,7 +83,7 @@ def _index_cache(indt: torch.Tensor) -> IndexArrays:
     return ent[1]
 
 
-def _check_x(x, check_finite=True):
+def _check_x(x):
     x = D.f64(x)
     if x.ndim != 1:
         raise ValueError(f"x must be a flat global vector, got shape {tuple(x.shape)}")

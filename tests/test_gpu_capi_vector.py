@@ -1,0 +1,70 @@
+"""The vector entry points of the C-ABI (ebs_dot, ebs_nrm2, ebs_axpby, ebs_check_finite,
+ebs_mask, ebs_gather, ebs_scatter_add, ebs_index_*) called directly through ctypes."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def P(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def test_reductions_and_axpby(gpu):
+    from paper_1911_03973_b200._lib import call
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for n in (0, 1, 1000, 1 << 20):
+        x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+        y = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+        out = torch.zeros(2, dtype=torch.float64, device="cuda")
+        call("ebs_dot", n, P(x), P(y), P(out), s)
+        call("ebs_nrm2", n, P(x), P(out[1:]), s)
+        assert abs(float(out[0]) - float(x @ y)) <= 1e-12 * max(1.0, float(x @ y))
+        assert abs(float(out[1]) - float(torch.linalg.vector_norm(x))) <= 1e-12 * max(1.0, n ** 0.5)
+        # deterministic: same bits run to run
+        again = torch.zeros(1, dtype=torch.float64, device="cuda")
+        call("ebs_dot", n, P(x), P(y), P(again), s)
+        assert float(again) == float(out[0])
+        y0 = y.clone()
+        call("ebs_axpby", n, 2.0, P(x), -0.5, P(y), s)
+        assert torch.equal(y, 2.0 * x + -0.5 * y0)
+
+
+def test_finite_mask_gather_scatter(gpu):
+    from paper_1911_03973_b200._lib import call
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    v = torch.arange(10, dtype=torch.float64, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    call("ebs_check_finite", 10, P(v), P(flag), s)
+    assert int(flag) == 0
+    v[7] = float("inf")
+    call("ebs_check_finite", 10, P(v), P(flag), s)
+    assert int(flag) == 1
+    v[7] = 7.0
+    nd = torch.tensor([1, 4], dtype=torch.int64, device="cuda")
+    out = torch.empty_like(v)
+    call("ebs_mask", 10, P(v), 2, P(nd), P(out), s)
+    exp = v.clone()
+    exp[nd] = 0.0
+    assert torch.equal(out, exp) and float(v[1]) == 1.0
+    idx = torch.tensor([9, 0, 3], dtype=torch.int64, device="cuda")
+    buf = torch.empty(3, dtype=torch.float64, device="cuda")
+    call("ebs_gather", 3, P(idx), P(v), P(buf), s)
+    assert buf.tolist() == [9.0, 0.0, 3.0]
+    call("ebs_scatter_add", 3, P(idx), P(buf), P(v), s)
+    assert v[[9, 0, 3]].tolist() == [18.0, 0.0, 6.0]
+    call("ebs_index_fill", 2, P(idx[:2]), -1.0, P(v), s)
+    assert v[[9, 0]].tolist() == [-1.0, -1.0]
+    dst = torch.zeros(10, dtype=torch.float64, device="cuda")
+    call("ebs_index_copy", 3, P(idx), P(v), P(dst), s)
+    assert dst[[9, 0, 3]].tolist() == [-1.0, -1.0, 6.0]
+    src_i = torch.tensor([0, 1], dtype=torch.int64, device="cuda")
+    dst_i = torch.tensor([5, 6], dtype=torch.int64, device="cuda")
+    call("ebs_index_move", 2, P(src_i), P(v), P(dst_i), P(dst), s)
+    call("ebs_index_add", 2, P(src_i), P(v), P(dst_i), P(dst), s)
+    assert dst[[5, 6]].tolist() == [2 * float(v[0]), 2 * float(v[1])]

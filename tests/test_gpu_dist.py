@@ -111,3 +111,23 @@ def test_fused_caller_numbering_residual(gpu, P):
             out[own] = r[own]
         ref = eb.residual(batch, x, deterministic=False)
         assert float((out - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_rank_local_assembly_equals_sliced(gpu, P):
+    """rank_operator assembles only the rank's slab; same operator as slicing the global
+    batch (bitwise partial sums, same PCG result)."""
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    pr = config_problem(4, seed=2, size=6)
+    m, batch, d = pr["mesh"], pr["batch"], pr["dirichlet"]
+    maps = dist.partition_maps(batch.index.indt, m.n_nodes, P)
+    x = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, m.n_nodes)).cuda()
+    for r in range(P):
+        a = dist.GpuRankOperator(batch, m.n_nodes, d, maps, r)
+        b, _ = dist.rank_operator(m, pr["nu"], pr["f"], d, P, r, maps=maps)
+        sa, sb = a.zeros(), b.zeros()
+        a.matvec_partial(a.to_internal(x), sa)
+        b.matvec_partial(b.to_internal(x), sb)
+        assert torch.equal(sa, sb)
+        assert torch.equal(a.rhs_partial(), b.rhs_partial())
