@@ -261,6 +261,25 @@ int ebs_vec_dot_owned(int64_t n, const double *x, const double *y, const uint8_t
 /* dinv = free ? (diag ? 1/diag : 1) : 0 */
 int ebs_vec_dinv(int64_t n, const double *diag, const uint8_t *free_m, double *dinv,
                  void *stream);
+/* Fused slab-rank steps (overlap of the halo exchange with interior work).  The SELL
+ * pass sweeps only the `chunks` listed (n_list of them); nodes with iface[m] = 1 (shared
+ * with another slab) store their partial sum in s_part / q and are completed after the
+ * exchange by the *_iface kernels over the interface node list idx; all other nodes are
+ * finished in the pass.  red[0] = sum over the nodes finished (owned) by that launch.
+ * Jacobi: r = free ? b - s : 0, x_out = x + omega*(dinv*r) (dinv NULL: Richardson).
+ * PCG matvec: q = free ? s : 0, red = p.q. */
+int ebs_dist_jacobi_sweep(ebs_plan_t plan, const int32_t *chunks, int64_t n_list, double omega,
+                          const double *x, double *x_out, const double *b, const double *dinv,
+                          const uint8_t *iface, double *s_part, double *red, void *ws,
+                          void *stream);
+int ebs_dist_matvec_sweep(ebs_plan_t plan, const int32_t *chunks, int64_t n_list, const double *pv,
+                          double *q, const uint8_t *iface, double *red, void *ws, void *stream);
+int ebs_dist_jacobi_iface(int64_t n, const int64_t *idx, double omega, const double *b,
+                          const double *s, const double *dinv, const uint8_t *free_m,
+                          const uint8_t *owned, const double *x, double *x_out, double *red,
+                          void *ws, void *stream);
+int ebs_dist_q_iface(int64_t n, const int64_t *idx, const uint8_t *free_m, const uint8_t *owned,
+                     const double *pv, double *q, double *red, void *ws, void *stream);
 /* plan internals in internal numbering: Dirichlet free flags, pre-assembled b, diag(A) */
 int ebs_plan_free_mask(ebs_plan_t plan, uint8_t *free_int, void *stream);
 int ebs_plan_internal_rhs(ebs_plan_t plan, double *b_int, void *stream);

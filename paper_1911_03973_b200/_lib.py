@@ -112,6 +112,16 @@ SIGNATURES = {
     "ebs_vec_dot_owned": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                   c_void_p]),
     "ebs_vec_dinv": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_dist_jacobi_sweep": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p]),
+    "ebs_dist_matvec_sweep": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p]),
+    "ebs_dist_jacobi_iface": (c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p]),
+    "ebs_dist_q_iface": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p, c_void_p]),
     "ebs_plan_free_mask": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ebs_plan_internal_rhs": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ebs_plan_internal_diag": (c_int, [c_void_p, c_void_p, c_void_p]),

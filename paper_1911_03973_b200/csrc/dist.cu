@@ -168,7 +168,7 @@ using namespace ebs;
 
 extern "C" {
 
-size_t ebs_vec_workspace_bytes(void) { return 256 + sizeof(double) * 2 * RED_MAX_BLOCKS; }
+size_t ebs_vec_workspace_bytes(void) { return 256 + sizeof(double) * 2 * 8192; }
 
 int ebs_index_fill(int64_t n, const int64_t *idx, double value, double *v, void *stream) {
     EBS_TRY
@@ -294,6 +294,192 @@ int ebs_plan_internal_rhs(ebs_plan_t plan, double *b_int, void *stream) {
     if (p->n_n)
         CU(cudaMemcpyAsync(b_int, p->b_int, sizeof(double) * p->n_n, cudaMemcpyDeviceToDevice,
                            S(stream)));
+    EBS_CATCH
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------
+// Fused slab-rank steps.  The SELL sweep covers a chunk list; nodes flagged `iface` (shared
+// with another slab) only store their partial sum for the halo exchange, all other nodes
+// (owned, complete) are finished in the epilogue exactly as the 1-GPU fused kernels do.
+// Sweeping the interface chunks first lets the host start the exchange while the
+// interior chunks are swept.
+#include "sell.cuh"
+
+namespace ebs {
+
+struct DistJacobiEpi {
+    double omega;
+    const double *__restrict__ b;
+    const double *__restrict__ dinv;
+    const uint8_t *__restrict__ free_m;
+    const uint8_t *__restrict__ iface;
+    double *__restrict__ x_out;
+    double *__restrict__ s_part;
+    double part[1];
+    __device__ __forceinline__ void operator()(int64_t m, double s, double xo) {
+        if (iface[m]) {
+            s_part[m] = s;
+            return;
+        }
+        double r = free_m[m] ? b[m] - s : 0.0;
+        part[0] += r * r;
+        if (x_out) x_out[m] = dinv ? xo + omega * (dinv[m] * r) : xo + omega * r;
+    }
+};
+
+template <int NB, int IDS>
+__global__ void EBS_SELL_BOUNDS(NB)
+    k_dist_jacobi_sweep(SellView v, const double *__restrict__ x, DistJacobiEpi epi,
+                        double *partials, unsigned int *counter, double *red) {
+    sell_sweep<NB, IDS, false, NB == 3>(v, x, epi);
+    double tot[1];
+    if (grid_sum_last<1>(epi.part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+struct DistMatvecEpi {
+    const uint8_t *__restrict__ free_m;
+    const uint8_t *__restrict__ iface;
+    double *__restrict__ q;
+    double part[1];
+    __device__ __forceinline__ void operator()(int64_t m, double s, double po) {
+        if (iface[m]) {
+            q[m] = s;  // partial; completed after the halo
+            return;
+        }
+        double qm = free_m[m] ? s : 0.0;
+        q[m] = qm;
+        part[0] += po * qm;
+    }
+};
+
+template <int NB, int IDS>
+__global__ void EBS_SELL_BOUNDS(NB)
+    k_dist_matvec_sweep(SellView v, const double *__restrict__ p, DistMatvecEpi epi,
+                        double *partials, unsigned int *counter, double *red) {
+    sell_sweep<NB, IDS, false>(v, p, epi);
+    double tot[1];
+    if (grid_sum_last<1>(epi.part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+// interface nodes after the halo: Jacobi completion (s combined) / PCG q completion
+__global__ void __launch_bounds__(256)
+    k_dist_jacobi_iface(int64_t n, const int64_t *__restrict__ idx, double omega,
+                        const double *__restrict__ b, const double *__restrict__ s,
+                        const double *__restrict__ dinv, const uint8_t *__restrict__ free_m,
+                        const uint8_t *__restrict__ owned, const double *__restrict__ x,
+                        double *__restrict__ x_out, double *partials, unsigned int *counter,
+                        double *red) {
+    double part[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = idx[i];
+        double r = free_m[m] ? b[m] - s[m] : 0.0;
+        if (owned[m]) part[0] += r * r;
+        if (x_out) x_out[m] = dinv ? x[m] + omega * (dinv[m] * r) : x[m] + omega * r;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+__global__ void __launch_bounds__(256)
+    k_dist_q_iface(int64_t n, const int64_t *__restrict__ idx, const uint8_t *__restrict__ free_m,
+                   const uint8_t *__restrict__ owned, const double *__restrict__ p,
+                   double *__restrict__ q, double *partials, unsigned int *counter, double *red) {
+    double part[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = idx[i];
+        double qm = free_m[m] ? q[m] : 0.0;
+        q[m] = qm;
+        if (owned[m]) part[0] += p[m] * qm;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+}  // namespace ebs
+
+extern "C" {
+
+int ebs_dist_jacobi_sweep(ebs_plan_t plan, const int32_t *chunks, int64_t n_list, double omega,
+                          const double *x, double *x_out, const double *b, const double *dinv,
+                          const uint8_t *iface, double *s_part, double *red, void *ws,
+                          void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && x && b && iface && s_part && red && ws, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(n_list >= 0 && (chunks || n_list == 0), "bad chunk list");
+    Scratch sc = scratch(ws);
+    if (n_list == 0) {
+        CU(cudaMemsetAsync(red, 0, sizeof(double), S(stream)));
+        return EBS_OK;
+    }
+    DistJacobiEpi epi{omega, b, dinv, p->free_int, iface, x_out, s_part, {0.0}};
+    SellView v = sell_view(p, chunks, n_list);
+#define EBS_DJ(NB_, IDS_)                                                                   \
+    {                                                                                       \
+        auto kern = k_dist_jacobi_sweep<NB_, IDS_>;                                         \
+        SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, n_list);              \
+        kern<<<SL.grid, SL.block, SL.smem, S(stream)>>>(v, x, epi, sc.partials, sc.counter, \
+                                                        red);                               \
+    }
+    EBS_SELL_DISPATCH(p, EBS_DJ);
+#undef EBS_DJ
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_dist_matvec_sweep(ebs_plan_t plan, const int32_t *chunks, int64_t n_list, const double *pv,
+                          double *q, const uint8_t *iface, double *red, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && pv && q && iface && red && ws, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(n_list >= 0 && (chunks || n_list == 0), "bad chunk list");
+    Scratch sc = scratch(ws);
+    if (n_list == 0) {
+        CU(cudaMemsetAsync(red, 0, sizeof(double), S(stream)));
+        return EBS_OK;
+    }
+    DistMatvecEpi epi{p->free_int, iface, q, {0.0}};
+    SellView v = sell_view(p, chunks, n_list);
+#define EBS_DM(NB_, IDS_)                                                                   \
+    {                                                                                       \
+        auto kern = k_dist_matvec_sweep<NB_, IDS_>;                                         \
+        SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, n_list);              \
+        kern<<<SL.grid, SL.block, SL.smem, S(stream)>>>(v, pv, epi, sc.partials, sc.counter, \
+                                                        red);                               \
+    }
+    EBS_SELL_DISPATCH(p, EBS_DM);
+#undef EBS_DM
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_dist_jacobi_iface(int64_t n, const int64_t *idx, double omega, const double *b,
+                          const double *s, const double *dinv, const uint8_t *free_m,
+                          const uint8_t *owned, const double *x, double *x_out, double *red,
+                          void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && b && s && free_m && owned && x && red && ws, "null argument");
+    Scratch sc = scratch(ws);
+    k_dist_jacobi_iface<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+        n, idx, omega, b, s, dinv, free_m, owned, x, x_out, sc.partials, sc.counter, red);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_dist_q_iface(int64_t n, const int64_t *idx, const uint8_t *free_m, const uint8_t *owned,
+                     const double *pv, double *q, double *red, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && free_m && owned && pv && q && red && ws, "null argument");
+    Scratch sc = scratch(ws);
+    k_dist_q_iface<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+        n, idx, free_m, owned, pv, q, sc.partials, sc.counter, red);
+    LAUNCHED();
     EBS_CATCH
 }
 

@@ -33,11 +33,13 @@ struct SellView {
     const double *__restrict__ be;
     const int32_t *__restrict__ tab;     // per-chunk offset tables (IDS_TABLE)
     const int32_t *__restrict__ taboff;  // n_chunks + 1 offsets into tab
+    const int32_t *__restrict__ clist;   // nullable: sweep only these chunks
+    int64_t nlist;                       // number of chunks swept (n_chunks or list size)
 };
 
-inline SellView sell_view(const Plan *p) {
+inline SellView sell_view(const Plan *p, const int32_t *clist = nullptr, int64_t nlist = -1) {
     return SellView{p->n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, p->slot,
-                    p->slot_be, p->tab, p->taboff};
+                    p->slot_be, p->tab, p->taboff, clist, clist ? nlist : p->n_chunks};
 }
 
 // id-plane layouts (Plan::packed)
@@ -268,7 +270,8 @@ __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *
     int32_t *stab = stab_all[threadIdx.x / LANES];
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / LANES;
-    for (int64_t c = warp; c < v.n_chunks; c += nwarps) {
+    for (int64_t ci = warp; ci < v.nlist; ci += nwarps) {
+        const int64_t c = v.clist ? (int64_t)v.clist[ci] : ci;
         if constexpr (IDS == IDS_TABLE) {
             const int t0 = v.taboff[c], t1 = v.taboff[c + 1];
             __syncwarp();
@@ -477,8 +480,10 @@ __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__re
                                            Epi &epi) {
 #if EBS_TMA
     if constexpr (IDS != IDS_TABLE) {
-        sell_sweep_tma<NB, IDS, EXACT>(v, x, epi);
-        return;
+        if (v.clist == nullptr) {  // the TMA ring sweeps all chunks
+            sell_sweep_tma<NB, IDS, EXACT>(v, x, epi);
+            return;
+        }
     }
 #endif
     sell_sweep_ldg<NB, IDS, EXACT, PIPE>(v, x, epi);

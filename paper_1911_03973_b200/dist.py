@@ -71,8 +71,9 @@ class TorchTransport:
         self.group = group
         self.stage_host = stage_host
 
-    def exchange(self, ops: list, sends: list) -> list:
-        """sends[i] = {q: tensor} for local rank ops[i] (len 1 here) -> recvs {q: tensor}."""
+    def exchange_start(self, ops: list, sends: list):
+        """Post the halo send/recv pairs (NCCL runs them on its own stream, after the work
+        already queued on the current stream); returns a handle for exchange_finish."""
         (op,), (snd,) = ops, sends
         p2p = []
         recvs = {}
@@ -85,12 +86,20 @@ class TorchTransport:
             recvs[q] = torch.empty_like(buf)
             p2p.append(self.dist.P2POp(self.dist.isend, buf, q, self.group))
             p2p.append(self.dist.P2POp(self.dist.irecv, recvs[q], q, self.group))
-        if p2p:
-            for w in self.dist.batch_isend_irecv(p2p):
-                w.wait()
+        works = self.dist.batch_isend_irecv(p2p) if p2p else []
+        return works, recvs, dev
+
+    def exchange_finish(self, handle) -> list:
+        works, recvs, dev = handle
+        for w in works:
+            w.wait()  # the current stream waits for the transfers
         if dev is not None:
             recvs = {q: t.to(dev) for q, t in recvs.items()}
         return [recvs]
+
+    def exchange(self, ops: list, sends: list) -> list:
+        """sends[i] = {q: tensor} for local rank ops[i] (len 1 here) -> recvs {q: tensor}."""
+        return self.exchange_finish(self.exchange_start(ops, sends))
 
     def allreduce(self, tensors: list):
         (t,) = tensors
@@ -104,6 +113,12 @@ class TorchTransport:
 
 class LocalTransport:
     """All P ranks in this process (one GPU): the exchange is a device copy."""
+
+    def exchange_start(self, ops: list, sends: list):
+        return self.exchange(ops, sends)
+
+    def exchange_finish(self, handle) -> list:
+        return handle
 
     def exchange(self, ops: list, sends: list) -> list:
         ranks = {op.rank: i for i, op in enumerate(ops)}
@@ -189,6 +204,17 @@ class GpuRankOperator:
         self.owned = (owner[self.global_of_int] == p).to(torch.uint8).contiguous()
         self.free = D.empty(n, torch.uint8)
         call("ebs_plan_free_mask", self.plan.handle, D.ptr(self.free), D.stream())
+        # interface flags and the chunk split (interface chunks are swept first so the
+        # halo exchange overlaps the interior sweep)
+        self.iface = torch.zeros(n, dtype=torch.uint8, device=gl.device)
+        if self.all_if.numel():
+            self.iface[self.all_if] = 1
+        n_chunks = (n + 31) // 32
+        has_if = torch.zeros(n_chunks, dtype=torch.bool, device=gl.device)
+        if self.all_if.numel():
+            has_if[self.all_if // 32] = True
+        self.if_chunks = torch.nonzero(has_if).reshape(-1).to(torch.int32).contiguous()
+        self.in_chunks = torch.nonzero(~has_if).reshape(-1).to(torch.int32).contiguous()
         m_own = self.owned.bool()
         self.owned_int = torch.nonzero(m_own).reshape(-1)
         self.owned_glob = self.global_of_int[self.owned_int].contiguous()
@@ -263,6 +289,24 @@ class GpuRankOperator:
                 idx = self.if_idx[r]
                 call("ebs_scatter_add", idx.numel(), D.ptr(idx), D.ptr(recvs[r]), D.ptr(acc), s)
         call("ebs_index_copy", self.all_if.numel(), D.ptr(self.all_if), D.ptr(acc), D.ptr(v), s)
+
+    def jacobi_sweep(self, chunks, omega, x, x_out, b, dinv, s_part, red):
+        call("ebs_dist_jacobi_sweep", self.plan.handle, D.ptr(chunks), chunks.numel(),
+             float(omega), D.ptr(x), D.ptr(x_out), D.ptr(b), D.ptr(dinv), D.ptr(self.iface),
+             D.ptr(s_part), D.ptr(red), D.ptr(self._ws), D.stream())
+
+    def jacobi_iface(self, omega, b, s_part, dinv, x, x_out, red):
+        call("ebs_dist_jacobi_iface", self.all_if.numel(), D.ptr(self.all_if), float(omega),
+             D.ptr(b), D.ptr(s_part), D.ptr(dinv), D.ptr(self.free), D.ptr(self.owned), D.ptr(x),
+             D.ptr(x_out), D.ptr(red), D.ptr(self._ws), D.stream())
+
+    def matvec_sweep(self, chunks, p, q, red):
+        call("ebs_dist_matvec_sweep", self.plan.handle, D.ptr(chunks), chunks.numel(), D.ptr(p),
+             D.ptr(q), D.ptr(self.iface), D.ptr(red), D.ptr(self._ws), D.stream())
+
+    def q_iface(self, p, q, red):
+        call("ebs_dist_q_iface", self.all_if.numel(), D.ptr(self.all_if), D.ptr(self.free),
+             D.ptr(self.owned), D.ptr(p), D.ptr(q), D.ptr(red), D.ptr(self._ws), D.stream())
 
     def vec_dinv(self, diag):
         dinv = D.empty(self.n)
@@ -359,20 +403,44 @@ def _graph_ok(ops) -> bool:
                isinstance(getattr(op, "free", None), torch.Tensor) and op.free.is_cuda for op in ops)
 
 
+def _fused_ok(ops) -> bool:
+    return all(hasattr(op, "jacobi_sweep") for op in ops)
+
+
 def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: bool = False,
-           graph: bool = False):
+           graph: bool = False, fused=None):
     """Damped Jacobi on P ranks (oracle/ebs_oracle.py jacobi semantics, fixed count).
 
     Returns (xs, norms) with norms[k] = ||mask(b - A x_k)||, k = 0..iters.  With
     graph=True the iterations are replayed from a captured CUDA graph of GRAPH_BATCH
-    iterations (same kernels, same results)."""
+    iterations (same kernels, same results).  fused (default: GPU ranks) runs the
+    overlapped interface/interior sweeps with the update fused into the SELL pass."""
     ops, comm = prob.ops, prob.comm
     xa = [x.clone() for x in xs0]
     xb = [op.zeros() for op in ops]
     ss = [op.zeros() for op in ops]
     red = [torch.zeros(iters + 1, dtype=torch.float64, device=x.device) for x in xa]
 
+    fused = _fused_ok(ops) if fused is None else fused
+    r3 = [torch.zeros(3, dtype=torch.float64, device=x.device) for x in xa]
+
     def step(src, dst, final, rslot):
+        if fused:  # interface chunks, exchange || interior chunks, interface completion
+            for i, op in enumerate(ops):
+                op.jacobi_sweep(op.if_chunks, omega, src[i], None if final else dst[i], prob.b[i],
+                                None if richardson else prob.dinv[i], ss[i], r3[i][0:1])
+            h = comm.exchange_start(ops, [{q: op.gather(idx, s_) for q, idx in op.if_idx.items()}
+                                          for op, s_ in zip(ops, ss)])
+            for i, op in enumerate(ops):
+                op.jacobi_sweep(op.in_chunks, omega, src[i], None if final else dst[i], prob.b[i],
+                                None if richardson else prob.dinv[i], ss[i], r3[i][1:2])
+            recvs = comm.exchange_finish(h)
+            for i, op in enumerate(ops):
+                op.combine(ss[i], recvs[i])
+                op.jacobi_iface(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i],
+                                src[i], None if final else dst[i], r3[i][2:3])
+                rslot[i].copy_(r3[i].sum(0, keepdim=True))
+            return
         for op, x, s_ in zip(ops, src, ss):
             op.matvec_partial(x, s_)
         halo(ops, comm, ss)
@@ -414,7 +482,7 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     return xa, torch.sqrt(red[0]).cpu().numpy()
 
 
-def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False):
+def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused=None):
     """Jacobi-PCG on P ranks (oracle/ebs_oracle.py pcg; with prob from setup(..,
     precondition=False) plain CG).  Two scalar all-reduces per iteration.  graph=True
     (fixed iteration count only) replays captured CUDA graphs of GRAPH_BATCH iterations."""
@@ -442,12 +510,28 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False):
         hist[i][0:1].copy_(red[i][0:1])
         scal[i][0:1].copy_(red[i][1:2])
 
+    fused = _fused_ok(ops) if fused is None else fused
+    pq3 = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in ops]
+
     def step(hslot):
-        for op, p_, q_ in zip(ops, ps, qs):
-            op.matvec_partial(p_, q_)
-        halo(ops, comm, qs)
-        for i, op in enumerate(ops):
-            op.vec_pcg_q(ps[i], qs[i], pq[i])
+        if fused:  # interface chunks, exchange || interior chunks, interface completion
+            for i, op in enumerate(ops):
+                op.matvec_sweep(op.if_chunks, ps[i], qs[i], pq3[i][0:1])
+            h = comm.exchange_start(ops, [{q: op.gather(idx, q_) for q, idx in op.if_idx.items()}
+                                          for op, q_ in zip(ops, qs)])
+            for i, op in enumerate(ops):
+                op.matvec_sweep(op.in_chunks, ps[i], qs[i], pq3[i][1:2])
+            recvs = comm.exchange_finish(h)
+            for i, op in enumerate(ops):
+                op.combine(qs[i], recvs[i])
+                op.q_iface(ps[i], qs[i], pq3[i][2:3])
+                pq[i].copy_(pq3[i].sum(0, keepdim=True))
+        else:
+            for op, p_, q_ in zip(ops, ps, qs):
+                op.matvec_partial(p_, q_)
+            halo(ops, comm, qs)
+            for i, op in enumerate(ops):
+                op.vec_pcg_q(ps[i], qs[i], pq[i])
         comm.allreduce(pq)
         for i, op in enumerate(ops):
             scal[i][1:2].copy_(pq[i])

@@ -131,3 +131,29 @@ def test_rank_local_assembly_equals_sliced(gpu, P):
         b.matvec_partial(b.to_internal(x), sb)
         assert torch.equal(sa, sb)
         assert torch.equal(a.rhs_partial(), b.rhs_partial())
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_fused_overlapped_steps_match_unfused(gpu, P):
+    """The overlapped interface/interior sweeps: Jacobi iterates bitwise equal to the
+    unfused rank loop, PCG within 1e-10 (the dot is summed in three groups)."""
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    for cfg, size, iters in ((4, 6, 30), (5, 6, 60)):
+        pr = config_problem(cfg, seed=5, size=size)
+        m = pr["mesh"]
+        prob, _ = dist.emulate(pr["batch"], m.n_nodes, pr["dirichlet"], P)
+        x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+        xin = [op.to_internal(x0) for op in prob.ops]
+        run = dist.jacobi if cfg == 4 else dist.pcg
+        xu, nu_ = run(prob, xin, iters, fused=False)
+        xf, nf = run(prob, xin, iters, fused=True)
+        xg, ng = run(prob, xin, iters, fused=True, graph=True)
+        np.testing.assert_allclose(nf, nu_, rtol=1e-8, atol=1e-10 * nu_[0])
+        np.testing.assert_array_equal(ng, nf)
+        for a, b, c in zip(xf, xu, xg):
+            assert torch.equal(a, c)
+            if cfg == 4:
+                assert torch.equal(a, b)
+            else:
+                assert float((a - b).abs().max()) <= 1e-10 * float(b.abs().max())
