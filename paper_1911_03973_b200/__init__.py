@@ -17,7 +17,7 @@ from .mesh import (MAX_LEVEL, IndexArrays, Mesh, boundary_nodes, build_grid_mesh
                    export_mesh, face_z0_nodes, jitter_interior, permute_nodes, signed_areas,
                    uniform_refine)
 from .operators import (DirichletData, apply_initial_guess, assemble_rhs, constant_dirichlet,
-                        diagonal, mask_dirichlet, matvec, residual)
+                        diagonal, mask_dirichlet, matvec, residual, residual_many)
 from .solvers import (ChebyshevCycle, ConvergenceHistory, SpectralBounds, cg, chebyshev2,
                       chebyshev3, chebyshev_roots, chebyshev_scaling_factor, jacobi, pcg,
                       richardson)
@@ -35,7 +35,7 @@ __all__ = [
     "build_unit_square_mesh", "cg", "combine_system", "constant_dirichlet", "diagonal",
     "face_z0_nodes", "jacobi", "jitter_interior", "local_load_batch", "local_mass_batch",
     "local_stiffness_batch", "mask_dirichlet", "matvec", "model_eigen_bounds",
-    "model_eigenvalues_all", "pcg", "permute_nodes", "residual", "richardson", "signed_areas",
+    "model_eigenvalues_all", "pcg", "permute_nodes", "residual", "residual_many", "richardson", "signed_areas",
 ]
 
 __version__ = "0.1.0"

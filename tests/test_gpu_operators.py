@@ -184,3 +184,33 @@ def test_c2_full_size_vs_oracle(gpu):
     ref = o.residual(A, b_e, indt, x, threads=8)
     npt.assert_array_equal(to_np(r_exact), ref)
     assert rel_max(to_np(r_fast), ref) <= TOL_FAST
+
+
+def test_residual_many_pipelined(gpu):
+    """residual_many: each row bit-identical to residual(); sequences, numpy, pageable and
+    pinned inputs, broadcast rows; non-finite rows raise; k = 0."""
+    import torch
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(2, seed=3, size=8)
+    batch, n = p["batch"], p["mesh"].n_nodes
+    rng = np.random.default_rng(5)
+    xs = rng.uniform(-1, 1, (7, n))
+    for det in (True, False):
+        ref = np.stack([to_np(eb.residual(batch, x, deterministic=det)) for x in xs])
+        npt.assert_array_equal(eb.residual_many(batch, xs, deterministic=det).numpy(), ref)
+        pinned = torch.from_numpy(xs).pin_memory()
+        out = torch.empty((7, n), dtype=torch.float64).pin_memory()
+        assert eb.residual_many(batch, pinned, out=out, deterministic=det) is out
+        npt.assert_array_equal(out.numpy(), ref)
+        npt.assert_array_equal(eb.residual_many(batch, list(xs), deterministic=det).numpy(), ref)
+    bcast = torch.from_numpy(xs[2]).pin_memory().unsqueeze(0).expand(5, n)
+    npt.assert_array_equal(eb.residual_many(batch, bcast).numpy(),
+                           np.broadcast_to(to_np(eb.residual(batch, xs[2])), (5, n)))
+    bad = xs.copy()
+    bad[4, 3] = np.nan
+    with pytest.raises(ValueError, match=r"x\[4\]"):
+        eb.residual_many(batch, bad)
+    assert eb.residual_many(batch, np.empty((0, n))).shape == (0, n)
+    with pytest.raises(ValueError):
+        eb.residual_many(batch, xs[0])
