@@ -103,6 +103,18 @@ struct Ctl {
     double rz, pq, alpha, beta;
 };
 
+// two-pass permutation schedule (perm.cu)
+struct Perm2 {
+    int64_t n = 0;
+    int T = 0;                 // nodes per tile
+    uint16_t *src1 = nullptr;  // pass 1: offset in the source tile of the q-th value written
+    int32_t *dst1 = nullptr;   // pass 1: its slot in the intermediate (destination-tile order)
+    uint16_t *dst2 = nullptr;  // pass 2: offset of intermediate slot k in its destination tile
+};
+
+constexpr int PERM_VEC = 8;  // workspace vector: the permutation intermediate
+constexpr int OUT_VEC = 9;   // workspace vector: internal-order operator output
+
 struct Plan {
     int nb;
     int64_t n_n, n_e;
@@ -129,7 +141,8 @@ struct Plan {
     uint8_t *free_int = nullptr;  // 1 free, 0 constrained (internal numbering)
     int64_t n_dirichlet = 0;
     // workspace (lazily grown)
-    double *wvec[8] = {nullptr};
+    double *wvec[10] = {nullptr};
+    Perm2 perm[2];  // 0: caller -> internal, 1: internal -> caller (built on first use)
     double *partials = nullptr;  // reduction partials
     Ctl *ctl = nullptr;          // device control block
     Ctl *ctl_host = nullptr;     // pinned mirror
@@ -139,6 +152,10 @@ struct Plan {
 };
 
 double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)
+const Perm2 *perm_get(Plan *p, int dir, cudaStream_t s);
+void perm_apply(Plan *p, const Perm2 *P, const double *in, double *out, int32_t *nonfinite,
+                cudaStream_t s);
+void perm_free(Plan *p);
 
 // ------------------------------------------------------ reductions ----------
 constexpr int RED_BLOCK = 256;

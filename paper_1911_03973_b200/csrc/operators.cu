@@ -92,12 +92,42 @@ __global__ void k_to_internal_scatter(int64_t n, const int32_t *__restrict__ new
 // gather orientation with 8 independent index->value chains per thread (memory-level
 // parallelism for the random 8 B reads)
 constexpr int PERM_ILP = 8;
+#ifndef EBS_PERM_PF
+#define EBS_PERM_PF 0  // 0 plain gathers, 1 L2::256B gather hint, 2 bulk L2 prefetch of x first
+#endif
+
+__device__ __forceinline__ double ld_x_perm(const double *p) {
+#if EBS_PERM_PF == 1
+    double v;
+    asm volatile("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 __global__ void __launch_bounds__(256)
     k_to_internal_ilp(int64_t n, const int32_t *__restrict__ old_of_new,
                       const double *__restrict__ x_user, double *__restrict__ x_int,
                       int32_t *nonfinite) {
     bool bad = false;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#if EBS_PERM_PF == 2
+    {   // stream this block's slice of x into L2 at sequential DRAM efficiency; the random
+        // gathers below then mostly hit L2 (a hint only: correctness never depends on it)
+        const int64_t bytes = n * 8;
+        const int64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 4095) & ~int64_t(4095);
+        const int64_t lo = (int64_t)blockIdx.x * per;
+        const int64_t hi = lo + per < bytes ? lo + per : bytes;
+        for (int64_t o = lo + (int64_t)threadIdx.x * 4096; o < hi;
+             o += (int64_t)blockDim.x * 4096) {
+            const uint32_t sz = (uint32_t)(bytes - o < 4096 ? bytes - o : 4096) & ~15u;
+            if (sz)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             :: "l"((const char *)x_user + o), "r"(sz) : "memory");
+        }
+    }
+#endif
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
          base += stride * PERM_ILP) {
         int32_t idx[PERM_ILP];
@@ -110,7 +140,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int u = 0; u < PERM_ILP; ++u) {
             const int64_t m = base + u * stride;
-            v[u] = m < n ? __ldg(x_user + idx[u]) : 0.0;
+            v[u] = m < n ? ld_x_perm(x_user + idx[u]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < PERM_ILP; ++u) {
@@ -129,9 +159,23 @@ __global__ void __launch_bounds__(256)
 #define EBS_TO_INTERNAL_SCATTER 2  // 0 gather, 1 scatter, 2 gather with ILP
 #endif
 
+#ifndef EBS_PERM2
+// 1: caller <-> internal permutations through the two-pass shared-memory schedule of
+// perm.cu (every global access coalesced).  Measured slower at C2 (2 passes 44 us vs the
+// direct gather's 33 us; profiles/README.md), so opt-in.
+#define EBS_PERM2 0
+#endif
+
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
                  cudaStream_t s) {
     if (p->n_n == 0) return;
+    if (EBS_PERM2) {
+        Plan *pm = const_cast<Plan *>(p);
+        if (const Perm2 *P = perm_get(pm, 0, s)) {
+            perm_apply(pm, P, x_user, x_int, nonfinite, s);
+            return;
+        }
+    }
     if (EBS_TO_INTERNAL_SCATTER == 2)
         k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
                             s>>>(p->n_n, p->old_of_new, x_user, x_int, nonfinite);
@@ -146,6 +190,13 @@ void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *no
 
 void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s) {
     if (p->n_n == 0) return;
+    if (EBS_PERM2) {
+        Plan *pm = const_cast<Plan *>(p);
+        if (const Perm2 *P = perm_get(pm, 1, s)) {
+            perm_apply(pm, P, v_int, v_user, nullptr, s);
+            return;
+        }
+    }
     k_to_user<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(p->n_n, p->old_of_new, v_int,
                                                               v_user);
     LAUNCHED();
@@ -187,14 +238,25 @@ void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *fre
                 const int32_t *old_of_new, double *out, cudaStream_t s) {
     double *dst = out;
     const int32_t *o2n = old_of_new;
-    if (EBS_OUT_PERM && old_of_new) {
+    const Perm2 *P = nullptr;
+    if (EBS_PERM2 && old_of_new && p->n_n) {
+        // internal-order (coalesced) output, then the two-pass permutation to caller order
+        Plan *pm = const_cast<Plan *>(p);
+        if ((P = perm_get(pm, 1, s))) {
+            dst = plan_vec(pm, OUT_VEC);
+            o2n = nullptr;
+        }
+    }
+    if (!P && EBS_OUT_PERM && old_of_new) {
         dst = plan_vec(const_cast<Plan *>(p), 7);
         o2n = nullptr;
     }
     if (mode == 0) launch_sell_op<0>(p, x_int, free_int, o2n, dst, s);
     else if (mode == 1) launch_sell_op<1>(p, x_int, free_int, o2n, dst, s);
     else launch_sell_op<2>(p, x_int, free_int, o2n, dst, s);
-    if (EBS_OUT_PERM && old_of_new && p->n_n) {
+    if (P) {
+        perm_apply(const_cast<Plan *>(p), P, dst, out, nullptr, s);
+    } else if (EBS_OUT_PERM && old_of_new && p->n_n) {
         k_from_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
                               s>>>(p->n_n, p->new_of_old, dst, out);
         LAUNCHED();

@@ -429,6 +429,7 @@ static void plan_free(Plan *p) {
     dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
     dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag);
     for (auto &v : p->wvec) dfree(v);
+    perm_free(p);
     if (p->ctl_host) cudaFreeHost(p->ctl_host);
     p->ctl_host = nullptr;
 }
