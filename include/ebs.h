@@ -155,6 +155,11 @@ int ebs_to_user(ebs_plan_t plan, const double *v_int, double *v, void *stream);
  * order (an element slab's partial sums / partial residuals for the halo). */
 int ebs_plan_apply_map(ebs_plan_t plan, int op, const double *x_int, double *out,
                        const int32_t *out_map, double *s_raw, int masked, void *stream);
+/* The same pass over a list of SELL chunks only (chunk c = internal nodes 32c .. 32c+31;
+ * a rank sweeps its interface chunks, posts the halo exchange, then sweeps the rest). */
+int ebs_plan_apply_map_chunks(ebs_plan_t plan, int op, const int32_t *chunks, int64_t n_list,
+                              const double *x_int, double *out, const int32_t *out_map,
+                              double *s_raw, int masked, void *stream);
 /* One SELL pass on internal vectors: op = 0 matvec, 1 fast residual, 2 exact residual;
  * out_user != 0 scatters the result to caller numbering, else writes internal order;
  * masked != 0 zeroes constrained rows. */

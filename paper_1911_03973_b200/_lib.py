@@ -99,6 +99,8 @@ SIGNATURES = {
     "ebs_index_add": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_plan_apply_map": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
                                    c_void_p]),
+    "ebs_plan_apply_map_chunks": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p,
+                                          c_void_p, c_void_p, c_int, c_void_p]),
     "ebs_vec_workspace_bytes": (c_size_t, []),
     "ebs_vec_jacobi": (c_int, [c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

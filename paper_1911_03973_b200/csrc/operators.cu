@@ -55,20 +55,23 @@ __global__ void EBS_SELL_BOUNDS(NB)
 }
 
 template <int NB, int IDS, int MODE>
-void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cudaStream_t s) {
+void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cudaStream_t s,
+                      const int32_t *chunks = nullptr, int64_t n_list = -1) {
     auto kern = k_sell_op<NB, IDS, MODE>;
-    const SellLaunch SL = sell_launch((const void *)kern, NB, p->rowb, p->n_chunks);
-    kern<<<SL.grid, SL.block, SL.smem, s>>>(sell_view(p), x_int, epi);
+    const SellView v = sell_view(p, chunks, n_list);
+    const SellLaunch SL = sell_launch((const void *)kern, NB, p->rowb, v.nlist);
+    kern<<<SL.grid, SL.block, SL.smem, s>>>(v, x_int, epi);
     LAUNCHED();
 }
 
 template <int MODE>
 void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
                     const int32_t *old_of_new, double *out, cudaStream_t s,
-                    double *s_raw = nullptr) {
-    if (p->n_n == 0) return;
+                    double *s_raw = nullptr, const int32_t *chunks = nullptr,
+                    int64_t n_list = -1) {
+    if (p->n_n == 0 || n_list == 0) return;
     OpEpi epi{MODE, p->b_int, free_int, old_of_new, out, s_raw};
-#define EBS_OP(NB_, IDS_) { launch_sell_op_t<NB_, IDS_, MODE>(p, x_int, epi, s); }
+#define EBS_OP(NB_, IDS_) { launch_sell_op_t<NB_, IDS_, MODE>(p, x_int, epi, s, chunks, n_list); }
     EBS_SELL_DISPATCH(p, EBS_OP);
 #undef EBS_OP
 }
@@ -341,6 +344,22 @@ int ebs_plan_apply_map(ebs_plan_t plan, int op, const double *x_int, double *out
     const uint8_t *fm = masked ? p->free_int : nullptr;
     if (op == 0) launch_sell_op<0>(p, x_int, fm, out_map, out, S(stream), s_raw);
     else launch_sell_op<1>(p, x_int, fm, out_map, out, S(stream), s_raw);
+    EBS_CATCH
+}
+
+int ebs_plan_apply_map_chunks(ebs_plan_t plan, int op, const int32_t *chunks, int64_t n_list,
+                              const double *x_int, double *out, const int32_t *out_map,
+                              double *s_raw, int masked, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && x_int && out && out_map, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    EBS_REQUIRE(op == 0 || op == 1, "bad op %d (matvec or fast residual)", op);
+    EBS_REQUIRE(n_list >= 0 && (chunks || n_list == 0), "bad chunk list");
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(op == 0 || p->has_be, "residual needs an operator loaded with b_e");
+    const uint8_t *fm = masked ? p->free_int : nullptr;
+    if (op == 0) launch_sell_op<0>(p, x_int, fm, out_map, out, S(stream), s_raw, chunks, n_list);
+    else launch_sell_op<1>(p, x_int, fm, out_map, out, S(stream), s_raw, chunks, n_list);
     EBS_CATCH
 }
 

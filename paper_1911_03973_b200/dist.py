@@ -243,6 +243,12 @@ class GpuRankOperator:
         call("ebs_plan_apply_map", self.plan.handle, 1, D.ptr(x_int), D.ptr(r_global),
              D.ptr(self.global_of_int32), D.ptr(s_raw), 0, D.stream())
 
+    def residual_caller_sweep(self, chunks, x_int, r_global, s_raw):
+        """residual_caller_partial over the SELL chunks in `chunks` only."""
+        call("ebs_plan_apply_map_chunks", self.plan.handle, 1, D.ptr(chunks), chunks.numel(),
+             D.ptr(x_int), D.ptr(r_global), D.ptr(self.global_of_int32), D.ptr(s_raw), 0,
+             D.stream())
+
     def correct_owned(self, r_global, recvs: dict):
         """Owned interface entries: add the neighbours' partial residuals."""
         for q in sorted(recvs):
@@ -366,19 +372,31 @@ def setup(ops, comm, precondition=True) -> DistProblem:
 
 
 def residual_caller(prob: DistProblem, x_global: torch.Tensor, r_globals: list, x_ints: list,
-                    s_raws: list):
+                    s_raws: list, overlap: bool = True):
     """r = b - A x with x and r in the caller's (global) numbering on P ranks, fused: one
     SELL pass per rank writes its slab's partial residual b_p - s_p straight into r
     (caller numbering) and keeps a copy in internal order; after the halo exchange each
     rank adds its neighbours' partial residuals on the interface nodes it owns (in
     ascending rank order).  Owned entries of r_globals[i] are the residual (within
-    rounding of the reassociated sum)."""
+    rounding of the reassociated sum).  overlap: sweep the interface chunks first and
+    the interior chunks while the halo exchange is in flight (same values)."""
     ops, comm = prob.ops, prob.comm
-    for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
-        op.gather_global(x_global, xi)
-        op.residual_caller_partial(xi, rg, sr)
-    sends = [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()} for op, sr in zip(ops, s_raws)]
-    recvs = comm.exchange(ops, sends)
+    if overlap:  # interface chunks, exchange in flight || interior chunks
+        for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
+            op.gather_global(x_global, xi)
+            op.residual_caller_sweep(op.if_chunks, xi, rg, sr)
+        h = comm.exchange_start(ops, [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()}
+                                      for op, sr in zip(ops, s_raws)])
+        for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
+            op.residual_caller_sweep(op.in_chunks, xi, rg, sr)
+        recvs = comm.exchange_finish(h)
+    else:
+        for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
+            op.gather_global(x_global, xi)
+            op.residual_caller_partial(xi, rg, sr)
+        sends = [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()}
+                 for op, sr in zip(ops, s_raws)]
+        recvs = comm.exchange(ops, sends)
     for op, rg, rc in zip(ops, r_globals, recvs):
         op.correct_owned(rg, rc)
 
@@ -635,16 +653,18 @@ def bench_rank(args, rank, world, local_rank):
 
     def step(ev=None):
         # r = b - A x in the caller's (permuted) numbering, as the 1-GPU residual: gather
-        # the slab's x, one SELL pass writing the partial residual into caller numbering
-        # (+ internal copy), NCCL halo of the partials, owned interface entries completed
+        # the slab's x; SELL pass over the interface chunks writing the partial residual
+        # into caller numbering (+ internal copy); NCCL halo of the interface partials in
+        # flight while the interior chunks are swept; owned interface entries completed
         op.gather_global(x_glob, x_int)
         if ev is not None:
             ev[0].record(stream)
-        op.residual_caller_partial(x_int, r_glob, s)
+        op.residual_caller_sweep(op.if_chunks, x_int, r_glob, s)
+        h = comm.exchange_start([op], [{q: op.gather(idx, s) for q, idx in op.if_idx.items()}])
+        op.residual_caller_sweep(op.in_chunks, x_int, r_glob, s)
         if ev is not None:
             ev[1].record(stream)
-        sends = [{q: op.gather(idx, s) for q, idx in op.if_idx.items()}]
-        recvs = comm.exchange([op], sends)
+        recvs = comm.exchange_finish(h)
         op.correct_owned(r_glob, recvs[0])
 
     for _ in range(max(3, args.warmup)):

@@ -100,17 +100,21 @@ def test_fused_caller_numbering_residual(gpu, P):
         m, batch = pr["mesh"], pr["batch"]
         prob, _ = dist.emulate(batch, m.n_nodes, None, P)
         x = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, m.n_nodes)).cuda()
-        rg = [torch.full((m.n_nodes,), float("nan"), dtype=torch.float64, device="cuda")
-              for _ in prob.ops]
-        xi = [op.zeros() for op in prob.ops]
-        sr = [op.zeros() for op in prob.ops]
-        dist.residual_caller(prob, x, rg, xi, sr)
-        out = torch.empty(m.n_nodes, dtype=torch.float64, device="cuda")
-        for op, r in zip(prob.ops, rg):
-            own = op.owned_glob
-            out[own] = r[own]
         ref = eb.residual(batch, x, deterministic=False)
-        assert float((out - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+        outs = []
+        for overlap in (True, False):
+            rg = [torch.full((m.n_nodes,), float("nan"), dtype=torch.float64, device="cuda")
+                  for _ in prob.ops]
+            xi = [op.zeros() for op in prob.ops]
+            sr = [op.zeros() for op in prob.ops]
+            dist.residual_caller(prob, x, rg, xi, sr, overlap=overlap)
+            out = torch.empty(m.n_nodes, dtype=torch.float64, device="cuda")
+            for op, r in zip(prob.ops, rg):
+                own = op.owned_glob
+                out[own] = r[own]
+            assert float((out - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+            outs.append(out)
+        assert torch.equal(outs[0], outs[1])  # the chunk split does not change any value
 
 
 @pytest.mark.parametrize("P", [2, 3])
