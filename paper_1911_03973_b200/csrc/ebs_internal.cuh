@@ -145,7 +145,9 @@ struct Plan {
     Perm2 perm[2];  // 0: caller -> internal, 1: internal -> caller (built on first use)
     double *partials = nullptr;  // reduction partials
     Ctl *ctl = nullptr;          // device control block
-    Ctl *ctl_host = nullptr;     // pinned mirror
+    Ctl *ctl_host = nullptr;     // pinned mirror: [0] synchronous reads, [1..2] batch ring
+    cudaStream_t cap_stream = nullptr;   // CUDA-graph capture of solver batches (solve.cu)
+    cudaEvent_t ring_ev[2] = {nullptr, nullptr};
     double *hist_dev = nullptr;  // device history (norms, errors)
     int64_t hist_cap = 0;
     int32_t *flag = nullptr;     // device scratch flag

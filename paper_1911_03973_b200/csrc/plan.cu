@@ -432,6 +432,12 @@ static void plan_free(Plan *p) {
     perm_free(p);
     if (p->ctl_host) cudaFreeHost(p->ctl_host);
     p->ctl_host = nullptr;
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    p->cap_stream = nullptr;
+    for (auto &e : p->ring_ev) {
+        if (e) cudaEventDestroy(e);
+        e = nullptr;
+    }
 }
 
 }  // namespace ebs
@@ -616,7 +622,7 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     // control block + reduction scratch
     p->ctl = dmalloc<Ctl>(1);
     CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
-    CU(cudaMallocHost(&p->ctl_host, sizeof(Ctl)));
+    CU(cudaMallocHost(&p->ctl_host, 3 * sizeof(Ctl)));  // [0] synchronous reads, [1..2] ring
     p->partials = dmalloc<double>(4 * 8192);
     p->free_int = dmalloc<uint8_t>(n_n);
     if (n_n) {

@@ -396,6 +396,85 @@ static void ensure_hist(Plan *p, int64_t n) {
 
 using namespace ebs;
 
+
+#ifndef EBS_SOLVE_GRAPH
+#define EBS_SOLVE_GRAPH 1  // replay 32-iteration batches from a captured CUDA graph
+#endif
+
+// Runs iterations [k0, iters) of a device-controlled solver loop in batches of `batch`:
+// `body(st)` enqueues one iteration on stream st (every launch identical -- the
+// iteration index and stop state live in the device control block).  Full batches after
+// the first are replayed from a CUDA graph captured on the plan's capture stream; one
+// batch stays queued ahead of the host's look at the stop flag (no per-batch bubble).
+// Returns the first iteration index not enqueued; *done = the device stopped the loop.
+template <class Body>
+static int run_batches(Plan *p, int k0, int iters, int batch, cudaStream_t s, Body body,
+                       bool *done) {
+    int k = k0;
+    *done = false;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    const bool use_graph = EBS_SOLVE_GRAPH && iters - k0 >= 3 * batch;
+    if (!p->ring_ev[0]) {
+        for (auto &e : p->ring_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    int pending = -1;  // ring slot of the batch whose stop flag has not been read yet
+    int slot = 0;
+    int64_t per_batch = 0;
+    try {
+        while (k < iters && !*done) {
+            const int kend = k + batch < iters ? k + batch : iters;
+            if (use_graph && kend - k == batch && k > k0) {
+                if (!exec) {
+                    if (!p->cap_stream)
+                        CU(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+                    const int64_t c0 = bump_launches(0);
+                    CU(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+                    try {
+                        for (int u = 0; u < batch; ++u) body(p->cap_stream);
+                    } catch (...) {
+                        cudaStreamEndCapture(p->cap_stream, &graph);
+                        throw;
+                    }
+                    CU(cudaStreamEndCapture(p->cap_stream, &graph));
+                    CU(cudaGraphInstantiate(&exec, graph, 0));
+                    per_batch = bump_launches(0) - c0;  // captured, not run: count at replay
+                    bump_launches(-per_batch);
+                }
+                CU(cudaGraphLaunch(exec, s));
+                bump_launches(per_batch);
+            } else {
+                for (int u = k; u < kend; ++u) body(s);
+            }
+            k = kend;
+            CU(cudaMemcpyAsync(p->ctl_host + 1 + slot, p->ctl, sizeof(Ctl),
+                               cudaMemcpyDeviceToHost, s));
+            CU(cudaEventRecord(p->ring_ev[slot], s));
+            if (pending >= 0) {
+                CU(cudaEventSynchronize(p->ring_ev[pending]));
+                *done = p->ctl_host[1 + pending].done != 0;
+            }
+            pending = slot;
+            slot ^= 1;
+        }
+        if (pending >= 0 && !*done) {
+            CU(cudaEventSynchronize(p->ring_ev[pending]));
+            *done = p->ctl_host[1 + pending].done != 0;
+        }
+    } catch (...) {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        cudaStreamSynchronize(s);
+        throw;
+    }
+    if (exec) {
+        CU(cudaStreamSynchronize(s));
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+    }
+    return k;
+}
+
 extern "C" {
 
 int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
@@ -472,12 +551,12 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         }
         const bool exact = P->exact != 0;
         double *rcb = (cb || P->r_out) ? r_int : nullptr;
-        auto step = [&](int final_step) {
+        auto step = [&](int final_step, cudaStream_t st) {
 #define EBS_JAC(NB_, PK_, EX_)                                                              \
     {                                                                                       \
         auto kern = k_jacobi_step<NB_, PK_, EX_>;                                           \
         const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
-        kern<<<SL.grid, SL.block, SL.smem, s>>>(v, L, xa, xb, p->b_int, p->free_int, dv,    \
+        kern<<<SL.grid, SL.block, SL.smem, st>>>(v, L, xa, xb, p->b_int, p->free_int, dv,   \
                                                  ref_int, rcb,                              \
                                  final_step, P->method, coef_a, coef_b, pbuf);              \
     }
@@ -489,9 +568,13 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         };
         int k = 0;
         bool done = false;
+        if (!cb) {
+            k = run_batches(p, 0, iters, batch, s, [&](cudaStream_t st) { step(0, st); }, &done);
+            read_ctl();  // final_buf below
+        }
         while (k < iters && !done && !aborted) {
             int kend = k + batch < iters ? k + batch : iters;
-            for (; k < kend; ++k) step(0);
+            for (; k < kend; ++k) step(0, s);
             read_ctl();
             done = p->ctl_host->done != 0;
             if (cb && p->ctl_host->cb_ok) {
@@ -501,7 +584,7 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
             }
         }
         if (!done && !aborted) {
-            step(1);
+            step(1, s);
             read_ctl();
             if (cb) do_callback(((iters & 1) ? xb : xa), iters);
         }
@@ -533,28 +616,30 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
             read_ctl();
             do_callback(xa, 0);
         }
-        int k = 0;
-        bool done = false;
-        while (k < iters && !done && !aborted) {
-            int kend = k + batch < iters ? k + batch : iters;
-            for (; k < kend; ++k) {
-                {
-                    PcgMatvecEpi me{p->free_int, qv, {0.0}};
+        auto iteration = [&](cudaStream_t st) {
+            {
+                PcgMatvecEpi me{p->free_int, qv, {0.0}};
 #define EBS_MV(NB_, PK_)                                                                    \
     {                                                                                       \
         auto kern = k_pcg_matvec<NB_, PK_>;                                                 \
         const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
-        kern<<<SL.grid, SL.block, SL.smem, s>>>(v, L, pv, me);                              \
+        kern<<<SL.grid, SL.block, SL.smem, st>>>(v, L, pv, me);                             \
     }
-                    EBS_SELL_DISPATCH(p, EBS_MV);
+                EBS_SELL_DISPATCH(p, EBS_MV);
 #undef EBS_MV
-                }
-                LAUNCHED();
-                k_pcg_update<<<vgrid, 256, 0, s>>>(n, L, xa, r_int, pv, qv, dinv, ref_int);
-                LAUNCHED();
-                k_pcg_direction<<<grid_for(n, 256), 256, 0, s>>>(n, p->ctl, pv, r_int, dinv);
-                LAUNCHED();
             }
+            LAUNCHED();
+            k_pcg_update<<<vgrid, 256, 0, st>>>(n, L, xa, r_int, pv, qv, dinv, ref_int);
+            LAUNCHED();
+            k_pcg_direction<<<grid_for(n, 256), 256, 0, st>>>(n, p->ctl, pv, r_int, dinv);
+            LAUNCHED();
+        };
+        int k = 0;
+        bool done = false;
+        if (!cb) k = run_batches(p, 0, iters, batch, s, iteration, &done);
+        while (k < iters && !done && !aborted) {
+            int kend = k + batch < iters ? k + batch : iters;
+            for (; k < kend; ++k) iteration(s);
             read_ctl();
             done = p->ctl_host->done != 0;
             if (cb && p->ctl_host->cb_ok) do_callback(xa, p->ctl_host->n_norms - 1);
