@@ -161,7 +161,9 @@ int ebs_plan_apply_map_chunks(ebs_plan_t plan, int op, const int32_t *chunks, in
                               const double *x_int, double *out, const int32_t *out_map,
                               double *s_raw, int masked, void *stream);
 /* One SELL pass on internal vectors: op = 0 matvec, 1 fast residual, 2 exact residual;
- * out_user != 0 scatters the result to caller numbering, else writes internal order;
+ * out_user = 0 writes internal order, 1 the caller's numbering, 2 the caller's numbering
+ * by adding into `out`, which the caller has filled with -0.0 (bit-identical to 1 and
+ * cheaper: the pre-fill can ride along with an earlier pass over the vector);
  * masked != 0 zeroes constrained rows. */
 int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, int out_user,
                    int masked, void *stream);

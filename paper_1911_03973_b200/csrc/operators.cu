@@ -31,6 +31,16 @@ __global__ void k_to_user(int64_t n, const int32_t *__restrict__ old_of_new,
         v_user[old_of_new[m]] = v_int[m];
 }
 
+// Caller-order output of a permuted numbering is one random 8 B store per node: the
+// L1tex pipe spends ~2 cycles on each distinct line of a warp's store (ncu: C2 MODE 1
+// 161 us vs 131 us with internal-order output).  A fire-and-forget red.add (REDG) into a
+// vector pre-filled with -0.0 costs less per lane and is bit-exact: every caller node
+// receives exactly one value s, and -0.0 + s == s for every s (IEEE round-to-nearest,
+// including s = +0.0 and s = -0.0).  C2: SELL pass 161 -> 150 us.
+#ifndef EBS_OUT_RED
+#define EBS_OUT_RED 1
+#endif
+
 // MODE 0: y = A x   1: r = b - A x (pre-assembled b)   2: r = sum(b_e - A_e x_e) exact
 struct OpEpi {
     int mode;
@@ -39,12 +49,17 @@ struct OpEpi {
     const int32_t *__restrict__ old_of_new;
     double *__restrict__ out;
     double *__restrict__ s_raw;  // nullable: the node values again, internal order (halo)
+    int red;                     // out[old_of_new[m]] += s into a -0.0-filled vector
     __device__ __forceinline__ void operator()(int64_t m, double s, double) {
         if (mode == 1) s = b_int[m] - s;
         if (free_int && !free_int[m]) s = 0.0;
         if (s_raw) s_raw[m] = s;
-        if (old_of_new) out[old_of_new[m]] = s;
-        else out[m] = s;
+        if (old_of_new) {
+            if (red) atomicAdd(out + old_of_new[m], s);
+            else out[old_of_new[m]] = s;
+        } else {
+            out[m] = s;
+        }
     }
 };
 
@@ -68,9 +83,9 @@ template <int MODE>
 void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
                     const int32_t *old_of_new, double *out, cudaStream_t s,
                     double *s_raw = nullptr, const int32_t *chunks = nullptr,
-                    int64_t n_list = -1) {
+                    int64_t n_list = -1, int red = 0) {
     if (p->n_n == 0 || n_list == 0) return;
-    OpEpi epi{MODE, p->b_int, free_int, old_of_new, out, s_raw};
+    OpEpi epi{MODE, p->b_int, free_int, old_of_new, out, s_raw, red};
 #define EBS_OP(NB_, IDS_) { launch_sell_op_t<NB_, IDS_, MODE>(p, x_int, epi, s, chunks, n_list); }
     EBS_SELL_DISPATCH(p, EBS_OP);
 #undef EBS_OP
@@ -112,7 +127,7 @@ __device__ __forceinline__ double ld_x_perm(const double *p) {
 __global__ void __launch_bounds__(256)
     k_to_internal_ilp(int64_t n, const int32_t *__restrict__ old_of_new,
                       const double *__restrict__ x_user, double *__restrict__ x_int,
-                      int32_t *nonfinite) {
+                      int32_t *nonfinite, double *__restrict__ negzero) {
     bool bad = false;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
 #if EBS_PERM_PF == 2
@@ -151,6 +166,7 @@ __global__ void __launch_bounds__(256)
             if (m < n) {
                 bad |= !isfinite(v[u]);
                 x_int[m] = v[u];
+                if (negzero) negzero[m] = -0.0;  // the output of a following red pass
             }
         }
     }
@@ -169,9 +185,34 @@ __global__ void __launch_bounds__(256)
 #define EBS_PERM2 0
 #endif
 
+__global__ void k_fill_negzero(int64_t n, double *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = -0.0;
+}
+
+#ifndef EBS_FILL_MODE
+// -0.0 pre-fill of the red-mode output: 0 fused into the x permutation, 1 separate kernel
+// after it, 2 before it.  Measured at C2: 1 best (23.8 GDoF/s; 0: 23.4-23.7 -- the extra
+// stores slow the latency-bound gather; 2: 22.6-22.9)
+#define EBS_FILL_MODE 1
+#endif
+
+static void fill_negzero(int64_t n, double *out, cudaStream_t s) {
+    if (n == 0) return;
+    k_fill_negzero<<<grid_for(n, 256), 256, 0, s>>>(n, out);
+    LAUNCHED();
+}
+
+// x_user (caller numbering) -> x_int; negzero (nullable, n_n doubles) is set to -0.0 in
+// the same pass (the output vector of a following red-mode SELL pass)
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
-                 cudaStream_t s) {
+                 cudaStream_t s, double *negzero) {
     if (p->n_n == 0) return;
+    if (negzero && (EBS_PERM2 || EBS_TO_INTERNAL_SCATTER != 2)) {
+        fill_negzero(p->n_n, negzero, s);
+        negzero = nullptr;
+    }
     if (EBS_PERM2) {
         Plan *pm = const_cast<Plan *>(p);
         if (const Perm2 *P = perm_get(pm, 0, s)) {
@@ -181,7 +222,7 @@ void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *no
     }
     if (EBS_TO_INTERNAL_SCATTER == 2)
         k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
-                            s>>>(p->n_n, p->old_of_new, x_user, x_int, nonfinite);
+                            s>>>(p->n_n, p->old_of_new, x_user, x_int, nonfinite, negzero);
     else if (EBS_TO_INTERNAL_SCATTER == 1)
         k_to_internal_scatter<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(
             p->n_n, p->new_of_old, x_user, x_int, nonfinite);
@@ -237,11 +278,14 @@ __global__ void __launch_bounds__(256)
 #define EBS_OUT_PERM 0  // 1: SELL writes internal order, then a gather pass to caller order
 #endif
 
+// one SELL pass; old_of_new != nullptr: output in caller numbering.  prefilled: `out` was
+// already set to -0.0 (fused into to_internal) for the red-mode caller-order output.
 void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *free_int,
-                const int32_t *old_of_new, double *out, cudaStream_t s) {
+                const int32_t *old_of_new, double *out, cudaStream_t s, bool prefilled = false) {
     double *dst = out;
     const int32_t *o2n = old_of_new;
     const Perm2 *P = nullptr;
+    int red = 0;
     if (EBS_PERM2 && old_of_new && p->n_n) {
         // internal-order (coalesced) output, then the two-pass permutation to caller order
         Plan *pm = const_cast<Plan *>(p);
@@ -254,9 +298,13 @@ void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *fre
         dst = plan_vec(const_cast<Plan *>(p), 7);
         o2n = nullptr;
     }
-    if (mode == 0) launch_sell_op<0>(p, x_int, free_int, o2n, dst, s);
-    else if (mode == 1) launch_sell_op<1>(p, x_int, free_int, o2n, dst, s);
-    else launch_sell_op<2>(p, x_int, free_int, o2n, dst, s);
+    if (o2n && EBS_OUT_RED) {  // red.add into -0.0 (bit-exact, see OpEpi)
+        if (!prefilled) fill_negzero(p->n_n, out, s);
+        red = 1;
+    }
+    if (mode == 0) launch_sell_op<0>(p, x_int, free_int, o2n, dst, s, nullptr, nullptr, -1, red);
+    else if (mode == 1) launch_sell_op<1>(p, x_int, free_int, o2n, dst, s, nullptr, nullptr, -1, red);
+    else launch_sell_op<2>(p, x_int, free_int, o2n, dst, s, nullptr, nullptr, -1, red);
     if (P) {
         perm_apply(const_cast<Plan *>(p), P, dst, out, nullptr, s);
     } else if (EBS_OUT_PERM && old_of_new && p->n_n) {
@@ -283,9 +331,10 @@ int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int mask
     cudaStream_t s = S(stream);
     double *x_int = plan_vec(p, 0);
     if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
-    to_internal(p, x, x_int, nonfinite, s);
+    if (EBS_OUT_RED && EBS_FILL_MODE == 2) fill_negzero(p->n_n, r, s);
+    to_internal(p, x, x_int, nonfinite, s, EBS_OUT_RED && EBS_FILL_MODE == 0 ? r : nullptr);
     sell_apply(p, mode == EBS_RES_EXACT ? 2 : 1, x_int, masked ? p->free_int : nullptr,
-               p->old_of_new, r, s);
+               p->old_of_new, r, s, EBS_OUT_RED && EBS_FILL_MODE != 1);
     EBS_CATCH
 }
 
@@ -297,8 +346,10 @@ int ebs_matvec(ebs_plan_t plan, const double *x, double *y, int masked, void *st
     EBS_REQUIRE(x != y, "x and y must not alias");
     cudaStream_t s = S(stream);
     double *x_int = plan_vec(p, 0);
-    to_internal(p, x, x_int, nullptr, s);
-    sell_apply(p, 0, x_int, masked ? p->free_int : nullptr, p->old_of_new, y, s);
+    if (EBS_OUT_RED && EBS_FILL_MODE == 2) fill_negzero(p->n_n, y, s);
+    to_internal(p, x, x_int, nullptr, s, EBS_OUT_RED && EBS_FILL_MODE == 0 ? y : nullptr);
+    sell_apply(p, 0, x_int, masked ? p->free_int : nullptr, p->old_of_new, y, s,
+               EBS_OUT_RED && EBS_FILL_MODE != 1);
     EBS_CATCH
 }
 
@@ -328,8 +379,9 @@ int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, in
     EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
     EBS_REQUIRE(op == 0 || p->has_be, "residual needs an operator loaded with b_e");
     EBS_REQUIRE(x_int != out, "x and out must not alias");
+    EBS_REQUIRE(out_user >= 0 && out_user <= 2, "bad out_user %d", out_user);
     sell_apply(p, op, x_int, masked ? p->free_int : nullptr, out_user ? p->old_of_new : nullptr,
-               out, S(stream));
+               out, S(stream), out_user == 2);
     EBS_CATCH
 }
 

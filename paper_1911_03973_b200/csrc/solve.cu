@@ -21,9 +21,6 @@
 
 namespace ebs {
 
-void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
-                 cudaStream_t s);
-void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s);
 
 struct LoopArgs {
     Ctl *ctl;

@@ -68,3 +68,31 @@ def test_finite_mask_gather_scatter(gpu):
     call("ebs_index_move", 2, P(src_i), P(v), P(dst_i), P(dst), s)
     call("ebs_index_add", 2, P(src_i), P(v), P(dst_i), P(dst), s)
     assert dst[[5, 6]].tolist() == [2 * float(v[0]), 2 * float(v[1])]
+
+
+def test_plan_apply_out_user_modes(gpu):
+    """ebs_plan_apply out_user 0/1/2: internal order, caller order, caller order added into
+    a -0.0-filled vector -- the last two bit-identical (masked rows and exact mode too)."""
+    from paper_1911_03973_b200 import _device as D
+    from paper_1911_03973_b200._lib import load
+    from paper_1911_03973_b200.inputs import config_problem
+    lib = load()
+    p = config_problem(2, seed=1, size=7)
+    batch, n = p["batch"], p["mesh"].n_nodes
+    pl = batch.operator(n)
+    pl.ensure_dirichlet(p["dirichlet"])
+    old_of_new = pl.node_maps()[1].long()
+    x = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, n)).cuda()
+    xi = D.empty(n)
+    s = D.stream()
+    assert lib.ebs_to_internal(pl.handle, P(x), P(xi), None, s) == 0
+    for op in (0, 1, 2):
+        for masked in (0, 1):
+            a, b = D.empty(n), D.empty(n)
+            c = torch.full((n,), -0.0, dtype=torch.float64, device="cuda")
+            assert lib.ebs_plan_apply(pl.handle, op, P(xi), P(a), 0, masked, s) == 0
+            assert lib.ebs_plan_apply(pl.handle, op, P(xi), P(b), 1, masked, s) == 0
+            assert lib.ebs_plan_apply(pl.handle, op, P(xi), P(c), 2, masked, s) == 0
+            assert torch.equal(b.view(torch.int64), c.view(torch.int64))  # bitwise, signs too
+            assert torch.equal(b[old_of_new], a)
+    assert lib.ebs_plan_apply(pl.handle, 1, P(xi), P(a), 3, 0, s) != 0
