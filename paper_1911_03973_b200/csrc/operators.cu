@@ -185,10 +185,19 @@ __global__ void __launch_bounds__(256)
 #define EBS_PERM2 0
 #endif
 
+// out[0..n) = -0.0 with 16 B stores (scalar head / tail for an unaligned or odd range)
 __global__ void k_fill_negzero(int64_t n, double *__restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+    const int64_t head = (reinterpret_cast<uintptr_t>(out) & 15) ? 1 : 0;
+    const int64_t n2 = n > head ? (n - head) / 2 : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (head && n > 0) out[0] = -0.0;
+        if (n > head && ((n - head) & 1)) out[n - 1] = -0.0;
+    }
+    double2 *o2 = reinterpret_cast<double2 *>(out + head);
+    const double2 v = make_double2(-0.0, -0.0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
          i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = -0.0;
+        o2[i] = v;
 }
 
 #ifndef EBS_FILL_MODE
@@ -200,7 +209,7 @@ __global__ void k_fill_negzero(int64_t n, double *__restrict__ out) {
 
 static void fill_negzero(int64_t n, double *out, cudaStream_t s) {
     if (n == 0) return;
-    k_fill_negzero<<<grid_for(n, 256), 256, 0, s>>>(n, out);
+    k_fill_negzero<<<grid_for((n + 1) / 2, 256, 148 * 8), 256, 0, s>>>(n, out);
     LAUNCHED();
 }
 
