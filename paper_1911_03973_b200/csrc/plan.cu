@@ -191,21 +191,24 @@ __global__ void __launch_bounds__(128)
         const int c_m = m < n_n ? cnt[m] : 0;
         const int wd = width[c];
         const int64_t row0 = rowbase[c];
-        for (int k = 0; k < c_m; ++k)
+        bool full = false;
+        for (int k = 0; k < c_m && !full; ++k)
             for (int t = 0; t < nb - 1; ++t) {
                 const int32_t d = (ids_abs[((row0 + k) * (nb - 1) + t) * 32 + lane] & ID_MASK) - (int32_t)m;
                 int h = tab_hash(d);
-                while (true) {
-                    int32_t old = atomicCAS(&key[h], TAB_EMPTY, d);
-                    if (old == TAB_EMPTY || old == d) break;
+                bool placed = false;
+                for (int probe = 0; probe < TAB_HASH && !placed; ++probe) {  // bounded: a
+                    int32_t old = atomicCAS(&key[h], TAB_EMPTY, d);           // full hash
+                    placed = old == TAB_EMPTY || old == d;                    // = overflow
                     h = (h + 1) & (TAB_HASH - 1);
                 }
+                full |= !placed;
             }
         __syncwarp();
         int K = 0;
         for (int h = lane; h < TAB_HASH; h += 32) K += key[h] != TAB_EMPTY;
         for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
-        if (K > cap) {
+        if (__any_sync(0xffffffffu, full) || K > cap) {
             if (lane == 0) atomicOr(overflow, 1);
             continue;
         }
