@@ -14,6 +14,10 @@
  *   - All array pointers are DEVICE pointers owned by the caller (torch); the library
  *     never frees caller memory.  `stream` is a cudaStream_t (NULL = legacy default).
  *     Calls are asynchronous on `stream` unless stated otherwise.
+ *   - A plan may be shared by host threads and streams: calls that use its device
+ *     workspace are serialised on the device in call order (a call on a new stream
+ *     waits for the previous call's work), as the reference allows concurrent
+ *     residual calls on a shared batch.
  *   - Connectivity is int32 structure-of-arrays `conn[j*n_e + e]` (j = local vertex),
  *     i.e. the reference `indt` (mesh.py:151-154) narrowed to int32.
  *   - Element matrices are element-major `A[(e*nb + i)*nb + j]`, the memory behind the

@@ -125,18 +125,54 @@ SellLaunch sell_launch(const void *kernel, int nb, int rowb, int64_t n_chunks) {
     return L;
 }
 
-// scratch for the standalone reductions (one per device is enough: stream-ordered use)
-static double *g_partials = nullptr;
-static unsigned int *g_counter = nullptr;
+OrderGuard::OrderGuard(StreamOrder &o, cudaStream_t s) : o_(o), s_(s), lk_(o.mu) {
+#ifdef EBS_NO_ORDER  // test builds only: demonstrates the race the guard prevents
+    return;
+#endif
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    active_ = st == cudaStreamCaptureStatusNone;
+    if (!active_) return;
+    if (!o_.ev) CU(cudaEventCreateWithFlags(&o_.ev, cudaEventDisableTiming));
+    if (o_.rec && o_.last != s) CU(cudaStreamWaitEvent(s, o_.ev, 0));
+}
+
+OrderGuard::~OrderGuard() {
+    if (!active_) return;
+    if (cudaEventRecord(o_.ev, s_) == cudaSuccess) {
+        o_.last = s_;
+        o_.rec = true;
+    } else {
+        cudaGetLastError();
+    }
+}
+
+// scratch for the standalone reductions, one per device; callers hold red_order(dev)
+constexpr int MAX_DEV = 64;
+static double *g_partials[MAX_DEV] = {};
+static unsigned int *g_counter[MAX_DEV] = {};
+static StreamOrder g_red_order[MAX_DEV];
+
+StreamOrder &red_order() {
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    return g_red_order[dev % MAX_DEV];
+}
 
 void reduce_scratch(double **partials, unsigned int **counter) {
-    if (!g_partials) {
-        CU(cudaMalloc(&g_partials, sizeof(double) * 4 * RED_MAX_BLOCKS));
-        CU(cudaMalloc(&g_counter, sizeof(unsigned int) * 4));
-        CU(cudaMemset(g_counter, 0, sizeof(unsigned int) * 4));
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    dev %= MAX_DEV;
+    if (!g_partials[dev]) {
+        CU(cudaMalloc(&g_partials[dev], sizeof(double) * 4 * RED_MAX_BLOCKS));
+        CU(cudaMalloc(&g_counter[dev], sizeof(unsigned int) * 4));
+        CU(cudaMemset(g_counter[dev], 0, sizeof(unsigned int) * 4));
     }
-    *partials = g_partials;
-    *counter = g_counter;
+    *partials = g_partials[dev];
+    *counter = g_counter[dev];
 }
 
 }  // namespace ebs
@@ -161,6 +197,7 @@ int ebs_dot(int64_t n, const double *x, const double *y, double *out, void *stre
     EBS_REQUIRE(n >= 0 && out, "ebs_dot: bad arguments");
     double *partials;
     unsigned int *counter;
+    OrderGuard order(red_order(), S(stream));
     reduce_scratch(&partials, &counter);
     k_dot<<<grid_for(n, RED_BLOCK, RED_MAX_BLOCKS), RED_BLOCK, 0, S(stream)>>>(
         n, x, y, partials, counter, out, 0);
@@ -173,6 +210,7 @@ int ebs_nrm2(int64_t n, const double *x, double *out, void *stream) {
     EBS_REQUIRE(n >= 0 && out, "ebs_nrm2: bad arguments");
     double *partials;
     unsigned int *counter;
+    OrderGuard order(red_order(), S(stream));
     reduce_scratch(&partials, &counter);
     k_dot<<<grid_for(n, RED_BLOCK, RED_MAX_BLOCKS), RED_BLOCK, 0, S(stream)>>>(
         n, x, x, partials, counter, out, 1);

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <mutex>
 #include <stdint.h>
 #include <cmath>
 #include <cstdio>
@@ -103,6 +105,32 @@ struct Ctl {
     double rz, pq, alpha, beta;
 };
 
+// Cross-stream ordering of a shared device workspace.  Calls that use a plan's (or the
+// process's) scratch vectors hold the mutex while enqueuing; a call on a different stream
+// than the previous one first waits for that call's work (event), so concurrent callers
+// on separate streams / host threads are serialised on the device in call order --
+// `residual` is safe to call concurrently on a shared batch (reference SPEC.md:273).
+// Not applied while the stream is being captured into a CUDA graph (the capture orders).
+struct StreamOrder {
+    std::recursive_mutex mu;  // recursive: a solver callback may call back into the plan
+    cudaEvent_t ev = nullptr;
+    cudaStream_t last = nullptr;
+    bool rec = false;
+};
+class OrderGuard {
+  public:
+    OrderGuard(StreamOrder &o, cudaStream_t s);
+    ~OrderGuard();
+    OrderGuard(const OrderGuard &) = delete;
+    OrderGuard &operator=(const OrderGuard &) = delete;
+
+  private:
+    StreamOrder &o_;
+    cudaStream_t s_;
+    bool active_ = false;
+    std::unique_lock<std::recursive_mutex> lk_;
+};
+
 // two-pass permutation schedule (perm.cu)
 struct Perm2 {
     int64_t n = 0;
@@ -143,6 +171,7 @@ struct Plan {
     // workspace (lazily grown)
     double *wvec[10] = {nullptr};
     Perm2 perm[2];  // 0: caller -> internal, 1: internal -> caller (built on first use)
+    StreamOrder order;  // cross-stream ordering of the workspace above
     double *partials = nullptr;  // reduction partials
     Ctl *ctl = nullptr;          // device control block
     Ctl *ctl_host = nullptr;     // pinned mirror: [0] synchronous reads, [1..2] batch ring
@@ -154,6 +183,7 @@ struct Plan {
 };
 
 double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)
+StreamOrder &red_order();           // ordering of the per-device reduction scratch
 // caller <-> internal numbering (operators.cu); negzero: also set that vector to -0.0
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
                  cudaStream_t s, double *negzero = nullptr);

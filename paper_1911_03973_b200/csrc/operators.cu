@@ -336,6 +336,7 @@ int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int mask
     EBS_TRY
     EBS_REQUIRE(plan && x && r, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
+    OrderGuard order(p->order, S(stream));
     EBS_REQUIRE(p->has_A && p->has_be, "residual needs an operator loaded with b_e");
     EBS_REQUIRE(mode == EBS_RES_EXACT || mode == EBS_RES_FAST, "bad residual mode %d", mode);
     EBS_REQUIRE(x != r, "x and r must not alias");
@@ -353,6 +354,7 @@ int ebs_matvec(ebs_plan_t plan, const double *x, double *y, int masked, void *st
     EBS_TRY
     EBS_REQUIRE(plan && x && y, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
+    OrderGuard order(p->order, S(stream));
     EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
     EBS_REQUIRE(x != y, "x and y must not alias");
     cudaStream_t s = S(stream);
@@ -369,6 +371,7 @@ int ebs_to_internal(ebs_plan_t plan, const double *x, double *x_int, int32_t *no
     EBS_TRY
     EBS_REQUIRE(plan && x && x_int, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
+    OrderGuard order(p->order, S(stream));
     if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), S(stream)));
     to_internal(p, x, x_int, nonfinite, S(stream));
     EBS_CATCH
@@ -377,7 +380,9 @@ int ebs_to_internal(ebs_plan_t plan, const double *x, double *x_int, int32_t *no
 int ebs_to_user(ebs_plan_t plan, const double *v_int, double *v, void *stream) {
     EBS_TRY
     EBS_REQUIRE(plan && v_int && v, "null argument");
-    to_user(reinterpret_cast<Plan *>(plan), v_int, v, S(stream));
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    OrderGuard order(p->order, S(stream));
+    to_user(p, v_int, v, S(stream));
     EBS_CATCH
 }
 
@@ -386,6 +391,7 @@ int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, in
     EBS_TRY
     EBS_REQUIRE(plan && x_int && out, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
+    OrderGuard order(p->order, S(stream));
     EBS_REQUIRE(op >= 0 && op <= 2, "bad op %d", op);
     EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
     EBS_REQUIRE(op == 0 || p->has_be, "residual needs an operator loaded with b_e");

@@ -437,6 +437,8 @@ static void plan_free(Plan *p) {
     p->ctl_host = nullptr;
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     p->cap_stream = nullptr;
+    if (p->order.ev) cudaEventDestroy(p->order.ev);
+    p->order.ev = nullptr;
     for (auto &e : p->ring_ev) {
         if (e) cudaEventDestroy(e);
         e = nullptr;
@@ -695,6 +697,7 @@ int ebs_plan_load(ebs_plan_t plan, const double *A_e, const double *b_e, void *s
     Plan *p = reinterpret_cast<Plan *>(plan);
     EBS_REQUIRE(A_e || p->n_e == 0, "null A_e");
     cudaStream_t s = S(stream);
+    OrderGuard order(p->order, s);
     const int64_t n_slots = p->n_rows * LANES;
     const bool want_be = b_e != nullptr || p->n_e == 0;  // an empty mesh has an (empty) b_e
     if (want_be && !p->slot_be) p->slot_be = dmalloc<double>(n_slots);
@@ -721,6 +724,7 @@ int ebs_plan_set_dirichlet(ebs_plan_t plan, const int64_t *nd, int64_t n_d, void
     EBS_REQUIRE(plan && n_d >= 0, "bad arguments");
     Plan *p = reinterpret_cast<Plan *>(plan);
     cudaStream_t s = S(stream);
+    OrderGuard order(p->order, s);
     if (p->n_n) {
         k_set_free<<<grid_for(p->n_n, 256), 256, 0, s>>>(p->n_n, p->free_int);
         LAUNCHED();

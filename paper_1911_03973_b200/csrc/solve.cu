@@ -478,6 +478,7 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
     EBS_TRY
     EBS_REQUIRE(plan && P, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
+    OrderGuard order(p->order, S(stream));
     EBS_REQUIRE(P->iters >= 0, "iteration count must be nonnegative, got %d", P->iters);
     EBS_REQUIRE(P->method >= EBS_RICHARDSON && P->method <= EBS_CHEB3, "bad method %d", P->method);
     EBS_REQUIRE(P->method != EBS_CHEB2 || P->coef_a || P->iters == 0, "CHEB2 needs coef_a");
@@ -671,6 +672,7 @@ int ebs_power_iteration(ebs_plan_t plan, const double *v0, int iters, double tol
     EBS_REQUIRE(plan && v0 && lam && its, "null argument");
     EBS_REQUIRE(iters >= 1, "need at least one iteration, got %d", iters);
     Plan *p = reinterpret_cast<Plan *>(plan);
+    OrderGuard order(p->order, S(stream));
     EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
     cudaStream_t s = S(stream);
     const int64_t n = p->n_n;

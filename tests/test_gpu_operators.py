@@ -214,3 +214,43 @@ def test_residual_many_pipelined(gpu):
     assert eb.residual_many(batch, np.empty((0, n))).shape == (0, n)
     with pytest.raises(ValueError):
         eb.residual_many(batch, xs[0])
+
+
+def test_concurrent_residuals_on_separate_streams(gpu):
+    """SPEC.md:273 of the reference: residual is safe to call concurrently on a shared
+    batch.  Host threads, each on its own CUDA stream, share one plan (and its device
+    workspace); every result equals the serial one bitwise."""
+    import threading
+    import torch
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(2, seed=6, size=9)
+    batch, n = p["batch"], p["mesh"].n_nodes
+    rng = np.random.default_rng(8)
+    xs = [torch.from_numpy(rng.uniform(-1, 1, n)).cuda() for _ in range(4)]
+    ref = [to_np(eb.residual(batch, x)) for x in xs]
+    torch.cuda.synchronize()
+    out = {}
+    errors = []
+
+    def work(t):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for rep in range(25):
+                    for i, x in enumerate(xs):
+                        r = eb.residual(batch, x, check_finite=False)
+                        out[(t, rep, i)] = r
+            st.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for (t, rep, i), r in out.items():
+        npt.assert_array_equal(to_np(r), ref[i], err_msg=f"thread {t} rep {rep} vector {i}")
