@@ -101,6 +101,15 @@ class TorchTransport:
         """sends[i] = {q: tensor} for local rank ops[i] (len 1 here) -> recvs {q: tensor}."""
         return self.exchange_finish(self.exchange_start(ops, sends))
 
+    def agree(self, ok: bool) -> bool:
+        """True iff `ok` on every rank (an eager all-reduce MIN, outside any capture)."""
+        if self.dist.get_world_size(self.group) == 1:
+            return bool(ok)
+        dev = "cpu" if (self.stage_host or self.dist.get_backend(self.group) == "gloo") else "cuda"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(int(t.item()))
+
     def allreduce(self, tensors: list):
         (t,) = tensors
         if self.stage_host and t.is_cuda:
@@ -127,6 +136,9 @@ class LocalTransport:
             for q, buf in sends[i].items():
                 recvs[ranks[q]][op.rank] = buf.clone()
         return recvs
+
+    def agree(self, ok: bool) -> bool:
+        return bool(ok)
 
     def allreduce(self, tensors: list):
         total = tensors[0].clone()
@@ -416,6 +428,35 @@ GRAPH_BATCH = 8  # iterations per captured CUDA graph (even: Jacobi ping-pong bu
 GRAPH_STATS = {"captured": 0, "fallback": 0, "last_error": None}
 
 
+def _capture(comm, body):
+    """Capture body() into a CUDA graph on every rank.  The decision is collective: the
+    graph is used only if every rank captured it (comm.agree), else all ranks drop it and
+    run eagerly -- ranks never mix graph replay with eager steps, whose NCCL calls would
+    not pair up.  EBS_DIST_GRAPH=0 disables capture."""
+    import os
+    if os.environ.get("EBS_DIST_GRAPH", "1") == "0":
+        return None
+    g, err = None, None
+    try:
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+    except Exception as e:  # noqa: BLE001 -- capture unsupported here: run eagerly
+        g, err = None, e
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+    agree = getattr(comm, "agree", None)
+    ok = agree(g is not None) if agree is not None else g is not None
+    if not ok:
+        GRAPH_STATS["fallback"] += 1
+        GRAPH_STATS["last_error"] = (f"{type(err).__name__}: {err}" if err is not None
+                                     else "another rank could not capture")
+        return None
+    GRAPH_STATS["captured"] += 1
+    return g
+
+
 def _graph_ok(ops) -> bool:
     return all(getattr(op, "n", 0) and torch.cuda.is_available() and
                isinstance(getattr(op, "free", None), torch.Tensor) and op.free.is_cuda for op in ops)
@@ -470,21 +511,12 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     k = 0
     if graph and iters >= B and _graph_ok(ops):
         bred = [torch.zeros(B, dtype=torch.float64, device=x.device) for x in xa]
-        g = None
-        try:
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                for u in range(B):  # B even: xa/xb roles return to the start
-                    src, dst = (xa, xb) if u % 2 == 0 else (xb, xa)
-                    step(src, dst, False, [r_[u:u + 1] for r_ in bred])
-        except Exception as e:  # capture unsupported here: run eagerly
-            g = None
-            GRAPH_STATS["fallback"] += 1
-            GRAPH_STATS["last_error"] = f"{type(e).__name__}: {e}"
-            torch.cuda.synchronize()
-        else:
-            GRAPH_STATS["captured"] += 1
+
+        def body():
+            for u in range(B):  # B even: xa/xb roles return to the start
+                src, dst = (xa, xb) if u % 2 == 0 else (xb, xa)
+                step(src, dst, False, [r_[u:u + 1] for r_ in bred])
+        g = _capture(comm, body)
         if g is not None:
             while k + B <= iters:
                 g.replay()
@@ -564,20 +596,11 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused
     k = 0
     if graph and tol is None and iters >= B and _graph_ok(ops):
         bh = [torch.zeros(B, dtype=torch.float64, device=dev) for _ in ops]
-        g = None
-        try:
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                for u in range(B):
-                    step([h[u:u + 1] for h in bh])
-        except Exception as e:
-            g = None
-            GRAPH_STATS["fallback"] += 1
-            GRAPH_STATS["last_error"] = f"{type(e).__name__}: {e}"
-            torch.cuda.synchronize()
-        else:
-            GRAPH_STATS["captured"] += 1
+
+        def body():
+            for u in range(B):
+                step([h[u:u + 1] for h in bh])
+        g = _capture(comm, body)
         if g is not None:
             while k + B <= iters:
                 g.replay()
@@ -681,21 +704,14 @@ def bench_rank(args, rank, world, local_rank):
     kern = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
     # timed pass: CUDA-graph replay of GRAPH_BATCH steps (eager fallback)
     GB = GRAPH_BATCH
-    graph = None
-    try:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for _ in range(GB):
-                step()
+
+    def body():
+        for _ in range(GB):
+            step()
+    graph = _capture(comm, body)
+    if graph is not None:
         graph.replay()
         torch.cuda.synchronize()
-    except Exception as e:  # noqa: BLE001
-        graph = None
-        GRAPH_STATS["fallback"] += 1
-        GRAPH_STATS["last_error"] = f"{type(e).__name__}: {e}"
-        torch.cuda.synchronize()
-    else:
-        GRAPH_STATS["captured"] += 1
     launches_per_step = None
     n0 = load().ebs_launch_count()
     step()

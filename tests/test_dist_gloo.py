@@ -103,3 +103,37 @@ def test_gloo_world2_matches_oracle(case):
     xp, hp = o.pcg(A, b_e, indt, nd, x0, 400, tol=1e-8)
     assert len(res["npcg"]) == len(hp["residual_norms"])
     assert np.linalg.norm(res["xp"] - xp) <= 1e-8 * np.linalg.norm(xp)
+
+
+def _agree_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_1911_03973_b200 import dist as D
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = D.TorchTransport()
+        res = [comm.agree(True), comm.agree(rank != 1), comm.agree(False)]
+        # a capture that cannot happen here (no CUDA) on every rank -> all ranks drop it
+        g = D._capture(comm, lambda: None)
+        out.put((rank, res, g is None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_graph_capture_decision_is_collective():
+    """dist._capture: the CUDA-graph decision is an all-ranks agreement (any rank that
+    cannot capture makes every rank run eagerly, so NCCL calls always pair up)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = sorted(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, res, dropped in got:
+        assert res == [True, False, False], (rank, res)
+        assert dropped
