@@ -201,7 +201,13 @@ __global__ void EBS_SELL_BOUNDS(NB)
     ctl->alpha = tot[0] != 0.0 ? ctl->rz / tot[0] : 0.0;
 }
 
-__global__ void __launch_bounds__(256, 3)
+#ifndef EBS_UPD_MINB
+#define EBS_UPD_MINB 3
+#endif
+#ifndef EBS_UPD_PERSIST
+#define EBS_UPD_PERSIST 1  // occupancy-sized grid, one wave (C3: 2775 -> 2824 it/s vs 1184 CTAs)
+#endif
+__global__ void __launch_bounds__(256, EBS_UPD_MINB)
     k_pcg_update(int64_t n, LoopArgs L, double *__restrict__ x, double *__restrict__ r,
                  const double *__restrict__ p, const double *__restrict__ q,
                  const double *__restrict__ dinv, const double *__restrict__ ref) {
@@ -509,6 +515,9 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
     const int block = 256;
     const int64_t sgrid = (p->n_chunks * LANES + block - 1) / block;
     const int vgrid = grid_for(n, 256, RED_MAX_BLOCKS);
+    const int ugrid = EBS_UPD_PERSIST
+                          ? persistent_grid((const void *)k_pcg_update, 256, (n + 255) / 256, 0)
+                          : vgrid;
     const bool cb = P->callback != nullptr;
     const int batch = cb ? 1 : 32;
     bool aborted = false;
@@ -627,7 +636,7 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
 #undef EBS_MV
             }
             LAUNCHED();
-            k_pcg_update<<<vgrid, 256, 0, st>>>(n, L, xa, r_int, pv, qv, dinv, ref_int);
+            k_pcg_update<<<ugrid, 256, 0, st>>>(n, L, xa, r_int, pv, qv, dinv, ref_int);
             LAUNCHED();
             k_pcg_direction<<<grid_for(n, 256), 256, 0, st>>>(n, p->ctl, pv, r_int, dinv);
             LAUNCHED();
