@@ -641,50 +641,37 @@ def emulate(batch, n_nodes, d, P, precondition=True):
 
 
 # ------------------------------------------------------------------- bench --
-def bench_rank(args, rank, world, local_rank):
-    """bench.py --gpus N under torchrun: the C2 residual strong-scaled over N element
-    slabs with the NCCL halo exchange; device-timed, max over ranks; rank 0 prints the
-    JSON line.  `value` = n_n * K / T_max (whole job); `e2e` adds each rank's host->device
-    copy of its x slab and device->host copy of its r slab inside the timed loop."""
-    import json
-    import os
+def _residual_measure(p, args, rank, world, comm, sampler):
+    """Time K residual steps r = b - A x (x, r in the caller's numbering) on `world`
+    element slabs of problem `p` (device time, max over ranks).  Returns a dict for rank
+    0's JSON line: per-step time, kernel time, launches, and the end-to-end time with
+    each rank's x slab copied in from pinned host memory and its owned r entries out."""
     import statistics
-    import sys
     import torch.distributed as dist
 
-    from .inputs import config_problem
-    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    import bench as B
-
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    peaks, peak_kind = B.load_peaks()
-    sampler = B.ClockSampler(index=local_rank).start()
-    p = config_problem(2, seed=args.seed, size=args.size, assemble=False)
     m = p["mesh"]
     op, maps = rank_operator(m, p["nu"], p["f"], None, world, rank)
-    comm = TorchTransport()
-    prob = setup([op], comm)
+    setup([op], comm)
     x_glob = torch.from_numpy(p["x"]).cuda()
-    x_int = op.to_internal(x_glob)
-    s, r = op.zeros(), op.zeros()
-    red = torch.zeros(1, dtype=torch.float64, device="cuda")
+    x_int = op.zeros()
+    s_raw = op.zeros()
     stream = torch.cuda.current_stream()
+    r_glob = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
     lo, hi = int(maps["bounds"][rank]), int(maps["bounds"][rank + 1])
 
-    r_glob = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
-
-    def step(ev=None):
-        # r = b - A x in the caller's (permuted) numbering, as the 1-GPU residual: gather
-        # the slab's x; SELL pass over the interface chunks writing the partial residual
-        # into caller numbering (+ internal copy); NCCL halo of the interface partials in
-        # flight while the interior chunks are swept; owned interface entries completed
-        op.gather_global(x_glob, x_int)
+    def step(ev=None, x_in=True):
+        # gather the slab's x (caller -> rank numbering); SELL pass over the interface
+        # chunks writing the partial residual into caller numbering (+ internal copy); NCCL
+        # halo of the interface partials in flight while the interior chunks are swept;
+        # owned interface entries completed with the neighbours' partials
+        if x_in:
+            op.gather_global(x_glob, x_int)
         if ev is not None:
             ev[0].record(stream)
-        op.residual_caller_sweep(op.if_chunks, x_int, r_glob, s)
-        h = comm.exchange_start([op], [{q: op.gather(idx, s) for q, idx in op.if_idx.items()}])
-        op.residual_caller_sweep(op.in_chunks, x_int, r_glob, s)
+        op.residual_caller_sweep(op.if_chunks, x_int, r_glob, s_raw)
+        h = comm.exchange_start([op], [{q: op.gather(idx, s_raw)
+                                        for q, idx in op.if_idx.items()}])
+        op.residual_caller_sweep(op.in_chunks, x_int, r_glob, s_raw)
         if ev is not None:
             ev[1].record(stream)
         recvs = comm.exchange_finish(h)
@@ -694,15 +681,13 @@ def bench_rank(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     sampler.on()
-    # per-kernel timing pass (eager, events around the SELL launch)
     dist.barrier()
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-    for k in range(args.steps):
+    for k in range(args.steps):  # per-kernel pass (eager, events around the SELL sweeps)
         step(evs[k])
     torch.cuda.synchronize()
     kern = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
-    # timed pass: CUDA-graph replay of GRAPH_BATCH steps (eager fallback)
     GB = GRAPH_BATCH
 
     def body():
@@ -712,7 +697,6 @@ def bench_rank(args, rank, world, local_rank):
     if graph is not None:
         graph.replay()
         torch.cuda.synchronize()
-    launches_per_step = None
     n0 = load().ebs_launch_count()
     step()
     torch.cuda.synchronize()
@@ -730,56 +714,107 @@ def bench_rank(args, rank, world, local_rank):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    launches = launches_per_step * args.steps
     dist.barrier()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3, kern], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    # end to end: this rank's x slab in from pinned host memory, its r slab out
-    x_host = x_int.cpu().pin_memory()
-    r_host = torch.empty(op.n, dtype=torch.float64).pin_memory()
+    # end to end: each rank's x slab (its local nodes) in from pinned host memory, its
+    # owned entries of r out to pinned host memory, every step
+    x_host = x_glob[op.global_of_int].cpu().pin_memory()
+    own = op.owned_glob
+    r_host = torch.empty(own.numel(), dtype=torch.float64).pin_memory()
     torch.cuda.synchronize()
     dist.barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for _ in range(args.steps):
         x_int.copy_(x_host, non_blocking=True)
-        step()
-        r_host.copy_(r, non_blocking=True)
+        step(x_in=False)
+        r_host.copy_(r_glob[own], non_blocking=True)
     e3.record(stream)
     torch.cuda.synchronize()
+    ref = r_glob[own].cpu()
+    assert torch.equal(r_host, ref), "end-to-end residual differs from the device-timed one"
+    te = torch.tensor([e2.elapsed_time(e3) / 1e3], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    byt = torch.tensor([8.0 * op.n, 8.0 * own.numel()], device="cuda")
+    dist.all_reduce(byt, op=dist.ReduceOp.SUM)
     sampler.off()
+    out = {"T": float(t[0]), "kern": float(t[1]), "te": float(te[0]),
+           "h2d": int(byt[0]), "d2h": int(byt[1]), "launches": launches_per_step * args.steps,
+           "n_nodes": m.n_nodes, "n_elements": m.n_elements,
+           "bytes_rank": __import__("bench").residual_bytes(op.n, hi - lo),
+           "graph": graph is not None}
+    del op, x_glob, x_int, s_raw, r_glob
+    torch.cuda.empty_cache()
+    return out
+
+
+def bench_rank(args, rank, world, local_rank):
+    """bench.py --gpus N under torchrun.  `value`: the C2 residual weak-scaled over N
+    element slabs -- N level-11 unit squares stacked in y (inputs.stacked_c2_problem), one
+    C2-sized slab per rank, the NCCL halo of the shared node rows -- whole-job GDoF/s =
+    total nodes x K / max-over-ranks device time.  Also reported: the fixed C2 mesh
+    strong-scaled over the same N slabs, and (extras) C4 / C5 solver strong scaling."""
+    import json
+    import os
+    import sys
+    import torch.distributed as dist
+
+    from .inputs import config_problem, stacked_c2_problem
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench as B
+
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    peaks, peak_kind = B.load_peaks()
+    sampler = B.ClockSampler(index=local_rank).start()
+    comm = TorchTransport()
+    weak = _residual_measure(stacked_c2_problem(world, seed=args.seed, size=args.size), args,
+                             rank, world, comm, sampler)
+    strong = None
+    if world > 1:
+        strong = _residual_measure(config_problem(2, seed=args.seed, size=args.size,
+                                                  assemble=False), args, rank, world, comm,
+                                   sampler)
     sampler.stop()
-    te = torch.tensor([e2.elapsed_time(e3) / 1e3, 8.0 * op.n], device="cuda")
-    dist.all_reduce(te[0:1], op=dist.ReduceOp.MAX)
-    dist.all_reduce(te[1:2], op=dist.ReduceOp.SUM)
-    T, K_max = float(t[0]), float(t[1])
-    n_loc_e = hi - lo
-    bytes_rank = B.residual_bytes(op.n, n_loc_e)
+    line = None
     if rank == 0:
         peak = float(peaks["hbm_gbs"])
-        line = {"metric": B.METRIC, "value": m.n_nodes * args.steps / T / 1e9, "unit": "GDoF/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        T = weak["T"]
+        line = {"metric": B.METRIC, "value": weak["n_nodes"] * args.steps / T / 1e9,
+                "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 mesh)",
-                "config": {"workload": "C2: 2D P1 unit square, level 11, permuted; element "
-                                       "residual r=b-Ax per step, element slabs + NCCL halo",
-                           "n_nodes": m.n_nodes, "n_elements": m.n_elements, "seed": args.seed,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 squares)",
+                "config": {"workload": f"C2 weak-scaled: {world} level-11 unit squares stacked "
+                                       "in y, one C2-sized element slab per GPU, NCCL halo of "
+                                       "the shared node rows; element residual r=b-Ax per step",
+                           "n_nodes": weak["n_nodes"], "n_elements": weak["n_elements"],
+                           "per_gpu": "one C2 square (4.2M nodes, 8.4M triangles)",
+                           "seed": args.seed,
                            "mode": "fast (pre-assembled b); x and r in the caller's numbering",
-                           "l2": "inputs larger than L2 per rank at N<=8 (~1/N GB slot stream)",
+                           "l2": "inputs larger than L2 (slot stream ~1 GB per rank); no flush",
                            "parallelism": f"element slabs x{world}",
                            "cuda_graph": dict(GRAPH_STATS)},
-                "roofline": {"bound": "hbm", "achieved": bytes_rank / K_max / 1e9, "peak": peak,
-                             "unit": "GB/s", "frac": bytes_rank / K_max / 1e9 / peak,
-                             "traffic": None, "kernel": "k_sell_op<3,1,0> (rank 0 slab)",
-                             "bytes_per_launch": bytes_rank, "kernel_ms": K_max * 1e3,
+                "roofline": {"bound": "hbm", "achieved": weak["bytes_rank"] / weak["kern"] / 1e9,
+                             "peak": peak, "unit": "GB/s",
+                             "frac": weak["bytes_rank"] / weak["kern"] / 1e9 / peak,
+                             "traffic": None,
+                             "kernel": "k_sell_op<3,1,1> over the slab's chunks (max over ranks)",
+                             "bytes_per_launch": weak["bytes_rank"], "kernel_ms": weak["kern"] * 1e3,
                              "peak_source": peak_kind},
-                "e2e": {"value": m.n_nodes * args.steps / float(te[0]) / 1e9, "unit": "GDoF/s",
-                        "h2d_bytes_per_step": int(te[1]), "d2h_bytes_per_step": int(te[1]),
-                        "api": "dist.residual step per rank with its x/r slab via pinned host"},
-                "gpu_launches": launches, "clocks": sampler.summary(), "cpu_baseline": None}
-    del op, prob, p, x_int, s, r
-    torch.cuda.empty_cache()
+                "e2e": {"value": weak["n_nodes"] * args.steps / weak["te"] / 1e9, "unit": "GDoF/s",
+                        "h2d_bytes_per_step": weak["h2d"], "d2h_bytes_per_step": weak["d2h"],
+                        "api": "per rank: x slab H2D from pinned host, dist residual step, "
+                               "owned r entries D2H to pinned host"},
+                "gpu_launches": weak["launches"], "clocks": sampler.summary(),
+                "cpu_baseline": None}
+        if strong is not None:
+            line["strong_c2"] = {
+                "value": strong["n_nodes"] * args.steps / strong["T"] / 1e9, "unit": "GDoF/s",
+                "ms_per_step": strong["T"] / args.steps * 1e3, "scaling": "strong",
+                "workload": "the fixed C2 mesh (4.2M nodes) over the same element slabs",
+                "kernel_ms": strong["kern"] * 1e3, "cuda_graph": strong["graph"]}
     solvers = {}
     if getattr(args, "extra", False):
         solvers = _bench_solvers(args, rank, world)

@@ -161,3 +161,40 @@ def test_fused_overlapped_steps_match_unfused(gpu, P):
                 assert torch.equal(a, b)
             else:
                 assert float((a - b).abs().max()) <= 1e-10 * float(b.abs().max())
+
+
+def test_stacked_c2_weak_scaling_input(gpu):
+    """bench.py's N>1 weak-scaling input: copies=1 is the C2 recipe exactly; with P copies
+    the element slabs np.linspace(0, n_e, P+1) are exactly one square each and the
+    distributed caller-numbering residual equals the single-GPU one."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem, stacked_c2_problem
+    a = stacked_c2_problem(1, seed=3, size=4)
+    b = config_problem(2, seed=3, size=4, assemble=False)
+    assert torch.equal(a["mesh"].nodes, b["mesh"].nodes)
+    assert torch.equal(a["mesh"].conn, b["mesh"].conn)
+    np.testing.assert_array_equal(a["x"], b["x"])
+    P, L = 3, 4
+    p = stacked_c2_problem(P, seed=3, size=L)
+    m = p["mesh"]
+    n = 2**L + 1
+    assert m.n_nodes == n * (2**L * P + 1) and m.n_elements == P * 2 * 4**L
+    assert float(m.nodes[:, 1].max()) == P
+    maps = dist.partition_maps(m.conn, m.n_nodes, P)
+    np.testing.assert_array_equal(maps["bounds"], [k * 2 * 4**L for k in range(P + 1)])
+    for r in range(P):
+        for q, ids in maps["interface"][r].items():
+            assert ids.numel() == n  # one shared node row per neighbour
+    batch = eb.build_element_batch(m, nu=p["nu"])
+    prob, _ = dist.emulate(batch, m.n_nodes, None, P)
+    x = torch.from_numpy(p["x"]).cuda()
+    rg = [torch.full((m.n_nodes,), float("nan"), dtype=torch.float64, device="cuda")
+          for _ in prob.ops]
+    dist.residual_caller(prob, x, rg, [op.zeros() for op in prob.ops],
+                         [op.zeros() for op in prob.ops])
+    out = torch.empty(m.n_nodes, dtype=torch.float64, device="cuda")
+    for op, r in zip(prob.ops, rg):
+        out[op.owned_glob] = r[op.owned_glob]
+    ref = eb.residual(batch, x, deterministic=False)
+    assert float((out - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
