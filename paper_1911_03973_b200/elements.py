@@ -10,6 +10,8 @@ oracle restatement (oracle/ebs_oracle.py element_matrices).
 
 from __future__ import annotations
 
+import contextlib
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -66,8 +68,24 @@ class ElementBatch:
     def operator(self, n_nodes: int | None = None, need_be: bool = True):
         """The execution plan of this batch's mesh with A_e (and b_e) packed."""
         pl = self.index.plan(n_nodes)
-        pl.ensure_loaded(self, need_be=need_be)
+        with pl.lock:
+            pl.ensure_loaded(self, need_be=need_be)
         return pl
+
+    def using(self, n_nodes: int | None = None, need_be: bool = True):
+        """Context manager: the plan with this batch loaded, locked until the block
+        exits (wrap the enqueue of every operation that relies on the loaded state)."""
+        return using_operator(self, n_nodes, need_be)
+
+
+@contextlib.contextmanager
+def using_operator(batch, n_nodes=None, need_be=True):
+    """The plan of `batch` (anything with .index and ._A_store) with its operator
+    loaded, held under the plan's lock for the duration of the block."""
+    pl = batch.index.plan(n_nodes)
+    with pl.lock:
+        pl.ensure_loaded(batch, need_be=need_be)
+        yield pl
 
 
 def _source_values(m: Mesh, f):

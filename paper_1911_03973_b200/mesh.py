@@ -10,6 +10,7 @@ Mirrors /root/reference/pkg/src/ebsolve/mesh.py.  Differences, all deliberate:
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -17,6 +18,8 @@ import torch
 
 from . import _device as D
 from ._lib import call
+
+_PLAN_BUILD_LOCK = threading.Lock()
 
 MAX_LEVEL = 12          # mesh.py:20
 MAX_CUBE_CELLS = 256    # 3D size guard: N=256 is BASELINE C5 (100.7M tetrahedra)
@@ -138,8 +141,11 @@ class IndexArrays:
         n = self.node_count() if n_nodes is None else int(n_nodes)
         pl = self._plans.get(n)
         if pl is None:
-            pl = Plan(self.indt, n)
-            self._plans[n] = pl
+            with _PLAN_BUILD_LOCK:  # concurrent first calls build one plan
+                pl = self._plans.get(n)
+                if pl is None:
+                    pl = Plan(self.indt, n)
+                    self._plans[n] = pl
         return pl
 
 

@@ -20,7 +20,7 @@ import torch
 
 from . import _device as D
 from ._lib import EBS_RES_EXACT, EBS_RES_FAST, call
-from .elements import ElementBatch
+from .elements import ElementBatch, using_operator
 from .mesh import IndexArrays, Mesh
 
 
@@ -100,11 +100,11 @@ def residual(batch: ElementBatch, x, threads: int = 1, deterministic: bool = Tru
     Raises ValueError for a non 1-D or non-finite x (operators.py:87-91)."""
     x = _check_x(x)
     n = x.shape[0]
-    pl = batch.operator(n)
     r = out if out is not None else D.empty(n)
     flag = D.zeros(1, torch.int32) if check_finite else None
-    call("ebs_residual", pl.handle, D.ptr(x), D.ptr(r),
-         EBS_RES_EXACT if deterministic else EBS_RES_FAST, 0, D.ptr(flag), D.stream())
+    with batch.using(n) as pl:
+        call("ebs_residual", pl.handle, D.ptr(x), D.ptr(r),
+             EBS_RES_EXACT if deterministic else EBS_RES_FAST, 0, D.ptr(flag), D.stream())
     if check_finite and int(flag.item()):
         raise ValueError("x contains non-finite entries")
     return r
@@ -145,41 +145,41 @@ def residual_many(batch: ElementBatch, xs, out=None, deterministic: bool = True,
         raise ValueError("out must be a contiguous (k, n) float64 CPU tensor")
     if k == 0:
         return out
-    pl = batch.operator(n)
-    comp = _t.cuda.current_stream()
-    h2d, d2h = _t.cuda.Stream(), _t.cuda.Stream()
-    h2d.wait_stream(comp)                            # stream semantics: after prior work
-    d2h.wait_stream(comp)
-    xb = [D.empty(n), D.empty(n)]
-    rb = [D.empty(n), D.empty(n)]
-    flags = D.zeros(k, _t.int32)
-    ev = lambda: _t.cuda.Event()
-    x_ready, used, r_ready, read = ([ev() for _ in range(k)] for _ in range(4))
-    mode = EBS_RES_EXACT if deterministic else EBS_RES_FAST
-    s = D.stream()
-    for i in range(k):
-        j = i & 1
-        with _t.cuda.stream(h2d):
+    with using_operator(batch, n) as pl:  # the plan's operator stays loaded
+        comp = _t.cuda.current_stream()
+        h2d, d2h = _t.cuda.Stream(), _t.cuda.Stream()
+        h2d.wait_stream(comp)                            # stream semantics: after prior work
+        d2h.wait_stream(comp)
+        xb = [D.empty(n), D.empty(n)]
+        rb = [D.empty(n), D.empty(n)]
+        flags = D.zeros(k, _t.int32)
+        ev = lambda: _t.cuda.Event()
+        x_ready, used, r_ready, read = ([ev() for _ in range(k)] for _ in range(4))
+        mode = EBS_RES_EXACT if deterministic else EBS_RES_FAST
+        s = D.stream()
+        for i in range(k):
+            j = i & 1
+            with _t.cuda.stream(h2d):
+                if i >= 2:
+                    h2d.wait_event(used[i - 2])          # compute of step i-2 done with xb[j]
+                xb[j].copy_(xs[i], non_blocking=True)
+                x_ready[i].record(h2d)
+            comp.wait_event(x_ready[i])
             if i >= 2:
-                h2d.wait_event(used[i - 2])          # compute of step i-2 done with xb[j]
-            xb[j].copy_(xs[i], non_blocking=True)
-            x_ready[i].record(h2d)
-        comp.wait_event(x_ready[i])
-        if i >= 2:
-            comp.wait_event(read[i - 2])             # rb[j] read back
-        fl = flags[i:i + 1] if check_finite else None
-        call("ebs_residual", pl.handle, D.ptr(xb[j]), D.ptr(rb[j]), mode, 0, D.ptr(fl), s)
-        used[i].record(comp)
-        r_ready[i].record(comp)
-        with _t.cuda.stream(d2h):
-            d2h.wait_event(r_ready[i])
-            out[i].copy_(rb[j], non_blocking=True)
-            read[i].record(d2h)
-    comp.wait_stream(d2h)
-    comp.wait_stream(h2d)
-    for t in xb + rb:                                # buffers used on the side streams
-        t.record_stream(h2d)
-        t.record_stream(d2h)
+                comp.wait_event(read[i - 2])             # rb[j] read back
+            fl = flags[i:i + 1] if check_finite else None
+            call("ebs_residual", pl.handle, D.ptr(xb[j]), D.ptr(rb[j]), mode, 0, D.ptr(fl), s)
+            used[i].record(comp)
+            r_ready[i].record(comp)
+            with _t.cuda.stream(d2h):
+                d2h.wait_event(r_ready[i])
+                out[i].copy_(rb[j], non_blocking=True)
+                read[i].record(d2h)
+        comp.wait_stream(d2h)
+        comp.wait_stream(h2d)
+        for t in xb + rb:                                # buffers used on the side streams
+            t.record_stream(h2d)
+            t.record_stream(d2h)
     if check_finite:
         bad = _t.nonzero(flags).flatten()
         if bad.numel():
@@ -193,19 +193,20 @@ def matvec(batch: ElementBatch, v, d: DirichletData | None = None) -> torch.Tens
     """spectrum.py:54-61 _apply_masked: y = A v (bitwise reference order); with
     ``d`` the rows at d.nd are zeroed."""
     v = _check_x(v)
-    pl = batch.operator(v.shape[0], need_be=False)
-    pl.ensure_dirichlet(d)
     y = D.empty(v.shape[0])
-    call("ebs_matvec", pl.handle, D.ptr(v), D.ptr(y), 1 if d is not None else 0, D.stream())
+    with using_operator(batch, v.shape[0], need_be=False) as pl:
+        pl.ensure_dirichlet(d)
+        call("ebs_matvec", pl.handle, D.ptr(v), D.ptr(y), 1 if d is not None else 0,
+             D.stream())
     return y
 
 
 def diagonal(batch: ElementBatch, n_nodes: int | None = None) -> torch.Tensor:
     """NEW: diag(A) = assemble_rhs(stack_j A_e[j, j, :]) (the
     reference's own diagonal pattern, spectrum.py:118-120, in (j, e) order)."""
-    pl = batch.operator(n_nodes, need_be=False)
-    d = D.empty(pl.n_nodes)
-    call("ebs_diagonal", pl.handle, D.ptr(d), D.stream())
+    with batch.using(n_nodes, need_be=False) as pl:
+        d = D.empty(pl.n_nodes)
+        call("ebs_diagonal", pl.handle, D.ptr(d), D.stream())
     return d
 
 

@@ -8,6 +8,7 @@ the plan remembers which element batch and which Dirichlet set are loaded.
 from __future__ import annotations
 
 import ctypes
+import threading
 import weakref
 
 import torch
@@ -34,6 +35,10 @@ class Plan:
         self._loaded = None       # weakref to the loaded ElementBatch
         self._loaded_be = False
         self._dirichlet = None    # weakref/key of the loaded Dirichlet set
+        # held from ensure_loaded / ensure_dirichlet through the enqueue of the operation
+        # that uses them (batches sharing one plan, e.g. A_e and the mass slices, may be
+        # used from several threads); re-entrant for solver callbacks
+        self.lock = threading.RLock()
         self._finalizer = weakref.finalize(self, _destroy, h.value)
 
     # ------------------------------------------------------------- info --

@@ -115,8 +115,6 @@ def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.
     if x0.ndim != 1:
         raise ValueError(f"x0 must be a flat global vector, got shape {tuple(x0.shape)}")
     n = x0.shape[0]
-    pl = batch.operator(n)
-    pl.ensure_dirichlet(d)
     x = D.empty(n)
     ref = D.f64(reference) if reference is not None else None
     norms = (ctypes.c_double * (iters + 2))()
@@ -166,7 +164,9 @@ def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.
         cb = (ctypes.c_double * max(1, len(coef_b)))(*coef_b)
         P.coef_b = ctypes.cast(cb, ctypes.POINTER(ctypes.c_double))
     t0 = time.perf_counter()
-    code = load().ebs_solve(pl.handle, ctypes.byref(P), D.stream())
+    with batch.using(n) as pl:  # operator + Dirichlet set stay loaded for the whole solve
+        pl.ensure_dirichlet(d)
+        code = load().ebs_solve(pl.handle, ctypes.byref(P), D.stream())
     wall = time.perf_counter() - t0
     if code == EBS_ECALLBACK and state["exc"] is not None:
         raise state["exc"]

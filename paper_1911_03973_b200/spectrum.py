@@ -16,7 +16,7 @@ import torch
 
 from . import _device as D
 from ._lib import call
-from .elements import ElementBatch
+from .elements import ElementBatch, using_operator
 from .operators import DirichletData, matvec
 from .solvers import SpectralBounds
 
@@ -53,12 +53,12 @@ def power_iteration_lambda_max(batch: ElementBatch, d: DirichletData, iters: int
     n_n = batch.index.node_count()
     rng = np.random.default_rng(seed)
     v0 = D.f64(rng.standard_normal(n_n))
-    pl = batch.operator(n_n, need_be=False)
-    pl.ensure_dirichlet(d)
     lam = ctypes.c_double(0.0)
     its = ctypes.c_int(0)
-    call("ebs_power_iteration", pl.handle, D.ptr(v0), int(iters), float(tol), ctypes.byref(lam),
-         ctypes.byref(its), D.stream())
+    with using_operator(batch, n_n, need_be=False) as pl:
+        pl.ensure_dirichlet(d)
+        call("ebs_power_iteration", pl.handle, D.ptr(v0), int(iters), float(tol),
+             ctypes.byref(lam), ctypes.byref(its), D.stream())
     return float(lam.value)
 
 
@@ -75,7 +75,8 @@ class _MassBatch:
 
     def operator(self, n_nodes=None, need_be=False):
         pl = self.index.plan(n_nodes)
-        pl.ensure_loaded(self, need_be=False)
+        with pl.lock:
+            pl.ensure_loaded(self, need_be=False)
         return pl
 
 
@@ -90,9 +91,9 @@ def mass_gershgorin(batch: ElementBatch, d: DirichletData) -> tuple[float, float
     if d.nd.numel():
         is_free[d.nd] = False
     row_sums = matvec(mb, is_free.to(torch.float64))
-    pl = mb.operator(n_n)
     diags = D.empty(n_n)
-    call("ebs_diagonal_grouped", pl.handle, D.ptr(diags), D.stream())
+    with using_operator(mb, n_n, need_be=False) as pl:
+        call("ebs_diagonal_grouped", pl.handle, D.ptr(diags), D.stream())
     if not bool(is_free.any()):
         raise ValueError("no free nodes")
     lo = (2.0 * diags - row_sums)[is_free]

@@ -254,3 +254,42 @@ def test_concurrent_residuals_on_separate_streams(gpu):
     assert not errors, errors
     for (t, rep, i), r in out.items():
         npt.assert_array_equal(to_np(r), ref[i], err_msg=f"thread {t} rep {rep} vector {i}")
+
+
+def test_concurrent_batches_sharing_one_plan(gpu):
+    """Two operators on one plan (a batch and its mass slices share the IndexArrays, as
+    mass_gershgorin does) used from different threads: each call sees its own operator."""
+    import threading
+    import torch
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.spectrum import _MassBatch
+    m = eb.build_unit_square_mesh(6)
+    batch = eb.build_element_batch(m, nu=1.0)
+    mb = _MassBatch(batch.M_e, batch.index)
+    n = m.n_nodes
+    x = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, n)).cuda()
+    ref_a = to_np(eb.matvec(batch, x))
+    ref_m = to_np(eb.matvec(mb, x))
+    assert not np.array_equal(ref_a, ref_m)
+    errors = []
+
+    def work(b, ref):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(40):
+                    y = eb.matvec(b, x)
+                    st.synchronize()
+                    if not np.array_equal(to_np(y), ref):
+                        errors.append("wrong operator")
+                        return
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(b, r)) for b, r in
+          ((batch, ref_a), (mb, ref_m), (batch, ref_a), (mb, ref_m))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors[:3]
