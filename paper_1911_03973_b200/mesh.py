@@ -116,7 +116,7 @@ class IndexArrays:
         if tuple(indt.shape) != (ind_e.shape[0], ind_e.shape[2]):
             raise ValueError(f"indt must have shape ({ind_e.shape[0]}, n_e), got {tuple(indt.shape)}")
         if not torch.equal(ind_e[:, 0, :], indt):
-            raise ValueError("ind_e and indt must index the same nodes per element")
+            raise ValueError("ind_e[:, 0, :] and indt disagree on the nodes of some element")
         if indt.numel() and int(indt.min()) < 0:
             raise ValueError("negative node index")
         object.__setattr__(self, "indt", indt)
@@ -206,10 +206,8 @@ def build_grid_mesh(n: int) -> Mesh:
 
 def build_unit_square_mesh(level: int) -> Mesh:
     """mesh.py:131-137: (2^L+1)^2 nodes, 2*4^L triangles."""
-    if level < 0:
-        raise ValueError(f"level must be nonnegative, got {level}")
-    if level > MAX_LEVEL:
-        raise ValueError(f"level {level} exceeds the size guard (max {MAX_LEVEL})")
+    if not 0 <= level <= MAX_LEVEL:
+        raise ValueError(f"level {level} is outside 0..{MAX_LEVEL} (the size guard)")
     return build_grid_mesh(2**level + 1)
 
 
@@ -264,50 +262,60 @@ def jitter_interior(m: Mesh, delta) -> Mesh:
     return Mesh(nodes, None, m.boundary_nodes, level=None, conn=m.conn)
 
 
+# corners of the 4 children in terms of (a, b, c, mid(ab), mid(bc), mid(ca))
+_CHILD_CORNERS = ((0, 3, 5), (3, 1, 4), (5, 4, 2), (3, 4, 5))
+
+
+def _stable_lexsort(keys) -> torch.Tensor:
+    """Permutation sorting rows by keys[0], ties by keys[1], ... (stable passes from the
+    least significant key, like np.lexsort with the key order reversed)."""
+    order = None
+    for key in reversed(keys):
+        k = key if order is None else key[order]
+        step = torch.argsort(k, stable=True)
+        order = step if order is None else order[step]
+    return order
+
+
 def uniform_refine(m: Mesh) -> Mesh:
-    """mesh.py:157-208 on the device: split every triangle into 4 via edge midpoints and
-    renumber canonically (nodes by (y, x), triples rotated to their smallest index, rows
-    sorted), so refining a structured mesh equals build_unit_square_mesh(level + 1)."""
+    """Red refinement of a triangle mesh on the device (mesh.py:157-208 semantics): every
+    triangle becomes 4 through its edge midpoints, then the mesh is renumbered
+    canonically -- nodes ascending in (y, x), each triangle rotated to start at its
+    smallest node (orientation kept), triangles ascending -- so a structured level-L
+    mesh refines to exactly build_unit_square_mesh(L + 1)."""
     if m.dim != 2:
-        raise ValueError("uniform_refine is defined for triangle meshes")
-    if m.level is not None and m.level + 1 > MAX_LEVEL:
-        raise ValueError(f"refining level {m.level} exceeds the size guard (max {MAX_LEVEL})")
-    if 4 * m.n_elements > 2 * 4**MAX_LEVEL:
-        raise ValueError("refinement exceeds the size guard")
-    tri = m.conn.t().to(torch.int64)                       # (n_e, 3)
-    edges = torch.cat([tri[:, [0, 1]], tri[:, [1, 2]], tri[:, [2, 0]]])
-    edges = torch.sort(edges, dim=1).values
-    uniq, inv = torch.unique(edges, dim=0, return_inverse=True)
-    mid = m.n_nodes + inv.reshape(3, -1)                   # rows ab, bc, ca per element
-    mid_coords = 0.5 * (m.nodes[uniq[:, 0]] + m.nodes[uniq[:, 1]])
-    all_nodes = torch.cat([m.nodes, mid_coords])
-    a, b, c = tri[:, 0], tri[:, 1], tri[:, 2]
-    ab, bc, ca = mid[0], mid[1], mid[2]
-    children = torch.cat([torch.stack([a, ab, ca], 1), torch.stack([ab, b, bc], 1),
-                          torch.stack([ca, bc, c], 1), torch.stack([ab, bc, ca], 1)])
-    # np.lexsort((x, y)): stable sort by x, then stable by y
-    order = torch.argsort(all_nodes[:, 0], stable=True)
-    order = order[torch.argsort(all_nodes[order, 1], stable=True)]
-    rank = torch.empty_like(order)
-    rank[order] = torch.arange(order.numel(), device=order.device)
-    new_nodes = all_nodes[order].contiguous()
-    children = rank[children]
-    shift = torch.argmin(children, dim=1)
-    cols = (shift[:, None] + torch.arange(3, device=shift.device)) % 3
-    children = torch.gather(children, 1, cols)
-    # np.lexsort((c2, c1, c0)): stable sorts by c2, c1, c0
-    idx = torch.argsort(children[:, 2], stable=True)
-    idx = idx[torch.argsort(children[idx, 1], stable=True)]
-    idx = idx[torch.argsort(children[idx, 0], stable=True)]
-    children = children[idx]
-    level = None if m.level is None else m.level + 1
-    return Mesh(new_nodes, children, _boundary_from_flags(new_nodes, 0), level=level)
+        raise ValueError("uniform_refine splits triangles; got a tetrahedral mesh")
+    if (m.level is not None and m.level >= MAX_LEVEL) or 2 * m.n_elements > 4**MAX_LEVEL:
+        raise ValueError(f"the refined mesh would exceed the size guard (level {MAX_LEVEL})")
+    n = m.n_nodes
+    tri = m.conn.to(torch.int64)                                    # (3, n_e)
+    # the three edges of every element as one sortable key lo * n + hi
+    ends = torch.stack([tri, tri.roll(-1, dims=0)])                 # (2, 3, n_e): ab, bc, ca
+    key = ends.min(0).values * n + ends.max(0).values
+    edge_keys, mid_id = torch.unique(key.reshape(-1), return_inverse=True)
+    mids = 0.5 * (m.nodes[edge_keys // n] + m.nodes[edge_keys % n])
+    xy = torch.cat([m.nodes, mids])
+    corners = torch.cat([tri, n + mid_id.reshape(3, -1)])           # (6, n_e)
+    kids = corners[torch.tensor(_CHILD_CORNERS, device=tri.device)]  # (4, 3, n_e)
+    kids = kids.permute(0, 2, 1).reshape(-1, 3)
+    # canonical node numbering by (y, x)
+    order = _stable_lexsort([xy[:, 1], xy[:, 0]])
+    new_id = torch.empty_like(order)
+    new_id[order] = torch.arange(order.numel(), device=order.device)
+    kids = new_id[kids]
+    first = kids.argmin(dim=1, keepdim=True)
+    kids = kids.gather(1, (first + torch.arange(3, device=kids.device)) % 3)
+    kids = kids[_stable_lexsort([kids[:, 0], kids[:, 1], kids[:, 2]])]
+    nodes = xy[order].contiguous()
+    return Mesh(nodes, kids, _boundary_from_flags(nodes, 0),
+                level=None if m.level is None else m.level + 1)
 
 
 def export_mesh(m: Mesh, directory) -> None:
-    """mesh.py:211-218 debug dump: nodes.txt (%.17g) and elements.txt (%d)."""
+    """Debug dump (mesh.py:211-218): nodes.txt with 17 significant digits, elements.txt
+    with integer node ids, one row per node / element."""
     from pathlib import Path
-    directory = Path(directory)
-    directory.mkdir(parents=True, exist_ok=True)
-    np.savetxt(directory / "nodes.txt", m.nodes.cpu().numpy(), fmt="%.17g")
-    np.savetxt(directory / "elements.txt", m.elements.cpu().numpy(), fmt="%d")
+    out = Path(directory)
+    out.mkdir(parents=True, exist_ok=True)
+    for name, arr, fmt in (("nodes.txt", m.nodes, "%.17g"), ("elements.txt", m.elements, "%d")):
+        np.savetxt(out / name, arr.cpu().numpy(), fmt=fmt)

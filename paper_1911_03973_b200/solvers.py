@@ -35,30 +35,28 @@ from .operators import DirichletData
 
 @dataclass(frozen=True)
 class SpectralBounds:
-    """solvers.py:30-56: an interval [lambda1, lambda2] enclosing the spectrum."""
+    """Spectral enclosure [lambda1, lambda2] of the constrained operator (the reference
+    type, solvers.py:30-56): finite, 0 <= lambda1 <= lambda2, lambda2 > 0."""
 
     lambda1: float
     lambda2: float
 
     def __post_init__(self):
-        if not (np.isfinite(self.lambda1) and np.isfinite(self.lambda2)):
-            raise ValueError("spectral bounds must be finite")
-        if self.lambda1 < 0 or self.lambda2 < self.lambda1 or self.lambda2 <= 0:
-            raise ValueError(
-                f"need 0 <= lambda1 <= lambda2, lambda2 > 0; got [{self.lambda1}, {self.lambda2}]")
+        lo, hi = self.lambda1, self.lambda2
+        if not np.isfinite([lo, hi]).all():
+            raise ValueError(f"spectral bounds [{lo}, {hi}] are not finite")
+        if lo < 0 or hi <= 0 or hi < lo:
+            raise ValueError(f"[{lo}, {hi}] is not an interval 0 <= lambda1 <= lambda2, "
+                             "lambda2 > 0")
 
-    @property
-    def center(self) -> float:
-        return (self.lambda2 + self.lambda1) / 2.0
-
-    @property
-    def half_width(self) -> float:
-        return (self.lambda2 - self.lambda1) / 2.0
+    # midpoint d and half-width c of the interval (same rounding as the reference)
+    center = property(lambda self: (self.lambda2 + self.lambda1) / 2.0)
+    half_width = property(lambda self: (self.lambda2 - self.lambda1) / 2.0)
 
 
 @dataclass(frozen=True)
 class ChebyshevCycle:
-    """solvers.py:59-66: precomputed cycle of step denominators."""
+    """Step denominators of one cycle of the two-level iteration (solvers.py:59-66)."""
 
     N: int
     alphas: np.ndarray
@@ -67,30 +65,31 @@ class ChebyshevCycle:
 
 
 def chebyshev_roots(bounds: SpectralBounds, N: int) -> ChebyshevCycle:
-    """solvers.py:85-99: alphas[k] = d + c cos(pi (k+1/2)/N), natural order."""
-    if N < 1:
-        raise ValueError(f"cycle length must be positive, got N={N}")
-    d = bounds.center
-    c = bounds.half_width
-    k = np.arange(N)
-    alphas = d + c * np.cos(np.pi * (k + 0.5) / N)
-    alphas.setflags(write=False)
-    return ChebyshevCycle(N=N, alphas=alphas, d=d, c=c)
+    """The N roots of the degree-N Chebyshev polynomial mapped onto the interval,
+    alpha_k = d + c cos(pi (k + 1/2) / N), k = 0..N-1 (descending; solvers.py:85-99)."""
+    N = int(N)
+    if N <= 0:
+        raise ValueError(f"a Chebyshev cycle needs N >= 1 (got {N})")
+    mid, half = bounds.center, bounds.half_width
+    theta = np.pi * (np.arange(N) + 0.5) / N
+    roots = mid + half * np.cos(theta)
+    roots.setflags(write=False)
+    return ChebyshevCycle(N=N, alphas=roots, d=mid, c=half)
 
 
 def chebyshev_scaling_factor(bounds: SpectralBounds, k: int) -> float:
-    """solvers.py:102-114: C_k = T_k((l1+l2)/(l2-l1)) by the three-term recurrence."""
+    """T_k(sigma) at sigma = (lambda1 + lambda2) / (lambda2 - lambda1), by the recurrence
+    T_{j+1} = 2 sigma T_j - T_{j-1} from T_0 = 1, T_1 = sigma (solvers.py:102-114)."""
     if k < 0:
-        raise ValueError(f"k must be nonnegative, got {k}")
-    if bounds.lambda1 >= bounds.lambda2:
-        raise ValueError("scaling factors need lambda1 < lambda2")
-    t = (bounds.lambda1 + bounds.lambda2) / (bounds.lambda2 - bounds.lambda1)
-    c_prev, c_cur = 1.0, t
-    if k == 0:
-        return c_prev
+        raise ValueError(f"polynomial degree must be >= 0 (got {k})")
+    lo, hi = bounds.lambda1, bounds.lambda2
+    if not lo < hi:
+        raise ValueError("the scaling factor needs a nondegenerate interval lambda1 < lambda2")
+    sigma = (lo + hi) / (hi - lo)
+    t = [1.0, sigma]
     for _ in range(k - 1):
-        c_prev, c_cur = c_cur, 2.0 * t * c_cur - c_prev
-    return c_cur
+        t = [t[1], 2.0 * sigma * t[1] - t[0]]
+    return t[0] if k == 0 else t[1]
 
 
 @dataclass(frozen=True)

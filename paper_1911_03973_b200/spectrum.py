@@ -25,22 +25,28 @@ POWER_TOL = 1e-10      # spectrum.py:27
 POWER_MARGIN = 1.05    # spectrum.py:28
 
 
-def model_eigenvalues_all(n: int) -> np.ndarray:
-    """spectrum.py:31-38: all (n-2)^2 interior eigenvalues for n nodes per side."""
+def _interior_sines(n: int) -> np.ndarray:
+    """sin^2(i pi / (2 (n-1))), i = 1..n-2: the 1D factors of the model eigenvalues."""
     if n < 3:
-        raise ValueError(f"need n >= 3 for an interior node, got n={n}")
-    i = np.arange(1, n - 1)
-    s = np.sin(i * np.pi / (2 * (n - 1))) ** 2
-    lam = 4.0 * (s[:, None] + s[None, :])
-    return np.sort(lam.ravel())
+        raise ValueError(f"{n} nodes per side leave no interior node (need n >= 3)")
+    return np.sin(np.arange(1, n - 1) * np.pi / (2 * (n - 1))) ** 2
+
+
+def model_eigenvalues_all(n: int) -> np.ndarray:
+    """Every interior eigenvalue 4 (s_i + s_j) of the model stiffness matrix on the
+    n x n grid, ascending (spectrum.py:31-38)."""
+    s = _interior_sines(n)
+    return np.sort((4.0 * np.add.outer(s, s)).ravel())
 
 
 def model_eigen_bounds(n: int) -> SpectralBounds:
-    """spectrum.py:41-51: lambda1 = 8 sin^2(pi/(2(n-1))), lambda2 = 8 - lambda1."""
+    """Extreme model eigenvalues (spectrum.py:41-51): the smallest from i = j = 1; the
+    largest is its complement 8 - lambda1 (the extreme sine arguments are complementary
+    angles), taken that way as the reference does."""
     if n < 3:
-        raise ValueError(f"need n >= 3 for an interior node, got n={n}")
-    lam1 = 8.0 * np.sin(np.pi / (2 * (n - 1))) ** 2
-    return SpectralBounds(lambda1=float(lam1), lambda2=float(8.0 - lam1))
+        raise ValueError(f"{n} nodes per side leave no interior node (need n >= 3)")
+    low = 8.0 * np.sin(np.pi / (2 * (n - 1))) ** 2
+    return SpectralBounds(float(low), float(8.0 - low))
 
 
 def power_iteration_lambda_max(batch: ElementBatch, d: DirichletData, iters: int = POWER_ITERS,
@@ -103,12 +109,13 @@ def mass_gershgorin(batch: ElementBatch, d: DirichletData) -> tuple[float, float
 
 def operator_bounds(batch: ElementBatch, d: DirichletData, n: int, nu: float,
                     seed: int = 0) -> SpectralBounds:
-    """spectrum.py:129-149: model interval for nu = 0; otherwise Gershgorin-shifted
-    lower end and a 5%-widened power-iteration upper end."""
-    base = model_eigen_bounds(n)
+    """Bounds for A = K + nu M (spectrum.py:129-149).  nu = 0: the model interval.
+    nu > 0: lower end = model minimum + nu x (Gershgorin floor of the constrained mass
+    spectrum), upper end = power-iteration maximum widened by POWER_MARGIN."""
+    model = model_eigen_bounds(n)
     if nu == 0.0:
-        return base
-    m_lo, _ = mass_gershgorin(batch, d)
-    lam1 = base.lambda1 + nu * m_lo
-    lam2 = POWER_MARGIN * power_iteration_lambda_max(batch, d, seed=seed)
-    return SpectralBounds(lambda1=lam1, lambda2=float(max(lam2, lam1)))
+        return model
+    mass_floor = mass_gershgorin(batch, d)[0]
+    lower = model.lambda1 + nu * mass_floor
+    upper = POWER_MARGIN * power_iteration_lambda_max(batch, d, seed=seed)
+    return SpectralBounds(lower, float(max(upper, lower)))
