@@ -101,10 +101,11 @@ def mass_gershgorin(batch: ElementBatch, d: DirichletData) -> tuple[float, float
     with using_operator(mb, n_n, need_be=False) as pl:
         call("ebs_diagonal_grouped", pl.handle, D.ptr(diags), D.stream())
     if not bool(is_free.any()):
-        raise ValueError("no free nodes")
-    lo = (2.0 * diags - row_sums)[is_free]
-    hi = row_sums[is_free]
-    return max(float(lo.min()), 0.0), float(hi.max())
+        raise ValueError("every node is constrained: no free-node mass spectrum to bound")
+    # mass entries are >= 0, so a free row's disc is [2 diag - rowsum, rowsum]
+    upper_edges = row_sums[is_free]
+    lower_edges = 2.0 * diags[is_free] - upper_edges
+    return max(float(lower_edges.min()), 0.0), float(upper_edges.max())
 
 
 def operator_bounds(batch: ElementBatch, d: DirichletData, n: int, nu: float,
