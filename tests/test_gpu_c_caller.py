@@ -1,0 +1,27 @@
+"""The C-ABI used from C (examples/residual_pcg.c): gcc against include/ebs.h and
+libebs.so, no Python on the compute path.  The program checks the device residual bit for
+bit against a CPU loop in the reference's (j, e) order and solves with Jacobi-PCG."""
+
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c_program_through_the_c_abi(gpu, tmp_path):
+    exe = tmp_path / "residual_pcg"
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    lib_dir = os.path.join(ROOT, "paper_1911_03973_b200")
+    cmd = ["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-Wall", "-Werror",
+           f"-I{ROOT}/include", f"-I{cuda}/include", f"{ROOT}/examples/residual_pcg.c",
+           f"-L{lib_dir}", "-lebs", f"-L{cuda}/lib64", "-lcudart", "-lm",
+           f"-Wl,-rpath,{lib_dir}", f"-Wl,-rpath,{cuda}/lib64", "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    for level in ("3", "7"):
+        r = subprocess.run([str(exe), level], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "mismatches: 0" in r.stdout and r.stdout.strip().endswith("OK"), r.stdout
