@@ -157,7 +157,10 @@ def run_reference(args):
         "config": workload_config(n_n, n_e, args, mode="reference order (bincount)"),
         "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": T, "kind": "port",
                          "sample": f"{args.steps} full C2 residuals (oracle/ebs_oracle.py "
-                                   f"residual, deterministic chunked mode, {T} threads)"},
+                                   f"residual, deterministic chunked mode, {T} threads)"
+                                   + ("" if int(os.environ.get("WORLD_SIZE", "1")) <= 1 else
+                                      "; one C2 square per step = one GPU's slab of the "
+                                      "stacked squares (GDoF/s is a rate)")},
         "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "setup_s": setup,
@@ -165,12 +168,25 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _stacked_nodes(n_square, copies):
+    side = int(round(n_square ** 0.5))
+    return side * ((side - 1) * copies + 1)
+
+
 def workload_config(n_n, n_e, args, mode):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:  # the GPU arm's weak-scaled workload (dist.bench_rank)
+        return {"workload": f"C2 weak-scaled: {world} level-11 unit squares stacked in y, "
+                            "one C2-sized element slab per GPU; element residual r=b-Ax per "
+                            "step", "per_gpu": "one C2 square (4.2M nodes, 8.4M triangles)",
+                "n_nodes": _stacked_nodes(n_n, world),
+                "n_elements": n_e * world, "seed": args.seed, "mode": mode,
+                "parallelism": f"element slabs x{world}"}
     return {"workload": "C2: 2D P1 unit square, level 11, permuted node numbering, "
                         "x~U[-1,1], nu=1, f=1; element residual r=b-Ax per step",
             "n_nodes": n_n, "n_elements": n_e, "seed": args.seed, "mode": mode,
             "l2": "inputs larger than L2 (slot stream ~1 GB vs 126 MB L2); no flush",
-            "parallelism": f"element slabs x{args.gpus}" if args.gpus > 1 else "single GPU"}
+            "parallelism": "single GPU"}
 
 
 # ---------------------------------------------------------------- GPU arm --
