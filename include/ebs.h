@@ -296,6 +296,25 @@ int ebs_plan_free_mask(ebs_plan_t plan, uint8_t *free_int, void *stream);
 int ebs_plan_internal_rhs(ebs_plan_t plan, double *b_int, void *stream);
 int ebs_plan_internal_diag(ebs_plan_t plan, double *d_int, void *stream);
 
+/* ------------------------------------------------- element-slab collectives ---- */
+/* the NCCL side of the element-slab path inside the library, so a C caller can
+ * run the multi-GPU residual / solvers without Python (one process = one GPU = one slab).
+ * NCCL is resolved at run time (dlopen libnccl.so.2): the NCCL already loaded in the
+ * process (e.g. PyTorch's) or the system one.  Failures return EBS_ENCCL. */
+#define EBS_DIST_ID_BYTES 128
+/* ncclGetUniqueId on rank 0; the caller broadcasts the EBS_DIST_ID_BYTES bytes. */
+int ebs_dist_unique_id(void *id_out);
+/* ncclCommInitRank on the current device; the communicator belongs to the plan (freed by
+ * ebs_plan_destroy).  Collective over the nranks processes. */
+int ebs_dist_init(ebs_plan_t plan, const void *id, int rank, int nranks);
+/* Halo exchange: for each of n_peers peers (host arrays peers[], counts[] and device
+ * buffer pointers send[] / recv[]), counts[i] doubles go to and come from peers[i], as one
+ * NCCL group on `stream` (a peer may be the caller's own rank). */
+int ebs_dist_exchange(ebs_plan_t plan, int n_peers, const int32_t *peers, const int64_t *counts,
+                      const double *const *send, double *const *recv, void *stream);
+/* In-place sum over the ranks of n device doubles (the PCG dots) on `stream`. */
+int ebs_dist_allreduce(ebs_plan_t plan, double *buf, int64_t n, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

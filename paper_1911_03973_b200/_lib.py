@@ -102,6 +102,11 @@ SIGNATURES = {
     "ebs_plan_apply_map_chunks": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p,
                                           c_void_p, c_void_p, c_int, c_void_p]),
     "ebs_vec_workspace_bytes": (c_size_t, []),
+    "ebs_dist_unique_id": (c_int, [c_void_p]),
+    "ebs_dist_init": (c_int, [c_void_p, c_void_p, c_int, c_int]),
+    "ebs_dist_exchange": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                  c_void_p]),
+    "ebs_dist_allreduce": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "ebs_vec_jacobi": (c_int, [c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p]),

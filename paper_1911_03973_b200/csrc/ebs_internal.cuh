@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <mutex>
+#include <type_traits>
 #include <stdint.h>
 #include <cmath>
 #include <cstdio>
@@ -172,6 +173,9 @@ struct Plan {
     double *wvec[10] = {nullptr};
     Perm2 perm[2];  // 0: caller -> internal, 1: internal -> caller (built on first use)
     StreamOrder order;  // cross-stream ordering of the workspace above
+    // element-slab collectives (nccl.cu): one NCCL communicator per plan
+    void *nccl_comm = nullptr;
+    int dist_rank = 0, dist_size = 1;
     double *partials = nullptr;  // reduction partials
     Ctl *ctl = nullptr;          // device control block
     Ctl *ctl_host = nullptr;     // pinned mirror: [0] synchronous reads, [1..2] batch ring
@@ -192,6 +196,7 @@ const Perm2 *perm_get(Plan *p, int dir, cudaStream_t s);
 void perm_apply(Plan *p, const Perm2 *P, const double *in, double *out, int32_t *nonfinite,
                 cudaStream_t s);
 void perm_free(Plan *p);
+void dist_free(Plan *p);
 
 // ------------------------------------------------------ reductions ----------
 constexpr int RED_BLOCK = 256;

@@ -20,6 +20,7 @@ The solver loops are written against two small protocols so the same code runs
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -118,6 +119,61 @@ class TorchTransport:
             t.copy_(h)
         else:
             self.dist.all_reduce(t, group=self.group)
+
+
+class NativeTransport:
+    """The halo exchange and reductions through libebs.so's own NCCL communicator
+    (ebs_dist_init / ebs_dist_exchange / ebs_dist_allreduce) -- the C-ABI path a caller
+    without PyTorch uses.  One GPU rank operator per process; the NCCL unique id travels
+    through torch.distributed's store here (any rendezvous works)."""
+
+    def __init__(self, op, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.op = op
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            call("ebs_dist_unique_id", uid)
+        if world > 1:
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        call("ebs_dist_init", op.plan.handle, uid, rank, world)
+        self.world = world
+
+    def exchange_start(self, ops: list, sends: list):
+        (op,), (snd,) = ops, sends
+        peers = sorted(snd)
+        bufs = [snd[q].contiguous() for q in peers]
+        recvs = {q: torch.empty_like(b) for q, b in zip(peers, bufs)}
+        n = len(peers)
+        if n:
+            P = (ctypes.c_int32 * n)(*peers)
+            C = (ctypes.c_int64 * n)(*[b.numel() for b in bufs])
+            Sp = (ctypes.c_void_p * n)(*[b.data_ptr() for b in bufs])
+            Rp = (ctypes.c_void_p * n)(*[recvs[q].data_ptr() for q in peers])
+            call("ebs_dist_exchange", op.plan.handle, n, P, C, Sp, Rp, D.stream())
+        return bufs, recvs  # keep the send buffers alive until the stream has used them
+
+    def exchange_finish(self, handle) -> list:
+        return [handle[1]]  # stream-ordered: later work on this stream sees the data
+
+    def exchange(self, ops: list, sends: list) -> list:
+        return self.exchange_finish(self.exchange_start(ops, sends))
+
+    def allreduce(self, tensors: list):
+        (t,) = tensors
+        if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ValueError("NativeTransport reduces contiguous float64 device tensors")
+        call("ebs_dist_allreduce", self.op.plan.handle, D.ptr(t), t.numel(), D.stream())
+
+    def agree(self, ok: bool) -> bool:
+        t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device="cuda")
+        self.allreduce([t])
+        return int(t.item()) == self.world
 
 
 class LocalTransport:

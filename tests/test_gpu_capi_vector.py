@@ -96,3 +96,37 @@ def test_plan_apply_out_user_modes(gpu):
             assert torch.equal(b.view(torch.int64), c.view(torch.int64))  # bitwise, signs too
             assert torch.equal(b[old_of_new], a)
     assert lib.ebs_plan_apply(pl.handle, 1, P(xi), P(a), 3, 0, s) != 0
+
+
+def test_native_nccl_collectives_single_rank(gpu):
+    """ebs_dist_*: libebs.so's own NCCL communicator (world size 1 on the one GPU): the
+    grouped send/recv (to the own rank) moves the buffers, the all-reduce is the identity,
+    misuse is rejected."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200._lib import load
+    lib = load()
+    m = eb.build_unit_square_mesh(3)
+    pl = eb.build_element_batch(m).operator()
+    h = pl.handle
+    x = torch.arange(10, dtype=torch.float64, device="cuda")
+    y = torch.zeros(10, dtype=torch.float64, device="cuda")
+    peers = (ctypes.c_int32 * 1)(0)
+    counts = (ctypes.c_int64 * 1)(10)
+    sp = (ctypes.c_void_p * 1)(x.data_ptr())
+    rp = (ctypes.c_void_p * 1)(y.data_ptr())
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.ebs_dist_exchange(h, 1, peers, counts, sp, rp, s) != 0      # no communicator yet
+    uid = ctypes.create_string_buffer(128)
+    assert lib.ebs_dist_unique_id(uid) == 0
+    assert lib.ebs_dist_init(h, uid, 1, 1) != 0                            # rank out of range
+    assert lib.ebs_dist_init(h, uid, 0, 1) == 0
+    assert lib.ebs_dist_init(h, uid, 0, 1) != 0                            # already initialised
+    assert lib.ebs_dist_exchange(h, 1, peers, counts, sp, rp, s) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    bad = (ctypes.c_int32 * 1)(3)
+    assert lib.ebs_dist_exchange(h, 1, bad, counts, sp, rp, s) != 0
+    z = x.clone()
+    assert lib.ebs_dist_allreduce(h, P(z), 10, s) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(z, x)

@@ -198,3 +198,24 @@ def test_stacked_c2_weak_scaling_input(gpu):
         out[op.owned_glob] = r[op.owned_glob]
     ref = eb.residual(batch, x, deterministic=False)
     assert float((out - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+
+
+def test_native_transport_matches_torch_transport(gpu):
+    """dist loops over libebs.so's NCCL communicator (NativeTransport) at world size 1:
+    the same iterates and histories as over torch.distributed / the device-copy transport."""
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    for cfg, iters in ((5, 24), (4, 16)):
+        pr = config_problem(cfg, seed=2, size=6)
+        m = pr["mesh"]
+        op, _ = dist.rank_operator(m, pr["nu"], pr["f"], pr["dirichlet"], 1, 0)
+        prob_l = dist.setup([op], dist.LocalTransport())
+        prob_n = dist.setup([op], dist.NativeTransport(op))
+        x0 = op.zeros()
+        run = dist.pcg if cfg == 5 else dist.jacobi
+        xl, nl = run(prob_l, [x0], iters)
+        xn, nn = run(prob_n, [x0], iters)
+        xg, ng = run(prob_n, [x0], iters, graph=True)
+        np.testing.assert_array_equal(nn, nl)
+        np.testing.assert_array_equal(ng, nl)
+        assert torch.equal(xn[0], xl[0]) and torch.equal(xg[0], xl[0])
