@@ -219,6 +219,8 @@ typedef struct {
     double *r_out;           /* device, nullable: final residual (caller numbering)       */
     const double *coef_a;    /* HOST, iters entries: CHEB2 step 1/alpha_{k mod N};         */
     const double *coef_b;    /*   CHEB3 alpha_k and beta_k (solvers.py:247-258)             */
+    int fused;               /* CG / PCG without callback: the whole loop as one cooperative */
+                             /*   persistent kernel (grid-wide barriers, no launches per it) */
 } ebs_solve_params;
 
 /* synchronous on `stream` (one host read of the history at the end) */

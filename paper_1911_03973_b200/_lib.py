@@ -47,6 +47,7 @@ class SolveParams(ctypes.Structure):
         ("callback", CALLBACK), ("user", c_void_p), ("cb_x", c_void_p), ("cb_r", c_void_p),
         ("r_out", c_void_p),
         ("coef_a", POINTER(c_double)), ("coef_b", POINTER(c_double)),
+        ("fused", c_int),
     ]
 
 

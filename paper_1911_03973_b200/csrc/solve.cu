@@ -17,6 +17,8 @@
 // the host only enqueues launches; it synchronises once per batch of iterations to stop
 // enqueuing after convergence (and every iteration when a callback is attached).
 // Reductions are fixed-order (deterministic run to run).
+#include <cooperative_groups.h>
+
 #include "sell.cuh"
 
 namespace ebs {
@@ -395,6 +397,156 @@ static void ensure_hist(Plan *p, int64_t n) {
     }
 }
 
+// --------------------------------------------------- fused single-kernel CG / PCG --
+// The whole iteration loop as ONE cooperative persistent kernel (north star: "an
+// optional fully fused per-iteration kernel"): per iteration three grid-wide barriers
+//   A  q = mask(A p) (SELL sweep), block partials of p.q            | grid.sync
+//   B  every block reduces the partials in the same fixed order -> alpha;
+//      x += alpha p, r -= alpha q, partials of r.r, r.z (+ err, non-finite count)  | sync
+//   C  every block reduces -> the _iterate rules (history, tol, divergence), beta;
+//      p = z + beta p                                                  | grid.sync
+// No launches or host round trips inside the solve; every block derives the same
+// scalars from the same partials, so the loop stays in lockstep.  Arithmetic per node
+// is that of k_pcg_update / k_pcg_direction; the dots are reduced over this kernel's
+// grid (same results up to rounding, deterministic run to run).
+template <int NV>
+__device__ __forceinline__ void grid_totals(const double *partials, int G, double (&tot)[NV],
+                                            double *smem, double *bc) {
+    double w[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double acc = 0.0;
+        for (int b = threadIdx.x; b < G; b += blockDim.x) acc += __ldcg(&partials[q * G + b]);
+        w[q] = acc;
+    }
+    block_sum<NV>(w, smem);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) bc[q] = w[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) tot[q] = bc[q];
+    __syncthreads();
+}
+
+// MINB: resident CTAs per SM the register budget is sized for.  Small (latency-bound)
+// meshes use 4 (no spills: C1 16.6 us/it vs 26 us/it for three launches); meshes that fill
+// the GPU use the SELL kernels' occupancy (6 / 8), at parity with the launch-per-step loop.
+template <int NB, int IDS, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_pcg_fused(SellView v, LoopArgs L, int64_t n, int iters, double *__restrict__ x,
+                double *__restrict__ r, double *__restrict__ p, double *__restrict__ q,
+                const double *__restrict__ dinv, const uint8_t *__restrict__ free_int,
+                const double *__restrict__ ref, double *__restrict__ gpart) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sm[4 * 32];
+    __shared__ double bc[4];
+    Ctl *ctl = L.ctl;
+    if (ctl->done) return;  // set by k_pcg_init (tol met at k = 0): uniform over the grid
+    const int G = gridDim.x;
+    double *pa = gpart, *pb = gpart + G;
+    double rz = ctl->rz;
+    const double norm0 = ctl->norm0;
+    const int64_t stride = (int64_t)G * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    int k = 0, done = 0, diverged = 0;
+    while (k < iters) {
+        // A: q = mask(A p), p.q
+        PcgMatvecEpi me{free_int, q, {0.0}};
+        sell_sweep<NB, IDS, false>(v, p, me);
+        double a1[1] = {me.part[0]};
+        block_sum<1>(a1, sm);
+        if (threadIdx.x == 0) pa[blockIdx.x] = a1[0];
+        grid.sync();
+        double pq[1];
+        grid_totals<1>(pa, G, pq, sm, bc);
+        const double alpha = pq[0] != 0.0 ? rz / pq[0] : 0.0;
+        // B: x, r update, r.r, r.z (+ error, non-finite count)
+        double part[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t m = tid; m < n; m += stride) {
+            const double xn = x[m] + alpha * p[m];
+            const double rn = r[m] - alpha * q[m];
+            x[m] = xn;
+            r[m] = rn;
+            part[0] += rn * rn;
+            part[1] += rn * (dinv[m] * rn);
+            if (ref) {
+                const double d = xn - ref[m];
+                part[2] += d * d;
+            }
+            part[3] += isfinite(xn) ? 0.0 : 1.0;
+        }
+        block_sum<4>(part, sm);
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pb[i * G + blockIdx.x] = part[i];
+        }
+        grid.sync();
+        double tot[4];
+        grid_totals<4>(pb, G, tot, sm, bc);
+        // C: the _iterate rules (solvers.py:117-160), identical in every block
+        ++k;
+        const double nr = sqrt(tot[0]);
+        if (tot[3] != 0.0 || !isfinite(nr)) {
+            if (leader) {
+                L.norms[k] = tot[3] != 0.0 ? INFINITY : nr;
+                if (L.errors) L.errors[k] = tot[3] != 0.0 ? INFINITY : sqrt(tot[2]);
+            }
+            diverged = done = 1;
+            break;
+        }
+        if (leader) {
+            L.norms[k] = nr;
+            if (L.errors) L.errors[k] = sqrt(tot[2]);
+        }
+        if (L.has_tol && nr <= L.tol * norm0) {
+            done = 1;
+            break;
+        }
+        const double beta = rz != 0.0 ? tot[1] / rz : 0.0;
+        rz = tot[1];
+        if (k == iters) break;  // the last direction update would be unused
+        for (int64_t m = tid; m < n; m += stride) p[m] = dinv[m] * r[m] + beta * p[m];
+        grid.sync();
+    }
+    if (leader) {
+        ctl->k = k;
+        ctl->n_norms = k + 1;
+        ctl->rz = rz;
+        ctl->diverged = diverged;
+        ctl->done = done;
+        ctl->cb_ok = 0;
+    }
+}
+
+template <int NB, int IDS>
+void launch_pcg_fused(Plan *p, const LoopArgs &L, int iters, double *x, double *r, double *pv,
+                      double *qv, const double *dinv, const double *ref, cudaStream_t s) {
+    constexpr int MINB_BIG = NB == 3 ? EBS_MINB2 : EBS_MINB3;
+    const bool small = (p->n_chunks * LANES + 255) / 256 < 148 * 4;
+    auto kern = small ? k_pcg_fused<NB, IDS, 4> : k_pcg_fused<NB, IDS, MINB_BIG>;
+    int per_sm = 0, sms = 0, dev = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int grid = per_sm * sms;  // co-resident by construction (cooperative launch checks it)
+    const int64_t work = (p->n_chunks * LANES + 255) / 256;
+    if (grid > work) grid = (int)(work > 0 ? work : 1);
+    if (grid > RED_MAX_BLOCKS) grid = RED_MAX_BLOCKS;
+    SellView v = sell_view(p);
+    int64_t n = p->n_n;
+    double *gpart = L.partials;  // 5 * RED_MAX_BLOCKS doubles (plan partials)
+    const uint8_t *fr = p->free_int;
+    void *args[] = {&v, const_cast<LoopArgs *>(&L), &n, &iters, &x, &r, &pv, &qv,
+                    const_cast<double **>(&dinv), const_cast<uint8_t **>(&fr),
+                    const_cast<double **>(&ref), &gpart};
+    CU(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, s));
+    bump_launches(1);
+}
+
 }  // namespace ebs
 
 using namespace ebs;
@@ -643,7 +795,15 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         };
         int k = 0;
         bool done = false;
-        if (!cb) k = run_batches(p, 0, iters, batch, s, iteration, &done);
+        if (P->fused && !cb && iters > 0) {  // the whole loop as one cooperative kernel
+#define EBS_FUSED(NB_, PK_) \
+    { launch_pcg_fused<NB_, PK_>(p, L, iters, xa, r_int, pv, qv, dinv, ref_int, s); }
+            EBS_SELL_DISPATCH(p, EBS_FUSED);
+#undef EBS_FUSED
+            k = iters;
+        } else if (!cb) {
+            k = run_batches(p, 0, iters, batch, s, iteration, &done);
+        }
         while (k < iters && !done && !aborted) {
             int kend = k + batch < iters ? k + batch : iters;
             for (; k < kend; ++k) iteration(s);

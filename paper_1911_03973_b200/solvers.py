@@ -107,7 +107,7 @@ class ConvergenceHistory:
 
 
 def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.0, exact=False,
-           tol=None, reference=None, callback=None, coef_a=None, coef_b=None):
+           tol=None, reference=None, callback=None, coef_a=None, coef_b=None, fused=False):
     if iters < 0:
         raise ValueError(f"iteration count must be nonnegative, got {iters}")
     x0 = D.f64(x0)
@@ -155,6 +155,7 @@ def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.
     P.cb_x = cb_x.data_ptr() if cb_x is not None else None
     P.cb_r = cb_r.data_ptr() if cb_r is not None else None
     P.r_out = None
+    P.fused = 1 if fused else 0
     ca = cb = None
     if coef_a is not None:
         ca = (ctypes.c_double * max(1, len(coef_a)))(*coef_a)
@@ -244,13 +245,18 @@ def jacobi(batch: ElementBatch, d: DirichletData, x0, iters: int, *, omega: floa
 
 
 def cg(batch: ElementBatch, d: DirichletData, x0, iters: int, *, tol=None, reference=None,
-       callback=None):
+       callback=None, fused: bool = False):
     """NEW: conjugate gradients on the Dirichlet-masked operator (oracle pcg with
-    dinv = 1); history holds the recursive residual norms."""
-    return _solve(EBS_CG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback)
+    dinv = 1); history holds the recursive residual norms.  fused=True (no callback):
+    the whole loop as one cooperative persistent kernel."""
+    return _solve(EBS_CG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback,
+                  fused=fused)
 
 
 def pcg(batch: ElementBatch, d: DirichletData, x0, iters: int, *, tol=None, reference=None,
-        callback=None):
-    """NEW: Jacobi (diagonal) preconditioned CG (oracle/ebs_oracle.py pcg)."""
-    return _solve(EBS_PCG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback)
+        callback=None, fused: bool = False):
+    """NEW: Jacobi (diagonal) preconditioned CG (oracle/ebs_oracle.py pcg).  fused=True
+    (no callback): the whole loop as one cooperative persistent kernel -- three grid-wide
+    barriers per iteration instead of three launches (small, latency-bound meshes)."""
+    return _solve(EBS_PCG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback,
+                  fused=fused)

@@ -190,3 +190,32 @@ def test_jacobi_c4_recipe_reduced(gpu):
     # exact-residual Jacobi reproduces the oracle iterate bit for bit
     x_ex, _ = eb.jacobi(p["batch"], p["dirichlet"], x0, 200, omega=0.8, deterministic=True)
     npt.assert_array_equal(to_np(x_ex), xo)
+
+
+@pytest.mark.parametrize("method", ["cg", "pcg"])
+def test_fused_single_kernel_cg_pcg(gpu, method):
+    """fused=True (one cooperative kernel for the whole loop): same iteration count and
+    solution as the launch-per-step solver within 1e-10, oracle within 1e-8; tol stop,
+    zero iterations and the divergence flag behave as in _iterate."""
+    import torch
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    run = getattr(eb, method)
+    for cfg, size in ((1, 5), (5, 10), (4, 6)):
+        pr = config_problem(cfg, seed=1, size=size)
+        m, b, d = pr["mesh"], pr["batch"], pr["dirichlet"]
+        x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+        x1, h1 = run(b, d, x0, 3000, tol=1e-9)
+        x2, h2 = run(b, d, x0, 3000, tol=1e-9, fused=True)
+        assert len(h2.residual_norms) == len(h1.residual_norms), cfg
+        np.testing.assert_allclose(h2.residual_norms, h1.residual_norms, rtol=1e-6,
+                                   atol=1e-12 * h1.residual_norms[0])
+        assert float((x2 - x1).norm()) <= 1e-10 * float(x1.norm())
+        # fixed count, with reference error norms
+        x3, h3 = run(b, d, x0, 25, reference=x1, fused=True)
+        x4, h4 = run(b, d, x0, 25, reference=x1)
+        assert len(h3.residual_norms) == 26 and h3.error_norms is not None
+        np.testing.assert_allclose(h3.error_norms, h4.error_norms, rtol=1e-8)
+        x5, h5 = run(b, d, x0, 0, fused=True)
+        assert len(h5.residual_norms) == 1 and torch.equal(x5, x0)
+        assert not h2.diverged
