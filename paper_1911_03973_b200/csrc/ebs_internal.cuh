@@ -188,9 +188,9 @@ struct Plan {
 
 double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)
 StreamOrder &red_order();           // ordering of the per-device reduction scratch
-// caller <-> internal numbering (operators.cu); negzero: also set that vector to -0.0
+// caller <-> internal numbering (operators.cu)
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
-                 cudaStream_t s, double *negzero = nullptr);
+                 cudaStream_t s);
 void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s);
 const Perm2 *perm_get(Plan *p, int dir, cudaStream_t s);
 void perm_apply(Plan *p, const Perm2 *P, const double *in, double *out, int32_t *nonfinite,

@@ -3,33 +3,12 @@
 //   ebs_residual  <- operators.py:72-111 residual (+ operators.py:114-118 mask)
 //   ebs_matvec    <- spectrum.py:54-61 _apply_masked
 //
-// Each call is two launches: a gather of x into the plan's internal numbering (with the
-// finiteness check of operators.py:90 fused in), then the SELL kernel, whose epilogue
-// scatters straight into the caller's numbering.
+// Each call: a gather of x into the plan's internal numbering (with the finiteness check
+// of operators.py:90 fused in), a -0.0 fill of the output, then the SELL kernel, whose
+// epilogue adds each node's value straight into the caller's numbering.
 #include "sell.cuh"
 
 namespace ebs {
-
-__global__ void k_to_internal(int64_t n, const int32_t *__restrict__ old_of_new,
-                              const double *__restrict__ x_user, double *__restrict__ x_int,
-                              int32_t *nonfinite) {
-    bool bad = false;
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
-         m += (int64_t)gridDim.x * blockDim.x) {
-        double v = x_user[old_of_new[m]];
-        bad |= !isfinite(v);
-        x_int[m] = v;
-    }
-    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
-        atomicOr(nonfinite, 1);
-}
-
-__global__ void k_to_user(int64_t n, const int32_t *__restrict__ old_of_new,
-                          const double *__restrict__ v_int, double *__restrict__ v_user) {
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
-         m += (int64_t)gridDim.x * blockDim.x)
-        v_user[old_of_new[m]] = v_int[m];
-}
 
 // Caller-order output of a permuted numbering is one random 8 B store per node: the
 // L1tex pipe spends ~2 cycles on each distinct line of a warp's store (ncu: C2 MODE 1
@@ -91,61 +70,19 @@ void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
 #undef EBS_OP
 }
 
-// scatter orientation: coalesced read of x in caller order, 8 B writes into the
-// L2-resident internal vector (writes do not stall the issuing warp)
-__global__ void k_to_internal_scatter(int64_t n, const int32_t *__restrict__ new_of_old,
-                                      const double *__restrict__ x_user,
-                                      double *__restrict__ x_int, int32_t *nonfinite) {
-    bool bad = false;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double v = x_user[i];
-        bad |= !isfinite(v);
-        x_int[new_of_old[i]] = v;
-    }
-    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
-        atomicOr(nonfinite, 1);
-}
-
-// gather orientation with 8 independent index->value chains per thread (memory-level
-// parallelism for the random 8 B reads)
+// caller -> internal numbering: x_int[m] = x_user[old_of_new[m]], 8 independent
+// index -> value chains per thread.  The random 8 B reads are L1tex-wavefront bound (~2
+// cycles per distinct line; C2 33 us): measured equal or slower were a plain gather, the
+// scatter orientation (also with red.add), L2::256B / bulk-L2-prefetch hints and the
+// two-pass shared-memory schedule of perm.cu (profiles/README.md).
 constexpr int PERM_ILP = 8;
-#ifndef EBS_PERM_PF
-#define EBS_PERM_PF 0  // 0 plain gathers, 1 L2::256B gather hint, 2 bulk L2 prefetch of x first
-#endif
-
-__device__ __forceinline__ double ld_x_perm(const double *p) {
-#if EBS_PERM_PF == 1
-    double v;
-    asm volatile("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
 
 __global__ void __launch_bounds__(256)
     k_to_internal_ilp(int64_t n, const int32_t *__restrict__ old_of_new,
                       const double *__restrict__ x_user, double *__restrict__ x_int,
-                      int32_t *nonfinite, double *__restrict__ negzero) {
+                      int32_t *nonfinite) {
     bool bad = false;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-#if EBS_PERM_PF == 2
-    {   // stream this block's slice of x into L2 at sequential DRAM efficiency; the random
-        // gathers below then mostly hit L2 (a hint only: correctness never depends on it)
-        const int64_t bytes = n * 8;
-        const int64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 4095) & ~int64_t(4095);
-        const int64_t lo = (int64_t)blockIdx.x * per;
-        const int64_t hi = lo + per < bytes ? lo + per : bytes;
-        for (int64_t o = lo + (int64_t)threadIdx.x * 4096; o < hi;
-             o += (int64_t)blockDim.x * 4096) {
-            const uint32_t sz = (uint32_t)(bytes - o < 4096 ? bytes - o : 4096) & ~15u;
-            if (sz)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                             :: "l"((const char *)x_user + o), "r"(sz) : "memory");
-        }
-    }
-#endif
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
          base += stride * PERM_ILP) {
         int32_t idx[PERM_ILP];
@@ -158,7 +95,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int u = 0; u < PERM_ILP; ++u) {
             const int64_t m = base + u * stride;
-            v[u] = m < n ? ld_x_perm(x_user + idx[u]) : 0.0;
+            v[u] = m < n ? __ldg(x_user + idx[u]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < PERM_ILP; ++u) {
@@ -166,17 +103,12 @@ __global__ void __launch_bounds__(256)
             if (m < n) {
                 bad |= !isfinite(v[u]);
                 x_int[m] = v[u];
-                if (negzero) negzero[m] = -0.0;  // the output of a following red pass
             }
         }
     }
     if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
         atomicOr(nonfinite, 1);
 }
-
-#ifndef EBS_TO_INTERNAL_SCATTER
-#define EBS_TO_INTERNAL_SCATTER 2  // 0 gather, 1 scatter, 2 gather with ILP
-#endif
 
 #ifndef EBS_PERM2
 // 1: caller <-> internal permutations through the two-pass shared-memory schedule of
@@ -185,7 +117,9 @@ __global__ void __launch_bounds__(256)
 #define EBS_PERM2 0
 #endif
 
-// out[0..n) = -0.0 with 16 B stores (scalar head / tail for an unaligned or odd range)
+// out[0..n) = -0.0 with 16 B stores (scalar head / tail for an unaligned or odd range).
+// Its own kernel after the x permutation: fusing the stores into the latency-bound
+// gather, or running it first, measured slower at C2.
 __global__ void k_fill_negzero(int64_t n, double *__restrict__ out) {
     const int64_t head = (reinterpret_cast<uintptr_t>(out) & 15) ? 1 : 0;
     const int64_t n2 = n > head ? (n - head) / 2 : 0;
@@ -200,28 +134,15 @@ __global__ void k_fill_negzero(int64_t n, double *__restrict__ out) {
         o2[i] = v;
 }
 
-#ifndef EBS_FILL_MODE
-// -0.0 pre-fill of the red-mode output: 0 fused into the x permutation, 1 separate kernel
-// after it, 2 before it.  Measured at C2: 1 best (23.8 GDoF/s; 0: 23.4-23.7 -- the extra
-// stores slow the latency-bound gather; 2: 22.6-22.9)
-#define EBS_FILL_MODE 1
-#endif
-
 static void fill_negzero(int64_t n, double *out, cudaStream_t s) {
     if (n == 0) return;
     k_fill_negzero<<<grid_for((n + 1) / 2, 256, 148 * 8), 256, 0, s>>>(n, out);
     LAUNCHED();
 }
 
-// x_user (caller numbering) -> x_int; negzero (nullable, n_n doubles) is set to -0.0 in
-// the same pass (the output vector of a following red-mode SELL pass)
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
-                 cudaStream_t s, double *negzero) {
+                 cudaStream_t s) {
     if (p->n_n == 0) return;
-    if (negzero && (EBS_PERM2 || EBS_TO_INTERNAL_SCATTER != 2)) {
-        fill_negzero(p->n_n, negzero, s);
-        negzero = nullptr;
-    }
     if (EBS_PERM2) {
         Plan *pm = const_cast<Plan *>(p);
         if (const Perm2 *P = perm_get(pm, 0, s)) {
@@ -229,20 +150,13 @@ void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *no
             return;
         }
     }
-    if (EBS_TO_INTERNAL_SCATTER == 2)
-        k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
-                            s>>>(p->n_n, p->old_of_new, x_user, x_int, nonfinite, negzero);
-    else if (EBS_TO_INTERNAL_SCATTER == 1)
-        k_to_internal_scatter<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(
-            p->n_n, p->new_of_old, x_user, x_int, nonfinite);
-    else
-        k_to_internal<<<grid_for(p->n_n, 256, 148 * 32), 256, 0, s>>>(p->n_n, p->old_of_new,
-                                                                      x_user, x_int, nonfinite);
+    k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0, s>>>(
+        p->n_n, p->old_of_new, x_user, x_int, nonfinite);
     LAUNCHED();
 }
 
-// out_user[n] = v_int[new_of_old[n]]: coalesced writes, random reads of an L2-resident
-// internal vector (ILP-8)
+// internal -> caller numbering: v_user[i] = v_int[new_of_old[i]] -- coalesced writes,
+// random reads (C4: 205 us vs 481 us for the scattered-store orientation)
 __global__ void __launch_bounds__(256)
     k_from_internal_ilp(int64_t n, const int32_t *__restrict__ new_of_old,
                         const double *__restrict__ v_int, double *__restrict__ v_user) {
@@ -278,19 +192,13 @@ void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s)
             return;
         }
     }
-    // gather orientation: coalesced writes, random reads (C4: 481 -> ~130 us vs the
-    // scattered-store orientation k_to_user)
     k_from_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
                           s>>>(p->n_n, p->new_of_old, v_int, v_user);
     LAUNCHED();
 }
 
-#ifndef EBS_OUT_PERM
-#define EBS_OUT_PERM 0  // 1: SELL writes internal order, then a gather pass to caller order
-#endif
-
-// one SELL pass; old_of_new != nullptr: output in caller numbering.  prefilled: `out` was
-// already set to -0.0 (fused into to_internal) for the red-mode caller-order output.
+// one SELL pass; old_of_new != nullptr: output in the caller's numbering (red.add into
+// -0.0, filled here unless the caller did: out_user = 2 of ebs_plan_apply)
 void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *free_int,
                 const int32_t *old_of_new, double *out, cudaStream_t s, bool prefilled = false) {
     double *dst = out;
@@ -305,10 +213,6 @@ void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *fre
             o2n = nullptr;
         }
     }
-    if (!P && EBS_OUT_PERM && old_of_new) {
-        dst = plan_vec(const_cast<Plan *>(p), 7);
-        o2n = nullptr;
-    }
     if (o2n && EBS_OUT_RED) {  // red.add into -0.0 (bit-exact, see OpEpi)
         if (!prefilled) fill_negzero(p->n_n, out, s);
         red = 1;
@@ -316,13 +220,7 @@ void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *fre
     if (mode == 0) launch_sell_op<0>(p, x_int, free_int, o2n, dst, s, nullptr, nullptr, -1, red);
     else if (mode == 1) launch_sell_op<1>(p, x_int, free_int, o2n, dst, s, nullptr, nullptr, -1, red);
     else launch_sell_op<2>(p, x_int, free_int, o2n, dst, s, nullptr, nullptr, -1, red);
-    if (P) {
-        perm_apply(const_cast<Plan *>(p), P, dst, out, nullptr, s);
-    } else if (EBS_OUT_PERM && old_of_new && p->n_n) {
-        k_from_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
-                              s>>>(p->n_n, p->new_of_old, dst, out);
-        LAUNCHED();
-    }
+    if (P) perm_apply(const_cast<Plan *>(p), P, dst, out, nullptr, s);
 }
 
 }  // namespace ebs
@@ -343,10 +241,9 @@ int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int mask
     cudaStream_t s = S(stream);
     double *x_int = plan_vec(p, 0);
     if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
-    if (EBS_OUT_RED && EBS_FILL_MODE == 2) fill_negzero(p->n_n, r, s);
-    to_internal(p, x, x_int, nonfinite, s, EBS_OUT_RED && EBS_FILL_MODE == 0 ? r : nullptr);
+    to_internal(p, x, x_int, nonfinite, s);
     sell_apply(p, mode == EBS_RES_EXACT ? 2 : 1, x_int, masked ? p->free_int : nullptr,
-               p->old_of_new, r, s, EBS_OUT_RED && EBS_FILL_MODE != 1);
+               p->old_of_new, r, s);
     EBS_CATCH
 }
 
@@ -359,10 +256,8 @@ int ebs_matvec(ebs_plan_t plan, const double *x, double *y, int masked, void *st
     EBS_REQUIRE(x != y, "x and y must not alias");
     cudaStream_t s = S(stream);
     double *x_int = plan_vec(p, 0);
-    if (EBS_OUT_RED && EBS_FILL_MODE == 2) fill_negzero(p->n_n, y, s);
-    to_internal(p, x, x_int, nullptr, s, EBS_OUT_RED && EBS_FILL_MODE == 0 ? y : nullptr);
-    sell_apply(p, 0, x_int, masked ? p->free_int : nullptr, p->old_of_new, y, s,
-               EBS_OUT_RED && EBS_FILL_MODE != 1);
+    to_internal(p, x, x_int, nullptr, s);
+    sell_apply(p, 0, x_int, masked ? p->free_int : nullptr, p->old_of_new, y, s);
     EBS_CATCH
 }
 
