@@ -697,238 +697,3 @@ def emulate(batch, n_nodes, d, P, precondition=True):
 
 
 # ------------------------------------------------------------------- bench --
-def _residual_measure(p, args, rank, world, comm, sampler):
-    """Time K residual steps r = b - A x (x, r in the caller's numbering) on `world`
-    element slabs of problem `p` (device time, max over ranks).  Returns a dict for rank
-    0's JSON line: per-step time, kernel time, launches, and the end-to-end time with
-    each rank's x slab copied in from pinned host memory and its owned r entries out."""
-    import statistics
-    import torch.distributed as dist
-
-    m = p["mesh"]
-    op, maps = rank_operator(m, p["nu"], p["f"], None, world, rank)
-    setup([op], comm)
-    x_glob = torch.from_numpy(p["x"]).cuda()
-    x_int = op.zeros()
-    s_raw = op.zeros()
-    stream = torch.cuda.current_stream()
-    r_glob = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
-    lo, hi = int(maps["bounds"][rank]), int(maps["bounds"][rank + 1])
-
-    def step(ev=None, x_in=True):
-        # gather the slab's x (caller -> rank numbering); SELL pass over the interface
-        # chunks writing the partial residual into caller numbering (+ internal copy); NCCL
-        # halo of the interface partials in flight while the interior chunks are swept;
-        # owned interface entries completed with the neighbours' partials
-        if x_in:
-            op.gather_global(x_glob, x_int)
-        if ev is not None:
-            ev[0].record(stream)
-        op.residual_caller_sweep(op.if_chunks, x_int, r_glob, s_raw)
-        h = comm.exchange_start([op], [{q: op.gather(idx, s_raw)
-                                        for q, idx in op.if_idx.items()}])
-        op.residual_caller_sweep(op.in_chunks, x_int, r_glob, s_raw)
-        if ev is not None:
-            ev[1].record(stream)
-        recvs = comm.exchange_finish(h)
-        op.correct_owned(r_glob, recvs[0])
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    sampler.on()
-    dist.barrier()
-    torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-    for k in range(args.steps):  # per-kernel pass (eager, events around the SELL sweeps)
-        step(evs[k])
-    torch.cuda.synchronize()
-    kern = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
-    GB = GRAPH_BATCH
-
-    def body():
-        for _ in range(GB):
-            step()
-    graph = _capture(comm, body)
-    if graph is not None:
-        graph.replay()
-        torch.cuda.synchronize()
-    n0 = load().ebs_launch_count()
-    step()
-    torch.cuda.synchronize()
-    launches_per_step = load().ebs_launch_count() - n0
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    done = 0
-    if graph is not None:
-        while done + GB <= args.steps:
-            graph.replay()
-            done += GB
-    for _ in range(args.steps - done):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1) / 1e3, kern], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    # end to end: each rank's x slab (its local nodes) in from pinned host memory, its
-    # owned entries of r out to pinned host memory, every step
-    x_host = x_glob[op.global_of_int].cpu().pin_memory()
-    own = op.owned_glob
-    r_host = torch.empty(own.numel(), dtype=torch.float64).pin_memory()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(stream)
-    for _ in range(args.steps):
-        x_int.copy_(x_host, non_blocking=True)
-        step(x_in=False)
-        r_host.copy_(r_glob[own], non_blocking=True)
-    e3.record(stream)
-    torch.cuda.synchronize()
-    ref = r_glob[own].cpu()
-    assert torch.equal(r_host, ref), "end-to-end residual differs from the device-timed one"
-    te = torch.tensor([e2.elapsed_time(e3) / 1e3], device="cuda")
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    byt = torch.tensor([8.0 * op.n, 8.0 * own.numel()], device="cuda")
-    dist.all_reduce(byt, op=dist.ReduceOp.SUM)
-    sampler.off()
-    out = {"T": float(t[0]), "kern": float(t[1]), "te": float(te[0]),
-           "h2d": int(byt[0]), "d2h": int(byt[1]), "launches": launches_per_step * args.steps,
-           "n_nodes": m.n_nodes, "n_elements": m.n_elements,
-           "bytes_rank": __import__("bench").residual_bytes(op.n, hi - lo),
-           "graph": graph is not None}
-    del op, x_glob, x_int, s_raw, r_glob
-    torch.cuda.empty_cache()
-    return out
-
-
-def bench_rank(args, rank, world, local_rank):
-    """bench.py --gpus N under torchrun.  `value`: the C2 residual weak-scaled over N
-    element slabs -- N level-11 unit squares stacked in y (inputs.stacked_c2_problem), one
-    C2-sized slab per rank, the NCCL halo of the shared node rows -- whole-job GDoF/s =
-    total nodes x K / max-over-ranks device time.  Also reported: the fixed C2 mesh
-    strong-scaled over the same N slabs, and (extras) C4 / C5 solver strong scaling."""
-    import json
-    import os
-    import sys
-    import torch.distributed as dist
-
-    from .inputs import config_problem, stacked_c2_problem
-    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    import bench as B
-
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    peaks, peak_kind = B.load_peaks()
-    sampler = B.ClockSampler(index=local_rank).start()
-    comm = TorchTransport()
-    weak = _residual_measure(stacked_c2_problem(world, seed=args.seed, size=args.size), args,
-                             rank, world, comm, sampler)
-    strong = None
-    if world > 1:
-        strong = _residual_measure(config_problem(2, seed=args.seed, size=args.size,
-                                                  assemble=False), args, rank, world, comm,
-                                   sampler)
-    sampler.stop()
-    line = None
-    if rank == 0:
-        peak = float(peaks["hbm_gbs"])
-        T = weak["T"]
-        line = {"metric": B.METRIC, "value": weak["n_nodes"] * args.steps / T / 1e9,
-                "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 squares)",
-                "config": {"workload": f"C2 weak-scaled: {world} level-11 unit squares stacked "
-                                       "in y, one C2-sized element slab per GPU, NCCL halo of "
-                                       "the shared node rows; element residual r=b-Ax per step",
-                           "n_nodes": weak["n_nodes"], "n_elements": weak["n_elements"],
-                           "per_gpu": "one C2 square (4.2M nodes, 8.4M triangles)",
-                           "seed": args.seed,
-                           "mode": "fast (pre-assembled b); x and r in the caller's numbering",
-                           "l2": "inputs larger than L2 (slot stream ~1 GB per rank); no flush",
-                           "parallelism": f"element slabs x{world}",
-                           "cuda_graph": dict(GRAPH_STATS)},
-                "roofline": {"bound": "hbm", "achieved": weak["bytes_rank"] / weak["kern"] / 1e9,
-                             "peak": peak, "unit": "GB/s",
-                             "frac": weak["bytes_rank"] / weak["kern"] / 1e9 / peak,
-                             "traffic": None,
-                             "kernel": "k_sell_op<3,1,1> over the slab's chunks (max over ranks)",
-                             "bytes_per_launch": weak["bytes_rank"], "kernel_ms": weak["kern"] * 1e3,
-                             "peak_source": peak_kind},
-                "e2e": {"value": weak["n_nodes"] * args.steps / weak["te"] / 1e9, "unit": "GDoF/s",
-                        "h2d_bytes_per_step": weak["h2d"], "d2h_bytes_per_step": weak["d2h"],
-                        "api": "per rank: x slab H2D from pinned host, dist residual step, "
-                               "owned r entries D2H to pinned host"},
-                "gpu_launches": weak["launches"], "clocks": sampler.summary(),
-                "cpu_baseline": None}
-        if strong is not None:
-            line["strong_c2"] = {
-                "value": strong["n_nodes"] * args.steps / strong["T"] / 1e9, "unit": "GDoF/s",
-                "ms_per_step": strong["T"] / args.steps * 1e3, "scaling": "strong",
-                "workload": "the fixed C2 mesh (4.2M nodes) over the same element slabs",
-                "kernel_ms": strong["kern"] * 1e3, "cuda_graph": strong["graph"]}
-    solvers = {}
-    if getattr(args, "extra", False):
-        solvers = _bench_solvers(args, rank, world)
-    if rank == 0:
-        if solvers:
-            line["solvers"] = solvers
-        print(json.dumps(line), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
-
-
-def _bench_solvers(args, rank, world):
-    """C4 damped Jacobi x200 and C5 Jacobi-PCG x500 on `world` element slabs (strong
-    scaling; device time, max over ranks).  Errors are reported, never raised."""
-    import gc
-    import torch.distributed as dist
-    from .inputs import config_problem
-    peaks = __import__("bench").load_peaks()[0]
-    out = {}
-    for cfg, iters in ((4, 200), (5, 500)):
-        if cfg not in getattr(args, "solver_configs", (4, 5)):
-            continue
-        try:
-            p = config_problem(cfg, seed=args.seed, assemble=False)
-            d, m = p["dirichlet"], p["mesh"]
-            op, maps = rank_operator(m, p["nu"], p["f"], d, world, rank)
-            del p
-            gc.collect()
-            torch.cuda.empty_cache()
-            comm = TorchTransport()
-            prob = setup([op], comm)
-            x0 = op.zeros()
-            run = (lambda: jacobi(prob, [x0], iters, 0.8, graph=True)) if cfg == 4 else \
-                (lambda: pcg(prob, [x0], iters, graph=True))
-            run()  # warm-up (creates the NCCL P2P communicators)
-            torch.cuda.synchronize()
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            _, norms = run()
-            e1.record()
-            torch.cuda.synchronize()
-            t = torch.tensor([e0.elapsed_time(e1) / 1e3], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            T = float(t)
-            nb = m.n_b
-            per_it = m.n_elements * (8 * nb * nb + 4 * nb) + (32 if cfg == 4 else 104) * m.n_nodes
-            out[f"C{cfg}"] = {"method": "jacobi" if cfg == 4 else "pcg", "iterations": iters,
-                              "ranks": world, "it_per_s": iters / T, "ms_per_it": T / iters * 1e3,
-                              "hbm_gbs_algorithmic_total": per_it * iters / T / 1e9,
-                              "frac_of_peak_per_gpu": per_it * iters / T / 1e9 / world /
-                              float(peaks["hbm_gbs"]),
-                              "final_norm": float(norms[-1]), "n_nodes": m.n_nodes,
-                              "cuda_graph": dict(GRAPH_STATS),
-                              "n_elements": m.n_elements}
-            del op, prob
-        except Exception as e:  # noqa: BLE001
-            out[f"C{cfg}"] = {"error": f"{type(e).__name__}: {e}"}
-        gc.collect()
-        torch.cuda.empty_cache()
-    return out
