@@ -184,6 +184,8 @@ struct Plan {
     double *hist_dev = nullptr;  // device history (norms, errors)
     int64_t hist_cap = 0;
     int32_t *flag = nullptr;     // device scratch flag
+    uint8_t *rowflag = nullptr;  // id layout 3 (3D): 1 per two-base row (sell.cuh IDS_DELTA2)
+    int64_t two_base_rows = 0;   // id layout 3: rows coded with two bases
 };
 
 double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)

@@ -16,6 +16,9 @@
 
 #include "ebs_internal.cuh"
 
+#ifndef EBS_IDS_DELTA2
+#define EBS_IDS_DELTA2 0  // 3D two-base row coding of the id plane (opt-in: measured slower)
+#endif
 #ifndef EBS_IDS_TABLE
 #define EBS_IDS_TABLE 0  // per-chunk delta-table id layout (opt-in: measured slower, profiles/README.md)
 #endif
@@ -252,6 +255,107 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// id layout 3 (3D): per slot row, the mode of the 32 lanes' delta triples is base 1, the
+// mode of the lanes more than 255 away from it base 2; when every valid lane lies within
+// +-255 of one of them the row is coded with 32-bit words (j:2 | base:1 | 3 x 9-bit
+// residual + 256) and the two bases at byte 128 of the id plane (rowflag = 1), else with
+// IDS_DELTA's 64-bit words (rowflag = 0).  One warp per chunk.
+__device__ __forceinline__ bool same3(int a0, int a1, int a2, int b0, int b1, int b2) {
+    return a0 == b0 && a1 == b1 && a2 == b2;
+}
+
+__global__ void __launch_bounds__(128)
+    k_write_ids_delta2(int64_t n_n, int64_t n_chunks, int rowb,
+                       const int32_t *__restrict__ rowbase, const int32_t *__restrict__ width,
+                       const int32_t *__restrict__ cnt, const int32_t *__restrict__ ids_abs,
+                       uint8_t *__restrict__ slot, uint8_t *__restrict__ rowflag,
+                       unsigned long long *two_rows) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long n_two = 0;
+    for (int64_t c = warp; c < n_chunks; c += nwarps) {
+        const int64_t m = c * LANES + lane;
+        const int64_t self = m < n_n ? m : 0;
+        const int c_m = m < n_n ? cnt[m] : 0;
+        const int w = width[c];
+        for (int k = 0; k < w; ++k) {
+            const int64_t row = (int64_t)rowbase[c] + k;
+            const int32_t *src = ids_abs + row * 3 * LANES + lane;
+            const bool valid = k < c_m;
+            const int32_t id0 = src[0];
+            const uint32_t j = (uint32_t)id0 >> J_SHIFT;
+            int d0 = 0, d1 = 0, d2 = 0;
+            if (valid) {
+                d0 = (int)((id0 & ID_MASK) - self);
+                d1 = (int)((src[LANES] & ID_MASK) - self);
+                d2 = (int)((src[2 * LANES] & ID_MASK) - self);
+            }
+            // base 1: the most frequent valid triple (ties: lowest lane)
+            int votes = 0;
+            for (int o = 0; o < LANES; ++o) {
+                const int e0 = __shfl_sync(0xffffffffu, d0, o), e1 = __shfl_sync(0xffffffffu, d1, o);
+                const int e2 = __shfl_sync(0xffffffffu, d2, o);
+                const bool vo = __shfl_sync(0xffffffffu, valid, o);
+                votes += vo && same3(e0, e1, e2, d0, d1, d2);
+            }
+            int key = valid ? votes * 64 + (31 - lane) : -1;
+            for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+            const int win1 = key >= 0 ? 31 - (key & 63) : 0;
+            const int b10 = __shfl_sync(0xffffffffu, d0, win1), b11 = __shfl_sync(0xffffffffu, d1, win1);
+            const int b12 = __shfl_sync(0xffffffffu, d2, win1);
+            auto near = [](int a0, int a1, int a2, int b0, int b1, int b2) {
+                return abs(a0 - b0) <= 255 && abs(a1 - b1) <= 255 && abs(a2 - b2) <= 255;
+            };
+            const bool fit1 = valid && near(d0, d1, d2, b10, b11, b12);
+            const bool far = valid && !fit1;
+            // base 2: the most frequent triple among the lanes base 1 does not cover
+            int votes2 = 0;
+            for (int o = 0; o < LANES; ++o) {
+                const int e0 = __shfl_sync(0xffffffffu, d0, o), e1 = __shfl_sync(0xffffffffu, d1, o);
+                const int e2 = __shfl_sync(0xffffffffu, d2, o);
+                const bool fo = __shfl_sync(0xffffffffu, far, o);
+                votes2 += fo && same3(e0, e1, e2, d0, d1, d2);
+            }
+            int key2 = far ? votes2 * 64 + (31 - lane) : -1;
+            for (int o = 16; o > 0; o >>= 1) key2 = max(key2, __shfl_xor_sync(0xffffffffu, key2, o));
+            const int win2 = key2 >= 0 ? 31 - (key2 & 63) : win1;
+            const int b20 = __shfl_sync(0xffffffffu, d0, win2), b21 = __shfl_sync(0xffffffffu, d1, win2);
+            const int b22 = __shfl_sync(0xffffffffu, d2, win2);
+            const bool fit2 = valid && near(d0, d1, d2, b20, b21, b22);
+            const bool two = __all_sync(0xffffffffu, !valid || fit1 || fit2);
+            uint8_t *dst = slot + row * rowb + 4 * 256;
+            if (two) {
+                uint32_t code = 0;
+                if (valid) {
+                    const bool sel = !fit1;
+                    const int c0 = d0 - (sel ? b20 : b10) + 256, c1 = d1 - (sel ? b21 : b11) + 256;
+                    const int c2 = d2 - (sel ? b22 : b12) + 256;
+                    code = (j << 30) | ((uint32_t)sel << 29) | ((uint32_t)c0 << 18) |
+                           ((uint32_t)c1 << 9) | (uint32_t)c2;
+                }
+                reinterpret_cast<uint32_t *>(dst)[lane] = code;
+                if (lane < 8) {
+                    const int h[8] = {b10, b11, b12, b20, b21, b22, 0, 0};
+                    reinterpret_cast<int32_t *>(dst + 128)[lane] = h[lane];
+                }
+                if (lane == 0) {
+                    rowflag[row] = 1;
+                    ++n_two;
+                }
+            } else {
+                unsigned long long wd = (unsigned long long)j << 62;
+                const int dd[3] = {d0, d1, d2};
+                for (int t = 0; t < 3; ++t)
+                    wd |= ((unsigned long long)(dd[t] + (1 << 19)) & 0xFFFFFull) << (20 * (2 - t));
+                reinterpret_cast<unsigned long long *>(dst)[lane] = wd;
+                if (lane == 0) rowflag[row] = 0;
+            }
+        }
+    }
+    if (lane == 0 && n_two) atomicAdd(two_rows, n_two);
+}
+
 // id plane of every slot row (sell.cuh layout): delta-packed or absolute
 __global__ void k_write_ids(int nb, int64_t n_n, int64_t n_chunks, int rowb, int packed,
                             const int32_t *__restrict__ rowbase, const int32_t *__restrict__ width,
@@ -430,7 +534,7 @@ static void plan_free(Plan *p) {
     dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->rowbase);
     dfree(p->width); dfree(p->slot_ej); dfree(p->slot); dfree(p->tab); dfree(p->taboff);
     dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
-    dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag);
+    dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag); dfree(p->rowflag);
     for (auto &v : p->wvec) dfree(v);
     perm_free(p);
     dist_free(p);
@@ -575,9 +679,10 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
         }
         const unsigned long long limit = nb == 3 ? (1ull << 14) - 1 : (1ull << 19) - 1;
         if (layout < 0) layout = max_delta <= limit ? 1 : 0;
+        if (layout == 1 && nb == 4 && EBS_IDS_DELTA2) layout = 3;  // same plane, two-base rows
         p->packed = layout;
         const int id_bytes = layout == 2 ? (nb == 3 ? 2 : 4) * LANES
-                                         : (layout == 1 ? (nb == 3 ? 4 : 8) * LANES
+                                         : (layout == 1 || layout == 3 ? (nb == 3 ? 4 : 8) * LANES
                                                         : 4 * (nb - 1) * LANES);
         p->rowb = nb * 8 * LANES + id_bytes;
         p->slot = dmalloc<uint8_t>((size_t)p->n_rows * p->rowb);
@@ -594,6 +699,20 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
                 nb, n_n, p->n_chunks, cap, p->rowbase, p->width, p->cnt, ids_abs, nullptr,
                 p->taboff, p->tab, p->slot, p->rowb, p->flag);
             LAUNCHED();
+        } else if (layout == 3 && p->n_chunks) {
+            p->tab = dmalloc<int32_t>(1);
+            p->rowflag = dmalloc<uint8_t>(p->n_rows);
+            unsigned long long *nt = dmalloc<unsigned long long>(1);
+            CU(cudaMemsetAsync(nt, 0, sizeof(unsigned long long), s));
+            k_write_ids_delta2<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
+                n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, ids_abs, p->slot,
+                p->rowflag, nt);
+            LAUNCHED();
+            unsigned long long h = 0;
+            CU(cudaMemcpyAsync(&h, nt, sizeof h, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            cudaFree(nt);
+            p->two_base_rows = (int64_t)h;
         } else if (p->n_chunks) {
             p->tab = dmalloc<int32_t>(1);
             k_write_ids<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
@@ -673,7 +792,8 @@ int ebs_plan_info(ebs_plan_t plan, int64_t *info) {
     int64_t slots = p->n_rows * LANES;
     info[5] = p->n_rows * (int64_t)p->rowb + (p->has_be ? slots * 8 : 0);
     info[6] = p->max_valence;
-    info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0) | (p->packed ? 4 : 0) | (p->packed == 2 ? 8 : 0);
+    info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0) | (p->packed ? 4 : 0) |
+              (p->packed == 2 ? 8 : 0) | (p->packed == 3 ? 16 : 0);
     EBS_CATCH
 }
 

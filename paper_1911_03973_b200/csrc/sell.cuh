@@ -35,17 +35,26 @@ struct SellView {
     const int32_t *__restrict__ taboff;  // n_chunks + 1 offsets into tab
     const int32_t *__restrict__ clist;   // nullable: sweep only these chunks
     int64_t nlist;                       // number of chunks swept (n_chunks or list size)
+    const uint8_t *__restrict__ rowflag; // IDS_DELTA2: 1 = two-base row, 0 = 64-bit deltas
 };
 
 inline SellView sell_view(const Plan *p, const int32_t *clist = nullptr, int64_t nlist = -1) {
     return SellView{p->n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, p->slot,
-                    p->slot_be, p->tab, p->taboff, clist, clist ? nlist : p->n_chunks};
+                    p->slot_be, p->tab, p->taboff, clist, clist ? nlist : p->n_chunks,
+                    p->rowflag};
 }
 
 // id-plane layouts (Plan::packed)
 constexpr int IDS_ABS = 0;    // NB-1 planes of int32 absolute ids, j in the top bits of plane 0
 constexpr int IDS_DELTA = 1;  // deltas to the node packed in 32 (2D) / 64 (3D) bits
 constexpr int IDS_TABLE = 2;  // indices into a per-chunk table of deltas: 16 (2D) / 32 (3D) bits
+// 3D only: rows whose 32 delta triples lie within +-255 of one of two row bases store a
+// 32-bit code per lane (j:2 | base:1 | 3 x 9-bit residual) in the first half of the id
+// plane and the two base triples at byte 128 (24 B, read once per row by the whole warp):
+// 160 B read per row instead of 256.  Other rows keep IDS_DELTA's 64-bit words; a 1-byte
+// flag per row (SellView::rowflag) says which.  No lookup on the id -> x-gather chain:
+// code, bases and flag are independent loads.
+constexpr int IDS_DELTA2 = 3;
 
 template <int NB>
 struct Tab;
@@ -156,6 +165,28 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
                     jj[u] = Pack<NB>::j(wd);
 #pragma unroll
                     for (int t = 0; t < NB - 1; ++t) nid[u][t] = (int32_t)(m + Pack<NB>::d(wd, t));
+                } else if constexpr (IDS == IDS_DELTA2) {
+                    static_assert(NB == 4, "IDS_DELTA2 is the 3D layout");
+                    const uint8_t *ip = rp + NB * 256;
+                    const int two = __ldg(v.rowflag + row);
+                    const uint32_t code = __ldcs(reinterpret_cast<const uint32_t *>(ip) + lane);
+                    const int4 h0 = __ldg(reinterpret_cast<const int4 *>(ip + 128));
+                    const int2 h1 = __ldg(reinterpret_cast<const int2 *>(ip + 144));
+                    if (two) {
+                        const bool second = (code >> 29) & 1u;
+                        const int b0 = second ? h0.w : h0.x, b1 = second ? h1.x : h0.y;
+                        const int b2 = second ? h1.y : h0.z;
+                        jj[u] = (int)(code >> 30);
+                        nid[u][0] = (int32_t)m + b0 + (int)((code >> 18) & 511u) - 256;
+                        nid[u][1] = (int32_t)m + b1 + (int)((code >> 9) & 511u) - 256;
+                        nid[u][2] = (int32_t)m + b2 + (int)(code & 511u) - 256;
+                    } else {
+                        const unsigned long long wd =
+                            __ldcs(reinterpret_cast<const unsigned long long *>(ip) + lane);
+                        jj[u] = Pack<4>::j(wd);
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) nid[u][t] = (int32_t)(m + Pack<4>::d(wd, t));
+                    }
                 } else {
                     const int32_t *ip = reinterpret_cast<const int32_t *>(rp + NB * 256) + lane;
 #pragma unroll
@@ -198,6 +229,7 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
 // Raw id word(s) of one slot and their decoding (IDS_DELTA / IDS_ABS).
 template <int NB, int IDS>
 struct IdWord {
+    static_assert(IDS == IDS_DELTA || IDS == IDS_ABS, "one-slot-ahead ids: DELTA / ABS only");
     using W = typename Pack<NB>::W;
     W w;
     int32_t a[NB - 1];
@@ -479,7 +511,7 @@ template <int NB, int IDS, bool EXACT, bool PIPE = false, class Epi>
 __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__restrict__ x,
                                            Epi &epi) {
 #if EBS_TMA
-    if constexpr (IDS != IDS_TABLE) {
+    if constexpr (IDS != IDS_TABLE && IDS != IDS_DELTA2) {
         if (v.clist == nullptr) {  // the TMA ring sweeps all chunks
             sell_sweep_tma<NB, IDS, EXACT>(v, x, epi);
             return;
@@ -498,6 +530,7 @@ __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__re
             else M(3, IDS_ABS)                                                           \
         } else {                                                                         \
             if ((p)->packed == IDS_TABLE) M(4, IDS_TABLE)                                \
+            else if ((p)->packed == IDS_DELTA2) M(4, IDS_DELTA2)                         \
             else if ((p)->packed == IDS_DELTA) M(4, IDS_DELTA)                           \
             else M(4, IDS_ABS)                                                           \
         }                                                                                \
