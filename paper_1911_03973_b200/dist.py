@@ -12,7 +12,9 @@ rank touching the node) and are all-reduced.  Maps (local node sets, interfaces,
 match oracle/ebs_oracle.py halo_maps bit for bit.
 
 The solver loops are written against two small protocols so the same code runs
-  * distributed: one ``GpuRankOperator`` per process, ``TorchTransport`` (NCCL / gloo);
+  * distributed: one ``GpuRankOperator`` per process, ``TorchTransport`` (NCCL / gloo
+                 through torch.distributed) or ``NativeTransport`` (libebs.so's own NCCL
+                 communicator, ebs_dist_*);
   * emulated:    P ``GpuRankOperator``s in one process on one GPU, ``LocalTransport``
                  (device copies; used by the GPU tests -- nothing waits on anything);
   * CPU tests:   a torch-CPU rank operator (tests/) over gloo, world size 2.
@@ -694,6 +696,3 @@ def emulate(batch, n_nodes, d, P, precondition=True):
     ops = [GpuRankOperator(batch, n_nodes, d, maps, p) for p in range(P)]
     comm = LocalTransport()
     return setup(ops, comm, precondition=precondition), maps
-
-
-# ------------------------------------------------------------------- bench --
