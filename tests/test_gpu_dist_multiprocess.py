@@ -38,6 +38,12 @@ def _worker(rank, world, port, out):
             x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
             if cfg == 4:
                 xs, norms = D.jacobi(prob, [op.to_internal(x0)], 30, 0.8)
+                # graph=True: host-staged gloo cannot be captured, on either rank -- the
+                # collective decision (dist._capture) sends both ranks down the eager path
+                before = dict(D.GRAPH_STATS)
+                xg_, ng_ = D.jacobi(prob, [op.to_internal(x0)], 30, 0.8, graph=True)
+                res["fallback"] = D.GRAPH_STATS["fallback"] - before["fallback"]
+                res["graph_equal"] = bool(np.array_equal(ng_, norms)) and torch.equal(xg_[0], xs[0])
             else:
                 xs, norms = D.pcg(prob, [op.to_internal(x0)], 500, tol=1e-8)
             xg = D.gather_global([op], xs, m.n_nodes, comm)
@@ -61,6 +67,7 @@ def test_two_gpu_rank_processes_match_single_gpu(gpu):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    assert res["fallback"] == 1 and res["graph_equal"]
     for cfg, size in ((4, 6), (3, 6)):
         pr = config_problem(cfg, seed=3, size=size)
         x0 = torch.zeros(pr["mesh"].n_nodes, dtype=torch.float64, device="cuda")
