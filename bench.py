@@ -490,6 +490,28 @@ def solver_extras(args):
             torch.cuda.empty_cache()
         except Exception as e:  # report, never kill the headline line
             out[f"C{cfg}"] = {"error": f"{type(e).__name__}: {e}"}
+    try:  # C1 (the reference's CPU-scale case): JPCG to 1e-8, three launches per
+        # iteration vs the whole loop as one cooperative kernel (pcg(..., fused=True))
+        p = config_problem(1, seed=args.seed)
+        batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+        x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+        c1 = {"method": "pcg", "n_nodes": m.n_nodes, "n_elements": m.n_elements}
+        for fused in (False, True):
+            eb.pcg(batch, d, x0, 10000, tol=1e-8, fused=fused)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, h = eb.pcg(batch, d, x0, 10000, tol=1e-8, fused=fused)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            c1["fused_kernel" if fused else "launch_loop"] = {
+                "iterations": h.iterations, "it_per_s": h.iterations / t,
+                "us_per_it": t / h.iterations * 1e6, "solve_ms": t * 1e3}
+        c1["note"] = "latency-bound (1.1 MB per iteration): no roofline claim"
+        out["C1"] = c1
+    except Exception as e:  # noqa: BLE001
+        out["C1"] = {"error": f"{type(e).__name__}: {e}"}
     return out
 
 
