@@ -113,8 +113,11 @@ def _agree_worker(rank, world, port, out):
     try:
         comm = D.TorchTransport()
         res = [comm.agree(True), comm.agree(rank != 1), comm.agree(False)]
-        # a capture that cannot happen here (no CUDA) on every rank -> all ranks drop it
-        g = D._capture(comm, lambda: None)
+
+        def body():  # rank 1 cannot capture (here or on a GPU box); rank 0 may
+            if rank == 1:
+                raise RuntimeError("capture not possible on this rank")
+        g = D._capture(comm, body)
         out.put((rank, res, g is None))
     finally:
         dist.destroy_process_group()
