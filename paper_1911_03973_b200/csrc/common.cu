@@ -75,6 +75,16 @@ __global__ void k_scatter_add(int64_t n, const int64_t *__restrict__ idx,
         v[idx[i]] += buf[i];
 }
 
+int sm_count() {
+    static int cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    int &c = cache[dev & 63];
+    if (c == 0 && cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        c = 148;
+    return c;
+}
+
 // occupancy-sized persistent grid, cached per (kernel, device)
 int persistent_grid(const void *kernel, int block, int64_t work_blocks, size_t smem) {
     struct Ent { const void *k; int dev; int block; size_t smem; int grid; };

@@ -78,7 +78,11 @@ void dfree(T *&p) {
 
 // grid for a 1-D elementwise launch: enough CTAs to fill the 148 SMs several
 // times over, grid-stride beyond that
-inline int grid_for(int64_t n, int block, int max_blocks = 148 * 16) {
+// streaming multiprocessors of the current device (cached per device; 148 on B200)
+int sm_count();
+
+inline int grid_for(int64_t n, int block, int max_blocks = -1) {
+    if (max_blocks < 0) max_blocks = sm_count() * 16;
     int64_t g = (n + block - 1) / block;
     if (g < 1) g = 1;
     if (g > max_blocks) g = max_blocks;

@@ -136,7 +136,7 @@ __global__ void k_fill_negzero(int64_t n, double *__restrict__ out) {
 
 static void fill_negzero(int64_t n, double *out, cudaStream_t s) {
     if (n == 0) return;
-    k_fill_negzero<<<grid_for((n + 1) / 2, 256, 148 * 8), 256, 0, s>>>(n, out);
+    k_fill_negzero<<<grid_for((n + 1) / 2, 256, sm_count() * 8), 256, 0, s>>>(n, out);
     LAUNCHED();
 }
 
@@ -150,7 +150,7 @@ void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *no
             return;
         }
     }
-    k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0, s>>>(
+    k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, sm_count() * 8), 256, 0, s>>>(
         p->n_n, p->old_of_new, x_user, x_int, nonfinite);
     LAUNCHED();
 }
@@ -192,7 +192,7 @@ void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s)
             return;
         }
     }
-    k_from_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, 148 * 8), 256, 0,
+    k_from_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, sm_count() * 8), 256, 0,
                           s>>>(p->n_n, p->new_of_old, v_int, v_user);
     LAUNCHED();
 }

@@ -671,7 +671,7 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
         if (EBS_IDS_TABLE && p->n_chunks) {
             counts = dmalloc<int32_t>(p->n_chunks);
             CU(cudaMemsetAsync(p->flag, 0, sizeof(int32_t), s));
-            k_chunk_tables<<<grid_for(p->n_chunks * 32, 128, 148 * 16), 128, 0, s>>>(
+            k_chunk_tables<<<grid_for(p->n_chunks * 32, 128, sm_count() * 16), 128, 0, s>>>(
                 nb, n_n, p->n_chunks, cap, p->rowbase, p->width, p->cnt, ids_abs, counts, nullptr,
                 nullptr, nullptr, 0, p->flag);
             LAUNCHED();
@@ -695,7 +695,7 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
                                cudaMemcpyHostToDevice, s));
             CU(cudaStreamSynchronize(s));
             p->tab = dmalloc<int32_t>(ntab);
-            k_chunk_tables<<<grid_for(p->n_chunks * 32, 128, 148 * 16), 128, 0, s>>>(
+            k_chunk_tables<<<grid_for(p->n_chunks * 32, 128, sm_count() * 16), 128, 0, s>>>(
                 nb, n_n, p->n_chunks, cap, p->rowbase, p->width, p->cnt, ids_abs, nullptr,
                 p->taboff, p->tab, p->slot, p->rowb, p->flag);
             LAUNCHED();
@@ -824,7 +824,7 @@ int ebs_plan_load(ebs_plan_t plan, const double *A_e, const double *b_e, void *s
     if (want_be && !p->slot_be) p->slot_be = dmalloc<double>(n_slots);
     if (want_be && !p->b_int) p->b_int = dmalloc<double>(p->n_n);
     if (n_slots) {
-        k_pack<<<grid_for(n_slots, 256, 148 * 64), 256, 0, s>>>(
+        k_pack<<<grid_for(n_slots, 256, sm_count() * 64), 256, 0, s>>>(
             p->nb, p->n_e, n_slots, p->rowb, p->slot_ej, A_e, b_e, p->slot,
             b_e ? p->slot_be : nullptr);
         LAUNCHED();

@@ -526,7 +526,7 @@ template <int NB, int IDS>
 void launch_pcg_fused(Plan *p, const LoopArgs &L, int iters, double *x, double *r, double *pv,
                       double *qv, const double *dinv, const double *ref, cudaStream_t s) {
     constexpr int MINB_BIG = NB == 3 ? EBS_MINB2 : EBS_MINB3;
-    const bool small = (p->n_chunks * LANES + 255) / 256 < 148 * 4;
+    const bool small = (p->n_chunks * LANES + 255) / 256 < sm_count() * 4;
     auto kern = small ? k_pcg_fused<NB, IDS, 4> : k_pcg_fused<NB, IDS, MINB_BIG>;
     int per_sm = 0, sms = 0, dev = 0;
     CU(cudaGetDevice(&dev));
