@@ -20,40 +20,44 @@ def _bench_module():
 
 
 def _residual_measure(p, args, rank, world, comm, sampler):
-    """Time K residual steps r = b - A x (x, r in the caller's numbering) on `world`
-    element slabs of problem `p` (device time, max over ranks).  Returns a dict for rank
-    0's JSON line: per-step time, kernel time, launches, and the end-to-end time with
-    each rank's x slab copied in from pinned host memory and its owned r entries out."""
+    """Time K residual steps r = b - A x on `world` element slabs of problem `p` (device
+    time, max over ranks), x and r in each rank's caller order -- its local nodes in
+    ascending global id (dist.residual_local).  Returns a dict for rank 0's JSON line:
+    per-step time, kernel time, launches, and the end-to-end time with each rank's x
+    slab copied in from pinned host memory and its owned r entries out."""
+    import ctypes
     import statistics
     import torch.distributed as dist
 
+    from paper_1911_03973_b200 import _device as D
+
+    lib = load()
     m = p["mesh"]
     op, maps = rank_operator(m, p["nu"], p["f"], None, world, rank)
     setup([op], comm)
-    x_glob = torch.from_numpy(p["x"]).cuda()
-    x_int = op.zeros()
-    s_raw = op.zeros()
+    x_local = torch.from_numpy(p["x"]).cuda()[op.global_ids].contiguous()
+    x_int, s_raw, r_local = op.zeros(), op.zeros(), op.zeros()
     stream = torch.cuda.current_stream()
-    r_glob = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
     lo, hi = int(maps["bounds"][rank]), int(maps["bounds"][rank + 1])
+    h, n = op.plan.handle, op.n
 
-    def step(ev=None, x_in=True):
-        # gather the slab's x (caller -> rank numbering); SELL pass over the interface
-        # chunks writing the partial residual into caller numbering (+ internal copy); NCCL
-        # halo of the interface partials in flight while the interior chunks are swept;
-        # owned interface entries completed with the neighbours' partials
-        if x_in:
-            op.gather_global(x_glob, x_int)
+    def step(ev=None):
+        # x to the slab's internal order, r := -0.0, partial residual of the interface
+        # chunks added into r (caller order), NCCL halo of the interface partials in flight
+        # while the interior chunks are swept, owned interface entries completed
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        lib.ebs_to_internal(h, D.ptr(x_local), D.ptr(x_int), None, s)
+        lib.ebs_fill(n, ctypes.c_double(-0.0), D.ptr(r_local), s)
         if ev is not None:
             ev[0].record(stream)
-        op.residual_caller_sweep(op.if_chunks, x_int, r_glob, s_raw)
-        h = comm.exchange_start([op], [{q: op.gather(idx, s_raw)
-                                        for q, idx in op.if_idx.items()}])
-        op.residual_caller_sweep(op.in_chunks, x_int, r_glob, s_raw)
+        op.residual_local_sweep(op.if_chunks, x_int, r_local, s_raw)
+        hd = comm.exchange_start([op], [{q: op.gather(idx, s_raw)
+                                         for q, idx in op.if_idx.items()}])
+        op.residual_local_sweep(op.in_chunks, x_int, r_local, s_raw)
         if ev is not None:
             ev[1].record(stream)
-        recvs = comm.exchange_finish(h)
-        op.correct_owned(r_glob, recvs[0])
+        recvs = comm.exchange_finish(hd)
+        op.correct_owned_local(r_local, recvs[0])
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -97,20 +101,20 @@ def _residual_measure(p, args, rank, world, comm, sampler):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     # end to end: each rank's x slab (its local nodes) in from pinned host memory, its
     # owned entries of r out to pinned host memory, every step
-    x_host = x_glob[op.global_of_int].cpu().pin_memory()
-    own = op.owned_glob
+    x_host = x_local.cpu().pin_memory()
+    own = op.owned_local
     r_host = torch.empty(own.numel(), dtype=torch.float64).pin_memory()
     torch.cuda.synchronize()
     dist.barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for _ in range(args.steps):
-        x_int.copy_(x_host, non_blocking=True)
-        step(x_in=False)
-        r_host.copy_(r_glob[own], non_blocking=True)
+        x_local.copy_(x_host, non_blocking=True)
+        step()
+        r_host.copy_(r_local[own], non_blocking=True)
     e3.record(stream)
     torch.cuda.synchronize()
-    ref = r_glob[own].cpu()
+    ref = r_local[own].cpu()
     assert torch.equal(r_host, ref), "end-to-end residual differs from the device-timed one"
     te = torch.tensor([e2.elapsed_time(e3) / 1e3], device="cuda")
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -122,7 +126,7 @@ def _residual_measure(p, args, rank, world, comm, sampler):
            "n_nodes": m.n_nodes, "n_elements": m.n_elements,
            "bytes_rank": _bench_module().residual_bytes(op.n, hi - lo),
            "graph": graph is not None}
-    del op, x_glob, x_int, s_raw, r_glob
+    del op, x_local, x_int, s_raw, r_local
     torch.cuda.empty_cache()
     return out
 
@@ -168,7 +172,8 @@ def bench_rank(args, rank, world, local_rank):
                            "n_nodes": weak["n_nodes"], "n_elements": weak["n_elements"],
                            "per_gpu": "one C2 square (4.2M nodes, 8.4M triangles)",
                            "seed": args.seed,
-                           "mode": "fast (pre-assembled b); x and r in the caller's numbering",
+                           "mode": "fast (pre-assembled b); x and r in each rank's caller "
+                                   "order (its local nodes by ascending global id)",
                            "l2": "inputs larger than L2 (slot stream ~1 GB per rank); no flush",
                            "parallelism": f"element slabs x{world}",
                            "cuda_graph": dict(GRAPH_STATS)},

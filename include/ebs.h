@@ -160,10 +160,15 @@ int ebs_to_user(ebs_plan_t plan, const double *v_int, double *v, void *stream);
 int ebs_plan_apply_map(ebs_plan_t plan, int op, const double *x_int, double *out,
                        const int32_t *out_map, double *s_raw, int masked, void *stream);
 /* The same pass over a list of SELL chunks only (chunk c = internal nodes 32c .. 32c+31;
- * a rank sweeps its interface chunks, posts the halo exchange, then sweeps the rest). */
+ * a rank sweeps its interface chunks, posts the halo exchange, then sweeps the rest).
+ * flags: EBS_APPLY_MASKED zeroes constrained rows; EBS_APPLY_ADD adds each value into
+ * out[out_map[m]] (out pre-filled with -0.0: bit-identical to storing, and cheaper for a
+ * scattered map). */
+#define EBS_APPLY_MASKED 1
+#define EBS_APPLY_ADD 2
 int ebs_plan_apply_map_chunks(ebs_plan_t plan, int op, const int32_t *chunks, int64_t n_list,
                               const double *x_int, double *out, const int32_t *out_map,
-                              double *s_raw, int masked, void *stream);
+                              double *s_raw, int flags, void *stream);
 /* One SELL pass on internal vectors: op = 0 matvec, 1 fast residual, 2 exact residual;
  * out_user = 0 writes internal order, 1 the caller's numbering, 2 the caller's numbering
  * by adding into `out`, which the caller has filled with -0.0 (bit-identical to 1 and
@@ -171,6 +176,9 @@ int ebs_plan_apply_map_chunks(ebs_plan_t plan, int op, const int32_t *chunks, in
  * masked != 0 zeroes constrained rows. */
 int ebs_plan_apply(ebs_plan_t plan, int op, const double *x_int, double *out, int out_user,
                    int masked, void *stream);
+/* out[0..n) = value (16 B stores); value -0.0 prepares the output of an EBS_APPLY_ADD /
+ * out_user = 2 pass. */
+int ebs_fill(int64_t n, double value, double *out, void *stream);
 /* all-finite check (operators.py:90): *flag (device int32) = 1 if any non-finite. */
 int ebs_check_finite(int64_t n, const double *v, int32_t *flag, void *stream);
 

@@ -25,6 +25,8 @@ EBS_ECALLBACK = -7
 
 EBS_RES_EXACT = 0
 EBS_RES_FAST = 1
+EBS_APPLY_MASKED = 1
+EBS_APPLY_ADD = 2
 
 EBS_RICHARDSON = 0
 EBS_JACOBI = 1
@@ -103,6 +105,7 @@ SIGNATURES = {
     "ebs_plan_apply_map_chunks": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p,
                                           c_void_p, c_void_p, c_int, c_void_p]),
     "ebs_vec_workspace_bytes": (c_size_t, []),
+    "ebs_fill": (c_int, [c_int64, c_double, c_void_p, c_void_p]),
     "ebs_dist_unique_id": (c_int, [c_void_p]),
     "ebs_dist_init": (c_int, [c_void_p, c_void_p, c_int, c_int]),
     "ebs_dist_exchange": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,

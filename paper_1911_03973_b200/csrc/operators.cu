@@ -117,28 +117,30 @@ __global__ void __launch_bounds__(256)
 #define EBS_PERM2 0
 #endif
 
-// out[0..n) = -0.0 with 16 B stores (scalar head / tail for an unaligned or odd range).
-// Its own kernel after the x permutation: fusing the stores into the latency-bound
-// gather, or running it first, measured slower at C2.
-__global__ void k_fill_negzero(int64_t n, double *__restrict__ out) {
+// out[0..n) = value with 16 B stores (scalar head / tail for an unaligned or odd range).
+// The -0.0 pre-fill of a red-mode output runs as its own kernel after the x permutation:
+// fusing the stores into the latency-bound gather, or running it first, measured slower.
+__global__ void k_fill(int64_t n, double value, double *__restrict__ out) {
     const int64_t head = (reinterpret_cast<uintptr_t>(out) & 15) ? 1 : 0;
     const int64_t n2 = n > head ? (n - head) / 2 : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (head && n > 0) out[0] = -0.0;
-        if (n > head && ((n - head) & 1)) out[n - 1] = -0.0;
+        if (head && n > 0) out[0] = value;
+        if (n > head && ((n - head) & 1)) out[n - 1] = value;
     }
     double2 *o2 = reinterpret_cast<double2 *>(out + head);
-    const double2 v = make_double2(-0.0, -0.0);
+    const double2 v = make_double2(value, value);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
          i += (int64_t)gridDim.x * blockDim.x)
         o2[i] = v;
 }
 
-static void fill_negzero(int64_t n, double *out, cudaStream_t s) {
+static void fill_value(int64_t n, double value, double *out, cudaStream_t s) {
     if (n == 0) return;
-    k_fill_negzero<<<grid_for((n + 1) / 2, 256, sm_count() * 8), 256, 0, s>>>(n, out);
+    k_fill<<<grid_for((n + 1) / 2, 256, sm_count() * 8), 256, 0, s>>>(n, value, out);
     LAUNCHED();
 }
+
+static void fill_negzero(int64_t n, double *out, cudaStream_t s) { fill_value(n, -0.0, out, s); }
 
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
                  cudaStream_t s) {
@@ -311,19 +313,30 @@ int ebs_plan_apply_map(ebs_plan_t plan, int op, const double *x_int, double *out
     EBS_CATCH
 }
 
+int ebs_fill(int64_t n, double value, double *out, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && (out || n == 0), "bad arguments");
+    fill_value(n, value, out, S(stream));
+    EBS_CATCH
+}
+
 int ebs_plan_apply_map_chunks(ebs_plan_t plan, int op, const int32_t *chunks, int64_t n_list,
                               const double *x_int, double *out, const int32_t *out_map,
-                              double *s_raw, int masked, void *stream) {
+                              double *s_raw, int flags, void *stream) {
     EBS_TRY
     EBS_REQUIRE(plan && x_int && out && out_map, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
     EBS_REQUIRE(op == 0 || op == 1, "bad op %d (matvec or fast residual)", op);
     EBS_REQUIRE(n_list >= 0 && (chunks || n_list == 0), "bad chunk list");
+    EBS_REQUIRE(flags >= 0 && flags <= 3, "bad flags %d", flags);
     EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
     EBS_REQUIRE(op == 0 || p->has_be, "residual needs an operator loaded with b_e");
-    const uint8_t *fm = masked ? p->free_int : nullptr;
-    if (op == 0) launch_sell_op<0>(p, x_int, fm, out_map, out, S(stream), s_raw, chunks, n_list);
-    else launch_sell_op<1>(p, x_int, fm, out_map, out, S(stream), s_raw, chunks, n_list);
+    const uint8_t *fm = (flags & EBS_APPLY_MASKED) ? p->free_int : nullptr;
+    const int red = (flags & EBS_APPLY_ADD) ? 1 : 0;
+    if (op == 0)
+        launch_sell_op<0>(p, x_int, fm, out_map, out, S(stream), s_raw, chunks, n_list, red);
+    else
+        launch_sell_op<1>(p, x_int, fm, out_map, out, S(stream), s_raw, chunks, n_list, red);
     EBS_CATCH
 }
 

@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _device as D
-from ._lib import call, load
+from ._lib import EBS_APPLY_ADD, call, load
 
 
 # ------------------------------------------------------------------------ maps --
@@ -292,9 +292,15 @@ class GpuRankOperator:
         # per neighbour: positions in the interface list whose node this rank owns, and
         # their global ids (the fused caller-numbering residual corrects only those)
         self.corr = {}
+        self.corr_local = {}
         for q, idx in self.if_idx.items():
             pos = torch.nonzero(m_own[idx]).reshape(-1).contiguous()
             self.corr[q] = (pos, self.global_of_int[idx[pos]].contiguous())
+            self.corr_local[q] = (pos, self.old_of_new[idx[pos]].contiguous())
+        # the slab's own caller order = its local nodes in ascending global id (the plan's
+        # caller numbering): old_of_new as the int32 output map of the SELL pass
+        self.old_of_new32 = self.old_of_new.to(torch.int32).contiguous()
+        self.owned_local = self.old_of_new[self.owned_int].contiguous()
         self._ws = D.zeros(int(load().ebs_vec_workspace_bytes()), torch.uint8)
         self._acc = D.zeros(n)
         self._flag = D.zeros(1, torch.int32)
@@ -318,6 +324,21 @@ class GpuRankOperator:
         call("ebs_plan_apply_map_chunks", self.plan.handle, 1, D.ptr(chunks), chunks.numel(),
              D.ptr(x_int), D.ptr(r_global), D.ptr(self.global_of_int32), D.ptr(s_raw), 0,
              D.stream())
+
+    def residual_local_sweep(self, chunks, x_int, r_local, s_raw):
+        """Partial residual b_p - s_p of the chunks in `chunks`, ADDED into r_local (the
+        slab's nodes in ascending global id, pre-filled with -0.0: bit-identical to a
+        store, cheaper for the scattered map) and stored in internal order in s_raw."""
+        call("ebs_plan_apply_map_chunks", self.plan.handle, 1, D.ptr(chunks), chunks.numel(),
+             D.ptr(x_int), D.ptr(r_local), D.ptr(self.old_of_new32), D.ptr(s_raw),
+             EBS_APPLY_ADD, D.stream())
+
+    def correct_owned_local(self, r_local, recvs: dict):
+        """Owned interface entries of r_local: add the neighbours' partial residuals."""
+        for q in sorted(recvs):
+            pos, loc = self.corr_local[q]
+            call("ebs_index_add", pos.numel(), D.ptr(pos), D.ptr(recvs[q]), D.ptr(loc),
+                 D.ptr(r_local), D.stream())
 
     def correct_owned(self, r_global, recvs: dict):
         """Owned interface entries: add the neighbours' partial residuals."""
@@ -469,6 +490,28 @@ def residual_caller(prob: DistProblem, x_global: torch.Tensor, r_globals: list, 
         recvs = comm.exchange(ops, sends)
     for op, rg, rc in zip(ops, r_globals, recvs):
         op.correct_owned(rg, rc)
+
+
+def residual_local(prob: DistProblem, x_locals: list, r_locals: list, x_ints: list,
+                   s_raws: list):
+    """r = b - A x on P ranks with each rank's x and r in ITS caller order: the slab's
+    local nodes in ascending global id (x_locals[i] = x[op.global_ids]).  Per rank: x to
+    internal order, r := -0.0, partial residual of the interface chunks added into r,
+    NCCL halo of the interface partials in flight while the interior chunks are swept,
+    owned interface entries completed in ascending rank order.  The owned entries
+    (op.owned_local) are the residual within rounding of the reassociated sum."""
+    ops, comm = prob.ops, prob.comm
+    for op, xl, rl, xi, sr in zip(ops, x_locals, r_locals, x_ints, s_raws):
+        call("ebs_to_internal", op.plan.handle, D.ptr(xl), D.ptr(xi), None, D.stream())
+        call("ebs_fill", rl.numel(), -0.0, D.ptr(rl), D.stream())
+        op.residual_local_sweep(op.if_chunks, xi, rl, sr)
+    h = comm.exchange_start(ops, [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()}
+                                  for op, sr in zip(ops, s_raws)])
+    for op, xi, rl, sr in zip(ops, x_ints, r_locals, s_raws):
+        op.residual_local_sweep(op.in_chunks, xi, rl, sr)
+    recvs = comm.exchange_finish(h)
+    for op, rl, rc in zip(ops, r_locals, recvs):
+        op.correct_owned_local(rl, rc)
 
 
 def residual(prob: DistProblem, xs, out=None):
