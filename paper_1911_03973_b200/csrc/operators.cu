@@ -6,6 +6,8 @@
 // Each call: a gather of x into the plan's internal numbering (with the finiteness check
 // of operators.py:90 fused in), a -0.0 fill of the output, then the SELL kernel, whose
 // epilogue adds each node's value straight into the caller's numbering.
+#include <cstdlib>
+
 #include "sell.cuh"
 
 namespace ebs {
@@ -111,11 +113,31 @@ __global__ void __launch_bounds__(256)
 }
 
 #ifndef EBS_PERM2
-// 1: caller <-> internal permutations through the two-pass shared-memory schedule of
-// perm.cu (every global access coalesced).  Measured slower at C2 (2 passes 44 us vs the
-// direct gather's 33 us; profiles/README.md), so opt-in.
-#define EBS_PERM2 0
+// caller <-> internal permutations: 0 direct (random 8 B gather / red-mode scatter),
+// 1 the two-pass shared-memory schedule of perm.cu (every global access coalesced),
+// 2 automatic: two-pass once a vector outgrows L2's reach.  Fast residual, caller order
+// (scripts/perm_crossover.py): direct 177 / 415 / 1166 us vs two-pass 215 / 418 / 827 us
+// at 4.2M / 8.4M / 16.8M nodes -- random accesses to DRAM-resident vectors pay 32 B
+// sectors for 8 B, the coalesced passes do not.
+#define EBS_PERM2 2
 #endif
+#ifndef EBS_PERM2_MIN_NODES
+#define EBS_PERM2_MIN_NODES (8ll << 20)  // 64 MB per vector: the measured crossover
+#endif
+
+// the crossover can be overridden by the environment (EBS_PERM2_MIN_NODES, read once):
+// tests force either path on small meshes
+static int64_t perm2_min_nodes() {
+    static const int64_t v = [] {
+        const char *e = getenv("EBS_PERM2_MIN_NODES");
+        return e ? (int64_t)atoll(e) : (int64_t)EBS_PERM2_MIN_NODES;
+    }();
+    return v;
+}
+
+static bool use_perm2(const Plan *p) {
+    return EBS_PERM2 == 1 || (EBS_PERM2 == 2 && p->n_n >= perm2_min_nodes());
+}
 
 // out[0..n) = value with 16 B stores (scalar head / tail for an unaligned or odd range).
 // The -0.0 pre-fill of a red-mode output runs as its own kernel after the x permutation:
@@ -145,7 +167,7 @@ static void fill_negzero(int64_t n, double *out, cudaStream_t s) { fill_value(n,
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
                  cudaStream_t s) {
     if (p->n_n == 0) return;
-    if (EBS_PERM2) {
+    if (use_perm2(p)) {
         Plan *pm = const_cast<Plan *>(p);
         if (const Perm2 *P = perm_get(pm, 0, s)) {
             perm_apply(pm, P, x_user, x_int, nonfinite, s);
@@ -187,7 +209,7 @@ __global__ void __launch_bounds__(256)
 
 void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s) {
     if (p->n_n == 0) return;
-    if (EBS_PERM2) {
+    if (use_perm2(p)) {
         Plan *pm = const_cast<Plan *>(p);
         if (const Perm2 *P = perm_get(pm, 1, s)) {
             perm_apply(pm, P, v_int, v_user, nullptr, s);
@@ -207,7 +229,7 @@ void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *fre
     const int32_t *o2n = old_of_new;
     const Perm2 *P = nullptr;
     int red = 0;
-    if (EBS_PERM2 && old_of_new && p->n_n) {
+    if (use_perm2(p) && old_of_new && p->n_n) {
         // internal-order (coalesced) output, then the two-pass permutation to caller order
         Plan *pm = const_cast<Plan *>(p);
         if ((P = perm_get(pm, 1, s))) {
