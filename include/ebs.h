@@ -268,13 +268,13 @@ int ebs_vec_jacobi(int64_t n, double omega, const double *b, const double *s, co
                    const uint8_t *free_m, const uint8_t *owned, const double *x, double *x_out,
                    double *r_out, double *red, int32_t *nonfinite, void *ws, void *stream);
 /* CG / PCG steps (oracle/ebs_oracle.py pcg):  q = free ? q : 0, red[0] = sum_owned p.q;
- * update with scal = [rz, pq]: alpha = rz/pq, x += alpha p, r -= alpha q,
+ * update with device scalars rz, pq: alpha = rz/pq, x += alpha p, r -= alpha q,
  * red = [sum_owned r.r, sum_owned r.(dinv r)];  direction: p = dinv r + (rz_new/rz_old) p */
 int ebs_vec_pcg_q(int64_t n, const uint8_t *free_m, const uint8_t *owned, const double *p,
                   double *q, double *red, void *ws, void *stream);
-int ebs_vec_pcg_update(int64_t n, const double *scal, const uint8_t *owned, const double *dinv,
-                       double *x, double *r, const double *p, const double *q, double *red,
-                       int32_t *nonfinite, void *ws, void *stream);
+int ebs_vec_pcg_update(int64_t n, const double *rz, const double *pq, const uint8_t *owned,
+                       const double *dinv, double *x, double *r, const double *p, const double *q,
+                       double *red, int32_t *nonfinite, void *ws, void *stream);
 int ebs_vec_pcg_direction(int64_t n, const double *rz_old, const double *rz_new,
                           const double *dinv, const double *r, double *p, void *stream);
 int ebs_vec_dot_owned(int64_t n, const double *x, const double *y, const uint8_t *owned,
@@ -297,10 +297,13 @@ int ebs_dist_matvec_sweep(ebs_plan_t plan, const int32_t *chunks, int64_t n_list
                           double *q, const uint8_t *iface, double *red, void *ws, void *stream);
 int ebs_dist_jacobi_iface(int64_t n, const int64_t *idx, double omega, const double *b,
                           const double *s, const double *dinv, const uint8_t *free_m,
-                          const uint8_t *owned, const double *x, double *x_out, double *red,
-                          void *ws, void *stream);
+                          const uint8_t *owned, const double *x, double *x_out,
+                          const double *prior, double *red, void *ws, void *stream);
+/* ... and red[0] = (prior[0] + prior[1]) + the interface nodes' owned p.q (prior, nullable:
+ * the interface- and interior-chunk partials of the sweeps): the rank's whole p.q. */
 int ebs_dist_q_iface(int64_t n, const int64_t *idx, const uint8_t *free_m, const uint8_t *owned,
-                     const double *pv, double *q, double *red, void *ws, void *stream);
+                     const double *pv, double *q, const double *prior, double *red, void *ws,
+                     void *stream);
 /* plan internals in internal numbering: Dirichlet free flags, pre-assembled b, diag(A) */
 int ebs_plan_free_mask(ebs_plan_t plan, uint8_t *free_int, void *stream);
 int ebs_plan_internal_rhs(ebs_plan_t plan, double *b_int, void *stream);

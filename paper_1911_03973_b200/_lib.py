@@ -117,7 +117,8 @@ SIGNATURES = {
     "ebs_vec_pcg_q": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_void_p]),
     "ebs_vec_pcg_update": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p]),
     "ebs_vec_pcg_direction": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p]),
     "ebs_vec_dot_owned": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -130,9 +131,9 @@ SIGNATURES = {
                                       c_void_p, c_void_p, c_void_p]),
     "ebs_dist_jacobi_iface": (c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                      c_void_p, c_void_p]),
+                                      c_void_p, c_void_p, c_void_p]),
     "ebs_dist_q_iface": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                 c_void_p, c_void_p, c_void_p]),
+                                 c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_plan_free_mask": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ebs_plan_internal_rhs": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ebs_plan_internal_diag": (c_int, [c_void_p, c_void_p, c_void_p]),

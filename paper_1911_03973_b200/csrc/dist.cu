@@ -85,28 +85,52 @@ __global__ void __launch_bounds__(256)
     if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
 }
 
-// alpha = pq != 0 ? rz/pq : 0 (scal = [rz, pq]);  x += alpha p;  r -= alpha q;
+// alpha = pq != 0 ? rz/pq : 0 (device scalars rz, pq);  x += alpha p;  r -= alpha q;
 // red = [sum_owned r^2, sum_owned r*(dinv*r)]
+// ILP-4: four independent node updates in flight per thread (the nodes a thread visits,
+// and the order it sums them in, are those of the plain grid-stride loop)
+constexpr int VEC_ILP = 4;
+
 __global__ void __launch_bounds__(256)
-    k_vec_pcg_update(int64_t n, const double *__restrict__ scal, const uint8_t *__restrict__ owned,
-                     const double *__restrict__ dinv, double *__restrict__ x,
-                     double *__restrict__ r, const double *__restrict__ p,
+    k_vec_pcg_update(int64_t n, const double *__restrict__ rz_p, const double *__restrict__ pq_p,
+                     const uint8_t *__restrict__ owned, const double *__restrict__ dinv,
+                     double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
                      const double *__restrict__ q, double *partials, unsigned int *counter,
                      double *red, int32_t *nonfinite) {
-    const double rz = scal[0], pq = scal[1];
+    const double rz = rz_p[0], pq = pq_p[0];
     const double alpha = pq != 0.0 ? rz / pq : 0.0;
     double part[2] = {0.0, 0.0};
     bool bad = false;
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
-         m += (int64_t)gridDim.x * blockDim.x) {
-        double xn = x[m] + alpha * p[m];
-        double rn = r[m] - alpha * q[m];
-        x[m] = xn;
-        r[m] = rn;
-        bad |= !isfinite(xn);
-        if (owned[m]) {
-            part[0] += rn * rn;
-            part[1] += rn * (dinv[m] * rn);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+         base += stride * VEC_ILP) {
+        double xv[VEC_ILP], rv[VEC_ILP], pv[VEC_ILP], qv[VEC_ILP], dv[VEC_ILP];
+        uint8_t ow[VEC_ILP];
+#pragma unroll
+        for (int u = 0; u < VEC_ILP; ++u) {
+            const int64_t m = base + u * stride;
+            const bool ok = m < n;
+            xv[u] = ok ? x[m] : 0.0;
+            rv[u] = ok ? r[m] : 0.0;
+            pv[u] = ok ? p[m] : 0.0;
+            qv[u] = ok ? q[m] : 0.0;
+            ow[u] = ok ? owned[m] : 0;
+            dv[u] = ok ? dinv[m] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < VEC_ILP; ++u) {
+            const int64_t m = base + u * stride;
+            if (m < n) {
+                const double xn = xv[u] + alpha * pv[u];
+                const double rn = rv[u] - alpha * qv[u];
+                x[m] = xn;
+                r[m] = rn;
+                bad |= !isfinite(xn);
+                if (ow[u]) {
+                    part[0] += rn * rn;
+                    part[1] += rn * (dv[u] * rn);
+                }
+            }
         }
     }
     if (bad) atomicOr(nonfinite, 1);
@@ -123,9 +147,24 @@ __global__ void __launch_bounds__(256)
                         const double *__restrict__ rz_new, const double *__restrict__ dinv,
                         const double *__restrict__ r, double *__restrict__ p) {
     const double beta = rz_old[0] != 0.0 ? rz_new[0] / rz_old[0] : 0.0;
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
-         m += (int64_t)gridDim.x * blockDim.x)
-        p[m] = dinv[m] * r[m] + beta * p[m];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+         base += stride * VEC_ILP) {
+        double rv[VEC_ILP], pv[VEC_ILP], dv[VEC_ILP];
+#pragma unroll
+        for (int u = 0; u < VEC_ILP; ++u) {
+            const int64_t m = base + u * stride;
+            const bool ok = m < n;
+            rv[u] = ok ? r[m] : 0.0;
+            pv[u] = ok ? p[m] : 0.0;
+            dv[u] = ok ? dinv[m] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < VEC_ILP; ++u) {
+            const int64_t m = base + u * stride;
+            if (m < n) p[m] = dv[u] * rv[u] + beta * pv[u];
+        }
+    }
 }
 
 // red[0] = sum_owned x*y (owned nullable: all)
@@ -233,15 +272,15 @@ int ebs_vec_pcg_q(int64_t n, const uint8_t *free_m, const uint8_t *owned, const 
     EBS_CATCH
 }
 
-int ebs_vec_pcg_update(int64_t n, const double *scal, const uint8_t *owned, const double *dinv,
-                       double *x, double *r, const double *p, const double *q, double *red,
-                       int32_t *nonfinite, void *ws, void *stream) {
+int ebs_vec_pcg_update(int64_t n, const double *rz, const double *pq, const uint8_t *owned,
+                       const double *dinv, double *x, double *r, const double *p, const double *q,
+                       double *red, int32_t *nonfinite, void *ws, void *stream) {
     EBS_TRY
-    EBS_REQUIRE(n >= 0 && scal && owned && dinv && x && r && p && q && red && nonfinite && ws,
+    EBS_REQUIRE(n >= 0 && rz && pq && owned && dinv && x && r && p && q && red && nonfinite && ws,
                 "null argument");
     Scratch sc = scratch(ws);
     k_vec_pcg_update<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
-        n, scal, owned, dinv, x, r, p, q, sc.partials, sc.counter, red, nonfinite);
+        n, rz, pq, owned, dinv, x, r, p, q, sc.partials, sc.counter, red, nonfinite);
     LAUNCHED();
     EBS_CATCH
 }
@@ -370,7 +409,7 @@ __global__ void __launch_bounds__(256)
                         const double *__restrict__ dinv, const uint8_t *__restrict__ free_m,
                         const uint8_t *__restrict__ owned, const double *__restrict__ x,
                         double *__restrict__ x_out, double *partials, unsigned int *counter,
-                        double *red) {
+                        const double *prior, double *red) {
     double part[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -380,13 +419,15 @@ __global__ void __launch_bounds__(256)
         if (x_out) x_out[m] = dinv ? x[m] + omega * (dinv[m] * r) : x[m] + omega * r;
     }
     double tot[1];
-    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0)
+        red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
 }
 
 __global__ void __launch_bounds__(256)
     k_dist_q_iface(int64_t n, const int64_t *__restrict__ idx, const uint8_t *__restrict__ free_m,
                    const uint8_t *__restrict__ owned, const double *__restrict__ p,
-                   double *__restrict__ q, double *partials, unsigned int *counter, double *red) {
+                   double *__restrict__ q, double *partials, unsigned int *counter,
+                   const double *prior, double *red) {
     double part[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -396,7 +437,8 @@ __global__ void __launch_bounds__(256)
         if (owned[m]) part[0] += p[m] * qm;
     }
     double tot[1];
-    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0)
+        red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
 }
 
 }  // namespace ebs
@@ -461,24 +503,25 @@ int ebs_dist_matvec_sweep(ebs_plan_t plan, const int32_t *chunks, int64_t n_list
 
 int ebs_dist_jacobi_iface(int64_t n, const int64_t *idx, double omega, const double *b,
                           const double *s, const double *dinv, const uint8_t *free_m,
-                          const uint8_t *owned, const double *x, double *x_out, double *red,
-                          void *ws, void *stream) {
+                          const uint8_t *owned, const double *x, double *x_out,
+                          const double *prior, double *red, void *ws, void *stream) {
     EBS_TRY
     EBS_REQUIRE(n >= 0 && b && s && free_m && owned && x && red && ws, "null argument");
     Scratch sc = scratch(ws);
     k_dist_jacobi_iface<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
-        n, idx, omega, b, s, dinv, free_m, owned, x, x_out, sc.partials, sc.counter, red);
+        n, idx, omega, b, s, dinv, free_m, owned, x, x_out, sc.partials, sc.counter, prior, red);
     LAUNCHED();
     EBS_CATCH
 }
 
 int ebs_dist_q_iface(int64_t n, const int64_t *idx, const uint8_t *free_m, const uint8_t *owned,
-                     const double *pv, double *q, double *red, void *ws, void *stream) {
+                     const double *pv, double *q, const double *prior, double *red, void *ws,
+                     void *stream) {
     EBS_TRY
     EBS_REQUIRE(n >= 0 && free_m && owned && pv && q && red && ws, "null argument");
     Scratch sc = scratch(ws);
     k_dist_q_iface<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
-        n, idx, free_m, owned, pv, q, sc.partials, sc.counter, red);
+        n, idx, free_m, owned, pv, q, sc.partials, sc.counter, prior, red);
     LAUNCHED();
     EBS_CATCH
 }

@@ -392,18 +392,19 @@ class GpuRankOperator:
              float(omega), D.ptr(x), D.ptr(x_out), D.ptr(b), D.ptr(dinv), D.ptr(self.iface),
              D.ptr(s_part), D.ptr(red), D.ptr(self._ws), D.stream())
 
-    def jacobi_iface(self, omega, b, s_part, dinv, x, x_out, red):
+    def jacobi_iface(self, omega, b, s_part, dinv, x, x_out, red, prior=None):
         call("ebs_dist_jacobi_iface", self.all_if.numel(), D.ptr(self.all_if), float(omega),
              D.ptr(b), D.ptr(s_part), D.ptr(dinv), D.ptr(self.free), D.ptr(self.owned), D.ptr(x),
-             D.ptr(x_out), D.ptr(red), D.ptr(self._ws), D.stream())
+             D.ptr(x_out), D.ptr(prior), D.ptr(red), D.ptr(self._ws), D.stream())
 
     def matvec_sweep(self, chunks, p, q, red):
         call("ebs_dist_matvec_sweep", self.plan.handle, D.ptr(chunks), chunks.numel(), D.ptr(p),
              D.ptr(q), D.ptr(self.iface), D.ptr(red), D.ptr(self._ws), D.stream())
 
-    def q_iface(self, p, q, red):
+    def q_iface(self, p, q, red, prior=None):
         call("ebs_dist_q_iface", self.all_if.numel(), D.ptr(self.all_if), D.ptr(self.free),
-             D.ptr(self.owned), D.ptr(p), D.ptr(q), D.ptr(red), D.ptr(self._ws), D.stream())
+             D.ptr(self.owned), D.ptr(p), D.ptr(q), D.ptr(prior), D.ptr(red), D.ptr(self._ws),
+             D.stream())
 
     def vec_dinv(self, diag):
         dinv = D.empty(self.n)
@@ -419,10 +420,10 @@ class GpuRankOperator:
         call("ebs_vec_pcg_q", self.n, D.ptr(self.free), D.ptr(self.owned), D.ptr(p), D.ptr(q),
              D.ptr(red), D.ptr(self._ws), D.stream())
 
-    def vec_pcg_update(self, scal, dinv, x, r, p, q, red):
-        call("ebs_vec_pcg_update", self.n, D.ptr(scal), D.ptr(self.owned), D.ptr(dinv), D.ptr(x),
-             D.ptr(r), D.ptr(p), D.ptr(q), D.ptr(red), D.ptr(self._flag), D.ptr(self._ws),
-             D.stream())
+    def vec_pcg_update(self, rz, pq, dinv, x, r, p, q, red):
+        call("ebs_vec_pcg_update", self.n, D.ptr(rz), D.ptr(pq), D.ptr(self.owned), D.ptr(dinv),
+             D.ptr(x), D.ptr(r), D.ptr(p), D.ptr(q), D.ptr(red), D.ptr(self._flag),
+             D.ptr(self._ws), D.stream())
 
     def vec_pcg_direction(self, rz_old, rz_new, dinv, r, p):
         call("ebs_vec_pcg_direction", self.n, D.ptr(rz_old), D.ptr(rz_new), D.ptr(dinv), D.ptr(r),
@@ -582,7 +583,7 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     red = [torch.zeros(iters + 1, dtype=torch.float64, device=x.device) for x in xa]
 
     fused = _fused_ok(ops) if fused is None else fused
-    r3 = [torch.zeros(3, dtype=torch.float64, device=x.device) for x in xa]
+    r3 = [torch.zeros(2, dtype=torch.float64, device=x.device) for x in xa]  # sweep partials
 
     def step(src, dst, final, rslot):
         if fused:  # interface chunks, exchange || interior chunks, interface completion
@@ -598,8 +599,7 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
             for i, op in enumerate(ops):
                 op.combine(ss[i], recvs[i])
                 op.jacobi_iface(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i],
-                                src[i], None if final else dst[i], r3[i][2:3])
-                rslot[i].copy_(r3[i].sum(0, keepdim=True))
+                                src[i], None if final else dst[i], rslot[i], prior=r3[i])
             return
         for op, x, s_ in zip(ops, src, ss):
             op.matvec_partial(x, s_)
@@ -635,48 +635,53 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
 
 def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused=None):
     """Jacobi-PCG on P ranks (oracle/ebs_oracle.py pcg; with prob from setup(..,
-    precondition=False) plain CG).  Two scalar all-reduces per iteration.  graph=True
-    (fixed iteration count only) replays captured CUDA graphs of GRAPH_BATCH iterations."""
+    precondition=False) plain CG).  Two scalar all-reduces per iteration, both in place and
+    with no copies between the kernels: the rank's p.q (the interface kernel adds the two
+    sweep partials to its own) and the iteration's [r.r, r.z] pair, kept in a ring of
+    GRAPH_BATCH slots that the next iteration reads as its rz.  graph=True (fixed iteration
+    count only) replays captured CUDA graphs of GRAPH_BATCH iterations."""
     ops, comm = prob.ops, prob.comm
     dev = xs0[0].device
+    f64 = dict(dtype=torch.float64, device=dev)
     xs = [x.clone() for x in xs0]
     rs = [op.zeros() for op in ops]
     ps = [op.zeros() for op in ops]
     qs = [op.zeros() for op in ops]
     ss = [op.zeros() for op in ops]
-    zero = torch.zeros(1, dtype=torch.float64, device=dev)
+    zero = torch.zeros(1, **f64)
     for op, x, s in zip(ops, xs, ss):
         op.matvec_partial(x, s)
     halo(ops, comm, ss)
-    hist = [torch.zeros(iters + 1, dtype=torch.float64, device=dev) for _ in ops]
-    red = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in ops]
-    scal = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in ops]
-    pq = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in ops]
+    B = GRAPH_BATCH
+    ring = [torch.zeros((B, 2), **f64) for _ in ops]   # iteration k: slot k % B
+    pq = [torch.zeros(1, **f64) for _ in ops]
+    part = [torch.zeros(2, **f64) for _ in ops]        # interface / interior sweep p.q
+    init = [rg[B - 1] for rg in ring]                  # iteration 0 reads its rz here
     for i, op in enumerate(ops):
-        op.vec_jacobi(0.0, prob.b[i], ss[i], None, xs[i], None, rs[i], red[i][0:1])
+        op.vec_jacobi(0.0, prob.b[i], ss[i], None, xs[i], None, rs[i], init[i][0:1])
         op.vec_pcg_direction(zero, zero, prob.dinv[i], rs[i], ps[i])  # p = dinv r
-        op.dot_owned(rs[i], ps[i], red[i][1:2])
-    comm.allreduce(red)
+        op.dot_owned(rs[i], ps[i], init[i][1:2])
+    comm.allreduce(init)
+    norm2 = [torch.zeros(iters + 1, **f64) for _ in ops]  # ||r_k||^2
     for i in range(len(ops)):
-        hist[i][0:1].copy_(red[i][0:1])
-        scal[i][0:1].copy_(red[i][1:2])
+        norm2[i][0:1].copy_(init[i][0:1])
 
     fused = _fused_ok(ops) if fused is None else fused
-    pq3 = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in ops]
 
-    def step(hslot):
+    def step(u):
+        slot = [rg[u] for rg in ring]
+        prev = [rg[(u - 1) % B] for rg in ring]
         if fused:  # interface chunks, exchange || interior chunks, interface completion
             for i, op in enumerate(ops):
-                op.matvec_sweep(op.if_chunks, ps[i], qs[i], pq3[i][0:1])
+                op.matvec_sweep(op.if_chunks, ps[i], qs[i], part[i][0:1])
             h = comm.exchange_start(ops, [{q: op.gather(idx, q_) for q, idx in op.if_idx.items()}
                                           for op, q_ in zip(ops, qs)])
             for i, op in enumerate(ops):
-                op.matvec_sweep(op.in_chunks, ps[i], qs[i], pq3[i][1:2])
+                op.matvec_sweep(op.in_chunks, ps[i], qs[i], part[i][1:2])
             recvs = comm.exchange_finish(h)
             for i, op in enumerate(ops):
                 op.combine(qs[i], recvs[i])
-                op.q_iface(ps[i], qs[i], pq3[i][2:3])
-                pq[i].copy_(pq3[i].sum(0, keepdim=True))
+                op.q_iface(ps[i], qs[i], pq[i], prior=part[i])
         else:
             for op, p_, q_ in zip(ops, ps, qs):
                 op.matvec_partial(p_, q_)
@@ -685,41 +690,38 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused
                 op.vec_pcg_q(ps[i], qs[i], pq[i])
         comm.allreduce(pq)
         for i, op in enumerate(ops):
-            scal[i][1:2].copy_(pq[i])
-            op.vec_pcg_update(scal[i], prob.dinv[i], xs[i], rs[i], ps[i], qs[i], red[i])
-        comm.allreduce(red)
+            op.vec_pcg_update(prev[i][1:2], pq[i], prob.dinv[i], xs[i], rs[i], ps[i], qs[i],
+                              slot[i])
+        comm.allreduce(slot)
         for i, op in enumerate(ops):
-            hslot[i].copy_(red[i][0:1])
-            op.vec_pcg_direction(scal[i][0:1], red[i][1:2], prob.dinv[i], rs[i], ps[i])
-            scal[i][0:1].copy_(red[i][1:2])
+            op.vec_pcg_direction(prev[i][1:2], slot[i][1:2], prob.dinv[i], rs[i], ps[i])
 
-    B = GRAPH_BATCH
     k = 0
     if graph and tol is None and iters >= B and _graph_ok(ops):
-        bh = [torch.zeros(B, dtype=torch.float64, device=dev) for _ in ops]
-
         def body():
             for u in range(B):
-                step([h[u:u + 1] for h in bh])
+                step(u)
         g = _capture(comm, body)
         if g is not None:
             while k + B <= iters:
                 g.replay()
                 for i in range(len(ops)):
-                    hist[i][k + 1:k + 1 + B].copy_(bh[i])
+                    norm2[i][k + 1:k + 1 + B].copy_(ring[i][:, 0])
                 k += B
     n0 = None
     k_done = iters
     for kk in range(k, iters):
         if tol is not None:
-            nk = float(torch.sqrt(hist[0][kk]))
+            nk = float(torch.sqrt(norm2[0][kk]))
             n0 = nk if n0 is None else n0
             if nk <= tol * n0:
                 k_done = kk
                 break
-        step([h[kk + 1:kk + 2] for h in hist])
+        step(kk % B)
+        for i in range(len(ops)):
+            norm2[i][kk + 1:kk + 2].copy_(ring[i][kk % B, 0:1])
     n = k_done + 1
-    return xs, torch.sqrt(hist[0][:n]).cpu().numpy()
+    return xs, torch.sqrt(norm2[0][:n]).cpu().numpy()
 
 
 def gather_global(ops, vs, n_nodes, comm=None):

@@ -91,8 +91,8 @@ class CpuRankOperator:
         q.copy_(torch.where(self.free.bool(), q, torch.zeros_like(q)))
         red.copy_((p * q)[self.owned.bool()].sum().reshape(1))
 
-    def vec_pcg_update(self, scal, dinv, x, r, p, q, red):
-        rz, pq = float(scal[0]), float(scal[1])
+    def vec_pcg_update(self, rz, pq, dinv, x, r, p, q, red):
+        rz, pq = float(rz[0]), float(pq[0])
         alpha = rz / pq if pq != 0.0 else 0.0
         x.add_(alpha * p)
         r.sub_(alpha * q)
