@@ -51,8 +51,7 @@ def _residual_measure(p, args, rank, world, comm, sampler):
         if ev is not None:
             ev[0].record(stream)
         op.residual_local_sweep(op.if_chunks, x_int, r_local, s_raw)
-        hd = comm.exchange_start([op], [{q: op.gather(idx, s_raw)
-                                         for q, idx in op.if_idx.items()}])
+        hd = comm.exchange_start([op], [op.gather_sends(s_raw)])
         op.residual_local_sweep(op.in_chunks, x_int, r_local, s_raw)
         if ev is not None:
             ev[1].record(stream)

@@ -299,6 +299,12 @@ int ebs_dist_jacobi_iface(int64_t n, const int64_t *idx, double omega, const dou
                           const double *s, const double *dinv, const uint8_t *free_m,
                           const uint8_t *owned, const double *x, double *x_out,
                           const double *prior, double *red, void *ws, void *stream);
+/* Shared-node completion after the halo exchange: v[all_if[i]] = sum over k of
+ * srcs[k][pos[i*n_src + k]] (entries with pos < 0 skipped), sources in ascending rank order
+ * -- the rank's own partials are the source whose positions are the nodes themselves.
+ * srcs is a HOST array of n_src (<= 8) device pointers. */
+int ebs_dist_combine(int64_t n_if, const int64_t *all_if, int n_src, const double *const *srcs,
+                     const int32_t *pos, double *v, void *stream);
 /* ... and red[0] = (prior[0] + prior[1]) + the interface nodes' owned p.q (prior, nullable:
  * the interface- and interior-chunk partials of the sweeps): the rank's whole p.q. */
 int ebs_dist_q_iface(int64_t n, const int64_t *idx, const uint8_t *free_m, const uint8_t *owned,

@@ -105,6 +105,8 @@ SIGNATURES = {
     "ebs_plan_apply_map_chunks": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p,
                                           c_void_p, c_void_p, c_int, c_void_p]),
     "ebs_vec_workspace_bytes": (c_size_t, []),
+    "ebs_dist_combine": (c_int, [c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                 c_void_p]),
     "ebs_fill": (c_int, [c_int64, c_double, c_void_p, c_void_p]),
     "ebs_dist_unique_id": (c_int, [c_void_p]),
     "ebs_dist_init": (c_int, [c_void_p, c_void_p, c_int, c_int]),

@@ -441,6 +441,31 @@ __global__ void __launch_bounds__(256)
         red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
 }
 
+// v[m] = sum of the contributions to shared node m, in ascending rank order (the own
+// partial among them): one thread per interface node, sources by value (<= COMBINE_MAX;
+// geometric slabs have 2 neighbours, thin ones a few more), pos[i * n_src + k] = index of node i in source k or -1.  Replaces a
+// fill, a gather and one scatter-add per source with one pass (same order of additions).
+constexpr int COMBINE_MAX = 8;
+struct CombineSrc {
+    const double *p[COMBINE_MAX];
+    int n;
+};
+
+__global__ void __launch_bounds__(256)
+    k_dist_combine(int64_t n_if, const int64_t *__restrict__ all_if, CombineSrc src,
+                   const int32_t *__restrict__ pos, double *v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = all_if[i];
+        double acc = 0.0;
+        for (int k = 0; k < src.n; ++k) {
+            const int32_t q = pos[i * src.n + k];
+            if (q >= 0) acc += src.p[k][q];
+        }
+        v[m] = acc;
+    }
+}
+
 }  // namespace ebs
 
 extern "C" {
@@ -510,6 +535,24 @@ int ebs_dist_jacobi_iface(int64_t n, const int64_t *idx, double omega, const dou
     Scratch sc = scratch(ws);
     k_dist_jacobi_iface<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
         n, idx, omega, b, s, dinv, free_m, owned, x, x_out, sc.partials, sc.counter, prior, red);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_dist_combine(int64_t n_if, const int64_t *all_if, int n_src, const double *const *srcs,
+                     const int32_t *pos, double *v, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n_if >= 0 && n_src >= 1 && n_src <= COMBINE_MAX && srcs &&
+                    (n_if == 0 || (all_if && pos && v)),
+                "bad arguments (1 <= n_src <= %d)", COMBINE_MAX);
+    if (n_if == 0) return EBS_OK;
+    CombineSrc cs{};
+    cs.n = n_src;
+    for (int k = 0; k < n_src; ++k) {
+        EBS_REQUIRE(srcs[k], "null source %d", k);
+        cs.p[k] = srcs[k];
+    }
+    k_dist_combine<<<grid_for(n_if, 256), 256, 0, S(stream)>>>(n_if, all_if, cs, pos, v);
     LAUNCHED();
     EBS_CATCH
 }

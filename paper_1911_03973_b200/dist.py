@@ -270,6 +270,25 @@ class GpuRankOperator:
                        for q, ids in maps["interface"][p].items()}
         self.all_if = (torch.unique(torch.cat(list(self.if_idx.values())))
                        if self.if_idx else torch.empty(0, dtype=torch.int64, device=gl.device))
+        # one gather for all neighbours' send buffers; one kernel for the shared-node sums:
+        # sources in ascending rank order (own partials = the nodes themselves)
+        peers = sorted(self.if_idx)
+        self.send_idx = (torch.cat([self.if_idx[q] for q in peers]).contiguous() if peers
+                         else torch.empty(0, dtype=torch.int64, device=gl.device))
+        offs = np.cumsum([0] + [self.if_idx[q].numel() for q in peers])
+        self.send_slices = {q: (int(offs[k]), int(offs[k + 1])) for k, q in enumerate(peers)}
+        self.combine_ranks = sorted(set(peers) | {p})
+        cols = []
+        for r in self.combine_ranks:
+            if r == p:
+                cols.append(self.all_if.to(torch.int32))
+            else:
+                col = torch.full((self.all_if.numel(),), -1, dtype=torch.int32, device=gl.device)
+                col[torch.searchsorted(self.all_if, self.if_idx[r])] = torch.arange(
+                    self.if_idx[r].numel(), dtype=torch.int32, device=gl.device)
+                cols.append(col)
+        self.combine_pos = (torch.stack(cols, 1).contiguous() if self.all_if.numel()
+                            else torch.empty(0, dtype=torch.int32, device=gl.device))
         owner = maps["owner"].to(gl.device)
         self.owned = (owner[self.global_of_int] == p).to(torch.uint8).contiguous()
         self.free = D.empty(n, torch.uint8)
@@ -370,22 +389,33 @@ class GpuRankOperator:
         call("ebs_gather", idx.numel(), D.ptr(idx), D.ptr(v), D.ptr(buf), D.stream())
         return buf
 
+    def gather_sends(self, v: torch.Tensor) -> dict:
+        """{neighbour: v at the interface nodes shared with it}: one gather, views of it."""
+        if not self.if_idx:
+            return {}
+        buf = self.gather(self.send_idx, v)
+        return {q: buf[a:b] for q, (a, b) in self.send_slices.items()}
+
     def combine(self, v: torch.Tensor, recvs: dict):
-        """v[shared] = sum over touching ranks in ascending rank order (own partial at p)."""
+        """v[shared] = sum over touching ranks in ascending rank order (own partial at p),
+        one kernel (ebs_dist_combine)."""
         if not self.if_idx:
             return
-        s = D.stream()
-        acc = self._acc
-        call("ebs_index_fill", self.all_if.numel(), D.ptr(self.all_if), 0.0, D.ptr(acc), s)
-        own = self.gather(self.all_if, v)
-        for r in sorted(set(recvs) | {self.rank}):
-            if r == self.rank:
-                call("ebs_scatter_add", self.all_if.numel(), D.ptr(self.all_if), D.ptr(own),
-                     D.ptr(acc), s)
-            else:
-                idx = self.if_idx[r]
-                call("ebs_scatter_add", idx.numel(), D.ptr(idx), D.ptr(recvs[r]), D.ptr(acc), s)
-        call("ebs_index_copy", self.all_if.numel(), D.ptr(self.all_if), D.ptr(acc), D.ptr(v), s)
+        if len(self.combine_ranks) > 8:  # more sources than the fused kernel takes
+            s = D.stream()
+            acc = self._acc
+            call("ebs_index_fill", self.all_if.numel(), D.ptr(self.all_if), 0.0, D.ptr(acc), s)
+            own = self.gather(self.all_if, v)
+            for r in self.combine_ranks:
+                idx, src = (self.all_if, own) if r == self.rank else (self.if_idx[r], recvs[r])
+                call("ebs_scatter_add", idx.numel(), D.ptr(idx), D.ptr(src), D.ptr(acc), s)
+            call("ebs_index_copy", self.all_if.numel(), D.ptr(self.all_if), D.ptr(acc), D.ptr(v),
+                 s)
+            return
+        srcs = [v if r == self.rank else recvs[r] for r in self.combine_ranks]
+        ptrs = (ctypes.c_void_p * len(srcs))(*[t.data_ptr() for t in srcs])
+        call("ebs_dist_combine", self.all_if.numel(), D.ptr(self.all_if), len(srcs), ptrs,
+             D.ptr(self.combine_pos), D.ptr(v), D.stream())
 
     def jacobi_sweep(self, chunks, omega, x, x_out, b, dinv, s_part, red):
         call("ebs_dist_jacobi_sweep", self.plan.handle, D.ptr(chunks), chunks.numel(),
@@ -477,7 +507,7 @@ def residual_caller(prob: DistProblem, x_global: torch.Tensor, r_globals: list, 
         for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
             op.gather_global(x_global, xi)
             op.residual_caller_sweep(op.if_chunks, xi, rg, sr)
-        h = comm.exchange_start(ops, [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()}
+        h = comm.exchange_start(ops, [op.gather_sends(sr)
                                       for op, sr in zip(ops, s_raws)])
         for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
             op.residual_caller_sweep(op.in_chunks, xi, rg, sr)
@@ -486,7 +516,7 @@ def residual_caller(prob: DistProblem, x_global: torch.Tensor, r_globals: list, 
         for op, xi, rg, sr in zip(ops, x_ints, r_globals, s_raws):
             op.gather_global(x_global, xi)
             op.residual_caller_partial(xi, rg, sr)
-        sends = [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()}
+        sends = [op.gather_sends(sr)
                  for op, sr in zip(ops, s_raws)]
         recvs = comm.exchange(ops, sends)
     for op, rg, rc in zip(ops, r_globals, recvs):
@@ -506,7 +536,7 @@ def residual_local(prob: DistProblem, x_locals: list, r_locals: list, x_ints: li
         call("ebs_to_internal", op.plan.handle, D.ptr(xl), D.ptr(xi), None, D.stream())
         call("ebs_fill", rl.numel(), -0.0, D.ptr(rl), D.stream())
         op.residual_local_sweep(op.if_chunks, xi, rl, sr)
-    h = comm.exchange_start(ops, [{q: op.gather(idx, sr) for q, idx in op.if_idx.items()}
+    h = comm.exchange_start(ops, [op.gather_sends(sr)
                                   for op, sr in zip(ops, s_raws)])
     for op, xi, rl, sr in zip(ops, x_ints, r_locals, s_raws):
         op.residual_local_sweep(op.in_chunks, xi, rl, sr)
@@ -590,7 +620,7 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
             for i, op in enumerate(ops):
                 op.jacobi_sweep(op.if_chunks, omega, src[i], None if final else dst[i], prob.b[i],
                                 None if richardson else prob.dinv[i], ss[i], r3[i][0:1])
-            h = comm.exchange_start(ops, [{q: op.gather(idx, s_) for q, idx in op.if_idx.items()}
+            h = comm.exchange_start(ops, [op.gather_sends(s_)
                                           for op, s_ in zip(ops, ss)])
             for i, op in enumerate(ops):
                 op.jacobi_sweep(op.in_chunks, omega, src[i], None if final else dst[i], prob.b[i],
@@ -674,7 +704,7 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused
         if fused:  # interface chunks, exchange || interior chunks, interface completion
             for i, op in enumerate(ops):
                 op.matvec_sweep(op.if_chunks, ps[i], qs[i], part[i][0:1])
-            h = comm.exchange_start(ops, [{q: op.gather(idx, q_) for q, idx in op.if_idx.items()}
+            h = comm.exchange_start(ops, [op.gather_sends(q_)
                                           for op, q_ in zip(ops, qs)])
             for i, op in enumerate(ops):
                 op.matvec_sweep(op.in_chunks, ps[i], qs[i], part[i][1:2])
