@@ -137,7 +137,7 @@ def test_rank_local_assembly_equals_sliced(gpu, P):
         assert torch.equal(a.rhs_partial(), b.rhs_partial())
 
 
-@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
 def test_fused_overlapped_steps_match_unfused(gpu, P):
     """The overlapped interface/interior sweeps: Jacobi iterates bitwise equal to the
     unfused rank loop, PCG within 1e-10 (the dot is summed in three groups)."""
