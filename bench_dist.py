@@ -7,6 +7,8 @@ Kept beside bench.py (not in the package): it is measurement code, not library c
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from paper_1911_03973_b200._lib import load
@@ -172,11 +174,19 @@ def bench_rank(args, rank, world, local_rank):
     from paper_1911_03973_b200.inputs import config_problem, stacked_c2_problem
     B = _bench_module()
 
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # EBS_BENCH_GLOO=1 (tests only): gloo with the halo staged through host memory and the
+    # ranks sharing the box's GPUs -- exercises every N > 1 branch of this driver on one
+    # GPU without any kernel waiting on another process.  Timings are meaningless then.
+    gloo = os.environ.get("EBS_BENCH_GLOO") == "1"
+    dev = local_rank % torch.cuda.device_count() if gloo else local_rank
+    torch.cuda.set_device(dev)
+    if gloo:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     peaks, peak_kind = B.load_peaks()
-    sampler = B.ClockSampler(index=local_rank).start()
-    comm = TorchTransport()
+    sampler = B.ClockSampler(index=dev).start()
+    comm = TorchTransport(stage_host=gloo)
     weak = _residual_measure(stacked_c2_problem(world, seed=args.seed, size=args.size), args,
                              rank, world, comm, sampler)
     strong = None
@@ -254,7 +264,7 @@ def _bench_solvers(args, rank, world):
             del p
             gc.collect()
             torch.cuda.empty_cache()
-            comm = TorchTransport()
+            comm = TorchTransport(stage_host=os.environ.get("EBS_BENCH_GLOO") == "1")
             prob = setup([op], comm)
             x0 = op.zeros()
             run = (lambda: jacobi(prob, [x0], iters, 0.8, graph=True)) if cfg == 4 else \
