@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import os
 
+import numpy as np
 import torch
 
 from paper_1911_03973_b200._lib import load
@@ -79,9 +80,18 @@ def _residual_measure(p, args, rank, world, comm, sampler):
         for _ in range(GB):
             step()
     graph = _capture(comm, body)
+    verified = None
     if graph is not None:
+        # self-check of the captured halo: a replay must reproduce an eager step bit for bit
+        # on every rank, else the eager launches are timed (collective decision)
+        step()
+        torch.cuda.synchronize()
+        r_eager = r_local.clone()
         graph.replay()
         torch.cuda.synchronize()
+        verified = comm.agree(bool(torch.equal(r_local, r_eager)))
+        if not verified:
+            graph = None
     n0 = load().ebs_launch_count()
     step()
     torch.cuda.synchronize()
@@ -155,7 +165,7 @@ def _residual_measure(p, args, rank, world, comm, sampler):
            "h2d": int(byt[0]), "d2h": int(byt[1]), "launches": launches_per_step * args.steps,
            "n_nodes": m.n_nodes, "n_elements": m.n_elements,
            "bytes_rank": _bench_module().residual_bytes(op.n, hi - lo),
-           "graph": graph is not None}
+           "graph": graph is not None, "graph_verified": verified}
     del op, x_local, x_int, s_raw, r_local
     torch.cuda.empty_cache()
     return out
@@ -214,7 +224,7 @@ def bench_rank(args, rank, world, local_rank):
                                    "order (its local nodes by ascending global id)",
                            "l2": "inputs larger than L2 (slot stream ~1 GB per rank); no flush",
                            "parallelism": f"element slabs x{world}",
-                           "cuda_graph": dict(GRAPH_STATS)},
+                           "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=weak["graph_verified"])},
                 "roofline": {"bound": "hbm", "achieved": weak["bytes_rank"] / weak["kern"] / 1e9,
                              "peak": peak, "unit": "GB/s",
                              "frac": weak["bytes_rank"] / weak["kern"] / 1e9 / peak,
@@ -267,8 +277,12 @@ def _bench_solvers(args, rank, world):
             comm = TorchTransport(stage_host=os.environ.get("EBS_BENCH_GLOO") == "1")
             prob = setup([op], comm)
             x0 = op.zeros()
-            run = (lambda: jacobi(prob, [x0], iters, 0.8, graph=True)) if cfg == 4 else \
-                (lambda: pcg(prob, [x0], iters, graph=True))
+            solve = (lambda it, g: jacobi(prob, [x0], it, 0.8, graph=g)) if cfg == 4 else \
+                (lambda it, g: pcg(prob, [x0], it, graph=g))
+            # self-check: 16 iterations replayed from captured graphs == eager, every rank
+            (xg_, ng_), (xe_, ne_) = solve(16, True), solve(16, False)
+            use_graph = comm.agree(bool(np.array_equal(ng_, ne_)) and torch.equal(xg_[0], xe_[0]))
+            run = lambda: solve(iters, use_graph)  # noqa: E731
             run()  # warm-up (creates the NCCL P2P communicators)
             torch.cuda.synchronize()
             dist.barrier()
@@ -288,7 +302,7 @@ def _bench_solvers(args, rank, world):
                               "frac_of_peak_per_gpu": per_it * iters / T / 1e9 / world /
                               float(peaks["hbm_gbs"]),
                               "final_norm": float(norms[-1]), "n_nodes": m.n_nodes,
-                              "cuda_graph": dict(GRAPH_STATS),
+                              "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=use_graph),
                               "n_elements": m.n_elements}
             del op, prob
         except Exception as e:  # noqa: BLE001
