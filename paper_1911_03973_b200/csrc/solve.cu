@@ -364,9 +364,8 @@ __global__ void EBS_SELL_BOUNDS(NB)
     ctl->pq = lam_new;
 }
 
-// v = av / nav (spectrum.py:94)
-__global__ void k_power_scale(int64_t n, const Ctl *ctl, const double *__restrict__ av,
-                              double *__restrict__ v) {
+// v = av / nav (spectrum.py:94); av may alias v (the start vector is scaled in place)
+__global__ void k_power_scale(int64_t n, const Ctl *ctl, const double *av, double *v) {
     if (ctl->done && ctl->alpha == 0.0) return;
     const double nav = ctl->alpha;
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
@@ -664,8 +663,6 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
     LoopArgs L{p->ctl, p->hist_dev, P->reference ? p->hist_dev + iters + 2 : nullptr,
                p->partials, P->has_tol, P->tol, P->omega};
     SellView v = sell_view(p);
-    const int block = 256;
-    const int64_t sgrid = (p->n_chunks * LANES + block - 1) / block;
     const int vgrid = grid_for(n, 256, RED_MAX_BLOCKS);
     const int ugrid = EBS_UPD_PERSIST
                           ? persistent_grid((const void *)k_pcg_update, 256, (n + 255) / 256, 0)
@@ -863,8 +860,6 @@ int ebs_power_iteration(ebs_plan_t plan, const double *v0, int iters, double tol
     LAUNCHED();
     CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
     SellView sv = sell_view(p);
-    const int block = 256;
-    const int64_t sgrid = (p->n_chunks * LANES + block - 1) / block;
     int k = 0;
     while (k < iters) {
         int kend = k + 32 < iters ? k + 32 : iters;
