@@ -157,6 +157,7 @@ struct Plan {
     int32_t *new_of_old = nullptr;  // caller id -> internal id
     int32_t *old_of_new = nullptr;  // internal id -> caller id
     int32_t *cnt = nullptr;         // valence per internal node
+    uint8_t *cnt8 = nullptr;        // the same in one byte (max valence <= 255; sweeps read it)
     int32_t *rowbase = nullptr;     // first slot row of each chunk
     int32_t *width = nullptr;       // slot rows of each chunk
     int32_t *slot_ej = nullptr;     // [row][lane]: e | j<<30, -1 for padding

@@ -73,6 +73,12 @@ __global__ void k_numbering(int64_t n_n, int64_t n_conn, const int32_t *__restri
     }
 }
 
+__global__ void k_cnt8(int64_t n_n, const int32_t *__restrict__ cnt, uint8_t *__restrict__ cnt8) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_n;
+         m += (int64_t)gridDim.x * blockDim.x)
+        cnt8[m] = (uint8_t)cnt[m];
+}
+
 __global__ void k_permute_cnt(int64_t n_n, const int32_t *__restrict__ old_of_new,
                               const int32_t *__restrict__ cnt_old, int32_t *__restrict__ cnt_new) {
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_n;
@@ -531,7 +537,7 @@ double *plan_vec(Plan *p, int i) {
 }
 
 static void plan_free(Plan *p) {
-    dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->rowbase);
+    dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->cnt8); dfree(p->rowbase);
     dfree(p->width); dfree(p->slot_ej); dfree(p->slot); dfree(p->tab); dfree(p->taboff);
     dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
     dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag); dfree(p->rowflag);
@@ -737,6 +743,12 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
             CU(e2);
         }
         p->max_valence = mv;
+    }
+    // one-byte valences for the sweeps (C2: 4.2 MB instead of 16.8 MB per pass)
+    if (p->max_valence <= 255 && n_n > 0) {
+        p->cnt8 = dmalloc<uint8_t>(n_n);
+        k_cnt8<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, p->cnt, p->cnt8);
+        LAUNCHED();
     }
     dfree(keys);
     dfree(rowptr);

@@ -29,6 +29,7 @@ struct SellView {
     const int32_t *__restrict__ rowbase;
     const int32_t *__restrict__ width;
     const int32_t *__restrict__ cnt;
+    const uint8_t *__restrict__ cnt8;  // nullable: one-byte valences (read instead of cnt)
     const uint8_t *__restrict__ slot;
     const double *__restrict__ be;
     const int32_t *__restrict__ tab;     // per-chunk offset tables (IDS_TABLE)
@@ -39,7 +40,7 @@ struct SellView {
 };
 
 inline SellView sell_view(const Plan *p, const int32_t *clist = nullptr, int64_t nlist = -1) {
-    return SellView{p->n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, p->slot,
+    return SellView{p->n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, p->cnt8, p->slot,
                     p->slot_be, p->tab, p->taboff, clist, clist ? nlist : p->n_chunks,
                     p->rowflag};
 }
@@ -312,7 +313,7 @@ __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *
         }
         const int64_t m = c * LANES + lane;
         const bool valid = m < v.n_n;
-        const int c_m = valid ? v.cnt[m] : 0;
+        const int c_m = valid ? (v.cnt8 ? (int)v.cnt8[m] : v.cnt[m]) : 0;
         const double xo = valid ? x[m] : 0.0;
         double s;
         if constexpr (PIPE && IDS != IDS_TABLE && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
@@ -437,7 +438,7 @@ __device__ __forceinline__ void sell_sweep_tma(const SellView &v, const double *
     for (int64_t c = warp; c < v.n_chunks; c += nwarps) {
         const int64_t m = c * LANES + lane;
         const bool valid = m < v.n_n;
-        const int c_m = valid ? v.cnt[m] : 0;
+        const int c_m = valid ? (v.cnt8 ? (int)v.cnt8[m] : v.cnt[m]) : 0;
         const double xo = valid ? x[m] : 0.0;
         const int w = v.width[c];
         const int64_t row0 = v.rowbase[c];

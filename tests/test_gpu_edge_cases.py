@@ -87,11 +87,12 @@ def test_empty_and_ragged_meshes(gpu):
     npt.assert_array_equal(to_np(eb.residual(b0, np.array([1.0, 2.0]))), [0.0, 0.0])
 
 
-def test_single_element_tetra_and_large_valence(gpu):
+@pytest.mark.parametrize("k", [40, 255, 300])
+def test_single_element_tetra_and_large_valence(gpu, k):
     import paper_1911_03973_b200 as eb
     import oracle as o
-    # a fan of many triangles around one node (valence 40, above the structured 6)
-    k = 40
+    # a fan of k triangles around one node (above the structured 6; 255 is the largest
+    # valence the one-byte valence array holds, 300 takes the int32 one)
     ang = np.linspace(0, 2 * np.pi, k, endpoint=False)
     nodes = np.vstack([[0.0, 0.0], np.column_stack([np.cos(ang), np.sin(ang)])])
     el = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)])
@@ -102,6 +103,8 @@ def test_single_element_tetra_and_large_valence(gpu):
     npt.assert_array_equal(to_np(eb.residual(batch, x)),
                            o.residual(A, b_e, np.ascontiguousarray(el.T), x))
     assert batch.operator().info()["max_valence"] == k
+    npt.assert_array_equal(to_np(eb.matvec(batch, x)),
+                           o.matvec_masked(A, np.ascontiguousarray(el.T), x, np.zeros(0, np.int64)))
     # one tetrahedron
     t = eb.Mesh(np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]]), np.array([[0, 1, 2, 3]]),
                 np.array([0]))
