@@ -32,7 +32,7 @@ __all__ = [
     "element_matrices", "centroids", "assemble_rhs", "local_residuals",
     "residual", "matvec_masked", "diagonal", "mask", "initial_guess",
     "richardson", "jacobi", "pcg", "cg", "element_slabs", "halo_maps",
-    "first_appearance_order", "node_slots", "config_inputs",
+    "first_appearance_order", "delta_alphabet", "grid_strides", "plan_numbering", "node_slots", "config_inputs",
     "chebyshev_roots", "chebyshev2", "chebyshev3", "chebyshev3_coefficients",
     "model_eigen_bounds", "power_iteration_lambda_max", "mass_gershgorin", "operator_bounds",
 ]
@@ -638,7 +638,8 @@ def halo_maps(indt, P):
 # ---------------------------------------------- execution-plan maps (tests)
 
 def first_appearance_order(indt, n):
-    """The GPU plan's internal node numbering: nodes in order of
+    """The GPU plan's internal node numbering when the caller's numbering is
+    not a structured grid (plan_numbering): nodes in order of
     first appearance when scanning elements e ascending, local vertex j
     ascending; nodes no element touches follow in ascending id order.
     Returns new_of_old (n,) i64."""
@@ -652,6 +653,60 @@ def first_appearance_order(indt, n):
     new_of_old = np.empty(n, dtype=np.int64)
     new_of_old[old_of_new] = np.arange(n)
     return new_of_old
+
+
+def delta_alphabet(indt, cap=32):
+    """The sorted set of (neighbour - node) id differences of a mesh,
+    d = indt[(j+t) % nb, e] - indt[j, e] over all e, j and t = 1..nb-1, or None
+    when it has more than ``cap`` values."""
+    nb = indt.shape[0]
+    seen = set()
+    for j in range(nb):
+        for t in range(1, nb):
+            seen.update(np.unique(indt[(j + t) % nb] - indt[j]).tolist())
+            if len(seen) > cap:
+                return None
+    return np.array(sorted(seen), dtype=np.int64)
+
+
+def grid_strides(indt):
+    """Axis strides s0 < s1 (< s2 in 3D) of a structured numbering: the first
+    choice, in lexicographic order over the positive id differences, for which
+    every difference is a*s0 + b*s1 (+ c*s2) with a, b, c in {-1, 0, 1}; None
+    when the differences have no such form.  The GPU plan keeps the caller's
+    numbering (identity maps, 2-bit coefficients per slot and axis) exactly when
+    this is not None; otherwise it uses first_appearance_order."""
+    diff = delta_alphabet(indt)
+    if diff is None:
+        return None
+    dim = indt.shape[0] - 1
+    pos = [int(d) for d in diff if d > 0]
+    coef = [(a, b, c) for c in (-1, 0, 1) for b in (-1, 0, 1) for a in (-1, 0, 1)
+            if dim == 3 or c == 0]
+
+    def fits(st):
+        st = tuple(st) + (0,) * (3 - len(st))
+        reach = {a * st[0] + b * st[1] + c * st[2] for a, b, c in coef}
+        return all(int(d) in reach for d in diff)
+
+    for i in range(len(pos)):
+        for k in range(i + 1, len(pos)):
+            if dim == 2:
+                if fits((pos[i], pos[k])):
+                    return (pos[i], pos[k])
+                continue
+            for m in range(k + 1, len(pos)):
+                if fits((pos[i], pos[k], pos[m])):
+                    return (pos[i], pos[k], pos[m])
+    return None
+
+
+def plan_numbering(indt, n):
+    """new_of_old of the GPU plan: identity for a structured numbering
+    (grid_strides), else first appearance."""
+    if indt.shape[1] and grid_strides(indt) is not None:
+        return np.arange(n, dtype=np.int64)
+    return first_appearance_order(indt, n)
 
 
 def node_slots(indt, n):

@@ -164,7 +164,8 @@ struct Plan {
     // slot blob: per row NB planes of 32 doubles (A rows) + the id plane (sell.cuh)
     uint8_t *slot = nullptr;
     int rowb = 0;                   // bytes per slot row
-    int packed = 0;                 // id layout: 0 absolute, 1 packed deltas, 2 per-chunk table
+    int packed = 0;                 // id layout: 0 absolute, 1 packed deltas, 2 per-chunk table,
+                                    // 3 two-base rows, 4 grid strides
     int32_t *tab = nullptr;         // per-chunk delta tables (layout 2)
     int32_t *taboff = nullptr;      // n_chunks + 1
     // loaded operator
@@ -191,6 +192,15 @@ struct Plan {
     int32_t *flag = nullptr;     // device scratch flag
     uint8_t *rowflag = nullptr;  // id layout 3 (3D): 1 per two-base row (sell.cuh IDS_DELTA2)
     int64_t two_base_rows = 0;   // id layout 3: rows coded with two bases
+    // structured caller numbering (plan.cu find_strides): kept as the internal one
+    // (identity maps); every (neighbour - node) id difference is a*stride[0] +
+    // b*stride[1] (+ c*stride[2]), a, b, c in {-1, 0, 1}
+    bool identity = false;
+    int32_t stride[3] = {0, 0, 0};
+    // id layout 4 (sell.cuh IDS_TUPLE): per slot a byte indexing the (j, differences) table
+    uint8_t *codes = nullptr;
+    int4 *tup = nullptr;
+    int n_tup = 0;
 };
 
 double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)

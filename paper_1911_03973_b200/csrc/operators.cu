@@ -136,6 +136,7 @@ static int64_t perm2_min_nodes() {
 }
 
 static bool use_perm2(const Plan *p) {
+    if (p->identity) return false;  // identity maps: the direct gather is a coalesced copy
     return EBS_PERM2 == 1 || (EBS_PERM2 == 2 && p->n_n >= perm2_min_nodes());
 }
 
@@ -226,10 +227,10 @@ void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s)
 void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *free_int,
                 const int32_t *old_of_new, double *out, cudaStream_t s, bool prefilled = false) {
     double *dst = out;
-    const int32_t *o2n = old_of_new;
+    const int32_t *o2n = p->identity ? nullptr : old_of_new;  // caller order = internal order
     const Perm2 *P = nullptr;
     int red = 0;
-    if (use_perm2(p) && old_of_new && p->n_n) {
+    if (use_perm2(p) && o2n && p->n_n) {
         // internal-order (coalesced) output, then the two-pass permutation to caller order
         Plan *pm = const_cast<Plan *>(p);
         if ((P = perm_get(pm, 1, s))) {

@@ -11,10 +11,19 @@
 // Internal numbering = first appearance when scanning elements e ascending, j ascending
 // (oracle/ebs_oracle.py first_appearance_order).  On structured meshes this recovers the
 // geometric row/plane order even when the caller's numbering is a random permutation
-// (BASELINE C2/C4), so the x gathers of a warp hit a few cache lines.
+// (BASELINE C2/C4), so the x gathers of a warp hit a few cache lines.  Exception: when
+// the caller's numbering is a structured grid (an unpermuted generated mesh, BASELINE
+// C1/C3/C5: every (neighbour - node) difference is a +-1 combination of axis strides),
+// that numbering is kept (identity maps)
+// (oracle/ebs_oracle.py grid_strides), and slots store one-byte codes of their
+// (j, differences) tuples (sell.cuh IDS_TUPLE).
 #include <cub/cub.cuh>
 
-#include "ebs_internal.cuh"
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "sell.cuh"
 
 #ifndef EBS_IDS_DELTA2
 #define EBS_IDS_DELTA2 0  // 3D two-base row coding of the id plane (opt-in: measured slower)
@@ -24,6 +33,30 @@
 #endif
 
 namespace ebs {
+
+// Identity numbering for structured caller numberings (EBS_IDS_GRID=0 in the environment
+// turns it off: comparisons against the first-appearance path)
+static int grid_mode() {
+    static const int v = [] {
+        const char *e = getenv("EBS_IDS_GRID");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+static bool grid_enabled() { return grid_mode() != 0; }
+
+// IDS_TUPLE codes: 3D plans up to EBS_TUPLE_MAX_NODES nodes (default 4M, vectors well
+// inside L2: C3 2859 -> 3020 it/s; C5 at 17M nodes 362 -> 352 and 2D kernels lose);
+// EBS_IDS_GRID=2 turns them off, =3 forces them on every structured plan (tests)
+static bool tuple_wanted(int nb, int64_t n_n) {
+    static const int64_t cap = [] {
+        const char *e = getenv("EBS_TUPLE_MAX_NODES");
+        return e ? (int64_t)atoll(e) : (int64_t)(4ll << 20);
+    }();
+    if (grid_mode() == 2) return false;
+    if (grid_mode() == 3) return true;
+    return nb == 4 && n_n <= cap;
+}
 
 // ------------------------------------------------------------- build kernels --
 __global__ void k_incidence(int nb, int64_t n_n, int64_t n_e, const int32_t *__restrict__ conn,
@@ -362,6 +395,176 @@ __global__ void __launch_bounds__(128)
     if (lane == 0 && n_two) atomicAdd(two_rows, n_two);
 }
 
+// The (neighbour - node) id differences of the caller numbering, d = conn[(j+t)%nb][e] -
+// conn[j][e], collected into a set of at most DIFF_CAP values: per CTA in shared
+// memory (linear probing; nearly every probe finds its value among the first few
+// entries), then merged into the global set.  *overflow = 1 when there are more.
+constexpr int32_t DIFF_EMPTY = (int32_t)0x80000000;
+
+__device__ __forceinline__ bool diff_insert(int32_t *set, int32_t d) {
+    for (int i = 0; i < DIFF_CAP; ++i) {
+        int32_t cur = *(volatile int32_t *)(set + i);
+        if (cur == d) return true;
+        if (cur == DIFF_EMPTY) {
+            cur = atomicCAS(set + i, DIFF_EMPTY, d);
+            if (cur == DIFF_EMPTY || cur == d) return true;
+        }
+    }
+    return false;
+}
+
+__global__ void k_diff_set(int nb, int64_t n_e, const int32_t *__restrict__ conn,
+                           int32_t *__restrict__ set, int32_t *overflow) {
+    __shared__ int32_t st[DIFF_CAP];
+    __shared__ int sover;
+    if (threadIdx.x < DIFF_CAP) st[threadIdx.x] = DIFF_EMPTY;
+    if (threadIdx.x == 0) sover = 0;
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_e;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (*(volatile int *)&sover) break;
+        int32_t v[4];
+        for (int j = 0; j < nb; ++j) v[j] = conn[j * n_e + e];
+        bool ok = true;
+        for (int j = 0; j < nb && ok; ++j)
+            for (int t = 1; t < nb && ok; ++t) ok = diff_insert(st, v[(j + t) % nb] - v[j]);
+        if (!ok) sover = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x < DIFF_CAP && st[threadIdx.x] != DIFF_EMPTY &&
+        !diff_insert(set, st[threadIdx.x]))
+        atomicOr(overflow, 1);
+    if (threadIdx.x == 0 && sover) atomicOr(overflow, 1);
+}
+
+__global__ void k_iota(int64_t n, int32_t *__restrict__ a, int32_t *__restrict__ b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = b[i] = (int32_t)i;
+}
+
+// id layout 4 (sell.cuh IDS_TUPLE): the distinct (j, d_1, .., d_{nb-1}) tuples of the
+// slots, as 64-bit keys j << 60 | biased 20-bit differences, collected into a set of at
+// most TUPLE_CAP (per CTA in shared memory, then merged); *overflow = 1 when there are
+// more.  Needs every |difference| < 2^19 (IDS_DELTA's range).
+constexpr unsigned long long TUP_EMPTY = ~0ull;
+
+__device__ __forceinline__ unsigned long long tuple_key(int nb, const int32_t *src, int64_t m) {
+    unsigned long long key = (unsigned long long)((uint32_t)src[0] >> J_SHIFT) << 60;
+    for (int t = 0; t < nb - 1; ++t) {
+        const int64_t d = (int64_t)(src[t * LANES] & ID_MASK) - m;
+        key |= (unsigned long long)((d + (1 << 19)) & 0xFFFFF) << (20 * t);
+    }
+    return key;
+}
+
+__device__ __forceinline__ bool tup_insert(unsigned long long *set, unsigned long long k) {
+    for (int i = 0; i < TUPLE_CAP; ++i) {
+        unsigned long long cur = *(volatile unsigned long long *)(set + i);
+        if (cur == k) return true;
+        if (cur == TUP_EMPTY) {
+            cur = atomicCAS(set + i, TUP_EMPTY, k);
+            if (cur == TUP_EMPTY || cur == k) return true;
+        }
+    }
+    return false;
+}
+
+__global__ void k_tuple_set(int nb, int64_t n_n, int64_t n_chunks,
+                            const int32_t *__restrict__ rowbase, const int32_t *__restrict__ cnt,
+                            const int32_t *__restrict__ ids_abs, unsigned long long *set,
+                            int32_t *overflow) {
+    __shared__ unsigned long long st[TUPLE_CAP];
+    __shared__ int sover;
+    if (threadIdx.x < TUPLE_CAP) st[threadIdx.x] = TUP_EMPTY;
+    if (threadIdx.x == 0) sover = 0;
+    __syncthreads();
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        if (*(volatile int *)&sover) break;
+        const int64_t c = m / LANES;
+        const int lane = (int)(m - c * LANES);
+        for (int k = 0; k < cnt[m]; ++k) {
+            const int64_t row = (int64_t)rowbase[c] + k;
+            if (!tup_insert(st, tuple_key(nb, ids_abs + row * (nb - 1) * LANES + lane, m))) {
+                sover = 1;
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < TUPLE_CAP && st[threadIdx.x] != TUP_EMPTY && !tup_insert(set, st[threadIdx.x]))
+        atomicOr(overflow, 1);
+    if (threadIdx.x == 0 && sover) atomicOr(overflow, 1);
+}
+
+// codes[row * 32 + lane] = index of the slot's tuple in the sorted key list (0 for padding)
+__global__ void k_write_codes(int nb, int64_t n_n, int64_t n_chunks,
+                              const int32_t *__restrict__ rowbase,
+                              const int32_t *__restrict__ width, const int32_t *__restrict__ cnt,
+                              const int32_t *__restrict__ ids_abs,
+                              const unsigned long long *__restrict__ keys, int n_keys,
+                              uint8_t *__restrict__ codes, int32_t *bad) {
+    const int64_t n_pad = n_chunks * LANES;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n_pad;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = m / LANES;
+        const int lane = (int)(m - c * LANES);
+        const int w = width[c];
+        const int c_m = m < n_n ? cnt[m] : 0;
+        for (int k = 0; k < w; ++k) {
+            const int64_t row = (int64_t)rowbase[c] + k;
+            int code = 0;
+            if (k < c_m) {
+                const unsigned long long key = tuple_key(nb, ids_abs + row * (nb - 1) * LANES + lane, m);
+                code = -1;
+                for (int i = 0; i < n_keys; ++i)
+                    if (keys[i] == key) code = i;
+                if (code < 0) { atomicOr(bad, 1); code = 0; }
+            }
+            codes[row * LANES + lane] = (uint8_t)code;
+        }
+    }
+}
+
+// Axis strides s0 < s1 (< s2) taken from the positive differences such that every
+// difference is a*s0 + b*s1 (+ c*s2), a, b, c in {-1, 0, 1}; the first such choice in
+// lexicographic order.  False when there is none.
+static bool find_strides(int dim, const std::vector<int32_t> &diff, int32_t (&st)[3]) {
+    std::vector<int64_t> pos;
+    for (int32_t d : diff)
+        if (d > 0) pos.push_back(d);
+    const size_t P = pos.size();
+    auto fits = [&](int64_t a0, int64_t a1, int64_t a2) {
+        for (int32_t d : diff) {
+            bool ok = false;
+            for (int q = 0; q < 27 && !ok; ++q) {
+                const int a = q % 3 - 1, b = (q / 3) % 3 - 1, c = q / 9 - 1;
+                if (dim == 2 && c != 0) continue;
+                ok = a * a0 + b * a1 + c * a2 == d;
+            }
+            if (!ok) return false;
+        }
+        return true;
+    };
+    for (size_t i = 0; i < P; ++i)
+        for (size_t k = i + 1; k < P; ++k) {
+            if (dim == 2) {
+                if (fits(pos[i], pos[k], 0)) {
+                    st[0] = (int32_t)pos[i], st[1] = (int32_t)pos[k], st[2] = 0;
+                    return true;
+                }
+                continue;
+            }
+            for (size_t l = k + 1; l < P; ++l)
+                if (fits(pos[i], pos[k], pos[l])) {
+                    st[0] = (int32_t)pos[i], st[1] = (int32_t)pos[k], st[2] = (int32_t)pos[l];
+                    return true;
+                }
+        }
+    return false;
+}
+
 // id plane of every slot row (sell.cuh layout): delta-packed or absolute
 __global__ void k_write_ids(int nb, int64_t n_n, int64_t n_chunks, int rowb, int packed,
                             const int32_t *__restrict__ rowbase, const int32_t *__restrict__ width,
@@ -537,7 +740,7 @@ double *plan_vec(Plan *p, int i) {
 }
 
 static void plan_free(Plan *p) {
-    dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->cnt8); dfree(p->rowbase);
+    dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->cnt8); dfree(p->codes); dfree(p->tup); dfree(p->rowbase);
     dfree(p->width); dfree(p->slot_ej); dfree(p->slot); dfree(p->tab); dfree(p->taboff);
     dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
     dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag); dfree(p->rowflag);
@@ -599,9 +802,37 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     }
     EBS_REQUIRE(read1(bad, s) == 0, "element connectivity references nonexistent nodes");
 
-    // 2. internal numbering
+    // 2. internal numbering: the caller's own when it is a structured grid (every id
+    // difference a combination of axis strides; sell.cuh IDS_TUPLE), else first appearance
     p->new_of_old = dmalloc<int32_t>(n_n);
     p->old_of_new = dmalloc<int32_t>(n_n);
+    if (grid_enabled() && total) {
+        int32_t *set = dmalloc<int32_t>(DIFF_CAP + 1);
+        int32_t h[DIFF_CAP + 1];
+        for (int i = 0; i < DIFF_CAP; ++i) h[i] = DIFF_EMPTY;
+        h[DIFF_CAP] = 0;
+        CU(cudaMemcpyAsync(set, h, sizeof h, cudaMemcpyHostToDevice, s));
+        k_diff_set<<<grid_for(n_e, 256, sm_count() * 8), 256, 0, s>>>(nb, n_e, conn, set,
+                                                                      set + DIFF_CAP);
+        LAUNCHED();
+        cudaError_t e1 = cudaMemcpyAsync(h, set, sizeof h, cudaMemcpyDeviceToHost, s);
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        cudaFree(set);
+        CU(e1);
+        CU(e2);
+        if (!h[DIFF_CAP]) {
+            std::vector<int32_t> a;
+            for (int i = 0; i < DIFF_CAP; ++i)
+                if (h[i] != DIFF_EMPTY) a.push_back(h[i]);
+            std::sort(a.begin(), a.end());
+            a.erase(std::unique(a.begin(), a.end()), a.end());
+            p->identity = find_strides(nb - 1, a, p->stride);
+        }
+    }
+    if (p->identity && n_n) {
+        k_iota<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, p->new_of_old, p->old_of_new);
+        LAUNCHED();
+    }
     flag = dmalloc<int32_t>(total);
     pos = dmalloc<int32_t>(total);
     int64_t n_conn = 0;
@@ -616,9 +847,11 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
         k_isolated_flags<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, cnt_old, iso);
         LAUNCHED();
         scan_i32(iso, iso_pos, n_n, s);
-        k_numbering<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, n_conn, cnt_old, first, pos, iso_pos,
-                                                      p->new_of_old, p->old_of_new);
-        LAUNCHED();
+        if (!p->identity) {
+            k_numbering<<<grid_for(n_n, 256), 256, 0, s>>>(n_n, n_conn, cnt_old, first, pos,
+                                                          iso_pos, p->new_of_old, p->old_of_new);
+            LAUNCHED();
+        }
     }
     cudaFree(iso_pos);
     dfree(flag);
@@ -684,10 +917,37 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
             if (read1(p->flag, s) == 0) layout = 2;
         }
         const unsigned long long limit = nb == 3 ? (1ull << 14) - 1 : (1ull << 19) - 1;
+        // structured caller numbering: one-byte tuple codes where they measured faster
+        std::vector<unsigned long long> tkeys;
+        if (p->identity && tuple_wanted(nb, n_n) && max_delta < (1ull << 19) && p->n_chunks) {
+            unsigned long long *set = dmalloc<unsigned long long>(TUPLE_CAP + 1);
+            std::vector<unsigned long long> h(TUPLE_CAP + 1, TUP_EMPTY);
+            h[TUPLE_CAP] = 0;
+            CU(cudaMemcpyAsync(set, h.data(), sizeof(unsigned long long) * (TUPLE_CAP + 1),
+                               cudaMemcpyHostToDevice, s));
+            k_tuple_set<<<grid_for(n_n, 256, sm_count() * 8), 256, 0, s>>>(
+                nb, n_n, p->n_chunks, p->rowbase, p->cnt, ids_abs, set,
+                reinterpret_cast<int32_t *>(set + TUPLE_CAP));
+            LAUNCHED();
+            cudaError_t e1 = cudaMemcpyAsync(h.data(), set, sizeof(unsigned long long) * (TUPLE_CAP + 1),
+                                             cudaMemcpyDeviceToHost, s);
+            cudaError_t e2 = cudaStreamSynchronize(s);
+            cudaFree(set);
+            CU(e1);
+            CU(e2);
+            if (h[TUPLE_CAP] == 0) {
+                for (int i = 0; i < TUPLE_CAP; ++i)
+                    if (h[i] != TUP_EMPTY) tkeys.push_back(h[i]);
+                std::sort(tkeys.begin(), tkeys.end());
+                tkeys.erase(std::unique(tkeys.begin(), tkeys.end()), tkeys.end());
+                if (!tkeys.empty()) layout = IDS_TUPLE;
+            }
+        }
         if (layout < 0) layout = max_delta <= limit ? 1 : 0;
         if (layout == 1 && nb == 4 && EBS_IDS_DELTA2) layout = 3;  // same plane, two-base rows
         p->packed = layout;
-        const int id_bytes = layout == 2 ? (nb == 3 ? 2 : 4) * LANES
+        const int id_bytes = layout == IDS_TUPLE ? 0
+                           : layout == 2 ? (nb == 3 ? 2 : 4) * LANES
                                          : (layout == 1 || layout == 3 ? (nb == 3 ? 4 : 8) * LANES
                                                         : 4 * (nb - 1) * LANES);
         p->rowb = nb * 8 * LANES + id_bytes;
@@ -705,6 +965,31 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
                 nb, n_n, p->n_chunks, cap, p->rowbase, p->width, p->cnt, ids_abs, nullptr,
                 p->taboff, p->tab, p->slot, p->rowb, p->flag);
             LAUNCHED();
+        } else if (layout == IDS_TUPLE) {
+            p->tab = dmalloc<int32_t>(1);
+            const int nk = (int)tkeys.size();
+            std::vector<int4> tab(TUPLE_CAP, make_int4(0, 0, 0, 0));
+            for (int i = 0; i < nk; ++i) {
+                const unsigned long long k = tkeys[i];
+                int d[3] = {0, 0, 0};
+                for (int t = 0; t < nb - 1; ++t)
+                    d[t] = (int)((k >> (20 * t)) & 0xFFFFF) - (1 << 19);
+                tab[i] = make_int4((int)(k >> 60), d[0], d[1], d[2]);
+            }
+            p->n_tup = nk;
+            p->tup = dmalloc<int4>(TUPLE_CAP);
+            CU(cudaMemcpyAsync(p->tup, tab.data(), sizeof(int4) * TUPLE_CAP, cudaMemcpyHostToDevice, s));
+            unsigned long long *dk = dmalloc<unsigned long long>(nk);
+            CU(cudaMemcpyAsync(dk, tkeys.data(), sizeof(unsigned long long) * nk, cudaMemcpyHostToDevice, s));
+            p->codes = dmalloc<uint8_t>((size_t)p->n_rows * LANES);
+            CU(cudaMemsetAsync(p->flag, 0, sizeof(int32_t), s));
+            k_write_codes<<<grid_for(p->n_chunks * LANES, 128), 128, 0, s>>>(
+                nb, n_n, p->n_chunks, p->rowbase, p->width, p->cnt, ids_abs, dk, nk, p->codes,
+                p->flag);
+            LAUNCHED();
+            const int32_t bad_code = read1(p->flag, s);
+            cudaFree(dk);
+            EBS_REQUIRE(bad_code == 0, "internal error: slot tuple missing from the table");
         } else if (layout == 3 && p->n_chunks) {
             p->tab = dmalloc<int32_t>(1);
             p->rowflag = dmalloc<uint8_t>(p->n_rows);
@@ -802,10 +1087,11 @@ int ebs_plan_info(ebs_plan_t plan, int64_t *info) {
     info[3] = p->n_chunks;
     info[4] = p->n_rows;
     int64_t slots = p->n_rows * LANES;
-    info[5] = p->n_rows * (int64_t)p->rowb + (p->has_be ? slots * 8 : 0);
+    info[5] = p->n_rows * (int64_t)p->rowb + (p->has_be ? slots * 8 : 0) + (p->codes ? slots : 0);
     info[6] = p->max_valence;
     info[7] = (p->has_A ? 1 : 0) | (p->has_be ? 2 : 0) | (p->packed ? 4 : 0) |
-              (p->packed == 2 ? 8 : 0) | (p->packed == 3 ? 16 : 0);
+              (p->packed == 2 ? 8 : 0) | (p->packed == 3 ? 16 : 0) |
+              (p->packed == IDS_TUPLE ? 32 : 0) | (p->identity ? 64 : 0);
     EBS_CATCH
 }
 

@@ -37,12 +37,14 @@ struct SellView {
     const int32_t *__restrict__ clist;   // nullable: sweep only these chunks
     int64_t nlist;                       // number of chunks swept (n_chunks or list size)
     const uint8_t *__restrict__ rowflag; // IDS_DELTA2: 1 = two-base row, 0 = 64-bit deltas
+    const uint8_t *__restrict__ codes;   // IDS_TUPLE: one byte per slot (row * 32 + lane)
+    const int4 *__restrict__ tup;        // IDS_TUPLE: the plan's (j, d_1, d_2[, d_3]) tuples
 };
 
 inline SellView sell_view(const Plan *p, const int32_t *clist = nullptr, int64_t nlist = -1) {
     return SellView{p->n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, p->cnt8, p->slot,
                     p->slot_be, p->tab, p->taboff, clist, clist ? nlist : p->n_chunks,
-                    p->rowflag};
+                    p->rowflag, p->codes, p->tup};
 }
 
 // id-plane layouts (Plan::packed)
@@ -56,6 +58,18 @@ constexpr int IDS_TABLE = 2;  // indices into a per-chunk table of deltas: 16 (2
 // flag per row (SellView::rowflag) says which.  No lookup on the id -> x-gather chain:
 // code, bases and flag are independent loads.
 constexpr int IDS_DELTA2 = 3;
+// Meshes whose caller numbering is already a structured grid keep it (identity maps, no
+// permutation at the API boundary; plan.cu find_strides).  There a slot's (j, neighbour
+// - node differences) tuple takes only a few values -- 6 in 2D, 24 for Kuhn cubes (6 tet
+// types x 4 vertices) -- so the plan can store the distinct tuples (<= TUPLE_CAP) and per
+// slot one byte indexing them, in an array of its own (32 B per row), instead of the
+// 8 B 3D id word; each warp keeps a copy of the table in shared memory and decodes with
+// one 16 B shared-memory load.  Measured (profiles/README.md): C3 (2.1M nodes) 2859 ->
+// 3020 it/s, but C5 (17M nodes) 362 -> 352 and the 2D kernels (32-register cap) lose, so
+// plans use it for 3D meshes up to EBS_TUPLE_MAX_NODES nodes only.
+constexpr int IDS_TUPLE = 4;
+constexpr int TUPLE_CAP = 32;
+constexpr int DIFF_CAP = 32;  // distinct differences collected while detecting the grid
 
 template <int NB>
 struct Tab;
@@ -166,6 +180,12 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
                     jj[u] = Pack<NB>::j(wd);
 #pragma unroll
                     for (int t = 0; t < NB - 1; ++t) nid[u][t] = (int32_t)(m + Pack<NB>::d(wd, t));
+                } else if constexpr (IDS == IDS_TUPLE) {
+                    const int4 tp = reinterpret_cast<const int4 *>(stab)[__ldcs(v.codes + row * LANES + lane)];
+                    jj[u] = tp.x;
+                    nid[u][0] = (int32_t)m + tp.y;
+                    nid[u][1] = (int32_t)m + tp.z;
+                    if constexpr (NB == 4) nid[u][2] = (int32_t)m + tp.w;
                 } else if constexpr (IDS == IDS_DELTA2) {
                     static_assert(NB == 4, "IDS_DELTA2 is the 3D layout");
                     const uint8_t *ip = rp + NB * 256;
@@ -234,7 +254,8 @@ struct IdWord {
     using W = typename Pack<NB>::W;
     W w;
     int32_t a[NB - 1];
-    __device__ __forceinline__ void load(const uint8_t *rp, int lane) {
+    __device__ __forceinline__ void load(const SellView &v, int64_t row, int lane) {
+        const uint8_t *rp = v.slot + row * v.rowb;
         if constexpr (IDS == IDS_DELTA) {
             w = __ldcs(reinterpret_cast<const W *>(rp + NB * 256) + lane);
         } else {
@@ -243,7 +264,7 @@ struct IdWord {
             for (int t = 0; t < NB - 1; ++t) a[t] = __ldcs(ip + t * LANES);
         }
     }
-    __device__ __forceinline__ int decode(int64_t m, int32_t (&nid)[NB - 1]) const {
+    __device__ __forceinline__ int decode(const SellView &, int64_t m, int32_t (&nid)[NB - 1]) const {
         if constexpr (IDS == IDS_DELTA) {
 #pragma unroll
             for (int t = 0; t < NB - 1; ++t) nid[t] = (int32_t)(m + Pack<NB>::d(w, t));
@@ -265,13 +286,13 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
                                                      const double *__restrict__ x, double xo) {
     double s = 0.0;
     IdWord<NB, IDS> nxt;
-    if (0 < c_m) nxt.load(v.slot + row0 * v.rowb, lane);
+    if (0 < c_m) nxt.load(v, row0, lane);
     for (int k = 0; k < w; ++k) {
         if (k < c_m) {
             const IdWord<NB, IDS> cur = nxt;
             const uint8_t *rp = v.slot + (row0 + k) * v.rowb;
             int32_t nid[NB - 1];
-            const int j = cur.decode(m, nid);
+            const int j = cur.decode(v, m, nid);
             double g[NB - 1];
 #pragma unroll
             for (int t = 0; t < NB - 1; ++t) g[t] = __ldg(x + nid[t]);
@@ -281,7 +302,7 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
             for (int i = 0; i < NB; ++i) a[i] = __ldcs(ap + i * LANES);
             double be = 0.0;
             if constexpr (EXACT) be = __ldcs(v.be + (row0 + k) * LANES + lane);
-            if (k + 1 < c_m) nxt.load(rp + v.rowb, lane);
+            if (k + 1 < c_m) nxt.load(v, row0 + k + 1, lane);
             double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
 #pragma unroll
             for (int i = 1; i < NB; ++i) loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
@@ -297,10 +318,14 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
 template <int NB, int IDS, bool EXACT, bool PIPE, class Epi>
 __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *__restrict__ x,
                                                Epi &epi) {
-    constexpr int CAP = IDS == IDS_TABLE ? Tab<NB>::CAP : 1;
-    __shared__ int32_t stab_all[256 / LANES][CAP];  // 256-thread CTAs: one table per warp
+    constexpr int CAP = IDS == IDS_TABLE ? Tab<NB>::CAP : (IDS == IDS_TUPLE ? 4 * TUPLE_CAP : 1);
+    __shared__ __align__(16) int32_t stab_all[256 / LANES][CAP];  // one table per warp
     const int lane = threadIdx.x & (LANES - 1);
     int32_t *stab = stab_all[threadIdx.x / LANES];
+    if constexpr (IDS == IDS_TUPLE) {
+        for (int i = lane; i < TUPLE_CAP; i += LANES) reinterpret_cast<int4 *>(stab)[i] = v.tup[i];
+        __syncwarp();
+    }
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / LANES;
     for (int64_t ci = warp; ci < v.nlist; ci += nwarps) {
@@ -316,7 +341,7 @@ __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *
         const int c_m = valid ? (v.cnt8 ? (int)v.cnt8[m] : v.cnt[m]) : 0;
         const double xo = valid ? x[m] : 0.0;
         double s;
-        if constexpr (PIPE && IDS != IDS_TABLE && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
+        if constexpr (PIPE && IDS != IDS_TABLE && IDS != IDS_TUPLE && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
             s = sell_node_sum_pipe<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m, c_m, x,
                                                    xo);
         else
@@ -512,7 +537,7 @@ template <int NB, int IDS, bool EXACT, bool PIPE = false, class Epi>
 __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__restrict__ x,
                                            Epi &epi) {
 #if EBS_TMA
-    if constexpr (IDS != IDS_TABLE && IDS != IDS_DELTA2) {
+    if constexpr (IDS != IDS_TABLE && IDS != IDS_DELTA2 && IDS != IDS_TUPLE) {
         if (v.clist == nullptr) {  // the TMA ring sweeps all chunks
             sell_sweep_tma<NB, IDS, EXACT>(v, x, epi);
             return;
@@ -526,11 +551,13 @@ __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__re
 #define EBS_SELL_DISPATCH(p, M)                                                          \
     do {                                                                                 \
         if ((p)->nb == 3) {                                                              \
-            if ((p)->packed == IDS_TABLE) M(3, IDS_TABLE)                                \
+            if ((p)->packed == IDS_TUPLE) M(3, IDS_TUPLE)                                  \
+            else if ((p)->packed == IDS_TABLE) M(3, IDS_TABLE)                           \
             else if ((p)->packed == IDS_DELTA) M(3, IDS_DELTA)                           \
             else M(3, IDS_ABS)                                                           \
         } else {                                                                         \
-            if ((p)->packed == IDS_TABLE) M(4, IDS_TABLE)                                \
+            if ((p)->packed == IDS_TUPLE) M(4, IDS_TUPLE)                                  \
+            else if ((p)->packed == IDS_TABLE) M(4, IDS_TABLE)                           \
             else if ((p)->packed == IDS_DELTA2) M(4, IDS_DELTA2)                         \
             else if ((p)->packed == IDS_DELTA) M(4, IDS_DELTA)                           \
             else M(4, IDS_ABS)                                                           \

@@ -118,6 +118,62 @@ def test_plan_numbering_matches_oracle(gpu):
     npt.assert_array_equal(old_of_new[new_of_old], np.arange(m.n_nodes))
     info = pl.info()
     assert info["max_valence"] == 6 and info["n_chunks"] == (m.n_nodes + 31) // 32
+    assert not info["loaded"] & 32                     # permuted: not a structured grid
+
+
+_STRUCTURED_CHECK = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle as o
+import paper_1911_03973_b200 as eb
+dim = int(sys.argv[2])
+nodes, el, nd = o.unit_square_mesh(4) if dim == 2 else o.kuhn_cube_mesh(4)
+m = eb.Mesh(nodes, el, nd)
+indt = np.ascontiguousarray(el.T)
+pl = eb.build_index_arrays(m).plan()
+new_of_old, old_of_new = (t.cpu().numpy() for t in pl.node_maps())
+assert np.array_equal(new_of_old, o.plan_numbering(indt, m.n_nodes))
+assert np.array_equal(old_of_new, np.arange(m.n_nodes))
+flags = pl.info()["loaded"]
+batch = eb.build_element_batch(m, nu=1.0)
+_, _, A, b_e = o.element_matrices(nodes, el, nu=1.0)
+x = np.random.default_rng(1).uniform(-1, 1, m.n_nodes)
+ref = o.residual(A, b_e, indt, x)
+assert np.array_equal(eb.residual(batch, x).cpu().numpy(), ref)
+assert np.array_equal(eb.matvec(batch, x).cpu().numpy(), o.matvec_masked(A, indt, x, np.zeros(0, np.int64)))
+fast = eb.residual(batch, x, deterministic=False).cpu().numpy()
+assert np.max(np.abs(fast - ref)) <= 1e-12 * np.max(np.abs(ref))
+d = eb.constant_dirichlet(m, 0.0)
+xs, hs = eb.pcg(batch, d, np.zeros(m.n_nodes), 200, tol=1e-10)
+xo, ho = o.pcg(A, b_e, indt, nd, np.zeros(m.n_nodes), 200, tol=1e-10)
+assert len(hs.residual_norms) == len(ho["residual_norms"])
+assert np.linalg.norm(xs.cpu().numpy() - xo) <= 1e-8 * np.linalg.norm(xo)
+print("FLAGS", flags)
+"""
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("mode", ["", "2", "3"])
+def test_plan_keeps_structured_numbering(gpu, dim, mode):
+    """Unpermuted generated grids: every (neighbour - node) difference is a +-1
+    combination of axis strides, so the plan keeps the caller's numbering (identity maps)
+    -- with packed-delta ids (EBS_IDS_GRID=2), one-byte tuple codes (=3), or the default
+    choice (tuples for small 3D plans).  Residual / matvec bitwise, PCG vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("EBS_IDS_GRID", None)
+    if mode:
+        env["EBS_IDS_GRID"] = mode
+    out = subprocess.run([sys.executable, "-c", _STRUCTURED_CHECK, root, str(dim)], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    flags = int(out.stdout.split("FLAGS")[1])
+    assert flags & 64                                  # identity numbering
+    tuples = mode == "3" or (mode == "" and dim == 3)
+    assert bool(flags & 32) == tuples
 
 
 @pytest.mark.parametrize("N", [2, 3])

@@ -112,3 +112,25 @@ def test_first_appearance_order_is_a_permutation():
     orig = np.empty_like(inp["perm"])
     orig[inp["perm"]] = np.arange(len(orig))
     assert new_of_old[inp["perm"][0]] == 0
+
+
+def test_grid_strides_of_generated_grids():
+    """Unpermuted grids: differences 2D +-{1, n, n+1} (strides 1, n), 3D the 14
+    Freudenthal edge offsets (strides 1, n, n^2); a random numbering has no small set of
+    differences (the plan then uses first_appearance_order)."""
+    _, el, _ = o.unit_square_mesh(3)
+    n = 9
+    npt.assert_array_equal(o.delta_alphabet(np.ascontiguousarray(el.T)),
+                           [-n - 1, -n, -1, 1, n, n + 1])
+    assert o.grid_strides(np.ascontiguousarray(el.T)) == (1, n)
+    _, el, _ = o.kuhn_cube_mesh(3)
+    n = 4
+    pos = sorted({1, n, n + 1, n * n, n * n + 1, n * n + n, n * n + n + 1})
+    npt.assert_array_equal(o.delta_alphabet(np.ascontiguousarray(el.T)),
+                           sorted([-d for d in pos] + pos))
+    assert o.grid_strides(np.ascontiguousarray(el.T)) == (1, n, n * n)
+    inp = o.config_inputs(2, seed=0, size=3)
+    indt = np.ascontiguousarray(inp["elements"].T)
+    assert o.delta_alphabet(indt) is None and o.grid_strides(indt) is None
+    npt.assert_array_equal(o.plan_numbering(indt, len(inp["nodes"])),
+                           o.first_appearance_order(indt, len(inp["nodes"])))
