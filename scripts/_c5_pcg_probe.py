@@ -1,11 +1,12 @@
 import sys, os
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
-import numpy as np, torch
+import torch
 import paper_1911_03973_b200 as eb
 from paper_1911_03973_b200.inputs import config_problem
 torch.cuda.set_device(0)
-p = config_problem(3, seed=0)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+p = config_problem(cfg, seed=0)
 x0 = torch.zeros(p["mesh"].n_nodes, dtype=torch.float64, device="cuda")
 for _ in range(2):
-    eb.pcg(p["batch"], p["dirichlet"], x0, 10)
+    eb.pcg(p["batch"], p["dirichlet"], x0, 6)
 torch.cuda.synchronize()
