@@ -479,11 +479,18 @@ def solver_extras(args):
             nb = m.n_b
             n_n, n_e = m.n_nodes, m.n_elements
             per_it = n_e * (8 * nb * nb + 4 * nb) + (32 if cfg == 4 else 104) * n_n
+            # the same with the plan's own id coding instead of the model's 4 B connectivity
+            # per slot (one-byte tuple codes / packed deltas / absolute ids)
+            flags = pl.info()["loaded"]
+            id_b = 1 if flags & 32 else ((4 if nb == 3 else 8) if flags & 4 else 4 * (nb - 1))
+            per_it_stored = n_e * (8 * nb * nb + id_b * nb) + (32 if cfg == 4 else 104) * n_n
             out[f"C{cfg}"] = {
                 "method": "jacobi" if cfg == 4 else "pcg", "iterations": its,
                 "it_per_s": its / t, "ms_per_it": t / its * 1e3,
                 "hbm_gbs_algorithmic": per_it * its / t / 1e9,
                 "frac_of_peak": per_it * its / t / 1e9 / float(peaks["hbm_gbs"]),
+                "id_bytes_per_slot": id_b,
+                "frac_of_peak_stored": per_it_stored * its / t / 1e9 / float(peaks["hbm_gbs"]),
                 "final_rel_residual": float(h.residual_norms[-1] / h.residual_norms[0]),
                 "n_nodes": n_n, "n_elements": n_e, "setup_s": setup}
             del p, batch, pl, x
