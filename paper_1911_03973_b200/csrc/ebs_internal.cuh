@@ -192,6 +192,10 @@ struct Plan {
     int32_t *flag = nullptr;     // device scratch flag
     uint8_t *rowflag = nullptr;  // id layout 3 (3D): 1 per two-base row (sell.cuh IDS_DELTA2)
     int64_t two_base_rows = 0;   // id layout 3: rows coded with two bases
+    // single-cluster solver launch (solve.cu k_pcg_cluster), decided once per plan:
+    // cl_state 0 unknown, 1 fits (cl_G CTAs of cl_cpb chunks, cl_smem bytes), -1 does not
+    int cl_state = 0, cl_G = 0, cl_cpb = 0;
+    size_t cl_smem = 0;
     // structured caller numbering (plan.cu find_strides): kept as the internal one
     // (identity maps); every (neighbour - node) id difference is a*stride[0] +
     // b*stride[1] (+ c*stride[2]), a, b, c in {-1, 0, 1}

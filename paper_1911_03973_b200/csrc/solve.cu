@@ -18,6 +18,8 @@
 // enqueuing after convergence (and every iteration when a callback is attached).
 // Reductions are fixed-order (deterministic run to run).
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <vector>
 
 #include "sell.cuh"
 
@@ -546,6 +548,294 @@ void launch_pcg_fused(Plan *p, const LoopArgs &L, int iters, double *x, double *
     bump_launches(1);
 }
 
+// ------------------------------------------- single-cluster CG / PCG (small meshes) --
+// pcg/cg(fused=True) on a mesh whose slot stream fits the shared memory of one thread-
+// block cluster (8, else up to 16 CTAs on as many SMs; C1: 4225 nodes, 715 KB of slot
+// rows; 5.3 us per iteration vs 11.6 for the cooperative grid kernel): CTA c
+// copies the slot rows of its chunks and a full copy of p into its shared memory once,
+// then every iteration runs from on-chip memory --
+//   A  q = mask(A p) for its own nodes (slot rows and x gathers from shared memory; each
+//      thread keeps its node's x, r, p, diag^-1 in registers), p.q block partial
+//      broadcast into every CTA's partial array (DSMEM stores)           | cluster barrier
+//   B  alpha from the partials summed in rank order (the same in every CTA); x, r
+//      update, r.r / r.z / error / non-finite partials broadcast          | cluster barrier
+//   C  the _iterate rules, beta; p = z + beta p written into every CTA's copy of p
+//                                                                         | cluster barrier
+// -- no global-memory traffic or grid-wide barriers inside the loop.  The row sums are
+// sell_node_sum's (same order, same bits); the dots are reduced over the cluster in a
+// fixed order (deterministic; equal to the other loops up to rounding).
+constexpr int CL_MAX = 16;
+constexpr int CL_HIST = 512;  // history entries buffered in shared memory
+
+// history entries k-cnt+1 .. k (1-based iteration index) from the buffer to global
+__device__ __forceinline__ void flush_hist(const LoopArgs &L, const double *hist, int k, int cnt) {
+    for (int i = 0; i < cnt; ++i) {
+        L.norms[k - cnt + 1 + i] = hist[i];
+        if (L.errors) L.errors[k - cnt + 1 + i] = hist[CL_HIST + i];
+    }
+}
+
+template <int NB, int IDS>
+__device__ __forceinline__ double smem_node_sum(const uint8_t *rows, int rowb, int64_t rrel,
+                                                int w, int lane, int64_t m, int c_m,
+                                                const double *ps, double xo) {
+    double s = 0.0;
+    for (int k = 0; k < w; ++k) {
+        if (k < c_m) {
+            const uint8_t *rp = rows + (rrel + k) * rowb;
+            const double *ap = reinterpret_cast<const double *>(rp) + lane;
+            double a[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) a[i] = ap[i * LANES];
+            int32_t nid[NB - 1];
+            int j;
+            if constexpr (IDS == IDS_DELTA) {
+                using W = typename Pack<NB>::W;
+                const W wd = reinterpret_cast<const W *>(rp + NB * 256)[lane];
+                j = Pack<NB>::j(wd);
+#pragma unroll
+                for (int t = 0; t < NB - 1; ++t) nid[t] = (int32_t)(m + Pack<NB>::d(wd, t));
+            } else {
+                const int32_t *ip = reinterpret_cast<const int32_t *>(rp + NB * 256) + lane;
+                j = (int)((uint32_t)ip[0] >> J_SHIFT);
+#pragma unroll
+                for (int t = 0; t < NB - 1; ++t) nid[t] = ip[t * LANES] & ID_MASK;
+            }
+            double g[NB - 1];
+#pragma unroll
+            for (int t = 0; t < NB - 1; ++t) g[t] = ps[nid[t]];
+            double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
+#pragma unroll
+            for (int i = 1; i < NB; ++i) loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
+            s = s + loc;
+        }
+    }
+    return s;
+}
+
+template <int NB, int IDS>
+__global__ void __launch_bounds__(1024, 1)
+    k_pcg_cluster(SellView v, LoopArgs L, int64_t n, int iters, int cpb, int64_t n_rows,
+                  double *__restrict__ x, double *__restrict__ r, double *__restrict__ p,
+                  const double *__restrict__ dinv, const uint8_t *__restrict__ free_int,
+                  const double *__restrict__ ref) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int G = (int)cl.num_blocks();
+    const int me = (int)cl.block_rank();
+    Ctl *ctl = L.ctl;
+    extern __shared__ __align__(16) uint8_t dsm[];
+    const int64_t npad = v.n_chunks * LANES;
+    double *ps = reinterpret_cast<double *>(dsm);  // full copy of p
+    double *pA = ps + npad;                        // [CL_MAX]      p.q partial per rank
+    double *pB = pA + CL_MAX;                      // [4 * CL_MAX]  r.r, r.z, err, non-finite
+    double *sm = pB + 4 * CL_MAX;                  // [4 * 32]      block_sum scratch
+    double *hist = sm + 4 * 32;                    // [2 * CL_HIST] norms / errors, flushed
+    uint8_t *rows = reinterpret_cast<uint8_t *>(hist + 2 * CL_HIST);
+    const int64_t c0 = (int64_t)me * cpb;
+    const int64_t c1 = c0 + cpb < v.n_chunks ? c0 + cpb : v.n_chunks;
+    const int64_t r0 = c0 < v.n_chunks ? v.rowbase[c0] : n_rows;
+    const int64_t r1 = c1 < v.n_chunks ? v.rowbase[c1] : n_rows;
+    {  // one-time staging: this CTA's slot rows, all of p
+        const int4 *src = reinterpret_cast<const int4 *>(v.slot + r0 * v.rowb);
+        int4 *dst = reinterpret_cast<int4 *>(rows);
+        const int64_t n16 = (r1 - r0) * v.rowb / 16;
+        for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+        for (int64_t i = threadIdx.x; i < npad; i += blockDim.x) ps[i] = i < n ? p[i] : 0.0;
+    }
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = c0 + wib;
+    const int64_t m = c * LANES + lane;
+    const bool mine = c < c1 && m < n;
+    const int w = c < c1 ? v.width[c] : 0;
+    const int c_m = mine ? v.cnt[m] : 0;
+    const int64_t rrel = c < c1 ? v.rowbase[c] - r0 : 0;
+    double xm = 0.0, rm = 0.0, pm = 0.0, dm = 0.0, refm = 0.0;
+    bool fm = false;
+    if (mine) {
+        xm = x[m], rm = r[m], pm = p[m], dm = dinv[m], fm = free_int[m] != 0;
+        if (ref) refm = ref[m];
+    }
+    double rz = ctl->rz;
+    const double norm0 = ctl->norm0;
+    const bool leader = me == 0 && threadIdx.x == 0;
+    int k = 0, done = ctl->done, diverged = 0;
+    cl.sync();  // staging complete everywhere (ps is read by the gathers)
+    while (!done && k < iters) {
+        // A: q = mask(A p), p.q
+        double qm = 0.0;
+        {
+            const double s = smem_node_sum<NB, IDS>(rows, v.rowb, rrel, w, lane, m, c_m, ps, pm);
+            if (mine) qm = fm ? s : 0.0;
+        }
+        double a1[1] = {pm * qm};
+        block_sum<1>(a1, sm);
+        if (wib == 0) {  // block total (lane 0 of warp 0) -> slot `me` of every CTA's pA
+            const double tv = __shfl_sync(0xffffffffu, a1[0], 0);
+            if (lane < G) *cl.map_shared_rank(pA + me, lane) = tv;
+        }
+        cl.sync();
+        double pq = 0.0;
+        for (int t = 0; t < G; ++t) pq += pA[t];
+        const double alpha = pq != 0.0 ? rz / pq : 0.0;
+        // B: x, r update, r.r, r.z (+ error, non-finite count)
+        double part[4] = {0.0, 0.0, 0.0, 0.0};
+        if (mine) {
+            xm = xm + alpha * pm;
+            rm = rm - alpha * qm;
+            part[0] = rm * rm;
+            part[1] = rm * (dm * rm);
+            if (ref) {
+                const double d = xm - refm;
+                part[2] = d * d;
+            }
+            part[3] = isfinite(xm) ? 0.0 : 1.0;
+        }
+        block_sum<4>(part, sm);
+        if (wib == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double tv = __shfl_sync(0xffffffffu, part[q], 0);
+                if (lane < G) *cl.map_shared_rank(pB + q * CL_MAX + me, lane) = tv;
+            }
+        }
+        cl.sync();
+        double tot[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int t = 0; t < G; ++t)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) tot[q] += pB[q * CL_MAX + t];
+        // C: the _iterate rules (solvers.py:117-160), identical in every CTA
+        ++k;
+        const double nr = sqrt(tot[0]);
+        // history entries go to a shared-memory buffer, flushed when full and at the end:
+        // a global store before a cluster barrier makes its release fence wait for it
+        const bool bad = tot[3] != 0.0 || !isfinite(nr);
+        if (leader) {
+            const int h = (k - 1) % CL_HIST;
+            hist[h] = bad && tot[3] != 0.0 ? INFINITY : nr;
+            hist[CL_HIST + h] = bad && tot[3] != 0.0 ? INFINITY : sqrt(tot[2]);
+            if (h == CL_HIST - 1) flush_hist(L, hist, k, h + 1);
+        }
+        if (bad) {
+            diverged = done = 1;
+            break;
+        }
+        if (L.has_tol && nr <= L.tol * norm0) {
+            done = 1;
+            break;
+        }
+        const double beta = rz != 0.0 ? tot[1] / rz : 0.0;
+        rz = tot[1];
+        if (k == iters) break;  // the last direction update would be unused
+        if (mine) {
+            pm = dm * rm + beta * pm;
+            for (int t = 0; t < G; ++t) *cl.map_shared_rank(ps + m, t) = pm;
+        }
+        cl.sync();
+    }
+    if (mine) {
+        x[m] = xm;
+        r[m] = rm;
+        p[m] = pm;
+    }
+    if (leader) {
+        if (k > 0 && (k - 1) % CL_HIST != CL_HIST - 1) flush_hist(L, hist, k, (k - 1) % CL_HIST + 1);
+        ctl->k = k;
+        ctl->n_norms = k + 1;
+        ctl->rz = rz;
+        ctl->diverged = diverged;
+        ctl->done = done;
+        ctl->cb_ok = 0;
+    }
+    cl.sync();  // no CTA exits while others may still write into its shared memory
+}
+
+#ifndef EBS_PCG_CLUSTER
+#define EBS_PCG_CLUSTER 1
+#endif
+
+// Launch k_pcg_cluster when the mesh fits one cluster; false: use the cooperative kernel.
+template <int NB, int IDS>
+bool launch_pcg_cluster(Plan *p, const LoopArgs &L, int iters, double *x, double *r, double *pv,
+                        const double *dinv, const double *ref, cudaStream_t s) {
+    if (!EBS_PCG_CLUSTER || getenv("EBS_NO_CLUSTER")) return false;
+    if constexpr (IDS != IDS_DELTA && IDS != IDS_ABS) {
+        return false;
+    } else {
+        auto kern = k_pcg_cluster<NB, IDS>;
+        if (p->cl_state == 0) {  // choose the cluster once per plan
+            p->cl_state = -1;
+            const int64_t nch = p->n_chunks;
+            if (nch < 1 || nch > (int64_t)CL_MAX * 32) return false;
+            std::vector<int32_t> rb(nch);
+            CU(cudaMemcpyAsync(rb.data(), p->rowbase, sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            const char *ge = getenv("EBS_CLUSTER_MAX");
+            const int gmax = ge ? atoi(ge) : CL_MAX;
+            for (int G : {8, CL_MAX, 4, 2}) {  // 8 first: C1 5.3 vs 5.6 us/it at 16
+                if (G > gmax) continue;
+                const int cpb = (int)((nch + G - 1) / G);
+                if (cpb * 32 > 1024) continue;
+                int64_t max_rows = 0;
+                for (int c = 0; c < G; ++c) {
+                    const int64_t a = (int64_t)c * cpb, b = a + cpb < nch ? a + cpb : nch;
+                    if (a >= nch) break;
+                    const int64_t ra = rb[a], rbnd = b < nch ? rb[b] : p->n_rows;
+                    max_rows = rbnd - ra > max_rows ? rbnd - ra : max_rows;
+                }
+                const size_t smem = sizeof(double) * (nch * 32 + 5 * CL_MAX + 4 * 32 + 2 * CL_HIST) +
+                                    (size_t)max_rows * p->rowb;
+                if (smem > 227 * 1024) continue;
+                if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+                    (G > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+                    cudaGetLastError();
+                    continue;
+                }
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(G);
+                cfg.blockDim = dim3(cpb * 32);
+                cfg.dynamicSmemBytes = smem;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = G;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                int clusters = 0;
+                if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters < 1) {
+                    cudaGetLastError();
+                    continue;
+                }
+                p->cl_state = 1, p->cl_G = G, p->cl_cpb = cpb, p->cl_smem = smem;
+                break;
+            }
+        }
+        if (p->cl_state != 1) return false;
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cl_smem));
+        if (p->cl_G > 8) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(p->cl_G);
+        cfg.blockDim = dim3(p->cl_cpb * 32);
+        cfg.dynamicSmemBytes = p->cl_smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = p->cl_G;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SellView v = sell_view(p);
+        int64_t n = p->n_n, n_rows = p->n_rows;
+        const int cpb = p->cl_cpb;
+        CU(cudaLaunchKernelEx(&cfg, kern, v, L, n, iters, cpb, n_rows, x, r, pv, dinv,
+                              (const uint8_t *)p->free_int, ref));
+        bump_launches(1);
+        return true;
+    }
+}
+
 }  // namespace ebs
 
 using namespace ebs;
@@ -793,8 +1083,11 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         int k = 0;
         bool done = false;
         if (P->fused && !cb && iters > 0) {  // the whole loop as one cooperative kernel
-#define EBS_FUSED(NB_, PK_) \
-    { launch_pcg_fused<NB_, PK_>(p, L, iters, xa, r_int, pv, qv, dinv, ref_int, s); }
+#define EBS_FUSED(NB_, PK_)                                                                  \
+    {                                                                                        \
+        if (!launch_pcg_cluster<NB_, PK_>(p, L, iters, xa, r_int, pv, dinv, ref_int, s))     \
+            launch_pcg_fused<NB_, PK_>(p, L, iters, xa, r_int, pv, qv, dinv, ref_int, s);    \
+    }
             EBS_SELL_DISPATCH(p, EBS_FUSED);
 #undef EBS_FUSED
             k = iters;
