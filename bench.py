@@ -515,7 +515,9 @@ def solver_extras(args):
             c1["fused_kernel" if fused else "launch_loop"] = {
                 "iterations": h.iterations, "it_per_s": h.iterations / t,
                 "us_per_it": t / h.iterations * 1e6, "solve_ms": t * 1e3}
-        c1["note"] = "latency-bound (1.1 MB per iteration): no roofline claim"
+        c1["note"] = ("latency-bound (1.1 MB per iteration): no roofline claim; fused_kernel = "
+                      "the whole solve in one thread-block cluster (k_pcg_cluster: slot rows and "
+                      "p in shared memory, DSMEM broadcasts, cluster barriers)")
         out["C1"] = c1
     except Exception as e:  # noqa: BLE001
         out["C1"] = {"error": f"{type(e).__name__}: {e}"}

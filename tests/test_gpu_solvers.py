@@ -196,11 +196,13 @@ def test_jacobi_c4_recipe_reduced(gpu):
 
 @pytest.mark.parametrize("method", ["cg", "pcg"])
 def test_fused_single_kernel_cg_pcg(gpu, method):
-    """fused=True (the whole loop in one kernel: a single thread-block cluster for small
-    2D meshes, else one cooperative grid): same iteration count and solution within 1e-8
-    of the launch-per-step solver (the north-star criterion; the dots are reduced in a
-    different order, which unpreconditioned CG amplifies in the tail of the residual
-    history); tol stop, zero iterations and the divergence flag behave as in _iterate."""
+    """fused=True (the whole loop in one kernel): the cooperative grid kernel reduces the
+    dots in the launch-per-step loop's order, so its histories match to 1e-6; the single
+    thread-block cluster kernel (small 2D meshes) reduces them over its own CTAs, so its
+    histories agree to rounding early on and (unpreconditioned CG amplifies rounding in
+    the tail) loosely later -- both with the same iteration count and solution within
+    1e-8 (the north-star criterion).  Tol stop, zero iterations and the divergence flag
+    behave as in _iterate."""
     import torch
     import paper_1911_03973_b200 as eb
     from paper_1911_03973_b200.inputs import config_problem
@@ -210,11 +212,23 @@ def test_fused_single_kernel_cg_pcg(gpu, method):
         m, b, d = pr["mesh"], pr["batch"], pr["dirichlet"]
         x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
         x1, h1 = run(b, d, x0, 3000, tol=1e-9)
-        x2, h2 = run(b, d, x0, 3000, tol=1e-9, fused=True)
+        n0 = h1.residual_norms[0]
+        os.environ["EBS_NO_CLUSTER"] = "1"
+        try:
+            x6, h6 = run(b, d, x0, 3000, tol=1e-9, fused=True)      # cooperative grid
+        finally:
+            del os.environ["EBS_NO_CLUSTER"]
+        assert len(h6.residual_norms) == len(h1.residual_norms), cfg
+        np.testing.assert_allclose(h6.residual_norms, h1.residual_norms, rtol=1e-6,
+                                   atol=1e-12 * n0)
+        assert float((x6 - x1).norm()) <= 1e-10 * float(x1.norm())
+        x2, h2 = run(b, d, x0, 3000, tol=1e-9, fused=True)          # cluster when it fits
         assert len(h2.residual_norms) == len(h1.residual_norms), cfg
+        np.testing.assert_allclose(h2.residual_norms[:40], h1.residual_norms[:40], rtol=1e-6)
         np.testing.assert_allclose(h2.residual_norms, h1.residual_norms, rtol=1e-6,
-                                   atol=1e-5 * h1.residual_norms[0])
+                                   atol=1e-4 * n0)
         assert float((x2 - x1).norm()) <= 1e-8 * float(x1.norm())
+        assert not h2.diverged
         # fixed count, with reference error norms
         x3, h3 = run(b, d, x0, 25, reference=x1, fused=True)
         x4, h4 = run(b, d, x0, 25, reference=x1)
@@ -222,13 +236,3 @@ def test_fused_single_kernel_cg_pcg(gpu, method):
         np.testing.assert_allclose(h3.error_norms, h4.error_norms, rtol=1e-6)
         x5, h5 = run(b, d, x0, 0, fused=True)
         assert len(h5.residual_norms) == 1 and torch.equal(x5, x0)
-        assert not h2.diverged
-        # small 2D meshes run as one thread-block cluster (k_pcg_cluster); the cooperative
-        # grid kernel (EBS_NO_CLUSTER) gives the same iterations and solution
-        os.environ["EBS_NO_CLUSTER"] = "1"
-        try:
-            x6, h6 = run(b, d, x0, 3000, tol=1e-9, fused=True)
-        finally:
-            del os.environ["EBS_NO_CLUSTER"]
-        assert len(h6.residual_norms) == len(h2.residual_norms), cfg
-        assert float((x6 - x2).norm()) <= 1e-8 * float(x2.norm())
