@@ -551,21 +551,56 @@ void launch_pcg_fused(Plan *p, const LoopArgs &L, int iters, double *x, double *
 // ------------------------------------------- single-cluster CG / PCG (small meshes) --
 // pcg/cg(fused=True) on a mesh whose slot stream fits the shared memory of one thread-
 // block cluster (8, else up to 16 CTAs on as many SMs; C1: 4225 nodes, 715 KB of slot
-// rows; 5.3 us per iteration vs 11.6 for the cooperative grid kernel): CTA c
+// rows; 4.8 us per iteration vs 11.8 for the cooperative grid kernel): CTA c
 // copies the slot rows of its chunks and a full copy of p into its shared memory once,
 // then every iteration runs from on-chip memory --
 //   A  q = mask(A p) for its own nodes (slot rows and x gathers from shared memory; each
 //      thread keeps its node's x, r, p, diag^-1 in registers), p.q block partial
-//      broadcast into every CTA's partial array (DSMEM stores)           | cluster barrier
+//      broadcast into every CTA's partial array                         | wait mbarrier A
 //   B  alpha from the partials summed in rank order (the same in every CTA); x, r
-//      update, r.r / r.z / error / non-finite partials broadcast          | cluster barrier
+//      update, r.r / r.z / error / non-finite partials broadcast          | wait mbarrier B
 //   C  the _iterate rules, beta; p = z + beta p written into every CTA's copy of p
-//                                                                         | cluster barrier
+//                                                                         | wait mbarrier C
+// The broadcasts are st.async DSMEM stores that complete transaction bytes on the
+// receiving CTA's mbarrier, so each CTA waits only for the data it needs -- no
+// cluster-wide barrier and fence per phase (C1: 693 -> 621 us per solve in-kernel).
+// Reuse is safe without barriers: a CTA sends phase-X data of iteration k+1 only after
+// it has received everyone's phase-C data of iteration k, which every CTA sends after
+// reading its phase-X data of iteration k.
 // -- no global-memory traffic or grid-wide barriers inside the loop.  The row sums are
 // sell_node_sum's (same order, same bits); the dots are reduced over the cluster in a
 // fixed order (deterministic; equal to the other loops up to rounding).
 constexpr int CL_MAX = 16;
 constexpr int CL_HIST = 512;  // history entries buffered in shared memory
+
+#ifndef EBS_CLUSTER_MBAR
+#define EBS_CLUSTER_MBAR 1  // DSMEM st.async + per-CTA mbarriers instead of cluster barriers
+#endif
+
+__device__ __forceinline__ uint32_t cl_mapa(const void *p, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(r)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+    return r;
+}
+// 8 B store into another CTA's shared memory, completing 8 tx bytes on its mbarrier
+__device__ __forceinline__ void cl_st_async(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "CLW_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra CLW_%=;\n"
+        "}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+        "r"(parity)
+        : "memory");
+}
 
 // history entries k-cnt+1 .. k (1-based iteration index) from the buffer to global
 __device__ __forceinline__ void flush_hist(const LoopArgs &L, const double *hist, int k, int cnt) {
@@ -632,6 +667,12 @@ __global__ void __launch_bounds__(1024, 1)
     double *sm = pB + 4 * CL_MAX;                  // [4 * 32]      block_sum scratch
     double *hist = sm + 4 * 32;                    // [2 * CL_HIST] norms / errors, flushed
     uint8_t *rows = reinterpret_cast<uint8_t *>(hist + 2 * CL_HIST);
+    __shared__ uint64_t mbar[3];  // A: p.q partials, B: four partials, C: the new p
+    if (EBS_CLUSTER_MBAR && threadIdx.x == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(&mbar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t phase = 0;  // parity bit per barrier
     const int64_t c0 = (int64_t)me * cpb;
     const int64_t c1 = c0 + cpb < v.n_chunks ? c0 + cpb : v.n_chunks;
     const int64_t r0 = c0 < v.n_chunks ? v.rowbase[c0] : n_rows;
@@ -670,11 +711,21 @@ __global__ void __launch_bounds__(1024, 1)
         }
         double a1[1] = {pm * qm};
         block_sum<1>(a1, sm);
-        if (wib == 0) {  // block total (lane 0 of warp 0) -> slot `me` of every CTA's pA
-            const double tv = __shfl_sync(0xffffffffu, a1[0], 0);
-            if (lane < G) *cl.map_shared_rank(pA + me, lane) = tv;
+        if (EBS_CLUSTER_MBAR) {
+            if (threadIdx.x == 0) mbar_expect_tx(&mbar[0], 8u * G);
+            if (wib == 0) {  // block total -> slot `me` of every CTA's pA, signalling its barrier
+                const double tv = __shfl_sync(0xffffffffu, a1[0], 0);
+                if (lane < G) cl_st_async(cl_mapa(pA + me, lane), tv, cl_mapa(&mbar[0], lane));
+            }
+            cl_wait(&mbar[0], phase & 1u);
+            phase ^= 1u;
+        } else {
+            if (wib == 0) {  // block total (lane 0 of warp 0) -> slot `me` of every CTA's pA
+                const double tv = __shfl_sync(0xffffffffu, a1[0], 0);
+                if (lane < G) *cl.map_shared_rank(pA + me, lane) = tv;
+            }
+            cl.sync();
         }
-        cl.sync();
         double pq = 0.0;
         for (int t = 0; t < G; ++t) pq += pA[t];
         const double alpha = pq != 0.0 ? rz / pq : 0.0;
@@ -692,14 +743,28 @@ __global__ void __launch_bounds__(1024, 1)
             part[3] = isfinite(xm) ? 0.0 : 1.0;
         }
         block_sum<4>(part, sm);
-        if (wib == 0) {
+        if (EBS_CLUSTER_MBAR) {
+            if (threadIdx.x == 0) mbar_expect_tx(&mbar[1], 32u * G);
+            if (wib == 0) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double tv = __shfl_sync(0xffffffffu, part[q], 0);
-                if (lane < G) *cl.map_shared_rank(pB + q * CL_MAX + me, lane) = tv;
+                for (int q = 0; q < 4; ++q) {
+                    const double tv = __shfl_sync(0xffffffffu, part[q], 0);
+                    if (lane < G)
+                        cl_st_async(cl_mapa(pB + q * CL_MAX + me, lane), tv, cl_mapa(&mbar[1], lane));
+                }
             }
+            cl_wait(&mbar[1], (phase >> 1) & 1u);
+            phase ^= 2u;
+        } else {
+            if (wib == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double tv = __shfl_sync(0xffffffffu, part[q], 0);
+                    if (lane < G) *cl.map_shared_rank(pB + q * CL_MAX + me, lane) = tv;
+                }
+            }
+            cl.sync();
         }
-        cl.sync();
         double tot[4] = {0.0, 0.0, 0.0, 0.0};
         for (int t = 0; t < G; ++t)
 #pragma unroll
@@ -727,11 +792,18 @@ __global__ void __launch_bounds__(1024, 1)
         const double beta = rz != 0.0 ? tot[1] / rz : 0.0;
         rz = tot[1];
         if (k == iters) break;  // the last direction update would be unused
-        if (mine) {
-            pm = dm * rm + beta * pm;
-            for (int t = 0; t < G; ++t) *cl.map_shared_rank(ps + m, t) = pm;
+        if (mine) pm = dm * rm + beta * pm;
+        if (EBS_CLUSTER_MBAR) {  // every node's p into every CTA's copy: 8 n bytes per CTA
+            if (threadIdx.x == 0) mbar_expect_tx(&mbar[2], (uint32_t)(8 * n));
+            if (mine)
+                for (int t = 0; t < G; ++t) cl_st_async(cl_mapa(ps + m, t), pm, cl_mapa(&mbar[2], t));
+            cl_wait(&mbar[2], (phase >> 2) & 1u);
+            phase ^= 4u;
+        } else {
+            if (mine)
+                for (int t = 0; t < G; ++t) *cl.map_shared_rank(ps + m, t) = pm;
+            cl.sync();
         }
-        cl.sync();
     }
     if (mine) {
         x[m] = xm;
