@@ -115,7 +115,10 @@ int ebs_plan_create(int nb, int64_t n_nodes, int64_t n_elems, const int32_t *con
                     void *stream, ebs_plan_t *out);
 int ebs_plan_destroy(ebs_plan_t plan);
 /* info[0]=n_nodes info[1]=n_elems info[2]=nb info[3]=n_chunks info[4]=n_rows
- * info[5]=slot bytes resident  info[6]=max valence  info[7]=loaded flags */
+ * info[5]=slot bytes resident  info[6]=max valence  info[7]=flags:
+ *   1 operator loaded, 2 b_e loaded, 4 packed-delta ids, 8 per-chunk delta tables,
+ *   16 two-base 3D rows, 32 one-byte tuple codes, 64 identity numbering (the caller's
+ *   numbering is a structured grid and is kept as the internal one) */
 int ebs_plan_info(ebs_plan_t plan, int64_t *info);
 /* copy the internal numbering maps out (device int32 arrays of n_nodes) */
 int ebs_plan_node_maps(ebs_plan_t plan, int32_t *new_of_old, int32_t *old_of_new,
