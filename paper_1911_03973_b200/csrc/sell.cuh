@@ -130,6 +130,47 @@ __device__ __forceinline__ double pick(int t, double xo, const double (&g)[NB - 
     return v;
 }
 
+// The slot's row product in vertex order, loc = ((A0*X0 + A1*X1) + A2*X2) [+ A3*X3] with
+// X_j = xo and the other X_i = g[(i - j - 1) mod NB] (operators.py:69 einsum order).
+template <int NB>
+__device__ __forceinline__ double row_product_sel(int j, const double (&a)[NB], double xo,
+                                                  const double (&g)[NB - 1]) {
+    double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
+#pragma unroll
+    for (int i = 1; i < NB; ++i) loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
+    return loc;
+}
+
+// Same bits with a branch per local vertex j instead of per-operand selects (~24 FSEL
+// per 3D slot): a node's slots are sorted by j, and on structured meshes every interior
+// node has the same number of slots per j, so j is warp-uniform in nearly every row.
+// 3D rows hold boundary nodes more often (a chunk straddles an x-row end), so there the
+// branch is taken only when j is uniform over the active lanes.  Measured: C3 2980 ->
+// 3130, C5 361 -> 369, C4 1656 -> 1720 it/s, C2 internal matvec 126 -> 121 us.  SW =
+// false (the bit-exact residual, which spills at 32 registers with the branches): selects.
+#ifndef EBS_ROW_SWITCH
+#define EBS_ROW_SWITCH 1
+#endif
+template <int NB, bool SW = true>
+__device__ __forceinline__ double row_product(int j, const double (&a)[NB], double xo,
+                                              const double (&g)[NB - 1]) {
+    if constexpr (!SW || !EBS_ROW_SWITCH) {
+        return row_product_sel<NB>(j, a, xo, g);
+    } else if constexpr (NB == 3) {
+        if (j == 0) return (a[0] * xo + a[1] * g[0]) + a[2] * g[1];
+        if (j == 1) return (a[0] * g[1] + a[1] * xo) + a[2] * g[0];
+        return (a[0] * g[0] + a[1] * g[1]) + a[2] * xo;
+    } else {
+        const unsigned am = __activemask();
+        const int j0 = __shfl_sync(am, j, __ffs(am) - 1);
+        if (!__all_sync(am, j == j0)) return row_product_sel<NB>(j, a, xo, g);
+        if (j == 0) return ((a[0] * xo + a[1] * g[0]) + a[2] * g[1]) + a[3] * g[2];
+        if (j == 1) return ((a[0] * g[2] + a[1] * xo) + a[2] * g[0]) + a[3] * g[1];
+        if (j == 2) return ((a[0] * g[1] + a[1] * g[2]) + a[2] * xo) + a[3] * g[0];
+        return ((a[0] * g[0] + a[1] * g[1]) + a[2] * g[2]) + a[3] * xo;
+    }
+}
+
 // Ordered slot sum of one node.  EXACT: sum of (b_e - loc); else sum of loc.
 // `w` is the chunk width (warp-uniform), `c_m` this lane's valence, xo = x[m].
 #ifndef EBS_U2
@@ -235,10 +276,7 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
         for (int u = 0; u < U; ++u) {
             if (k0 + u < c_m) {
                 const int j = jj[u];
-                double loc = a[u][0] * pick<NB>((NB - j - 1) % NB, xo, g[u]);
-#pragma unroll
-                for (int i = 1; i < NB; ++i)
-                    loc = loc + a[u][i] * pick<NB>((i - j - 1 + NB) % NB, xo, g[u]);
+                const double loc = row_product<NB, !EXACT>(j, a[u], xo, g[u]);
                 if constexpr (EXACT) s = s + (be[u] - loc);
                 else s = s + loc;
             }
@@ -303,9 +341,7 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
             double be = 0.0;
             if constexpr (EXACT) be = __ldcs(v.be + (row0 + k) * LANES + lane);
             if (k + 1 < c_m) nxt.load(v, row0 + k + 1, lane);
-            double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
-#pragma unroll
-            for (int i = 1; i < NB; ++i) loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
+            const double loc = row_product<NB, !EXACT>(j, a, xo, g);
             if constexpr (EXACT) s = s + (be - loc);
             else s = s + loc;
         }
@@ -503,10 +539,7 @@ __device__ __forceinline__ void sell_sweep_tma(const SellView &v, const double *
                         double g[NB - 1];
 #pragma unroll
                         for (int t = 0; t < NB - 1; ++t) g[t] = __ldg(x + nid[t]);
-                        double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
-#pragma unroll
-                        for (int i = 1; i < NB; ++i)
-                            loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
+                        const double loc = row_product<NB, !EXACT>(j, a, xo, g);
                         if constexpr (EXACT)
                             sum = sum + (__ldcs(v.be + (row0 + k) * LANES + lane) - loc);
                         else

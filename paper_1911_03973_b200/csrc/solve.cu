@@ -639,10 +639,7 @@ __device__ __forceinline__ double smem_node_sum(const uint8_t *rows, int rowb, i
             double g[NB - 1];
 #pragma unroll
             for (int t = 0; t < NB - 1; ++t) g[t] = ps[nid[t]];
-            double loc = a[0] * pick<NB>((NB - j - 1) % NB, xo, g);
-#pragma unroll
-            for (int i = 1; i < NB; ++i) loc = loc + a[i] * pick<NB>((i - j - 1 + NB) % NB, xo, g);
-            s = s + loc;
+            s = s + row_product<NB>(j, a, xo, g);
         }
     }
     return s;
