@@ -45,17 +45,13 @@ static int grid_mode() {
 }
 static bool grid_enabled() { return grid_mode() != 0; }
 
-// IDS_TUPLE codes: 3D plans up to EBS_TUPLE_MAX_NODES nodes (default 4M, vectors well
-// inside L2: C3 2859 -> 3020 it/s; C5 at 17M nodes 362 -> 352 and 2D kernels lose);
-// EBS_IDS_GRID=2 turns them off, =3 forces them on every structured plan (tests)
-static bool tuple_wanted(int nb, int64_t n_n) {
-    static const int64_t cap = [] {
-        const char *e = getenv("EBS_TUPLE_MAX_NODES");
-        return e ? (int64_t)atoll(e) : (int64_t)(4ll << 20);
-    }();
+// IDS_TUPLE codes on 3D structured plans (with the row-product branch: C3 2818 -> 3115,
+// C5 369 -> 393 it/s); 2D plans keep the 4 B delta word.  EBS_IDS_GRID=2 turns the codes
+// off, =3 forces them on every structured plan (tests)
+static bool tuple_wanted(int nb, int64_t) {
     if (grid_mode() == 2) return false;
     if (grid_mode() == 3) return true;
-    return nb == 4 && n_n <= cap;
+    return nb == 4;
 }
 
 // ------------------------------------------------------------- build kernels --
