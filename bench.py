@@ -251,8 +251,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         launches = lib.ebs_launch_count() - n0
         total = e0.elapsed_time(e1) / 1e3
-        # per-kernel pass: the same two kernels called separately (the -0.0 pre-fill of r
-        # that ebs_residual fuses into the x permutation is done outside the events)
+        # per-step pass: the same two kernels called separately with events around each
+        # step (the -0.0 pre-fill of r that ebs_residual runs is done outside the events)
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
         for k in range(K):
             r_dev.fill_(-0.0)
@@ -262,10 +262,12 @@ def run_ours(args):
             lib.ebs_plan_apply(h, op, xip, rp, 2, 0, s)
             evs[k][2].record(stream)
         torch.cuda.synchronize()
-        gather = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
-        sell = statistics.mean(ev[1].elapsed_time(ev[2]) for ev in evs) / 1e3
         per_step = sorted(ev[0].elapsed_time(ev[2]) for ev in evs)
         unit_stats.update(median_ms=statistics.median(per_step), best_ms=per_step[0])
+        # per-kernel durations inside the step sequence: the median over the K steps (the
+        # mean would count the rare host gaps of an eager launch loop)
+        gather = statistics.median(ev[0].elapsed_time(ev[1]) for ev in evs) / 1e3
+        sell = statistics.median(ev[1].elapsed_time(ev[2]) for ev in evs) / 1e3
         return total, gather, sell, launches
 
     # warm-up: W steps, then keep the clocks busy for ~1 s before timing
@@ -414,7 +416,9 @@ def run_ours(args):
                            "with r := -0.0 fused, SELL pass adding into r) replayed from a "
                            "captured CUDA graph of 10 steps; eager: one ctypes call per step; "
                            "per_step_events_ms: the unfused split (ebs_to_internal, "
-                           "ebs_plan_apply out_user=2) with events around each launch"},
+                           "ebs_plan_apply out_user=2) with events around each launch; "
+                           "roofline.kernel_ms / gather_kernel_ms: the medians of those "
+                           "per-launch intervals"},
         "internal_matvec": {"kernel_ms": t_int * 1e3,
                             "achieved_gbs": (bytes_alg - 8 * n_n) / t_int / 1e9,
                             "frac": (bytes_alg - 8 * n_n) / t_int / 1e9 / peak,
