@@ -1,3 +1,5 @@
+"""C1 Jacobi-PCG to 1e-8 with fused=True: solve time and the CUPTI kernel list (the
+single-cluster kernel, or the cooperative one with EBS_NO_CLUSTER=1)."""
 import sys, os, collections
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import torch

@@ -1,3 +1,6 @@
+"""ncu target: builds a BASELINE config (argv[1], default 5) and runs two short PCG solves
+(6 iterations each), e.g. `ncu --set full -k regex:k_pcg_ -s 6 -c 3 python
+scripts/pcg_ncu_target.py 5`."""
 import sys, os
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import torch

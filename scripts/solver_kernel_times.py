@@ -1,3 +1,6 @@
+"""Warm per-kernel times of a PCG solve (torch.profiler / CUPTI, 100 iterations) and the
+solve rate, for BASELINE config argv[1] (3 or 5): `EBS_IDS_GRID=2|3 python
+scripts/solver_kernel_times.py 5` compares id codings."""
 import sys, os, collections
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import torch
