@@ -613,7 +613,8 @@ __device__ __forceinline__ void flush_hist(const LoopArgs &L, const double *hist
 template <int NB, int IDS>
 __device__ __forceinline__ double smem_node_sum(const uint8_t *rows, int rowb, int64_t rrel,
                                                 int w, int lane, int64_t m, int c_m,
-                                                const double *ps, double xo) {
+                                                const double *ps, double xo,
+                                                const uint8_t *codes, const int4 *tab) {
     double s = 0.0;
     for (int k = 0; k < w; ++k) {
         if (k < c_m) {
@@ -624,7 +625,13 @@ __device__ __forceinline__ double smem_node_sum(const uint8_t *rows, int rowb, i
             for (int i = 0; i < NB; ++i) a[i] = ap[i * LANES];
             int32_t nid[NB - 1];
             int j;
-            if constexpr (IDS == IDS_DELTA) {
+            if constexpr (IDS == IDS_TUPLE) {
+                const int4 tp = tab[codes[(rrel + k) * LANES + lane]];
+                j = tp.x;
+                nid[0] = (int32_t)m + tp.y;
+                nid[1] = (int32_t)m + tp.z;
+                if constexpr (NB == 4) nid[2] = (int32_t)m + tp.w;
+            } else if constexpr (IDS == IDS_DELTA) {
                 using W = typename Pack<NB>::W;
                 const W wd = reinterpret_cast<const W *>(rp + NB * 256)[lane];
                 j = Pack<NB>::j(wd);
@@ -663,7 +670,8 @@ __global__ void __launch_bounds__(1024, 1)
     double *pB = pA + CL_MAX;                      // [4 * CL_MAX]  r.r, r.z, err, non-finite
     double *sm = pB + 4 * CL_MAX;                  // [4 * 32]      block_sum scratch
     double *hist = sm + 4 * 32;                    // [2 * CL_HIST] norms / errors, flushed
-    uint8_t *rows = reinterpret_cast<uint8_t *>(hist + 2 * CL_HIST);
+    int4 *tabs = reinterpret_cast<int4 *>(hist + 2 * CL_HIST);  // [TUPLE_CAP] (IDS_TUPLE)
+    uint8_t *rows = reinterpret_cast<uint8_t *>(tabs + TUPLE_CAP);
     __shared__ uint64_t mbar[3];  // A: p.q partials, B: four partials, C: the new p
     if (EBS_CLUSTER_MBAR && threadIdx.x == 0) {
         for (int i = 0; i < 3; ++i) mbar_init(&mbar[i], 1);
@@ -680,7 +688,14 @@ __global__ void __launch_bounds__(1024, 1)
         const int64_t n16 = (r1 - r0) * v.rowb / 16;
         for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
         for (int64_t i = threadIdx.x; i < npad; i += blockDim.x) ps[i] = i < n ? p[i] : 0.0;
+        if constexpr (IDS == IDS_TUPLE) {  // the row codes (32 B per row) and the table
+            const int4 *cs = reinterpret_cast<const int4 *>(v.codes + r0 * LANES);
+            int4 *cd = reinterpret_cast<int4 *>(rows + (r1 - r0) * v.rowb);
+            for (int64_t i = threadIdx.x; i < (r1 - r0) * 2; i += blockDim.x) cd[i] = cs[i];
+            for (int i = threadIdx.x; i < TUPLE_CAP; i += blockDim.x) tabs[i] = v.tup[i];
+        }
     }
+    const uint8_t *codes = rows + (r1 - r0) * v.rowb;
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c = c0 + wib;
     const int64_t m = c * LANES + lane;
@@ -703,7 +718,8 @@ __global__ void __launch_bounds__(1024, 1)
         // A: q = mask(A p), p.q
         double qm = 0.0;
         {
-            const double s = smem_node_sum<NB, IDS>(rows, v.rowb, rrel, w, lane, m, c_m, ps, pm);
+            const double s = smem_node_sum<NB, IDS>(rows, v.rowb, rrel, w, lane, m, c_m, ps, pm,
+                                                    codes, tabs);
             if (mine) qm = fm ? s : 0.0;
         }
         double a1[1] = {pm * qm};
@@ -828,7 +844,7 @@ template <int NB, int IDS>
 bool launch_pcg_cluster(Plan *p, const LoopArgs &L, int iters, double *x, double *r, double *pv,
                         const double *dinv, const double *ref, cudaStream_t s) {
     if (!EBS_PCG_CLUSTER || getenv("EBS_NO_CLUSTER")) return false;
-    if constexpr (IDS != IDS_DELTA && IDS != IDS_ABS) {
+    if constexpr (IDS != IDS_DELTA && IDS != IDS_ABS && IDS != IDS_TUPLE) {
         return false;
     } else {
         auto kern = k_pcg_cluster<NB, IDS>;
@@ -853,7 +869,8 @@ bool launch_pcg_cluster(Plan *p, const LoopArgs &L, int iters, double *x, double
                     max_rows = rbnd - ra > max_rows ? rbnd - ra : max_rows;
                 }
                 const size_t smem = sizeof(double) * (nch * 32 + 5 * CL_MAX + 4 * 32 + 2 * CL_HIST) +
-                                    (size_t)max_rows * p->rowb;
+                                    sizeof(int4) * TUPLE_CAP +
+                                    (size_t)max_rows * (p->rowb + (IDS == IDS_TUPLE ? LANES : 0));
                 if (smem > 227 * 1024) continue;
                 if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
                     (G > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
