@@ -288,13 +288,16 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
 // Raw id word(s) of one slot and their decoding (IDS_DELTA / IDS_ABS).
 template <int NB, int IDS>
 struct IdWord {
-    static_assert(IDS == IDS_DELTA || IDS == IDS_ABS, "one-slot-ahead ids: DELTA / ABS only");
+    static_assert(IDS == IDS_DELTA || IDS == IDS_ABS || IDS == IDS_TUPLE,
+                  "one-slot-ahead ids: DELTA / ABS / TUPLE only");
     using W = typename Pack<NB>::W;
     W w;
     int32_t a[NB - 1];
     __device__ __forceinline__ void load(const SellView &v, int64_t row, int lane) {
         const uint8_t *rp = v.slot + row * v.rowb;
-        if constexpr (IDS == IDS_DELTA) {
+        if constexpr (IDS == IDS_TUPLE) {
+            w = (W)__ldcs(v.codes + row * LANES + lane);
+        } else if constexpr (IDS == IDS_DELTA) {
             w = __ldcs(reinterpret_cast<const W *>(rp + NB * 256) + lane);
         } else {
             const int32_t *ip = reinterpret_cast<const int32_t *>(rp + NB * 256) + lane;
@@ -302,8 +305,15 @@ struct IdWord {
             for (int t = 0; t < NB - 1; ++t) a[t] = __ldcs(ip + t * LANES);
         }
     }
-    __device__ __forceinline__ int decode(const SellView &, int64_t m, int32_t (&nid)[NB - 1]) const {
-        if constexpr (IDS == IDS_DELTA) {
+    __device__ __forceinline__ int decode(const SellView &, int64_t m, int32_t (&nid)[NB - 1],
+                                          const int32_t *stab) const {
+        if constexpr (IDS == IDS_TUPLE) {
+            const int4 tp = reinterpret_cast<const int4 *>(stab)[(int)w];
+            nid[0] = (int32_t)m + tp.y;
+            nid[1] = (int32_t)m + tp.z;
+            if constexpr (NB == 4) nid[2] = (int32_t)m + tp.w;
+            return tp.x;
+        } else if constexpr (IDS == IDS_DELTA) {
 #pragma unroll
             for (int t = 0; t < NB - 1; ++t) nid[t] = (int32_t)(m + Pack<NB>::d(w, t));
             return Pack<NB>::j(w);
@@ -321,7 +331,8 @@ struct IdWord {
 template <int NB, int IDS, bool EXACT>
 __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t row0, int w,
                                                      int lane, int64_t m, int c_m,
-                                                     const double *__restrict__ x, double xo) {
+                                                     const double *__restrict__ x, double xo,
+                                                     const int32_t *stab) {
     double s = 0.0;
     IdWord<NB, IDS> nxt;
     if (0 < c_m) nxt.load(v, row0, lane);
@@ -330,7 +341,7 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
             const IdWord<NB, IDS> cur = nxt;
             const uint8_t *rp = v.slot + (row0 + k) * v.rowb;
             int32_t nid[NB - 1];
-            const int j = cur.decode(v, m, nid);
+            const int j = cur.decode(v, m, nid, stab);
             double g[NB - 1];
 #pragma unroll
             for (int t = 0; t < NB - 1; ++t) g[t] = __ldg(x + nid[t]);
@@ -349,6 +360,10 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
     return s;
 }
 
+
+#ifndef EBS_TUPLE_PIPE
+#define EBS_TUPLE_PIPE 1
+#endif  // tuple-coded plans: codes one slot ahead (see PIPE below)
 
 // Grid-stride sweep over chunks: epi(m, s, xo) for every valid node (direct loads).
 template <int NB, int IDS, bool EXACT, bool PIPE, class Epi>
@@ -377,9 +392,10 @@ __device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *
         const int c_m = valid ? (v.cnt8 ? (int)v.cnt8[m] : v.cnt[m]) : 0;
         const double xo = valid ? x[m] : 0.0;
         double s;
-        if constexpr (PIPE && IDS != IDS_TABLE && IDS != IDS_TUPLE && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
+        if constexpr ((PIPE || (IDS == IDS_TUPLE && EBS_TUPLE_PIPE)) && IDS != IDS_TABLE &&
+                      IDS != IDS_DELTA2 && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
             s = sell_node_sum_pipe<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m, c_m, x,
-                                                   xo);
+                                                   xo, stab);
         else
             s = sell_node_sum<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m, c_m, x, xo,
                                               stab);
@@ -564,8 +580,11 @@ __device__ __forceinline__ void sell_sweep_tma(const SellView &v, const double *
 #define EBS_SELL_BOUNDS(NB) __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
 #endif
 
-// PIPE: load the id plane one slot ahead (sell_node_sum_pipe) -- measured faster only
-// for the 2D Jacobi step, slower for the other kernels (profiles/README.md)
+// PIPE: load the id plane one slot ahead (sell_node_sum_pipe) -- measured faster for the
+// 2D Jacobi step, slower for the other delta-coded kernels (profiles/README.md).  Tuple-
+// coded plans always run it (EBS_TUPLE_PIPE): the one-byte code of slot k+1 is loaded
+// while slot k is processed, so the table lookup and the gathers start at once -- C5 PCG
+// matvec 2239 -> 2072 us (392 -> 423 it/s), C3 290 -> 272 us.
 template <int NB, int IDS, bool EXACT, bool PIPE = false, class Epi>
 __device__ __forceinline__ void sell_sweep(const SellView &v, const double *__restrict__ x,
                                            Epi &epi) {
