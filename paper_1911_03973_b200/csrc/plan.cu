@@ -45,14 +45,10 @@ static int grid_mode() {
 }
 static bool grid_enabled() { return grid_mode() != 0; }
 
-// IDS_TUPLE codes on 3D structured plans (with the row-product branch: C3 2818 -> 3115,
-// C5 369 -> 393 it/s); 2D plans keep the 4 B delta word.  EBS_IDS_GRID=2 turns the codes
-// off, =3 forces them on every structured plan (tests)
-static bool tuple_wanted(int nb, int64_t) {
-    if (grid_mode() == 2) return false;
-    if (grid_mode() == 3) return true;
-    return nb == 4;
-}
+// IDS_TUPLE codes on structured plans (loaded a slot ahead, with the row-product
+// branch: C3 2818 -> 3340, C5 369 -> 424 it/s; 2D paper experiment 6.05 -> 5.94 ms).
+// EBS_IDS_GRID=2 turns them off (packed deltas), =3 forces them (tests)
+static bool tuple_wanted(int, int64_t) { return grid_mode() != 2; }
 
 // ------------------------------------------------------------- build kernels --
 __global__ void k_incidence(int nb, int64_t n_n, int64_t n_e, const int32_t *__restrict__ conn,

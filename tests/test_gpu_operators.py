@@ -157,8 +157,8 @@ print("FLAGS", flags)
 def test_plan_keeps_structured_numbering(gpu, dim, mode):
     """Unpermuted generated grids: every (neighbour - node) difference is a +-1
     combination of axis strides, so the plan keeps the caller's numbering (identity maps)
-    -- with packed-delta ids (EBS_IDS_GRID=2), one-byte tuple codes (=3), or the default
-    choice (tuples for small 3D plans).  Residual / matvec bitwise, PCG vs the oracle."""
+    -- with packed-delta ids (EBS_IDS_GRID=2) or one-byte tuple codes (default, =3).
+    Residual / matvec bitwise, PCG vs the oracle."""
     import os
     import subprocess
     import sys
@@ -172,7 +172,7 @@ def test_plan_keeps_structured_numbering(gpu, dim, mode):
     assert out.returncode == 0, out.stderr[-3000:]
     flags = int(out.stdout.split("FLAGS")[1])
     assert flags & 64                                  # identity numbering
-    tuples = mode == "3" or (mode == "" and dim == 3)
+    tuples = mode != "2"
     assert bool(flags & 32) == tuples
 
 
