@@ -12,9 +12,13 @@
 // row of each lane's slot) followed by one id plane: per lane the local vertex j and the
 // other vertices of the element (cyclic from j+1) as deltas to m packed in 32 bits (2D,
 // 2 x 15 bit) or 64 bits (3D, 3 x 20 bit); meshes whose internal numbering is not local
-// enough fall back to absolute int32 ids (NB-1 planes).  A warp streams 256 B per plane,
-// fully coalesced, with evict-first loads; only the x gathers go through L1/L2, and they
-// hit because the internal numbering keeps a chunk's neighbours within a few lines.
+// enough fall back to absolute int32 ids (NB-1 planes).  Structured caller numberings
+// (kept as the internal one) drop the id plane for one byte per slot indexing the plan's
+// table of (j, differences) tuples (IDS_TUPLE, loaded one slot ahead).  A warp streams
+// 256 B per plane, fully coalesced, with evict-first loads; only the x gathers go
+// through L1/L2, and they hit because the internal numbering keeps a chunk's neighbours
+// within a few lines.  The sweeps are close to issue-bound: per slot, decode and
+// operand selection cost as much as the bytes (row_product branches on j).
 //
 // Kernels are persistent: a fixed grid (occupancy-sized, so per-launch reductions have
 // a fixed, deterministic order) of warps sweeps the chunks grid-stride.
