@@ -44,9 +44,26 @@ struct OpEpi {
     }
 };
 
+// Programmatic dependent launch: the SELL pass is launched with programmatic stream
+// serialisation, so its CTAs are scheduled while the kernel before it (the -0.0 fill,
+// which triggers at its start) drains; griddepcontrol.wait then blocks until that grid
+// has completed and its writes are visible.  Without the attribute the wait is a no-op.
+// EBS_PDL=0 in the environment launches it the plain way (A/B in profiles/README.md).
+static bool use_pdl() {
+    static const bool v = [] {
+        const char *e = getenv("EBS_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 template <int NB, int IDS, int MODE>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_sell_op(SellView v, const double *__restrict__ x, OpEpi epi) {
+    pdl_wait();
     sell_sweep<NB, IDS, MODE == 2>(v, x, epi);
 }
 
@@ -56,7 +73,21 @@ void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cuda
     auto kern = k_sell_op<NB, IDS, MODE>;
     const SellView v = sell_view(p, chunks, n_list);
     const SellLaunch SL = sell_launch((const void *)kern, NB, p->rowb, v.nlist);
-    kern<<<SL.grid, SL.block, SL.smem, s>>>(v, x_int, epi);
+    if (use_pdl()) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(SL.grid);
+        cfg.blockDim = dim3(SL.block);
+        cfg.dynamicSmemBytes = SL.smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, v, x_int, epi);
+    } else {
+        kern<<<SL.grid, SL.block, SL.smem, s>>>(v, x_int, epi);
+    }
     LAUNCHED();
 }
 
@@ -144,6 +175,7 @@ static bool use_perm2(const Plan *p) {
 // The -0.0 pre-fill of a red-mode output runs as its own kernel after the x permutation:
 // fusing the stores into the latency-bound gather, or running it first, measured slower.
 __global__ void k_fill(int64_t n, double value, double *__restrict__ out) {
+    pdl_trigger();  // a PDL-launched SELL pass may be scheduled now (it still waits)
     const int64_t head = (reinterpret_cast<uintptr_t>(out) & 15) ? 1 : 0;
     const int64_t n2 = n > head ? (n - head) / 2 : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
