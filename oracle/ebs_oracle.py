@@ -31,7 +31,7 @@ __all__ = [
     "detect_face_z0", "signed_measure", "jitter_interior", "permute_mesh",
     "element_matrices", "centroids", "assemble_rhs", "local_residuals",
     "residual", "matvec_masked", "diagonal", "mask", "initial_guess",
-    "richardson", "jacobi", "pcg", "cg", "element_slabs", "halo_maps",
+    "richardson", "jacobi", "pcg", "cg", "StreamedOperator", "element_slabs", "halo_maps",
     "first_appearance_order", "delta_alphabet", "grid_strides", "plan_numbering", "node_slots", "config_inputs",
     "chebyshev_roots", "chebyshev2", "chebyshev3", "chebyshev3_coefficients",
     "model_eigen_bounds", "power_iteration_lambda_max", "mass_gershgorin", "operator_bounds",
@@ -254,6 +254,90 @@ def element_matrices(nodes, elements, nu=0.0, f=None, f_vals=None):
 
 # --------------------------------------------------------------- operators
 
+class StreamedOperator:
+    """RESTATEMENT for meshes whose whole-mesh element arrays are too large to
+    build at once on the host (BASELINE C4 / C5 at full size): the operator of
+    element_matrices(nodes, elements, nu, f_vals) evaluated chunk by chunk.
+
+    * Each element's K/M/A/b_e depend only on its own nodes, so building them for
+      an element range [lo, hi) gives bit-identical entries to the whole-mesh
+      call (elements.py:56-137 is elementwise).
+    * The per-element local products of every chunk go into ONE (n_b, n_e) array
+      that is reduced by ONE bincount over indt -- exactly the reference's
+      threaded deterministic mode (operators.py:96-107: chunk-local residuals,
+      concatenated, one bincount), so residual / matvec_masked / diagonal are
+      bitwise identical to the whole-mesh functions, in the same (j, e) order.
+    * Chunks run on a thread pool (NumPy releases the GIL in its loops); element
+      matrices are kept per chunk when ``cache`` (C5: 12.9 GB of A_e), else
+      rebuilt on every pass.
+
+    Pass it as ``A_e`` to residual / matvec_masked / diagonal / pcg / jacobi
+    (b_e and indt arguments are then ignored in favour of the operator's own)."""
+
+    def __init__(self, nodes, elements, nu=0.0, f_vals=None, chunk=1 << 21, threads=None,
+                 cache=True):
+        import os
+        self.nodes = nodes
+        self.elements = elements
+        self.nu = nu
+        self.f_vals = f_vals
+        self.n = nodes.shape[0]
+        self.nb = elements.shape[1]
+        self.n_e = elements.shape[0]
+        self.indt = np.ascontiguousarray(elements.T)
+        self.bounds = [(lo, min(lo + chunk, self.n_e)) for lo in range(0, self.n_e, chunk)]
+        self.threads = threads or min(32, os.cpu_count() or 1)
+        self.cache = {} if cache else None
+
+    def matrices(self, c):
+        """(A_e, b_e) of chunk c: (n_b, n_b, m) view, (n_b, m)."""
+        if self.cache is not None and c in self.cache:
+            return self.cache[c]
+        lo, hi = self.bounds[c]
+        fv = None if self.f_vals is None else self.f_vals[lo:hi]
+        _, _, A, b_e = element_matrices(self.nodes, self.elements[lo:hi], nu=self.nu, f_vals=fv)
+        A = np.ascontiguousarray(A.transpose(2, 0, 1)).transpose(1, 2, 0)  # drop K, M
+        if self.cache is not None:
+            self.cache[c] = (A, b_e)
+        return A, b_e
+
+    def _pass(self, fill):
+        out = np.empty((self.nb, self.n_e))
+
+        def work(c):
+            lo, hi = self.bounds[c]
+            A, b_e = self.matrices(c)
+            out[:, lo:hi] = fill(A, b_e, lo, hi)
+        with ThreadPoolExecutor(max_workers=self.threads) as pool:
+            list(pool.map(work, range(len(self.bounds))))
+        return out
+
+    def _products(self, A, v, lo, hi):
+        return _local_products(A, self.indt[:, lo:hi], v, 0, hi - lo)
+
+    def residual(self, x):
+        """operators.py:72-107: one bincount of the chunk-local residuals."""
+        rt = self._pass(lambda A, b_e, lo, hi: b_e - self._products(A, x, lo, hi))
+        return np.bincount(self.indt.ravel(), weights=rt.ravel(), minlength=self.n)
+
+    def matvec_masked(self, v, nd):
+        """spectrum.py:54-61."""
+        av = self._pass(lambda A, b_e, lo, hi: self._products(A, v, lo, hi))
+        out = np.bincount(self.indt.ravel(), weights=av.ravel(), minlength=self.n)
+        out[nd] = 0.0
+        return out
+
+    def diagonal(self):
+        """diagonal(): assemble_rhs of the stacked A_e[j, j, :]."""
+        dg = self._pass(lambda A, b_e, lo, hi: np.stack([A[j, j, :] for j in range(self.nb)]))
+        return assemble_rhs(dg, self.indt, self.n)
+
+    def rhs(self):
+        """assemble_rhs(b_e, indt) (operators.py:58-63)."""
+        be = self._pass(lambda A, b_e, lo, hi: b_e)
+        return assemble_rhs(be, self.indt, self.n)
+
+
 def assemble_rhs(b_e, indt, n=None):
     """operators.py:58-63: bincount in (j, e) order."""
     if n is None:
@@ -298,6 +382,8 @@ def residual(A_e, b_e, indt, x, threads=1):
         raise ValueError(f"x must be a flat global vector, got shape {x.shape}")
     if not np.all(np.isfinite(x)):
         raise ValueError("x contains non-finite entries")
+    if isinstance(A_e, StreamedOperator):
+        return A_e.residual(x)
     n_e = indt.shape[1]
     if threads <= 1 or n_e < 2 * threads:
         rt = local_residuals(A_e, b_e, indt, x, 0, n_e)
@@ -314,6 +400,8 @@ def residual(A_e, b_e, indt, x, threads=1):
 def matvec_masked(A_e, indt, v, nd):
     """spectrum.py:54-61 (_apply_masked): y = A v by (j, e)-ordered bincount,
     then y[nd] = 0."""
+    if isinstance(A_e, StreamedOperator):
+        return A_e.matvec_masked(v, nd)
     av = _local_products(A_e, indt, v, 0, indt.shape[1])
     out = np.bincount(indt.ravel(), weights=av.ravel(), minlength=v.shape[0])
     out[nd] = 0.0
@@ -324,6 +412,8 @@ def diagonal(A_e, indt, n):
     """RESTATEMENT: diag(A) = assemble_rhs(stack_j A_e[j,j,:])
     -- the reference's own assemble_rhs (operators.py:58-63) applied to the
     diagonal slices, in the residual's (j, e) order."""
+    if isinstance(A_e, StreamedOperator):
+        return A_e.diagonal()
     nb = indt.shape[0]
     d = np.stack([A_e[j, j, :] for j in range(nb)])
     return assemble_rhs(d, indt, n)

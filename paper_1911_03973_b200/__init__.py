@@ -10,6 +10,7 @@ Arrays are torch tensors on the CUDA device; the compute is libebs.so
 fallback.
 """
 
+from .cli import ExperimentConfig, ExperimentReport, run_experiment
 from .elements import (ElementBatch, build_element_batch, combine_system, local_load_batch,
                        local_mass_batch, local_stiffness_batch)
 from .mesh import (MAX_LEVEL, IndexArrays, Mesh, boundary_nodes, build_grid_mesh,
@@ -26,6 +27,7 @@ from .spectrum import (mass_gershgorin, model_eigen_bounds, model_eigenvalues_al
                        operator_bounds, power_iteration_lambda_max)
 
 __all__ = [
+    "ExperimentConfig", "ExperimentReport", "run_experiment",
     "ChebyshevCycle", "chebyshev2", "chebyshev3", "chebyshev_roots", "chebyshev_scaling_factor",
     "mass_gershgorin", "operator_bounds", "power_iteration_lambda_max", "assemble_sparse",
     "uniform_refine", "export_mesh",

@@ -103,7 +103,7 @@ struct Ctl {
     int final_buf;      // ping-pong buffer that holds the returned iterate
     int nonfinite;      // set by any thread writing a non-finite iterate
     int cb_ok;          // r_k of the last step was recorded normally (callback due)
-    int pad_;
+    int x0_nonfinite;   // the solver's x0 held a non-finite entry (reference: ValueError)
     unsigned int counter;  // last-block-done counter of the fused reductions
     unsigned int pad2_;
     double norm0;

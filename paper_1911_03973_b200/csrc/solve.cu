@@ -1031,7 +1031,15 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
     double *dinv = plan_vec(p, 4), *ref_int = nullptr;
     CU(cudaMemsetAsync(p->ctl, 0, sizeof(Ctl), s));
     CU(cudaMemsetAsync(p->hist_dev, 0, sizeof(double) * 2 * ((int64_t)iters + 2), s));
-    to_internal(p, P->x0, xa, nullptr, s);
+    to_internal(p, P->x0, xa, &p->ctl->x0_nonfinite, s);
+    if (P->callback) {  // the reference raises before its first callback
+        CU(cudaMemcpyAsync(p->ctl_host, p->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (p->ctl_host->x0_nonfinite) {
+            set_error("x contains non-finite entries");
+            return EBS_ENONFINITE;
+        }
+    }
     if (P->reference) {
         ref_int = plan_vec(p, 7);
         to_internal(p, P->reference, ref_int, nullptr, s);
@@ -1204,6 +1212,10 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
                                cudaMemcpyDeviceToHost, s));
     }
     CU(cudaStreamSynchronize(s));
+    if (p->ctl_host->x0_nonfinite) {  // _iterate's first residual() raises (operators.py:90)
+        set_error("x contains non-finite entries");
+        return EBS_ENONFINITE;
+    }
     if (aborted) {
         set_error("solve stopped by callback");
         return EBS_ECALLBACK;

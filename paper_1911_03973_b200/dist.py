@@ -482,6 +482,27 @@ class DistProblem:
     comm: object
     b: list       # full (combined) b per rank, internal numbering
     dinv: list    # Jacobi 1/diag (0 at constrained nodes)
+    diverged: bool = False  # last jacobi/pcg: a non-finite iterate or norm on any rank
+                            # (solvers.py:138-152 -- flagged, never raised)
+
+
+def _reset_flags(ops):
+    for op in ops:
+        flag = getattr(op, "_flag", None)
+        if flag is not None:
+            flag.zero_()
+
+
+def _diverged(prob, norms) -> bool:
+    """Divergence as the reference's _iterate reports it: any rank's vector kernels saw a
+    non-finite iterate, or a residual norm is not finite; identical on every rank."""
+    bad = not bool(np.isfinite(norms).all())
+    for op in prob.ops:
+        flag = getattr(op, "_flag", None)
+        if flag is not None:
+            bad |= bool(int(flag.item()))
+    agree = getattr(prob.comm, "agree", None)
+    return (not agree(not bad)) if agree is not None else bad
 
 
 def setup(ops, comm, precondition=True) -> DistProblem:
@@ -607,6 +628,7 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     iterations (same kernels, same results).  fused (default: GPU ranks) runs the
     overlapped interface/interior sweeps with the update fused into the SELL pass."""
     ops, comm = prob.ops, prob.comm
+    _reset_flags(ops)
     xa = [x.clone() for x in xs0]
     xb = [op.zeros() for op in ops]
     ss = [op.zeros() for op in ops]
@@ -660,7 +682,9 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
         if not final:
             xa, xb = xb, xa
     comm.allreduce(red)
-    return xa, torch.sqrt(red[0]).cpu().numpy()
+    norms = torch.sqrt(red[0]).cpu().numpy()
+    prob.diverged = _diverged(prob, norms)
+    return xa, norms
 
 
 def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused=None):
@@ -673,6 +697,7 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused
     ops, comm = prob.ops, prob.comm
     dev = xs0[0].device
     f64 = dict(dtype=torch.float64, device=dev)
+    _reset_flags(ops)
     xs = [x.clone() for x in xs0]
     rs = [op.zeros() for op in ops]
     ps = [op.zeros() for op in ops]
@@ -751,7 +776,9 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused
         for i in range(len(ops)):
             norm2[i][kk + 1:kk + 2].copy_(ring[i][kk % B, 0:1])
     n = k_done + 1
-    return xs, torch.sqrt(norm2[0][:n]).cpu().numpy()
+    norms = torch.sqrt(norm2[0][:n]).cpu().numpy()
+    prob.diverged = _diverged(prob, norms)
+    return xs, norms
 
 
 def gather_global(ops, vs, n_nodes, comm=None):
@@ -760,8 +787,8 @@ def gather_global(ops, vs, n_nodes, comm=None):
     out = torch.zeros(n_nodes, dtype=torch.float64, device=vs[0].device)
     for op, v in zip(ops, vs):
         op.scatter_owned(v, out)
-    if comm is not None and isinstance(comm, TorchTransport):
-        comm.allreduce([out])
+    if comm is not None and not isinstance(comm, LocalTransport):
+        comm.allreduce([out])  # owned parts are disjoint: the sum is the global vector
     return out
 
 

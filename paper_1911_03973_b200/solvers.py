@@ -4,7 +4,9 @@ All methods run the reference's shared loop (`_iterate`, solvers.py:117-160) ins
 libebs.so (``ebs_solve``): the residual norms stay on the device and are read once
 at the end; the iteration stops on ``tol`` relative to ||r_0||; divergence sets a
 flag and is never raised; ``callback(k, x, r)`` is called for k = 0..iters with
-device tensors in the caller's numbering (reused buffers -- clone to keep them).
+fresh device tensors in the caller's numbering, as the reference hands a new x and r at
+every k (solvers.py:137-149); ``reuse_callback_buffers=True`` passes the same two buffers
+every time instead (no per-iteration copy; clone to keep them).
 
   richardson  x += omega r, omega = 2/(l1+l2)          solvers.py:163-183
   chebyshev2  x += (1/alpha_{k mod N}) r               solvers.py:186-213
@@ -107,7 +109,8 @@ class ConvergenceHistory:
 
 
 def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.0, exact=False,
-           tol=None, reference=None, callback=None, coef_a=None, coef_b=None, fused=False):
+           tol=None, reference=None, callback=None, coef_a=None, coef_b=None, fused=False,
+           reuse_callback_buffers=False):
     if iters < 0:
         raise ValueError(f"iteration count must be nonnegative, got {iters}")
     x0 = D.f64(x0)
@@ -129,7 +132,10 @@ def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.
 
         def _cb(user, k):
             try:
-                callback(int(k), cb_x, cb_r)
+                if reuse_callback_buffers:
+                    callback(int(k), cb_x, cb_r)
+                else:
+                    callback(int(k), cb_x.clone(), cb_r.clone())
                 return 0
             except BaseException as e:  # re-raised after the C call returns
                 state["exc"] = e
@@ -181,26 +187,28 @@ def _solve(method, batch: ElementBatch, d: DirichletData, x0, iters, *, omega=1.
 
 def richardson(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds, iters: int, *,
                tol=None, reference=None, callback=None, threads: int = 1,
-               deterministic: bool = True):
+               deterministic: bool = True, reuse_callback_buffers: bool = False):
     """solvers.py:163-183: damped Richardson with the step 2/(lambda1+lambda2).
 
     With ``deterministic=True`` the residual is the reference-order exact one, so
     the iterates are bit-identical to ebsolve.richardson."""
     omega = 2.0 / (bounds.lambda1 + bounds.lambda2)
     return _solve(EBS_RICHARDSON, batch, d, x0, iters, omega=omega, exact=deterministic, tol=tol,
-                  reference=reference, callback=callback)
+                  reference=reference, callback=callback,
+                  reuse_callback_buffers=reuse_callback_buffers)
 
 
 def chebyshev2(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds, N: int,
                iters: int, *, tol=None, reference=None, callback=None, threads: int = 1,
-               deterministic: bool = True):
+               deterministic: bool = True, reuse_callback_buffers: bool = False):
     """solvers.py:186-213: cyclic two-level Chebyshev, roots in natural order."""
     cycle = chebyshev_roots(bounds, N)
     if iters < 0:
         raise ValueError(f"iteration count must be nonnegative, got {iters}")
     coef = [1.0 / cycle.alphas[k % cycle.N] for k in range(iters)]
     return _solve(EBS_CHEB2, batch, d, x0, iters, exact=deterministic, tol=tol,
-                  reference=reference, callback=callback, coef_a=coef)
+                  reference=reference, callback=callback, coef_a=coef,
+                  reuse_callback_buffers=reuse_callback_buffers)
 
 
 def _chebyshev3_coefficients(bounds: SpectralBounds, iters: int):
@@ -225,7 +233,7 @@ def _chebyshev3_coefficients(bounds: SpectralBounds, iters: int):
 
 def chebyshev3(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds, iters: int, *,
                tol=None, reference=None, callback=None, threads: int = 1,
-               deterministic: bool = True):
+               deterministic: bool = True, reuse_callback_buffers: bool = False):
     """solvers.py:216-261: three-level Chebyshev via the stable two-term recurrence."""
     if not bounds.lambda1 < bounds.lambda2:
         raise ValueError("chebyshev3 needs lambda1 < lambda2")
@@ -233,30 +241,33 @@ def chebyshev3(batch: ElementBatch, d: DirichletData, x0, bounds: SpectralBounds
         raise ValueError(f"iteration count must be nonnegative, got {iters}")
     a, b = _chebyshev3_coefficients(bounds, iters)
     return _solve(EBS_CHEB3, batch, d, x0, iters, exact=deterministic, tol=tol,
-                  reference=reference, callback=callback, coef_a=a, coef_b=b)
+                  reference=reference, callback=callback, coef_a=a, coef_b=b,
+                  reuse_callback_buffers=reuse_callback_buffers)
 
 
 def jacobi(batch: ElementBatch, d: DirichletData, x0, iters: int, *, omega: float = 0.8,
-           tol=None, reference=None, callback=None, deterministic: bool = False):
+           tol=None, reference=None, callback=None, deterministic: bool = False,
+           reuse_callback_buffers: bool = False):
     """NEW: damped Jacobi x += omega * (D^-1 mask(b - A x)), D = diagonal(batch),
     on the _iterate loop (oracle/ebs_oracle.py jacobi)."""
     return _solve(EBS_JACOBI, batch, d, x0, iters, omega=omega, exact=deterministic, tol=tol,
-                  reference=reference, callback=callback)
+                  reference=reference, callback=callback,
+                  reuse_callback_buffers=reuse_callback_buffers)
 
 
 def cg(batch: ElementBatch, d: DirichletData, x0, iters: int, *, tol=None, reference=None,
-       callback=None, fused: bool = False):
+       callback=None, fused: bool = False, reuse_callback_buffers: bool = False):
     """NEW: conjugate gradients on the Dirichlet-masked operator (oracle pcg with
     dinv = 1); history holds the recursive residual norms.  fused=True (no callback):
     the whole loop as one cooperative persistent kernel."""
     return _solve(EBS_CG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback,
-                  fused=fused)
+                  fused=fused, reuse_callback_buffers=reuse_callback_buffers)
 
 
 def pcg(batch: ElementBatch, d: DirichletData, x0, iters: int, *, tol=None, reference=None,
-        callback=None, fused: bool = False):
+        callback=None, fused: bool = False, reuse_callback_buffers: bool = False):
     """NEW: Jacobi (diagonal) preconditioned CG (oracle/ebs_oracle.py pcg).  fused=True
     (no callback): the whole loop as one cooperative persistent kernel -- three grid-wide
     barriers per iteration instead of three launches (small, latency-bound meshes)."""
     return _solve(EBS_PCG, batch, d, x0, iters, tol=tol, reference=reference, callback=callback,
-                  fused=fused)
+                  fused=fused, reuse_callback_buffers=reuse_callback_buffers)

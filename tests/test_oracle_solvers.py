@@ -134,3 +134,31 @@ def test_grid_strides_of_generated_grids():
     assert o.delta_alphabet(indt) is None and o.grid_strides(indt) is None
     npt.assert_array_equal(o.plan_numbering(indt, len(inp["nodes"])),
                            o.first_appearance_order(indt, len(inp["nodes"])))
+
+
+def test_streamed_operator_is_bitwise_the_whole_mesh_operator():
+    """oracle.StreamedOperator (chunked element matrices, one bincount: the reference's
+    threaded deterministic mode, operators.py:96-107) == the whole-mesh functions, bit for
+    bit, in 2D (jittered + permuted C4 recipe) and 3D (Kuhn cube); the solver loops give
+    identical iterates through it."""
+    for cfg, size in ((4, 4), (5, 3)):
+        inp = o.config_inputs(cfg, seed=3, size=size)
+        nodes, elements, nd = inp["nodes"], inp["elements"], inp["dirichlet"]
+        _, _, A, b_e = o.element_matrices(nodes, elements, nu=inp["nu"], f_vals=inp["f_vals"])
+        indt = np.ascontiguousarray(elements.T)
+        op = o.StreamedOperator(nodes, elements, nu=inp["nu"], f_vals=inp["f_vals"], chunk=37,
+                                threads=3)
+        x = np.random.default_rng(1).uniform(-1, 1, nodes.shape[0])
+        np.testing.assert_array_equal(op.residual(x), o.residual(A, b_e, indt, x))
+        np.testing.assert_array_equal(o.residual(op, None, None, x), o.residual(A, b_e, indt, x))
+        np.testing.assert_array_equal(op.matvec_masked(x, nd), o.matvec_masked(A, indt, x, nd))
+        np.testing.assert_array_equal(op.diagonal(), o.diagonal(A, indt, nodes.shape[0]))
+        np.testing.assert_array_equal(op.rhs(), o.assemble_rhs(b_e, indt, nodes.shape[0]))
+        x0 = np.zeros(nodes.shape[0])
+        xs, hs = o.pcg(op, None, None, nd, x0, 7)
+        xw, hw = o.pcg(A, b_e, indt, nd, x0, 7)
+        np.testing.assert_array_equal(xs, xw)
+        np.testing.assert_array_equal(hs["residual_norms"], hw["residual_norms"])
+        xs, hs = o.jacobi(op, None, None, nd, x0, 0.8, 3)
+        xw, hw = o.jacobi(A, b_e, indt, nd, x0, 0.8, 3)
+        np.testing.assert_array_equal(xs, xw)
