@@ -121,35 +121,3 @@ def test_c5_full_size(gpu):
         1e-9 * h.residual_norms[-1]
     del batch, p, x, b
     _free()
-
-
-@pytest.mark.slow
-def test_c3_pcg_vs_scipy_cg_jacobi(gpu):
-    """SURVEY 8d C3 check: device Jacobi-PCG vs SciPy's cg with M = Jacobi (the reference's
-    only CG, reference.py:70) on the assembled, Dirichlet-eliminated system at full size
-    (2.1M unknowns): same iteration count, solutions within 1e-10 (measured 1.7e-13)."""
-    import scipy.sparse as sp
-    import scipy.sparse.linalg as spla
-    import paper_1911_03973_b200 as eb
-    from paper_1911_03973_b200.inputs import config_problem
-    p = config_problem(3)
-    batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
-    x, h = eb.pcg(batch, d, torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda"), 20000,
-                  tol=1e-8)
-    A = eb.assemble_sparse(batch.A_e, batch.index, m.n_nodes)
-    crow, col, val = (t.cpu().numpy() for t in (A.crow_indices(), A.col_indices(), A.values()))
-    n = m.n_nodes
-    free = np.ones(n, bool)
-    free[d.nd.cpu().numpy()] = False
-    Af = sp.csr_matrix((val, col, crow), shape=(n, n))[free][:, free].tocsr()
-    bf = eb.assemble_rhs(batch.b_e, batch.index).cpu().numpy()[free]
-    dinv = 1.0 / Af.diagonal()
-    M = spla.LinearOperator(Af.shape, matvec=lambda v: dinv * v)
-    its = [0]
-    xs, info = spla.cg(Af, bf, rtol=1e-8, atol=0.0, maxiter=20000, M=M,
-                       callback=lambda xk: its.__setitem__(0, its[0] + 1))
-    assert info == 0 and its[0] == h.iterations
-    xg = x.cpu().numpy()[free]
-    assert np.linalg.norm(xg - xs) <= 1e-10 * np.linalg.norm(xs)
-    del batch, p, x, A
-    _free()
