@@ -152,15 +152,12 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE C2 recipe)",
         "config": workload_config(n_n, n_e, args, mode="reference order (bincount)"),
         "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": T, "kind": "port",
                          "sample": f"{args.steps} full C2 residuals (oracle/ebs_oracle.py "
-                                   f"residual, deterministic chunked mode, {T} threads)"
-                                   + ("" if int(os.environ.get("WORLD_SIZE", "1")) <= 1 else
-                                      "; one C2 square per step = one GPU's slab of the "
-                                      "stacked squares (GDoF/s is a rate)")},
+                                   f"residual, deterministic chunked mode, {T} threads)"},
         "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "setup_s": setup,
@@ -168,25 +165,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _stacked_nodes(n_square, copies):
-    side = int(round(n_square ** 0.5))
-    return side * ((side - 1) * copies + 1)
-
-
 def workload_config(n_n, n_e, args, mode):
+    """The bench workload: BASELINE C2 at every N (one GPU, or strong-scaled over N element
+    slabs np.linspace(0, n_e, N+1) -- operators.py:100's chunk rule -- under torchrun)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:  # the GPU arm's weak-scaled workload (bench_dist.bench_rank)
-        return {"workload": f"C2 weak-scaled: {world} level-11 unit squares stacked in y, "
-                            "one C2-sized element slab per GPU; element residual r=b-Ax per "
-                            "step", "per_gpu": "one C2 square (4.2M nodes, 8.4M triangles)",
-                "n_nodes": _stacked_nodes(n_n, world),
-                "n_elements": n_e * world, "seed": args.seed, "mode": mode,
-                "parallelism": f"element slabs x{world}"}
     return {"workload": "C2: 2D P1 unit square, level 11, permuted node numbering, "
                         "x~U[-1,1], nu=1, f=1; element residual r=b-Ax per step",
             "n_nodes": n_n, "n_elements": n_e, "seed": args.seed, "mode": mode,
             "l2": "inputs larger than L2 (slot stream ~1 GB vs 126 MB L2); no flush",
-            "parallelism": "single GPU"}
+            "parallelism": "single GPU" if world <= 1 else
+            f"element slabs x{world} (strong scaling of the fixed C2 mesh, NCCL halo)"}
 
 
 # ---------------------------------------------------------------- GPU arm --
@@ -399,7 +387,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 mesh, x~U[-1,1])",
         "config": workload_config(n_n, n_e, args, mode="fast (pre-assembled b)"),
         "hbm_gbs_algorithmic": bytes_alg / (total / args.steps) / 1e9,
@@ -574,6 +562,8 @@ def main():
     ap.add_argument("--extra", action=argparse.BooleanOptionalAction, default=True,
                     help="also time the C3/C4/C5 solvers (default on; --no-extra to skip)")
     ap.add_argument("--solver-configs", type=int, nargs="*", default=[3, 4, 5])
+    ap.add_argument("--c4-size", type=int, default=None, help="override the C4 level (tests)")
+    ap.add_argument("--c5-size", type=int, default=None, help="override the C5 N (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

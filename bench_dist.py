@@ -143,7 +143,8 @@ def _residual_measure(p, args, rank, world, comm, sampler):
         if i >= 2:
             stream.wait_event(read[i - 2])
         step(xl=xb[j], rl=rb[j])
-        torch.index_select(rb[j], 0, own, out=ob[j])
+        lib.ebs_gather(own.numel(), D.ptr(own), D.ptr(rb[j]), D.ptr(ob[j]),
+                       ctypes.c_void_p(stream.cuda_stream))  # owned entries, one kernel
         used[i].record(stream)
         r_ready[i].record(stream)
         with torch.cuda.stream(d2h):
@@ -172,11 +173,12 @@ def _residual_measure(p, args, rank, world, comm, sampler):
 
 
 def bench_rank(args, rank, world, local_rank):
-    """bench.py --gpus N under torchrun.  `value`: the C2 residual weak-scaled over N
-    element slabs -- N level-11 unit squares stacked in y (inputs.stacked_c2_problem), one
-    C2-sized slab per rank, the NCCL halo of the shared node rows -- whole-job GDoF/s =
-    total nodes x K / max-over-ranks device time.  Also reported: the fixed C2 mesh
-    strong-scaled over the same N slabs, and (extras) C4 / C5 solver strong scaling."""
+    """bench.py --gpus N under torchrun.  `value`: the fixed BASELINE C2 residual (the N=1
+    workload: level-11 permuted unit square, 4.2M nodes) strong-scaled over N element slabs
+    with the NCCL halo of the slab interfaces -- GDoF/s = C2 nodes x K / max-over-ranks
+    device time.  Extras: the C2 residual weak-scaled (N level-11 squares stacked in y, one
+    per GPU) and the C4 damped-Jacobi x200 / C5 Jacobi-PCG x500 strong scaling against an
+    in-job single-GPU run, E(N) = T1 / (N T_N)."""
     import json
 
     import torch.distributed as dist
@@ -197,68 +199,103 @@ def bench_rank(args, rank, world, local_rank):
     peaks, peak_kind = B.load_peaks()
     sampler = B.ClockSampler(index=dev).start()
     comm = TorchTransport(stage_host=gloo)
-    weak = _residual_measure(stacked_c2_problem(world, seed=args.seed, size=args.size), args,
-                             rank, world, comm, sampler)
-    strong = None
-    if world > 1:
-        strong = _residual_measure(config_problem(2, seed=args.seed, size=args.size,
-                                                  assemble=False), args, rank, world, comm,
-                                   sampler)
+    strong = _residual_measure(config_problem(2, seed=args.seed, size=args.size, assemble=False),
+                               args, rank, world, comm, sampler)
+    weak = None
+    if getattr(args, "extra", False):
+        weak = _residual_measure(stacked_c2_problem(world, seed=args.seed, size=args.size), args,
+                                 rank, world, comm, sampler)
     sampler.stop()
     line = None
     if rank == 0:
         peak = float(peaks["hbm_gbs"])
-        T = weak["T"]
-        line = {"metric": B.METRIC, "value": weak["n_nodes"] * args.steps / T / 1e9,
+        T = strong["T"]
+        line = {"metric": B.METRIC, "value": strong["n_nodes"] * args.steps / T / 1e9,
                 "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 squares)",
-                "config": {"workload": f"C2 weak-scaled: {world} level-11 unit squares stacked "
-                                       "in y, one C2-sized element slab per GPU, NCCL halo of "
-                                       "the shared node rows; element residual r=b-Ax per step",
-                           "n_nodes": weak["n_nodes"], "n_elements": weak["n_elements"],
-                           "per_gpu": "one C2 square (4.2M nodes, 8.4M triangles)",
-                           "seed": args.seed,
-                           "mode": "fast (pre-assembled b); x and r in each rank's caller "
-                                   "order (its local nodes by ascending global id)",
-                           "l2": "inputs larger than L2 (slot stream ~1 GB per rank); no flush",
-                           "parallelism": f"element slabs x{world}",
-                           "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=weak["graph_verified"])},
-                "roofline": {"bound": "hbm", "achieved": weak["bytes_rank"] / weak["kern"] / 1e9,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded BASELINE C2 recipe: permuted level-11 mesh, "
+                        "x~U[-1,1])",
+                "config": B.workload_config(strong["n_nodes"], strong["n_elements"], args,
+                                            mode="fast (pre-assembled b); x and r in each "
+                                                 "rank's caller order (its local nodes by "
+                                                 "ascending global id)"),
+                "roofline": {"bound": "hbm",
+                             "achieved": strong["bytes_rank"] / strong["kern"] / 1e9,
                              "peak": peak, "unit": "GB/s",
-                             "frac": weak["bytes_rank"] / weak["kern"] / 1e9 / peak,
+                             "frac": strong["bytes_rank"] / strong["kern"] / 1e9 / peak,
                              "traffic": None,
-                             "kernel": "k_sell_op<3,1,1> over the slab's chunks (max over ranks)",
-                             "bytes_per_launch": weak["bytes_rank"], "kernel_ms": weak["kern"] * 1e3,
-                             "peak_source": peak_kind},
-                "e2e": {"value": weak["n_nodes"] * args.steps / weak["te"] / 1e9, "unit": "GDoF/s",
-                        "h2d_bytes_per_step": weak["h2d"], "d2h_bytes_per_step": weak["d2h"],
+                             "kernel": "k_sell_op<3,1,1> over the slab's chunks (max over "
+                                       "ranks; bytes of the largest slab)",
+                             "bytes_per_launch": strong["bytes_rank"],
+                             "kernel_ms": strong["kern"] * 1e3, "peak_source": peak_kind},
+                "e2e": {"value": strong["n_nodes"] * args.steps / strong["te"] / 1e9,
+                        "unit": "GDoF/s", "h2d_bytes_per_step": strong["h2d"],
+                        "d2h_bytes_per_step": strong["d2h"],
                         "api": "per rank: x slab H2D from pinned host, dist residual step, "
-                               "owned r entries D2H to pinned host; copies of consecutive "
-                               "steps overlapped (two buffer sets, copy streams)"},
-                "gpu_launches": weak["launches"], "clocks": sampler.summary(),
+                               "owned r entries gathered (ebs_gather) and D2H to pinned host; "
+                               "copies of consecutive steps overlapped (two buffer sets, copy "
+                               "streams)"},
+                "gpu_launches": strong["launches"], "clocks": sampler.summary(),
+                "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=strong["graph_verified"]),
                 "cpu_baseline": None}
-        if strong is not None:
-            line["strong_c2"] = {
-                "value": strong["n_nodes"] * args.steps / strong["T"] / 1e9, "unit": "GDoF/s",
-                "ms_per_step": strong["T"] / args.steps * 1e3, "scaling": "strong",
-                "workload": "the fixed C2 mesh (4.2M nodes) over the same element slabs",
-                "kernel_ms": strong["kern"] * 1e3, "cuda_graph": strong["graph"]}
+        line["config"]["cuda_graph"] = strong["graph"]
+        if weak is not None:
+            line["weak_c2"] = {
+                "value": weak["n_nodes"] * args.steps / weak["T"] / 1e9, "unit": "GDoF/s",
+                "ms_per_step": weak["T"] / args.steps * 1e3, "scaling": "weak",
+                "workload": f"{world} level-11 unit squares stacked in y, one C2-sized element "
+                            "slab per GPU, NCCL halo of the shared node rows",
+                "n_nodes": weak["n_nodes"], "kernel_ms": weak["kern"] * 1e3,
+                "e2e_value": weak["n_nodes"] * args.steps / weak["te"] / 1e9,
+                "cuda_graph": weak["graph"]}
     solvers = {}
     if getattr(args, "extra", False):
         solvers = _bench_solvers(args, rank, world)
     if rank == 0:
         if solvers:
-            line["solvers"] = solvers
+            line["strong_scaling"] = solvers
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
 
+def _single_gpu_reference(cfg, iters, args):
+    """Rank 0 alone: the BASELINE solve on ONE GPU through the 1-GPU product path
+    (eb.jacobi / eb.pcg, ebs_solve) -- T1 of E(N) = T1 / (N T_N) and the norm history the
+    N-rank solve is checked against."""
+    import gc
+
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(cfg, seed=args.seed, size=_solver_size(cfg, args))
+    batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+    x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+    solve = (lambda: eb.jacobi(batch, d, x0, iters, omega=0.8)) if cfg == 4 else \
+        (lambda: eb.pcg(batch, d, x0, iters))
+    solve()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, h = solve()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    del p, batch, x0
+    gc.collect()
+    torch.cuda.empty_cache()
+    return t, h.residual_norms
+
+
+def _solver_size(cfg, args):
+    return {4: getattr(args, "c4_size", None), 5: getattr(args, "c5_size", None)}.get(cfg)
+
+
 def _bench_solvers(args, rank, world):
-    """C4 damped Jacobi x200 and C5 Jacobi-PCG x500 on `world` element slabs (strong
-    scaling; device time, max over ranks).  Errors are reported, never raised."""
+    """C4 damped Jacobi x200 and C5 Jacobi-PCG x500 on `world` element slabs: strong scaling
+    (device time, max over ranks) against the in-job single-GPU run of the same solve,
+    E(N) = T1 / (N T_N); the N-rank norm history is checked against the 1-GPU one.
+    Errors are reported, never raised."""
     import gc
     import torch.distributed as dist
     from paper_1911_03973_b200.inputs import config_problem
@@ -268,7 +305,14 @@ def _bench_solvers(args, rank, world):
         if cfg not in getattr(args, "solver_configs", (4, 5)):
             continue
         try:
-            p = config_problem(cfg, seed=args.seed, assemble=False)
+            t1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+            h1 = None
+            if rank == 0:
+                T1, h1 = _single_gpu_reference(cfg, iters, args)
+                t1.fill_(T1)
+            dist.broadcast(t1, src=0)
+            T1 = float(t1)
+            p = config_problem(cfg, seed=args.seed, size=_solver_size(cfg, args), assemble=False)
             d, m = p["dirichlet"], p["mesh"]
             op, maps = rank_operator(m, p["nu"], p["f"], d, world, rank)
             del p
@@ -296,14 +340,29 @@ def _bench_solvers(args, rank, world):
             T = float(t)
             nb = m.n_b
             per_it = m.n_elements * (8 * nb * nb + 4 * nb) + (32 if cfg == 4 else 104) * m.n_nodes
-            out[f"C{cfg}"] = {"method": "jacobi" if cfg == 4 else "pcg", "iterations": iters,
-                              "ranks": world, "it_per_s": iters / T, "ms_per_it": T / iters * 1e3,
-                              "hbm_gbs_algorithmic_total": per_it * iters / T / 1e9,
-                              "frac_of_peak_per_gpu": per_it * iters / T / 1e9 / world /
-                              float(peaks["hbm_gbs"]),
-                              "final_norm": float(norms[-1]), "n_nodes": m.n_nodes,
-                              "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=use_graph),
-                              "n_elements": m.n_elements}
+            row = {"method": "jacobi" if cfg == 4 else "pcg (single all-reduce per iteration)",
+                   "iterations": iters, "ranks": world, "it_per_s": iters / T,
+                   "ms_per_it": T / iters * 1e3, "t1_it_per_s": iters / T1,
+                   "efficiency": T1 / (world * T),
+                   "hbm_gbs_algorithmic_total": per_it * iters / T / 1e9,
+                   "frac_of_peak_per_gpu": per_it * iters / T / 1e9 / world /
+                   float(peaks["hbm_gbs"]),
+                   "final_norm": float(norms[-1]), "n_nodes": m.n_nodes,
+                   "n_elements": m.n_elements, "diverged": bool(prob.diverged),
+                   "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=use_graph),
+                   "t1": "in-job single-GPU run of the same solve (eb.jacobi / eb.pcg, "
+                         "ebs_solve) on rank 0"}
+            if h1 is not None:
+                # relative difference of ||r_k|| wherever the 1-GPU norm is above the
+                # rounding floor (1e-10 ||r_0||; at full C5 that is all 501 entries)
+                ok_len = len(h1) == len(norms)
+                live = np.abs(h1) >= 1e-10 * abs(h1[0]) if ok_len else None
+                dev_ = (float(np.max(np.abs(norms[live] - h1[live]) / np.abs(h1[live])))
+                        if ok_len else None)
+                row["history_vs_1gpu"] = {"max_rel_diff": dev_,
+                                          "entries_compared": int(live.sum()) if ok_len else 0,
+                                          "ok_1e-8": bool(ok_len and dev_ <= 1e-8)}
+            out[f"C{cfg}"] = row
             del op, prob
         except Exception as e:  # noqa: BLE001
             out[f"C{cfg}"] = {"error": f"{type(e).__name__}: {e}"}

@@ -280,6 +280,24 @@ int ebs_vec_pcg_update(int64_t n, const double *rz, const double *pq, const uint
                        double *red, int32_t *nonfinite, void *ws, void *stream);
 int ebs_vec_pcg_direction(int64_t n, const double *rz_old, const double *rz_new,
                           const double *dinv, const double *r, double *p, void *stream);
+/* Single-reduction Jacobi-PCG step (Chronopoulos-Gear; one all-reduce per iteration).
+ * cur = [gamma_k = r.u, delta_k = w.u, rr_k = r.r, alpha_k (written)] of iteration k, with
+ * [0..2] already all-reduced; prev = the same of iteration k-1 (prev[0] == 0: first step,
+ * beta = 0).  beta = gamma_k/gamma_{k-1}, alpha = gamma_k/(delta_k - beta gamma_k/alpha_{k-1});
+ * p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = dinv r;
+ * next[0] = sum_owned r.u, next[2] = sum_owned r.r (next[1] = the matvec's w.u, from
+ * ebs_dist_matvec_sweep / ebs_dist_q_iface or ebs_vec_pcg_q with p := u, q := w).
+ * ctl (device int32[4], nullable) = [stop, k_stop, k, diverged]: the _iterate loop rules
+ * (solvers.py:117-160) on the device -- instead of updating, the launch sets stop (k_stop = k)
+ * when sqrt(rr_k) <= tol*sqrt(rr0[0]) (tol >= 0) or rr_k is not finite (diverged = 1);
+ * once stop is set every launch is a no-op.  No host synchronisation anywhere. */
+int ebs_vec_cg1_update(int64_t n, double *cur, const double *prev, const double *rr0, double tol,
+                       int32_t *ctl, const uint8_t *owned, const double *dinv, double *x,
+                       double *r, double *u, const double *w, double *p, double *s,
+                       double *next, int32_t *nonfinite, void *ws, void *stream);
+/* The plan's fused matvec sweeps (ebs_dist_matvec_sweep) become no-ops while *stop != 0
+ * (device int32, e.g. ctl[0] above; NULL clears). */
+int ebs_dist_set_stop(ebs_plan_t plan, const int32_t *stop);
 int ebs_vec_dot_owned(int64_t n, const double *x, const double *y, const uint8_t *owned,
                       double *red, void *ws, void *stream);
 /* dinv = free ? (diag ? 1/diag : 1) : 0 */
@@ -336,6 +354,15 @@ int ebs_dist_exchange(ebs_plan_t plan, int n_peers, const int32_t *peers, const 
                       const double *const *send, double *const *recv, void *stream);
 /* In-place sum over the ranks of n device doubles (the PCG dots) on `stream`. */
 int ebs_dist_allreduce(ebs_plan_t plan, double *buf, int64_t n, void *stream);
+/* Failure detection.  ebs_dist_poll: ncclCommGetAsyncError; on an error the communicator is
+ * aborted (ncclCommAbort) and EBS_ENCCL returned.  ebs_dist_wait: wait until `stream` is
+ * idle while polling; after timeout_s seconds (< 0: never) the communicator is aborted --
+ * which also releases NCCL kernels waiting on a lost peer -- and EBS_ENCCL returned.
+ * ebs_dist_abort: abort explicitly.  After an abort every collective of the plan returns
+ * EBS_ENCCL until ebs_dist_init is called again. */
+int ebs_dist_poll(ebs_plan_t plan);
+int ebs_dist_wait(ebs_plan_t plan, void *stream, double timeout_s);
+int ebs_dist_abort(ebs_plan_t plan);
 
 #ifdef __cplusplus
 }

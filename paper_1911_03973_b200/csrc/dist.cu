@@ -167,6 +167,95 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Single-reduction Jacobi-PCG (Chronopoulos-Gear): the three dots of an iteration,
+// [gamma = r.u, delta = w.u, rr = r.r], are all-reduced together (one collective per
+// iteration instead of two).  cur = those of iteration k (+ cur[3] = alpha_k, written here),
+// prev = iteration k-1 (prev[0] == 0: first iteration, beta = 0):
+//   beta = gamma_k / gamma_{k-1};  alpha = gamma_k / (delta_k - beta gamma_k / alpha_{k-1})
+//   p = u + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s;  u = dinv r
+//   next = [sum_owned r.u, (delta: the matvec), sum_owned r.r]
+// ctl = [stop, k_stop, k, diverged]: the loop rules of _iterate (solvers.py:117-160) on the
+// device -- stop when ||r_k|| <= tol ||r_0|| (tol >= 0) or ||r_k|| is not finite; every
+// later launch (and the plan's fused matvec sweeps, ebs_dist_set_stop) is a no-op.
+__global__ void __launch_bounds__(256)
+    k_vec_cg1_update(int64_t n, double *cur, const double *__restrict__ prev,
+                     const double *__restrict__ rr0, double tol, int32_t *ctl,
+                     const uint8_t *__restrict__ owned, const double *__restrict__ dinv,
+                     double *__restrict__ x, double *__restrict__ r, double *__restrict__ u,
+                     const double *__restrict__ w, double *__restrict__ p,
+                     double *__restrict__ s, double *partials, unsigned int *counter,
+                     double *next, int32_t *nonfinite) {
+    if (ctl && ctl[0]) return;
+    const double gamma = cur[0], delta = cur[1], rr = cur[2];
+    if (ctl) {
+        const double nk = sqrt(rr);
+        const bool bad = !isfinite(nk);
+        if (bad || (tol >= 0.0 && nk <= tol * sqrt(rr0[0]))) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                ctl[1] = ctl[2];
+                ctl[3] = bad ? 1 : 0;
+                ctl[0] = 1;
+            }
+            return;  // every block takes the same decision from the same scalars
+        }
+    }
+    const double g_prev = prev[0], a_prev = prev[3];
+    const double beta = g_prev != 0.0 ? gamma / g_prev : 0.0;
+    const double denom = (beta != 0.0 && a_prev != 0.0) ? delta - beta * gamma / a_prev : delta;
+    const double alpha = denom != 0.0 ? gamma / denom : 0.0;
+    double part[2] = {0.0, 0.0};
+    bool bad = false;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+         base += stride * VEC_ILP) {
+        double uv[VEC_ILP], wv[VEC_ILP], pv[VEC_ILP], sv[VEC_ILP], xv[VEC_ILP], rv[VEC_ILP],
+            dv[VEC_ILP];
+        uint8_t ow[VEC_ILP];
+#pragma unroll
+        for (int q = 0; q < VEC_ILP; ++q) {
+            const int64_t m = base + q * stride;
+            const bool ok = m < n;
+            uv[q] = ok ? u[m] : 0.0;
+            wv[q] = ok ? w[m] : 0.0;
+            pv[q] = ok ? p[m] : 0.0;
+            sv[q] = ok ? s[m] : 0.0;
+            xv[q] = ok ? x[m] : 0.0;
+            rv[q] = ok ? r[m] : 0.0;
+            dv[q] = ok ? dinv[m] : 0.0;
+            ow[q] = ok ? owned[m] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < VEC_ILP; ++q) {
+            const int64_t m = base + q * stride;
+            if (m < n) {
+                const double pn = uv[q] + beta * pv[q];
+                const double sn = wv[q] + beta * sv[q];
+                const double xn = xv[q] + alpha * pn;
+                const double rn = rv[q] - alpha * sn;
+                const double un = dv[q] * rn;
+                p[m] = pn;
+                s[m] = sn;
+                x[m] = xn;
+                r[m] = rn;
+                u[m] = un;
+                bad |= !isfinite(xn);
+                if (ow[q]) {
+                    part[0] += rn * un;
+                    part[1] += rn * rn;
+                }
+            }
+        }
+    }
+    if (bad) atomicOr(nonfinite, 1);
+    double tot[2];
+    if (grid_sum_last<2>(part, partials, counter, tot) && threadIdx.x == 0) {
+        next[0] = tot[0];
+        next[2] = tot[1];
+        cur[3] = alpha;
+        if (ctl) ctl[2] += 1;
+    }
+}
+
 // red[0] = sum_owned x*y (owned nullable: all)
 __global__ void __launch_bounds__(256)
     k_vec_dot_owned(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
@@ -295,6 +384,29 @@ int ebs_vec_pcg_direction(int64_t n, const double *rz_old, const double *rz_new,
     EBS_CATCH
 }
 
+int ebs_vec_cg1_update(int64_t n, double *cur, const double *prev, const double *rr0, double tol,
+                       int32_t *ctl, const uint8_t *owned, const double *dinv, double *x,
+                       double *r, double *u, const double *w, double *p, double *s,
+                       double *next, int32_t *nonfinite, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && cur && prev && owned && dinv && x && r && u && w && p && s && next &&
+                    nonfinite && ws && (rr0 || tol < 0.0),
+                "null argument");
+    Scratch sc = scratch(ws);
+    k_vec_cg1_update<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+        n, cur, prev, rr0, tol, ctl, owned, dinv, x, r, u, w, p, s, sc.partials, sc.counter,
+        next, nonfinite);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_dist_set_stop(ebs_plan_t plan, const int32_t *stop) {
+    EBS_TRY
+    EBS_REQUIRE(plan, "null argument");
+    reinterpret_cast<Plan *>(plan)->dist_stop = stop;
+    EBS_CATCH
+}
+
 int ebs_vec_dot_owned(int64_t n, const double *x, const double *y, const uint8_t *owned,
                       double *red, void *ws, void *stream) {
     EBS_TRY
@@ -396,7 +508,9 @@ struct DistMatvecEpi {
 template <int NB, int IDS>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_dist_matvec_sweep(SellView v, const double *__restrict__ p, DistMatvecEpi epi,
-                        double *partials, unsigned int *counter, double *red) {
+                        double *partials, unsigned int *counter, double *red,
+                        const int32_t *stop) {
+    if (stop && *stop) return;  // single-reduction PCG already stopped (ebs_dist_set_stop)
     sell_sweep<NB, IDS, false>(v, p, epi);
     double tot[1];
     if (grid_sum_last<1>(epi.part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
@@ -518,7 +632,7 @@ int ebs_dist_matvec_sweep(ebs_plan_t plan, const int32_t *chunks, int64_t n_list
         auto kern = k_dist_matvec_sweep<NB_, IDS_>;                                         \
         SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, n_list);              \
         kern<<<SL.grid, SL.block, SL.smem, S(stream)>>>(v, pv, epi, sc.partials, sc.counter, \
-                                                        red);                               \
+                                                        red, p->dist_stop);                 \
     }
     EBS_SELL_DISPATCH(p, EBS_DM);
 #undef EBS_DM

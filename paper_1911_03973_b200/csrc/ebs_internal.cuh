@@ -182,6 +182,9 @@ struct Plan {
     // element-slab collectives (nccl.cu): one NCCL communicator per plan
     void *nccl_comm = nullptr;
     int dist_rank = 0, dist_size = 1;
+    bool dist_aborted = false;           // ncclCommAbort after an async error / timeout
+    const int32_t *dist_stop = nullptr;  // device stop flag of a single-reduction PCG
+                                         // (ebs_dist_set_stop): fused matvec sweeps no-op
     double *partials = nullptr;  // reduction partials
     Ctl *ctl = nullptr;          // device control block
     Ctl *ctl_host = nullptr;     // pinned mirror: [0] synchronous reads, [1..2] batch ring

@@ -175,7 +175,23 @@ class NativeTransport:
     def agree(self, ok: bool) -> bool:
         t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device="cuda")
         self.allreduce([t])
+        self.sync()
         return int(t.item()) == self.world
+
+    def sync(self, timeout: float | None = None):
+        """Wait for the current stream while polling NCCL for asynchronous errors; a lost
+        peer or a stream still busy after `timeout` s (default EBS_NCCL_TIMEOUT, 600)
+        aborts the communicator and raises (ebs_dist_wait) instead of hanging."""
+        import os
+        if timeout is None:
+            timeout = float(os.environ.get("EBS_NCCL_TIMEOUT", "600"))
+        call("ebs_dist_wait", self.op.plan.handle, D.stream(), ctypes.c_double(timeout))
+
+    def poll(self):
+        call("ebs_dist_poll", self.op.plan.handle)
+
+    def abort(self):
+        call("ebs_dist_abort", self.op.plan.handle)
 
 
 class LocalTransport:
@@ -459,6 +475,15 @@ class GpuRankOperator:
         call("ebs_vec_pcg_direction", self.n, D.ptr(rz_old), D.ptr(rz_new), D.ptr(dinv), D.ptr(r),
              D.ptr(p), D.stream())
 
+    def vec_cg1_update(self, cur, prev, rr0, tol, ctl, dinv, x, r, u, w, p, s_, nxt):
+        call("ebs_vec_cg1_update", self.n, D.ptr(cur), D.ptr(prev), D.ptr(rr0), float(tol),
+             D.ptr(ctl), D.ptr(self.owned), D.ptr(dinv), D.ptr(x), D.ptr(r), D.ptr(u), D.ptr(w),
+             D.ptr(p), D.ptr(s_), D.ptr(nxt), D.ptr(self._flag), D.ptr(self._ws), D.stream())
+
+    def set_stop(self, ctl):
+        """Fused matvec sweeps of this rank's plan no-op while ctl[0] != 0 (None clears)."""
+        call("ebs_dist_set_stop", self.plan.handle, D.ptr(ctl))
+
     def dot_owned(self, x, y, red):
         call("ebs_vec_dot_owned", self.n, D.ptr(x), D.ptr(y), D.ptr(self.owned), D.ptr(red),
              D.ptr(self._ws), D.stream())
@@ -687,9 +712,160 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     return xa, norms
 
 
-def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused=None):
+def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused=None,
+        reductions: int = 1):
     """Jacobi-PCG on P ranks (oracle/ebs_oracle.py pcg; with prob from setup(..,
-    precondition=False) plain CG).  Two scalar all-reduces per iteration, both in place and
+    precondition=False) plain CG), same stopping rule and history as _iterate
+    (solvers.py:117-160).  Returns (xs, norms); prob.diverged is set.
+
+    reductions=1 (default): the single-reduction (Chronopoulos-Gear) recurrence -- ONE
+    all-reduce of [r.u, w.u, r.r] per iteration, the loop rules (tol, divergence) decided on
+    the device, CUDA-graph batches also with a tolerance and no host synchronisation inside
+    the solve.  reductions=2: the textbook recurrence of the oracle, two all-reduces per
+    iteration (p.q, then [r.r, r.z]); a tolerance costs a host read per iteration there."""
+    if reductions == 1:
+        return _pcg_single_reduction(prob, xs0, iters, tol=tol, graph=graph, fused=fused)
+    if reductions != 2:
+        raise ValueError(f"reductions must be 1 or 2, got {reductions}")
+    return _pcg_two_reductions(prob, xs0, iters, tol=tol, graph=graph, fused=fused)
+
+
+def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False,
+                          fused=None):
+    """Chronopoulos-Gear PCG (oracle pcg in exact arithmetic; rounding differs):
+        r = mask(b - A x0), u = dinv r, w = mask(A u);  [gamma, delta, rr] all-reduced
+        loop k: beta = gamma_k/gamma_{k-1}, alpha = gamma_k/(delta_k - beta gamma_k/alpha_{k-1})
+                p = u + beta p; s = w + beta s; x += alpha p; r -= alpha s; u = dinv r
+                                                      (ebs_vec_cg1_update: r.u, r.r partials)
+                w = mask(A u) and w.u                  (fused sweeps / halo / interface)
+                all-reduce [r.u, w.u, r.r]             (ONE collective)
+    Scalars live in a ring of GRAPH_BATCH slots [gamma, delta, rr, alpha]; iteration k reads
+    slot k % B (and k-1 for beta), writes slot k+1.  ctl = [stop, k_stop, k, diverged]
+    per rank: the update kernel stops the loop on the device (tol / non-finite norm), after
+    which every kernel is a no-op -- so the host enqueues graph batches and reads ctl one
+    batch behind (never idling the device), and the returned x is x_{k_stop} exactly."""
+    if iters < 0:
+        raise ValueError(f"iteration count must be nonnegative, got {iters}")
+    ops, comm = prob.ops, prob.comm
+    dev = xs0[0].device
+    f64 = dict(dtype=torch.float64, device=dev)
+    _reset_flags(ops)
+    B = GRAPH_BATCH
+    xs = [x.clone() for x in xs0]
+    rs, us, ws, ps, ss = ([op.zeros() for op in ops] for _ in range(5))
+    ring = [torch.zeros((B, 4), **f64) for _ in ops]   # [gamma, delta, rr, alpha]
+    part = [torch.zeros(2, **f64) for _ in ops]        # interface / interior sweep w.u
+    ctl = [torch.zeros(4, dtype=torch.int32, device=dev) for _ in ops]
+    rr0 = [torch.zeros(1, **f64) for _ in ops]
+    zero = torch.zeros(1, **f64)
+    fused = _fused_ok(ops) if fused is None else fused
+    tol_ = -1.0 if tol is None else float(tol)
+    for op, c in zip(ops, ctl):
+        if hasattr(op, "set_stop"):
+            op.set_stop(c if fused else None)
+
+    def matvec_w(slot):  # w = mask(A u), slot[1] = the rank's owned w.u
+        if fused:
+            for i, op in enumerate(ops):
+                op.matvec_sweep(op.if_chunks, us[i], ws[i], part[i][0:1])
+            h = comm.exchange_start(ops, [op.gather_sends(w_) for op, w_ in zip(ops, ws)])
+            for i, op in enumerate(ops):
+                op.matvec_sweep(op.in_chunks, us[i], ws[i], part[i][1:2])
+            recvs = comm.exchange_finish(h)
+            for i, op in enumerate(ops):
+                op.combine(ws[i], recvs[i])
+                op.q_iface(us[i], ws[i], slot[i][1:2], prior=part[i])
+        else:
+            for op, u_, w_ in zip(ops, us, ws):
+                op.matvec_partial(u_, w_)
+            halo(ops, comm, ws)
+            for i, op in enumerate(ops):
+                op.vec_pcg_q(us[i], ws[i], slot[i][1:2])
+
+    # r_0, u_0, w_0 and the first scalars (slot 0); slot B-1 = "iteration -1" (gamma 0)
+    for op, x, s_ in zip(ops, xs, ss):
+        op.matvec_partial(x, s_)
+    halo(ops, comm, ss)
+    slot0 = [rg[0] for rg in ring]
+    for i, op in enumerate(ops):
+        op.vec_jacobi(0.0, prob.b[i], ss[i], None, xs[i], None, rs[i], slot0[i][2:3])
+        op.vec_pcg_direction(zero, zero, prob.dinv[i], rs[i], us[i])  # u = dinv r
+        op.dot_owned(rs[i], us[i], slot0[i][0:1])
+        ss[i].zero_()
+    matvec_w(slot0)
+    comm.allreduce([sl[0:3] for sl in slot0])
+    norm2 = [torch.zeros(iters + 1, **f64) for _ in ops]
+    for i in range(len(ops)):
+        rr0[i].copy_(slot0[i][2:3])
+        norm2[i][0:1].copy_(slot0[i][2:3])
+
+    def step(k):
+        cur = [rg[k % B] for rg in ring]
+        prev = [rg[(k - 1) % B] for rg in ring]
+        nxt = [rg[(k + 1) % B] for rg in ring]
+        for i, op in enumerate(ops):
+            op.vec_cg1_update(cur[i], prev[i], rr0[i], tol_, ctl[i], prob.dinv[i], xs[i], rs[i],
+                              us[i], ws[i], ps[i], ss[i], nxt[i])
+        matvec_w(nxt)
+        comm.allreduce([sl[0:3] for sl in nxt])
+
+    g = None
+    if graph and iters >= B and _graph_ok(ops):
+        def body():
+            for u in range(B):
+                step(u)
+        g = _capture(comm, body)  # recorded only: nothing ran, the ring is untouched
+    # batches of B iterations (graph replay or eager); the stop flags of batch j are read
+    # while batch j+1 is queued, so the device never waits for the host
+    on_dev = dev.type == "cuda"
+    host_ctl = [torch.zeros((2, 4), dtype=torch.int32, pin_memory=on_dev) for _ in ops]
+    pending = None
+    k, j = 0, 0
+    while k < iters:
+        nb = min(B, iters - k)
+        if g is not None and nb == B:
+            g.replay()
+            for i in range(len(ops)):  # iterations k..k+B-1 wrote slots 1..B-1, 0
+                norm2[i][k + 1:k + B].copy_(ring[i][1:B, 2])
+                norm2[i][k + B:k + B + 1].copy_(ring[i][0:1, 2])
+        else:
+            for kk in range(k, k + nb):
+                step(kk)
+                for i in range(len(ops)):
+                    norm2[i][kk + 1:kk + 2].copy_(ring[i][(kk + 1) % B, 2:3])
+        k += nb
+        if k >= iters:
+            break
+        for i in range(len(ops)):
+            host_ctl[i][j & 1].copy_(ctl[i], non_blocking=on_dev)
+        ev = torch.cuda.Event() if on_dev else None
+        if ev is not None:
+            ev.record()
+        if pending is not None:  # batch j-1's flags, while batch j runs
+            pev, pj = pending
+            if pev is not None:
+                pev.synchronize()
+            if any(int(h[pj & 1][0]) for h in host_ctl):
+                break
+        pending = (ev, j)
+        j += 1
+    sync = getattr(comm, "sync", None)
+    if sync is not None:
+        sync()
+    c = ctl[0].cpu()
+    for op in ops:
+        if hasattr(op, "set_stop"):
+            op.set_stop(None)
+    n = int(c[1]) + 1 if int(c[0]) else iters + 1
+    norms = torch.sqrt(norm2[0][:n]).cpu().numpy()
+    diverged = _diverged(prob, norms)  # collective: every rank calls it
+    prob.diverged = diverged or bool(int(c[3]))
+    return xs, norms
+
+
+def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False,
+                        fused=None):
+    """The oracle's recurrence: two scalar all-reduces per iteration, both in place and
     with no copies between the kernels: the rank's p.q (the interface kernel adds the two
     sweep partials to its own) and the iteration's [r.r, r.z] pair, kept in a ring of
     GRAPH_BATCH slots that the next iteration reads as its rz.  graph=True (fixed iteration
@@ -769,7 +945,7 @@ def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused
         if tol is not None:
             nk = float(torch.sqrt(norm2[0][kk]))
             n0 = nk if n0 is None else n0
-            if nk <= tol * n0:
+            if nk <= tol * n0 or not np.isfinite(nk):
                 k_done = kk
                 break
         step(kk % B)

@@ -103,6 +103,32 @@ class CpuRankOperator:
         beta = float(rz_new[0]) / float(rz_old[0]) if float(rz_old[0]) != 0.0 else 0.0
         p.copy_(dinv * r + beta * p)
 
+    def vec_cg1_update(self, cur, prev, rr0, tol, ctl, dinv, x, r, u, w, p, s, nxt):
+        """ebs_vec_cg1_update (include/ebs.h) restated with torch CPU ops."""
+        if int(ctl[0]):
+            return
+        gamma, delta, rr = (float(v) for v in cur[0:3])
+        nk = rr ** 0.5 if rr >= 0 else float("nan")
+        if not np.isfinite(nk) or (tol >= 0 and nk <= tol * float(rr0[0]) ** 0.5):
+            ctl[1] = ctl[2]
+            ctl[3] = 0 if np.isfinite(nk) else 1
+            ctl[0] = 1
+            return
+        g_prev, a_prev = float(prev[0]), float(prev[3])
+        beta = gamma / g_prev if g_prev != 0.0 else 0.0
+        denom = delta - beta * gamma / a_prev if (beta != 0.0 and a_prev != 0.0) else delta
+        alpha = gamma / denom if denom != 0.0 else 0.0
+        p.copy_(u + beta * p)
+        s.copy_(w + beta * s)
+        x.add_(alpha * p)
+        r.sub_(alpha * s)
+        u.copy_(dinv * r)
+        o = self.owned.bool()
+        nxt[0] = (r * u)[o].sum()
+        nxt[2] = (r * r)[o].sum()
+        cur[3] = alpha
+        ctl[2] += 1
+
     def dot_owned(self, x, y, red):
         red.copy_((x * y)[self.owned.bool()].sum().reshape(1))
 

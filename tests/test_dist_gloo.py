@@ -63,11 +63,19 @@ def _worker(rank, world, port, case, out):
         r_glob = D.gather_global([op], r, n, comm)
         xj, nj = D.jacobi(prob, [op.to_internal(torch.zeros(n, dtype=torch.float64))], 30, 0.8)
         xj_glob = D.gather_global([op], xj, n, comm)
-        xp, npcg = D.pcg(prob, [op.to_internal(torch.zeros(n, dtype=torch.float64))], 400, tol=1e-8)
-        xp_glob = D.gather_global([op], xp, n, comm)
+        res = {}
+        for red in (1, 2):  # single-reduction (Chronopoulos-Gear) and textbook recurrences
+            xp, npcg = D.pcg(prob, [op.to_internal(torch.zeros(n, dtype=torch.float64))], 400,
+                             tol=1e-8, reductions=red)
+            assert not prob.diverged
+            res[f"xp{red}"] = D.gather_global([op], xp, n, comm).numpy()
+            res[f"npcg{red}"] = npcg
+            # fixed count (no tol): the full history
+            _, nfix = D.pcg(prob, [op.to_internal(torch.zeros(n, dtype=torch.float64))], 9,
+                            reductions=red)
+            res[f"nfix{red}"] = nfix
         if rank == 0:
-            out.put(dict(r=r_glob.numpy(), xj=xj_glob.numpy(), nj=nj, xp=xp_glob.numpy(),
-                         npcg=npcg, x=x.numpy()))
+            out.put(dict(r=r_glob.numpy(), xj=xj_glob.numpy(), nj=nj, x=x.numpy(), **res))
     finally:
         dist.destroy_process_group()
 
@@ -101,8 +109,13 @@ def test_gloo_world2_matches_oracle(case):
     np.testing.assert_allclose(res["nj"], hj["residual_norms"], rtol=1e-10)
     assert np.linalg.norm(res["xj"] - xj) <= 1e-10 * np.linalg.norm(xj)
     xp, hp = o.pcg(A, b_e, indt, nd, x0, 400, tol=1e-8)
-    assert len(res["npcg"]) == len(hp["residual_norms"])
-    assert np.linalg.norm(res["xp"] - xp) <= 1e-8 * np.linalg.norm(xp)
+    _, hfix = o.pcg(A, b_e, indt, nd, x0, 9)
+    for red in (1, 2):
+        assert len(res[f"npcg{red}"]) == len(hp["residual_norms"]), red
+        np.testing.assert_allclose(res[f"npcg{red}"], hp["residual_norms"], rtol=1e-6)
+        assert np.linalg.norm(res[f"xp{red}"] - xp) <= 1e-8 * np.linalg.norm(xp), red
+        assert len(res[f"nfix{red}"]) == 10
+        np.testing.assert_allclose(res[f"nfix{red}"], hfix["residual_norms"], rtol=1e-9)
 
 
 def _agree_worker(rank, world, port, out):
