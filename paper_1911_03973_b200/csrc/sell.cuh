@@ -122,6 +122,13 @@ struct Pack<4> {
     }
 };
 
+// How a sweep reads the vector it multiplies (x[i] for internal node i): the read-only
+// path (the vector is not written during the kernel).
+struct XLdg {
+    const double *__restrict__ x;
+    __device__ __forceinline__ double operator()(int i) const { return __ldg(x + i); }
+};
+
 template <int NB>
 __device__ __forceinline__ double pick(int t, double xo, const double (&g)[NB - 1]) {
     // t = (i - j - 1) mod NB: position of vertex i in the cyclic neighbour list; NB-1 = self
@@ -152,6 +159,9 @@ __device__ __forceinline__ double row_product_sel(int j, const double (&a)[NB], 
 // branch is taken only when j is uniform over the active lanes.  Measured: C3 2980 ->
 // 3130, C5 361 -> 369, C4 1656 -> 1720 it/s, C2 internal matvec 126 -> 121 us.  SW =
 // false (the bit-exact residual, which spills at 32 registers with the branches): selects.
+#ifndef EBS_TUPLE_PIPE
+#define EBS_TUPLE_PIPE 1  // tuple-coded plans: codes one slot ahead (see sell_sweep)
+#endif
 #ifndef EBS_ROW_SWITCH
 #define EBS_ROW_SWITCH 1
 #endif
@@ -190,9 +200,9 @@ __device__ __forceinline__ double row_product(int j, const double (&a)[NB], doub
 #define EBS_MINB3 6  // min resident 256-thread CTAs per SM, 3D SELL kernels
 #endif
 
-template <int NB, int IDS, bool EXACT>
+template <int NB, int IDS, bool EXACT, class XL>
 __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0, int w, int lane,
-                                                int64_t m, int c_m, const double *__restrict__ x,
+                                                int64_t m, int c_m, const XL &x,
                                                 double xo, const int32_t *stab) {
     constexpr int U = NB == 3 ? EBS_U2 : EBS_U3;
     double s = 0.0;
@@ -275,7 +285,7 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int t = 0; t < NB - 1; ++t)
-                g[u][t] = k0 + u < c_m ? __ldg(x + nid[u][t]) : 0.0;
+                g[u][t] = k0 + u < c_m ? x(nid[u][t]) : 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (k0 + u < c_m) {
@@ -332,11 +342,10 @@ struct IdWord {
 // One slot in flight, with the id word of slot k+1 loaded while slot k is processed, so
 // the x gathers of a slot issue at the start of its iteration (overlapping the A-row
 // loads) instead of waiting a DRAM round trip for the ids.
-template <int NB, int IDS, bool EXACT>
+template <int NB, int IDS, bool EXACT, class XL>
 __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t row0, int w,
-                                                     int lane, int64_t m, int c_m,
-                                                     const double *__restrict__ x, double xo,
-                                                     const int32_t *stab) {
+                                                     int lane, int64_t m, int c_m, const XL &x,
+                                                     double xo, const int32_t *stab) {
     double s = 0.0;
     IdWord<NB, IDS> nxt;
     if (0 < c_m) nxt.load(v, row0, lane);
@@ -348,7 +357,7 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
             const int j = cur.decode(v, m, nid, stab);
             double g[NB - 1];
 #pragma unroll
-            for (int t = 0; t < NB - 1; ++t) g[t] = __ldg(x + nid[t]);
+            for (int t = 0; t < NB - 1; ++t) g[t] = x(nid[t]);
             const double *ap = reinterpret_cast<const double *>(rp) + lane;
             double a[NB];
 #pragma unroll
@@ -365,45 +374,80 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
 }
 
 
-#ifndef EBS_TUPLE_PIPE
-#define EBS_TUPLE_PIPE 1
-#endif  // tuple-coded plans: codes one slot ahead (see PIPE below)
+// Per-warp shared-memory table of the id coding (IDS_TABLE: per chunk; IDS_TUPLE: the
+// plan's tuples, loaded once).
+template <int NB, int IDS>
+struct SellStab {
+    static constexpr int CAP = IDS == IDS_TABLE ? Tab<NB>::CAP : (IDS == IDS_TUPLE ? 4 * TUPLE_CAP : 1);
+};
 
-// Grid-stride sweep over chunks: epi(m, s, xo) for every valid node (direct loads).
-template <int NB, int IDS, bool EXACT, bool PIPE, class Epi>
-__device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *__restrict__ x,
-                                               Epi &epi) {
-    constexpr int CAP = IDS == IDS_TABLE ? Tab<NB>::CAP : (IDS == IDS_TUPLE ? 4 * TUPLE_CAP : 1);
-    __shared__ __align__(16) int32_t stab_all[256 / LANES][CAP];  // one table per warp
+template <int NB, int IDS>
+__device__ __forceinline__ int32_t *sell_stab_init(const SellView &v, int32_t (*stab_all)[SellStab<NB, IDS>::CAP]) {
     const int lane = threadIdx.x & (LANES - 1);
     int32_t *stab = stab_all[threadIdx.x / LANES];
     if constexpr (IDS == IDS_TUPLE) {
         for (int i = lane; i < TUPLE_CAP; i += LANES) reinterpret_cast<int4 *>(stab)[i] = v.tup[i];
         __syncwarp();
     }
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / LANES;
-    for (int64_t ci = warp; ci < v.nlist; ci += nwarps) {
-        const int64_t c = v.clist ? (int64_t)v.clist[ci] : ci;
-        if constexpr (IDS == IDS_TABLE) {
-            const int t0 = v.taboff[c], t1 = v.taboff[c + 1];
-            __syncwarp();
-            for (int i = lane; i < t1 - t0; i += LANES) stab[i] = v.tab[t0 + i];
-            __syncwarp();
-        }
-        const int64_t m = c * LANES + lane;
-        const bool valid = m < v.n_n;
-        const int c_m = valid ? (v.cnt8 ? (int)v.cnt8[m] : v.cnt[m]) : 0;
-        const double xo = valid ? x[m] : 0.0;
-        double s;
-        if constexpr ((PIPE || (IDS == IDS_TUPLE && EBS_TUPLE_PIPE)) && IDS != IDS_TABLE &&
-                      IDS != IDS_DELTA2 && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
-            s = sell_node_sum_pipe<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m, c_m, x,
-                                                   xo, stab);
-        else
-            s = sell_node_sum<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, m, c_m, x, xo,
-                                              stab);
-        if (valid) epi(m, s, xo);
+    return stab;
+}
+
+// One chunk c (32 consecutive internal nodes, one per lane): the node sum s of this lane's
+// node m (and xo = x[m]); `valid` false for the padding lanes of the last chunk.
+struct ChunkSum {
+    int m;
+    bool valid;
+    double s, xo;
+};
+
+template <int NB, int IDS, bool EXACT, bool PIPE, class XL>
+__device__ __forceinline__ ChunkSum sell_chunk_sum(const SellView &v, int c, int lane,
+                                                   int32_t *stab, const XL &x) {
+    if constexpr (IDS == IDS_TABLE) {
+        const int t0 = v.taboff[c], t1 = v.taboff[c + 1];
+        __syncwarp();
+        for (int i = lane; i < t1 - t0; i += LANES) stab[i] = v.tab[t0 + i];
+        __syncwarp();
+    }
+    ChunkSum r;
+    r.m = c * LANES + lane;
+    r.valid = r.m < v.n_n;
+    const int c_m = r.valid ? (v.cnt8 ? (int)v.cnt8[r.m] : v.cnt[r.m]) : 0;
+    r.xo = r.valid ? x(r.m) : 0.0;
+    if constexpr ((PIPE || (IDS == IDS_TUPLE && EBS_TUPLE_PIPE)) && IDS != IDS_TABLE &&
+                  IDS != IDS_DELTA2 && (NB == 3 ? EBS_U2 : EBS_U3) == 1)
+        r.s = sell_node_sum_pipe<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, r.m, c_m, x,
+                                                 r.xo, stab);
+    else
+        r.s = sell_node_sum<NB, IDS, EXACT>(v, v.rowbase[c], v.width[c], lane, r.m, c_m, x,
+                                            r.xo, stab);
+    return r;
+}
+
+// ... and its epilogue: epi(m, s, xo) per valid node.
+template <int NB, int IDS, bool EXACT, bool PIPE, class XL, class Epi>
+__device__ __forceinline__ void sell_chunk(const SellView &v, int c, int lane, int32_t *stab,
+                                           const XL &x, Epi &epi) {
+    const ChunkSum r = sell_chunk_sum<NB, IDS, EXACT, PIPE>(v, c, lane, stab, x);
+    if (r.valid) epi(r.m, r.s, r.xo);
+}
+
+// Grid-stride sweep over chunks: epi(m, s, xo) for every valid node (direct loads).
+template <int NB, int IDS, bool EXACT, bool PIPE, class Epi>
+__device__ __forceinline__ void sell_sweep_ldg(const SellView &v, const double *__restrict__ x,
+                                               Epi &epi) {
+    __shared__ __align__(16) int32_t stab_all[256 / LANES][SellStab<NB, IDS>::CAP];  // per warp
+    const int lane = threadIdx.x & (LANES - 1);
+    int32_t *stab = sell_stab_init<NB, IDS>(v, stab_all);
+    const XLdg xl{x};
+    // 32-bit chunk / node indices (plans hold < 2^30 nodes): the 64-bit loop counter of
+    // the 2D kernels was the one value spilled at their 32-register cap
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+    const int nwarps = (int)((gridDim.x * blockDim.x) / LANES);
+    const int nlist = (int)v.nlist;
+    for (int ci = warp; ci < nlist; ci += nwarps) {
+        const int c = v.clist ? v.clist[ci] : ci;
+        sell_chunk<NB, IDS, EXACT, PIPE>(v, c, lane, stab, xl, epi);
     }
 }
 

@@ -44,72 +44,102 @@ __device__ __forceinline__ void flag_nonfinite(Ctl *ctl, bool bad) {
 }
 
 // ---------------------------------------------------------- Richardson/Jacobi --
-// stationary steps on the _iterate loop:
-//   0 Richardson x + omega*r            1 Jacobi x + omega*(dinv*r)
-//   4 Chebyshev-2 x + a_k*r             5 Chebyshev-3 p = k ? r + b_k*p : r;  x + a_k*p
+// stationary steps on the _iterate loop, KIND (template) x method:
+//   JK_PLAIN  x + omega*r       Richardson (omega), Chebyshev-2 (omega = a_k)
+//   JK_JACOBI x + omega*(dinv*r)
+//   JK_CHEB3  p = k ? r + b_k*p : r;  x + a_k*p
+// The loop-invariant pointers come from a __grid_constant__ argument block (read from
+// the constant bank where used, never held in registers): with the per-method template
+// the 2D kernels fit the 32-register cap of 64 warps/SM without spilling.
+constexpr int JK_PLAIN = 0, JK_JACOBI = 1, JK_CHEB3 = 2;
+
+struct JacArgs {
+    const double *b_int;
+    const uint8_t *free_int;
+    const double *dinv;
+    const double *ref;
+    double *r_out;
+    double *xa, *xb;
+    double *pbuf;
+    const double *ca, *cb;
+    int final_step;
+};
+
+template <int KIND, bool EXACT>
 struct JacobiEpi {
-    const double *__restrict__ b_int;
-    const uint8_t *__restrict__ free_int;
-    const double *__restrict__ dinv;
-    const double *__restrict__ ref;
-    double *__restrict__ r_out;
-    double *__restrict__ xn_buf;
-    double *__restrict__ p;
-    double omega, coef_b;
-    int method, k, exact, final_step;
-    double part[2];
-    bool bad;
+    const JacArgs &A;
+    const LoopArgs &L;
+    double part[1];
     __device__ __forceinline__ void operator()(int64_t m, double s, double xo) {
-        double r = exact ? s : b_int[m] - s;
-        if (!free_int[m]) r = 0.0;
+        double r = EXACT ? s : A.b_int[m] - s;
+        if (!A.free_int[m]) r = 0.0;
         part[0] += r * r;
-        if (ref) {
-            double d = xo - ref[m];
-            part[1] += d * d;
-        }
-        if (r_out) r_out[m] = r;
-        if (!final_step) {
+        if (A.r_out) A.r_out[m] = r;
+        if (!A.final_step) {
+            // the step's scalars are re-read here (L1 / constant-bank hits) instead of
+            // being carried in registers across the sweep: no spills at 32 registers
+            const int k = __ldg(&L.ctl->k);
+            double *xn_buf = (k & 1) ? A.xa : A.xb;
             double xn;
-            if (method == EBS_JACOBI) {
-                xn = xo + omega * (dinv[m] * r);
-            } else if (method == EBS_CHEB3) {
-                double pm = k == 0 ? r : r + coef_b * p[m];
-                p[m] = pm;
-                xn = xo + omega * pm;
+            if constexpr (KIND == JK_JACOBI) {
+                xn = xo + L.omega * (A.dinv[m] * r);
+            } else if constexpr (KIND == JK_CHEB3) {
+                const double om = __ldg(A.ca + k);
+                double pm = k == 0 ? r : r + __ldg(A.cb + k) * A.pbuf[m];
+                A.pbuf[m] = pm;
+                xn = xo + om * pm;
             } else {
-                xn = xo + omega * r;  // Richardson (omega) and Chebyshev-2 (omega = a_k)
+                const double om = A.ca ? __ldg(A.ca + k) : L.omega;
+                xn = xo + om * r;
             }
             xn_buf[m] = xn;
-            bad |= !isfinite(xn);
+            if (!isfinite(xn)) flag_nonfinite(L.ctl, true);  // rare: no per-thread flag
         }
     }
 };
 
-template <int NB, int IDS, bool EXACT>
-__global__ void EBS_SELL_BOUNDS(NB)
-    k_jacobi_step(SellView v, LoopArgs L, double *__restrict__ xa, double *__restrict__ xb,
-                  const double *__restrict__ b_int, const uint8_t *__restrict__ free_int,
-                  const double *__restrict__ dinv, const double *__restrict__ ref,
-                  double *__restrict__ r_out, int final_step, int method,
-                  const double *__restrict__ ca, const double *__restrict__ cb,
-                  double *__restrict__ pbuf) {
+// ||x_k - ref||^2 of the iterate step k reads (the stationary loop with a reference
+// solution, solvers.py:146-148): its own fixed-order reduction, launched before the step,
+// so the step kernel carries one accumulator (no spills at the 2D register cap).
+__global__ void __launch_bounds__(256)
+    k_err_norm(int64_t n, LoopArgs L, const double *__restrict__ xa,
+               const double *__restrict__ xb, const double *__restrict__ ref) {
     Ctl *ctl = L.ctl;
     if (ctl->done) return;
     const int k = ctl->k;
     const double *x = (k & 1) ? xb : xa;
-    const bool cheb = method == EBS_CHEB2 || method == EBS_CHEB3;
-    const double om = (cheb && !final_step) ? ca[k] : L.omega;
-    const double cbk = (method == EBS_CHEB3 && !final_step) ? cb[k] : 0.0;
-    JacobiEpi epi{b_int, free_int, dinv, ref, r_out, (k & 1) ? xa : xb, pbuf, om, cbk, method, k,
-                  EXACT ? 1 : 0, final_step, {0.0, 0.0}, false};
-    sell_sweep<NB, IDS, EXACT, NB == 3>(v, x, epi);
-    flag_nonfinite(ctl, epi.bad);
-    double tot[2];
-    if (!grid_sum_last<2>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
+    double part[1] = {0.0};
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const double d = x[m] - ref[m];
+        part[0] += d * d;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, L.partials, &ctl->counter, tot) && threadIdx.x == 0)
+        L.errors[k] = sqrt(tot[0]);
+}
+
+#ifndef EBS_JAC_MINB2
+#define EBS_JAC_MINB2 EBS_MINB2
+#endif
+#ifndef EBS_JAC_PIPE
+#define EBS_JAC_PIPE 1
+#endif
+template <int NB, int IDS, bool EXACT, int KIND>
+__global__ void __launch_bounds__(256, (NB) == 3 ? EBS_JAC_MINB2 : EBS_MINB3)
+    k_jacobi_step(SellView v, const __grid_constant__ LoopArgs L,
+                  const __grid_constant__ JacArgs A) {
+    Ctl *ctl = L.ctl;
+    if (ctl->done) return;
+    const int k = ctl->k;
+    JacobiEpi<KIND, EXACT> epi{A, L, {0.0}};
+    sell_sweep<NB, IDS, EXACT, NB == 3 && EBS_JAC_PIPE>(v, (k & 1) ? A.xb : A.xa, epi);
+    double tot[1];
+    if (!grid_sum_last<1>(epi.part, L.partials, &ctl->counter, tot) || threadIdx.x != 0) return;
     // ---- loop rules (single thread) ----
+    __threadfence();  // the rare non-finite flags of this grid (flag_nonfinite) are visible
     const double nr = sqrt(tot[0]);
     L.norms[k] = nr;
-    if (L.errors) L.errors[k] = sqrt(tot[1]);
     if (k == 0) ctl->norm0 = nr;
     ctl->n_norms = k + 1;
     ctl->cb_ok = 1;
@@ -119,7 +149,7 @@ __global__ void EBS_SELL_BOUNDS(NB)
         ctl->done = 1;
         return;
     }
-    if (final_step) {
+    if (A.final_step) {
         ctl->done = 1;
         return;
     }
@@ -1092,17 +1122,30 @@ int ebs_solve(ebs_plan_t plan, const ebs_solve_params *P, void *stream) {
         const bool exact = P->exact != 0;
         double *rcb = (cb || P->r_out) ? r_int : nullptr;
         auto step = [&](int final_step, cudaStream_t st) {
-#define EBS_JAC(NB_, PK_, EX_)                                                              \
+            if (ref_int) {
+                k_err_norm<<<vgrid, 256, 0, st>>>(n, L, xa, xb, ref_int);
+                LAUNCHED();
+            }
+            JacArgs A{p->b_int, p->free_int, dv, ref_int, rcb, xa, xb, pbuf, coef_a, coef_b,
+                      final_step};
+            const int kind = P->method == EBS_JACOBI ? JK_JACOBI
+                                                     : (P->method == EBS_CHEB3 ? JK_CHEB3 : JK_PLAIN);
+#define EBS_JAC(NB_, PK_, EX_, KD_)                                                         \
     {                                                                                       \
-        auto kern = k_jacobi_step<NB_, PK_, EX_>;                                           \
+        auto kern = k_jacobi_step<NB_, PK_, EX_, KD_>;                                      \
         const SellLaunch SL = sell_launch((const void *)kern, NB_, p->rowb, p->n_chunks);   \
-        kern<<<SL.grid, SL.block, SL.smem, st>>>(v, L, xa, xb, p->b_int, p->free_int, dv,   \
-                                                 ref_int, rcb,                              \
-                                 final_step, P->method, coef_a, coef_b, pbuf);              \
+        kern<<<SL.grid, SL.block, SL.smem, st>>>(v, L, A);                                  \
     }
-#define EBS_JAC_T(NB_, IDS_) { if (exact) EBS_JAC(NB_, IDS_, true) else EBS_JAC(NB_, IDS_, false) }
+#define EBS_JAC_K(NB_, PK_, EX_)                                                            \
+    {                                                                                       \
+        if (kind == JK_JACOBI) EBS_JAC(NB_, PK_, EX_, JK_JACOBI)                            \
+        else if (kind == JK_CHEB3) EBS_JAC(NB_, PK_, EX_, JK_CHEB3)                         \
+        else EBS_JAC(NB_, PK_, EX_, JK_PLAIN)                                               \
+    }
+#define EBS_JAC_T(NB_, IDS_) { if (exact) EBS_JAC_K(NB_, IDS_, true) else EBS_JAC_K(NB_, IDS_, false) }
             EBS_SELL_DISPATCH(p, EBS_JAC_T);
 #undef EBS_JAC_T
+#undef EBS_JAC_K
 #undef EBS_JAC
             LAUNCHED();
         };
