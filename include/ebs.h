@@ -84,6 +84,15 @@ int ebs_mesh_check(int dim, int64_t n_n, int64_t n_e, const double *nodes,
 /* signed area (mesh.py:96-101) / volume per element */
 int ebs_mesh_measure(int dim, int64_t n_e, const double *nodes, const int32_t *conn,
                      double *measure, void *stream);
+/* uniform_refine (mesh.py:157-208): red refinement of a triangle mesh -- 4 children per
+ * triangle through the edge midpoints 0.5*(x[lo] + x[hi]), nodes renumbered ascending in
+ * (y, x), each child rotated to start at its smallest node (orientation kept), children
+ * sorted ascending; a structured level-L mesh becomes build_unit_square_mesh(L+1) bit for bit.
+ * coords (n_n, 2) f64, conn (3, n_e) int32 SoA; coords_out needs room for n_n + 3 n_e
+ * nodes, conn_out (3, 4 n_e); *n_out (HOST) = the refined node count.  Synchronises
+ * `stream` (the node count is data dependent). */
+int ebs_refine_tri(int64_t n_n, int64_t n_e, const double *coords, const int32_t *conn,
+                   double *coords_out, int32_t *conn_out, int64_t *n_out, void *stream);
 /* NEW: relabel nodes, new id of old node i = perm[i] (BASELINE C2/C4 recipe). */
 int ebs_mesh_permute(int dim, int64_t n_n, int64_t n_e, const int64_t *perm,
                      const double *nodes, const int32_t *conn, double *nodes_out,

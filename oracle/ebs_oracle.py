@@ -27,7 +27,7 @@ import numpy as np
 __all__ = [
     "MAX_LEVEL", "BOUNDARY_TOL", "EPS_AREA", "EPS_VOLUME",
     "MASS_PATTERN_2D", "MASS_PATTERN_3D", "KUHN_PERMS",
-    "grid_mesh", "unit_square_mesh", "kuhn_cube_mesh", "detect_boundary",
+    "grid_mesh", "unit_square_mesh", "kuhn_cube_mesh", "detect_boundary", "uniform_refine",
     "detect_face_z0", "signed_measure", "jitter_interior", "permute_mesh",
     "element_matrices", "centroids", "assemble_rhs", "local_residuals",
     "residual", "matvec_masked", "diagonal", "mask", "initial_guess",
@@ -118,6 +118,31 @@ def kuhn_cube_mesh(N: int):
             v2, v3 = v3, v2
         elements[t::6] = np.column_stack([v0, v1, v2, v3])
     return nodes, elements, detect_face_z0(nodes)
+
+
+def uniform_refine(nodes, elements):
+    """mesh.py:157-208 restated: 4 children per triangle through the edge midpoints
+    (one per geometric edge, edges as sorted node pairs in np.unique order, midpoint
+    0.5*(x[lo] + x[hi])), nodes renumbered by np.lexsort((x, y)), each child rotated to
+    its smallest node, rows sorted by np.lexsort((c2, c1, c0)).
+    Returns (fine_nodes, fine_elements)."""
+    n = nodes.shape[0]
+    tri = np.asarray(elements, dtype=np.int64)
+    edges = np.sort(np.concatenate([tri[:, [0, 1]], tri[:, [1, 2]], tri[:, [2, 0]]]), axis=1)
+    uniq, inv = np.unique(edges, axis=0, return_inverse=True)
+    ab, bc, ca = n + inv.reshape(3, -1)
+    xy = np.vstack([nodes, 0.5 * (nodes[uniq[:, 0]] + nodes[uniq[:, 1]])])
+    a, b, c = tri.T
+    kids = np.concatenate([np.column_stack(t) for t in
+                           ((a, ab, ca), (ab, b, bc), (ca, bc, c), (ab, bc, ca))])
+    order = np.lexsort((xy[:, 0], xy[:, 1]))
+    rank = np.empty(len(xy), dtype=np.int64)
+    rank[order] = np.arange(len(xy))
+    kids = rank[kids]
+    shift = np.argmin(kids, axis=1)
+    kids = np.take_along_axis(kids, (shift[:, None] + np.arange(3)) % 3, axis=1)
+    kids = kids[np.lexsort((kids[:, 2], kids[:, 1], kids[:, 0]))]
+    return xy[order], kids
 
 
 def signed_measure(nodes, elements):

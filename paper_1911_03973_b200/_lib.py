@@ -95,6 +95,8 @@ SIGNATURES = {
     "ebs_power_iteration": (c_int, [c_void_p, c_void_p, c_int, c_double, POINTER(c_double),
                                     POINTER(c_int), c_void_p]),
     "ebs_gather": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_refine_tri": (c_int, [c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                               POINTER(c_int64), c_void_p]),
     "ebs_scatter_add": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_index_fill": (c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p]),
     "ebs_index_copy": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -262,52 +262,26 @@ def jitter_interior(m: Mesh, delta) -> Mesh:
     return Mesh(nodes, None, m.boundary_nodes, level=None, conn=m.conn)
 
 
-# corners of the 4 children in terms of (a, b, c, mid(ab), mid(bc), mid(ca))
-_CHILD_CORNERS = ((0, 3, 5), (3, 1, 4), (5, 4, 2), (3, 4, 5))
-
-
-def _stable_lexsort(keys) -> torch.Tensor:
-    """Permutation sorting rows by keys[0], ties by keys[1], ... (stable passes from the
-    least significant key, like np.lexsort with the key order reversed)."""
-    order = None
-    for key in reversed(keys):
-        k = key if order is None else key[order]
-        step = torch.argsort(k, stable=True)
-        order = step if order is None else order[step]
-    return order
-
-
 def uniform_refine(m: Mesh) -> Mesh:
     """Red refinement of a triangle mesh on the device (mesh.py:157-208 semantics): every
     triangle becomes 4 through its edge midpoints, then the mesh is renumbered
     canonically -- nodes ascending in (y, x), each triangle rotated to start at its
     smallest node (orientation kept), triangles ascending -- so a structured level-L
-    mesh refines to exactly build_unit_square_mesh(L + 1)."""
+    mesh refines to exactly build_unit_square_mesh(L + 1).  One libebs call
+    (ebs_refine_tri: radix-sorted edge keys, two stable coordinate sorts, child sort)."""
     if m.dim != 2:
         raise ValueError("uniform_refine splits triangles; got a tetrahedral mesh")
     if (m.level is not None and m.level >= MAX_LEVEL) or 2 * m.n_elements > 4**MAX_LEVEL:
         raise ValueError(f"the refined mesh would exceed the size guard (level {MAX_LEVEL})")
-    n = m.n_nodes
-    tri = m.conn.to(torch.int64)                                    # (3, n_e)
-    # the three edges of every element as one sortable key lo * n + hi
-    ends = torch.stack([tri, tri.roll(-1, dims=0)])                 # (2, 3, n_e): ab, bc, ca
-    key = ends.min(0).values * n + ends.max(0).values
-    edge_keys, mid_id = torch.unique(key.reshape(-1), return_inverse=True)
-    mids = 0.5 * (m.nodes[edge_keys // n] + m.nodes[edge_keys % n])
-    xy = torch.cat([m.nodes, mids])
-    corners = torch.cat([tri, n + mid_id.reshape(3, -1)])           # (6, n_e)
-    kids = corners[torch.tensor(_CHILD_CORNERS, device=tri.device)]  # (4, 3, n_e)
-    kids = kids.permute(0, 2, 1).reshape(-1, 3)
-    # canonical node numbering by (y, x)
-    order = _stable_lexsort([xy[:, 1], xy[:, 0]])
-    new_id = torch.empty_like(order)
-    new_id[order] = torch.arange(order.numel(), device=order.device)
-    kids = new_id[kids]
-    first = kids.argmin(dim=1, keepdim=True)
-    kids = kids.gather(1, (first + torch.arange(3, device=kids.device)) % 3)
-    kids = kids[_stable_lexsort([kids[:, 0], kids[:, 1], kids[:, 2]])]
-    nodes = xy[order].contiguous()
-    return Mesh(nodes, kids, _boundary_from_flags(nodes, 0),
+    import ctypes
+    n, n_e = m.n_nodes, m.n_elements
+    xy = D.empty((n + 3 * n_e, 2))
+    conn = D.empty((3, 4 * n_e), torch.int32)
+    n_out = ctypes.c_int64(0)
+    call("ebs_refine_tri", n, n_e, D.ptr(m.nodes.contiguous()), D.ptr(m.conn), D.ptr(xy),
+         D.ptr(conn), ctypes.byref(n_out), D.stream())
+    nodes = xy[:n_out.value].contiguous()
+    return Mesh(nodes, None, _boundary_from_flags(nodes, 0), conn=conn,
                 level=None if m.level is None else m.level + 1)
 
 

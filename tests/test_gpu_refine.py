@@ -55,3 +55,23 @@ def test_export_mesh_roundtrip(gpu, tmp_path):
     eb.export_mesh(m, tmp_path)
     npt.assert_array_equal(np.loadtxt(tmp_path / "nodes.txt"), to_np(m.nodes))
     npt.assert_array_equal(np.loadtxt(tmp_path / "elements.txt", dtype=np.int64), to_np(m.elements))
+
+
+def test_refine_is_native_and_large(gpu):
+    """ebs_refine_tri (libebs) at size: level 9 -> 10 equals the generator bit for bit, and
+    a jittered + permuted (unstructured numbering) mesh refines like the oracle restatement
+    of mesh.py:157-208."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200._lib import launch_count
+    n0 = launch_count()
+    fine = eb.uniform_refine(eb.build_unit_square_mesh(9))
+    assert launch_count() > n0  # device kernels, not host code
+    direct = eb.build_unit_square_mesh(10)
+    npt.assert_array_equal(to_np(fine.nodes), to_np(direct.nodes))
+    npt.assert_array_equal(to_np(fine.conn), to_np(direct.conn))
+    inp = o.config_inputs(4, seed=3, size=5)
+    m = eb.Mesh(inp["nodes"], inp["elements"], inp["dirichlet"])
+    fine = eb.uniform_refine(m)
+    ref_nodes, ref_elements = o.uniform_refine(inp["nodes"], inp["elements"])
+    npt.assert_array_equal(to_np(fine.nodes), ref_nodes)
+    npt.assert_array_equal(to_np(fine.elements), ref_elements)
