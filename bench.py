@@ -126,28 +126,78 @@ def oracle_residual_rate(A, b_e, indt, x, budget_s=10.0, min_calls=3, threads=No
     return x.shape[0] * calls / dt / 1e9, T, calls, dt
 
 
-def run_reference(args):
-    """--impl reference: the reference algorithm (CPU oracle port) on this host."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_package():
+    """The unmodified reference package `ebsolve`, pip-installed into baseline/_ref
+    (`python -m pip install --no-index --no-build-isolation --no-deps --target
+    baseline/_ref <copy of /root/reference/pkg>`), or None when it is not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "ebsolve")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import ebsolve
+        return ebsolve
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def reference_c2_inputs(eb_ref, seed, size):
+    """The BASELINE C2 workload built with the reference's own public API: the level-11
+    unit square (mesh.py:104-137), nodes relabelled by the seeded permutation (new id of
+    old node i = perm[i]; oracle config_inputs' recipe: one default_rng(seed), permutation
+    then x ~ U[-1, 1]), build_element_batch(nu=1, f=1) (elements.py:124-137)."""
     import numpy as np
-    import oracle as o
+    level = 11 if size is None else size
+    m0 = eb_ref.build_unit_square_mesh(level)
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(m0.n_nodes)
+    nodes = np.empty_like(m0.nodes)
+    nodes[perm] = m0.nodes
+    m = eb_ref.Mesh(nodes, perm[m0.elements], np.sort(perm[m0.boundary_nodes]))
+    x = rng.uniform(-1.0, 1.0, m.n_nodes)
+    return eb_ref.build_element_batch(m, nu=1.0), x, m
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path on this host's
+    cores -- the unmodified `ebsolve.residual(batch, x, threads=T, deterministic=True)`
+    (operators.py:72-111) from baseline/_ref when installed ("kind": "reference"), else the
+    oracle port of the same algorithm (oracle/ebs_oracle.py, "kind": "port")."""
+    import numpy as np
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    size = args.size if args.size is not None else None
-    t_setup = time.perf_counter()
-    inp = o.config_inputs(2, seed=args.seed, size=size)
-    _, _, A, b_e = o.element_matrices(inp["nodes"], inp["elements"], nu=inp["nu"])
-    indt = np.ascontiguousarray(inp["elements"].T)
-    x = inp["x"]
     T = cpu_threads()
+    t_setup = time.perf_counter()
+    eb_ref = _reference_package()
+    if eb_ref is not None:
+        batch, x, m = reference_c2_inputs(eb_ref, args.seed, args.size)
+        n_n, n_e = m.n_nodes, m.n_elements
+        kind = "reference"
+        run = lambda: eb_ref.residual(batch, x, threads=T, deterministic=True)  # noqa: E731
+        what = (f"ebsolve.residual(batch, x, threads={T}, deterministic=True) -- the unmodified "
+                "reference package from baseline/_ref")
+    else:
+        import oracle as o
+        inp = o.config_inputs(2, seed=args.seed, size=args.size)
+        _, _, A, b_e = o.element_matrices(inp["nodes"], inp["elements"], nu=inp["nu"])
+        indt = np.ascontiguousarray(inp["elements"].T)
+        x = inp["x"]
+        n_n, n_e = x.shape[0], indt.shape[1]
+        kind = "port"
+        run = lambda: o.residual(A, b_e, indt, x, threads=T)  # noqa: E731
+        what = (f"oracle/ebs_oracle.py residual (the reference algorithm restated, deterministic "
+                f"chunked mode, {T} threads; baseline/_ref not installed)")
     setup = time.perf_counter() - t_setup
     for _ in range(args.warmup):
-        o.residual(A, b_e, indt, x, threads=T)
+        run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        o.residual(A, b_e, indt, x, threads=T)
+        run()
     dt = time.perf_counter() - t0
-    n_n, n_e = x.shape[0], indt.shape[1]
     value = n_n * args.steps / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s",
@@ -155,9 +205,8 @@ def run_reference(args):
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE C2 recipe)",
         "config": workload_config(n_n, n_e, args, mode="reference order (bincount)"),
-        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": T, "kind": "port",
-                         "sample": f"{args.steps} full C2 residuals (oracle/ebs_oracle.py "
-                                   f"residual, deterministic chunked mode, {T} threads)"},
+        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": T, "kind": kind,
+                         "sample": f"{args.steps} full C2 residuals: {what}"},
         "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "setup_s": setup,
@@ -395,7 +444,10 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_sell_op<3,1,1> (fused gather-product-ordered-sum, packed ids, red.add caller-order output)",
                      "bytes_per_launch": bytes_alg, "kernel_ms": sell * 1e3,
-                     "gather_kernel_ms": gather * 1e3, "peak_source": peak_kind},
+                     "gather_kernel_ms": gather * 1e3, "peak_source": peak_kind,
+                     "step_frac": bytes_alg / (total / args.steps) / 1e9 / peak,
+                     "step_note": "step_frac: the same algorithmic bytes over the whole "
+                                  "ms_per_step (x permutation + -0.0 fill + SELL pass)"},
         "timing": {"mode": "cuda_graph" if total_graph is not None else "eager",
                    "eager_value": n_n * args.steps / total_eager / 1e9,
                    "eager_ms_per_step": total_eager / args.steps * 1e3,
@@ -429,6 +481,13 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "setup_s": setup,
     }
+    if cpu:  # like-for-like speed-ups over the CPU reference algorithm (reference order)
+        line["vs_cpu_baseline"] = {
+            "fast": value / cpu["value"],
+            "exact": line["exact_mode"]["value"] / cpu["value"],
+            "e2e": line["e2e"]["value"] / cpu["value"],
+            "note": "exact: the bit-identical (reference-order) GPU residual vs the same "
+                    "algorithm on the host; fast: pre-assembled b (within 1e-12)"}
     if extra:
         line["solvers"] = extra
     if paper:
@@ -445,12 +504,27 @@ def solver_extras(args):
     from paper_1911_03973_b200.inputs import config_problem
     out = {}
     peaks, _ = load_peaks()
-    for cfg, iters, tol in ((3, 20000, 1e-8), (4, 200, None), (5, 500, None)):
+    runs = [(3, 20000, 1e-8, False), (4, 200, None, False), (5, 500, None, False),
+            (3, 20000, 1e-8, True)]
+    for cfg, iters, tol, permuted in runs:
         if cfg not in args.solver_configs:
             continue
         try:
             t0 = time.perf_counter()
-            p = config_problem(cfg, seed=args.seed)
+            if permuted:
+                # the unstructured-numbering 3D path: C3 with its node labels randomly
+                # permuted (seeded), so the plan falls back from the one-byte tuple codes
+                # of a structured numbering to first-appearance ids + 8 B delta words
+                p = config_problem(cfg, seed=args.seed, assemble=False)
+                perm = np.random.default_rng(args.seed + 1).permutation(p["mesh"].n_nodes)
+                m = eb.permute_nodes(p["mesh"], perm)
+                nd = eb.face_z0_nodes(m)
+                d = eb.DirichletData(nd, torch.zeros(nd.numel(), dtype=torch.float64,
+                                                     device="cuda"))
+                batch = eb.build_element_batch(m, nu=p["nu"])
+                p = {"batch": batch, "dirichlet": d, "mesh": m}
+            else:
+                p = config_problem(cfg, seed=args.seed)
             batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
             pl = batch.operator(m.n_nodes)
             pl.ensure_dirichlet(d)
@@ -476,7 +550,7 @@ def solver_extras(args):
             flags = pl.info()["loaded"]
             id_b = 1 if flags & 32 else ((4 if nb == 3 else 8) if flags & 4 else 4 * (nb - 1))
             per_it_stored = n_e * (8 * nb * nb + id_b * nb) + (32 if cfg == 4 else 104) * n_n
-            out[f"C{cfg}"] = {
+            out[f"C{cfg}" + ("_permuted" if permuted else "")] = {
                 "method": "jacobi" if cfg == 4 else "pcg", "iterations": its,
                 "it_per_s": its / t, "ms_per_it": t / its * 1e3,
                 "hbm_gbs_algorithmic": per_it * its / t / 1e9,
@@ -488,7 +562,8 @@ def solver_extras(args):
             del p, batch, pl, x
             torch.cuda.empty_cache()
         except Exception as e:  # report, never kill the headline line
-            out[f"C{cfg}"] = {"error": f"{type(e).__name__}: {e}"}
+            out[f"C{cfg}" + ("_permuted" if permuted else "")] = {
+                "error": f"{type(e).__name__}: {e}"}
     try:  # C1 (the reference's CPU-scale case): JPCG to 1e-8, three launches per
         # iteration vs the whole loop as one cooperative kernel (pcg(..., fused=True))
         p = config_problem(1, seed=args.seed)
