@@ -13,6 +13,17 @@
 
 #include "../../include/ebs.h"
 
+// Device-side index checks (compute-sanitizer is not available on the GPU pool): build
+// with -DEBS_DEVICE_CHECKS (scripts/checked_build.sh) and every gather / scatter index of
+// the SELL sweeps, permutations, CSR fill and refinement is asserted in range; a violation
+// traps the kernel with the file, line and condition.  Compiled out otherwise.
+#ifdef EBS_DEVICE_CHECKS
+#include <cassert>
+#define EBS_DCHECK(cond) assert(cond)
+#else
+#define EBS_DCHECK(cond) ((void)0)
+#endif
+
 namespace ebs {
 
 // ---------------------------------------------------------------- errors ----

@@ -36,6 +36,7 @@ struct OpEpi {
         if (free_int && !free_int[m]) s = 0.0;
         if (s_raw) s_raw[m] = s;
         if (old_of_new) {
+            EBS_DCHECK(old_of_new[m] >= 0);
             if (red) atomicAdd(out + old_of_new[m], s);
             else out[old_of_new[m]] = s;
         } else {
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int u = 0; u < PERM_ILP; ++u) {
             const int64_t m = base + u * stride;
+            EBS_DCHECK(m >= n || (idx[u] >= 0 && idx[u] < n));
             v[u] = m < n ? __ldg(x_user + idx[u]) : 0.0;
         }
 #pragma unroll
@@ -230,6 +232,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int u = 0; u < PERM_ILP; ++u) {
             const int64_t i = base + u * stride;
+            EBS_DCHECK(i >= n || (idx[u] >= 0 && idx[u] < n));
             v[u] = i < n ? v_int[idx[u]] : 0.0;
         }
 #pragma unroll

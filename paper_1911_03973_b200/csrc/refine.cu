@@ -101,6 +101,9 @@ __global__ void k_children(int64_t n_e, int64_t n_n, const int32_t *__restrict__
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t q = i / n_e, e = i - q * n_e;
+        EBS_DCHECK(conn[e] >= 0 && conn[e] < n_n && conn[n_e + e] >= 0 &&
+                   conn[n_e + e] < n_n && conn[2 * n_e + e] >= 0 && conn[2 * n_e + e] < n_n);
+        EBS_DCHECK(mid[e] >= 0 && mid[n_e + e] >= 0 && mid[2 * n_e + e] >= 0);
         const int32_t a = rank[conn[e]], b = rank[conn[n_e + e]], c = rank[conn[2 * n_e + e]];
         const int32_t ab = rank[n_n + mid[e]], bc = rank[n_n + mid[n_e + e]],
                       ca = rank[n_n + mid[2 * n_e + e]];

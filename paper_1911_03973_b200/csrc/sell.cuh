@@ -38,6 +38,7 @@ struct SellView {
     const double *__restrict__ be;
     const int32_t *__restrict__ tab;     // per-chunk offset tables (IDS_TABLE)
     const int32_t *__restrict__ taboff;  // n_chunks + 1 offsets into tab
+    int64_t n_rows;                      // slot rows of the blob (index checks)
     const int32_t *__restrict__ clist;   // nullable: sweep only these chunks
     int64_t nlist;                       // number of chunks swept (n_chunks or list size)
     const uint8_t *__restrict__ rowflag; // IDS_DELTA2: 1 = two-base row, 0 = 64-bit deltas
@@ -47,7 +48,7 @@ struct SellView {
 
 inline SellView sell_view(const Plan *p, const int32_t *clist = nullptr, int64_t nlist = -1) {
     return SellView{p->n_n, p->n_chunks, p->rowb, p->rowbase, p->width, p->cnt, p->cnt8, p->slot,
-                    p->slot_be, p->tab, p->taboff, clist, clist ? nlist : p->n_chunks,
+                    p->slot_be, p->tab, p->taboff, p->n_rows, clist, clist ? nlist : p->n_chunks,
                     p->rowflag, p->codes, p->tup};
 }
 
@@ -285,7 +286,9 @@ __device__ __forceinline__ double sell_node_sum(const SellView &v, int64_t row0,
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int t = 0; t < NB - 1; ++t)
-                g[u][t] = k0 + u < c_m ? x(nid[u][t]) : 0.0;
+                g[u][t] = k0 + u < c_m ? (EBS_DCHECK(nid[u][t] >= 0 && nid[u][t] < v.n_n),
+                                          x(nid[u][t]))
+                                       : 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (k0 + u < c_m) {
@@ -357,7 +360,10 @@ __device__ __forceinline__ double sell_node_sum_pipe(const SellView &v, int64_t 
             const int j = cur.decode(v, m, nid, stab);
             double g[NB - 1];
 #pragma unroll
-            for (int t = 0; t < NB - 1; ++t) g[t] = x(nid[t]);
+            for (int t = 0; t < NB - 1; ++t) {
+                EBS_DCHECK(nid[t] >= 0 && nid[t] < v.n_n);
+                g[t] = x(nid[t]);
+            }
             const double *ap = reinterpret_cast<const double *>(rp) + lane;
             double a[NB];
 #pragma unroll
@@ -409,6 +415,8 @@ __device__ __forceinline__ ChunkSum sell_chunk_sum(const SellView &v, int c, int
         for (int i = lane; i < t1 - t0; i += LANES) stab[i] = v.tab[t0 + i];
         __syncwarp();
     }
+    EBS_DCHECK(c >= 0 && c < v.n_chunks);
+    EBS_DCHECK(v.rowbase[c] >= 0 && (int64_t)v.rowbase[c] + v.width[c] <= v.n_rows);
     ChunkSum r;
     r.m = c * LANES + lane;
     r.valid = r.m < v.n_n;
