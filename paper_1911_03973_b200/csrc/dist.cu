@@ -177,7 +177,10 @@ __global__ void __launch_bounds__(256)
 // ctl = [stop, k_stop, k, diverged]: the loop rules of _iterate (solvers.py:117-160) on the
 // device -- stop when ||r_k|| <= tol ||r_0|| (tol >= 0) or ||r_k|| is not finite; every
 // later launch (and the plan's fused matvec sweeps, ebs_dist_set_stop) is a no-op.
-__global__ void __launch_bounds__(256)
+#ifndef EBS_CG1_MINB
+#define EBS_CG1_MINB 1
+#endif
+__global__ void __launch_bounds__(256, EBS_CG1_MINB)
     k_vec_cg1_update(int64_t n, double *cur, const double *__restrict__ prev,
                      const double *__restrict__ rr0, double tol, int32_t *ctl,
                      const uint8_t *__restrict__ owned, const double *__restrict__ dinv,

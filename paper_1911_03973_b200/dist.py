@@ -23,7 +23,7 @@ The solver loops are written against two small protocols so the same code runs
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -509,6 +509,36 @@ class DistProblem:
     dinv: list    # Jacobi 1/diag (0 at constrained nodes)
     diverged: bool = False  # last jacobi/pcg: a non-finite iterate or norm on any rank
                             # (solvers.py:138-152 -- flagged, never raised)
+    # per-solver device workspaces and their captured CUDA graphs, kept across solves: the
+    # graph of a loop is captured once per problem (and solver settings) and replayed by
+    # every later solve -- a capture per solve costs host time, graph-pool allocations and
+    # their release, which measured as erratic 1.5-4x slower solves
+    cache: dict = field(default_factory=dict)
+
+
+class _Workspace:
+    """Named device buffers of one solver loop + its captured graph (None: not captured,
+    or capture not possible -- `tried` records the collective decision)."""
+
+    def __init__(self, **bufs):
+        self.__dict__.update(bufs)
+        self.graph = None
+        self.tried = False
+
+
+def _workspace(prob, key, make):
+    ws = prob.cache.get(key)
+    if ws is None:
+        ws = prob.cache[key] = make()
+    return ws
+
+
+def _graph_for(prob, ws, body):
+    """The workspace's captured graph, capturing it on first use (collective decision)."""
+    if not ws.tried:
+        ws.graph = _capture(prob.comm, body)
+        ws.tried = True
+    return ws.graph
 
 
 def _reset_flags(ops):
@@ -654,13 +684,19 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     overlapped interface/interior sweeps with the update fused into the SELL pass."""
     ops, comm = prob.ops, prob.comm
     _reset_flags(ops)
-    xa = [x.clone() for x in xs0]
-    xb = [op.zeros() for op in ops]
-    ss = [op.zeros() for op in ops]
-    red = [torch.zeros(iters + 1, dtype=torch.float64, device=x.device) for x in xa]
-
     fused = _fused_ok(ops) if fused is None else fused
-    r3 = [torch.zeros(2, dtype=torch.float64, device=x.device) for x in xa]  # sweep partials
+    B = GRAPH_BATCH
+    dev = xs0[0].device
+    ws = _workspace(prob, ("jacobi", float(omega), bool(richardson), bool(fused)),
+                    lambda: _Workspace(
+                        xa=[op.zeros() for op in ops], xb=[op.zeros() for op in ops],
+                        ss=[op.zeros() for op in ops],
+                        r3=[torch.zeros(2, dtype=torch.float64, device=dev) for _ in ops],
+                        bred=[torch.zeros(B, dtype=torch.float64, device=dev) for _ in ops]))
+    for a, x in zip(ws.xa, xs0):
+        a.copy_(x)
+    xa, xb, ss, r3 = list(ws.xa), list(ws.xb), ws.ss, ws.r3  # sweep partials in r3
+    red = [torch.zeros(iters + 1, dtype=torch.float64, device=dev) for _ in ops]
 
     def step(src, dst, final, rslot):
         if fused:  # interface chunks, exchange || interior chunks, interface completion
@@ -685,16 +721,15 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
             op.vec_jacobi(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i], src[i],
                           None if final else dst[i], None, rslot[i])
 
-    B = GRAPH_BATCH
     k = 0
     if graph and iters >= B and _graph_ok(ops):
-        bred = [torch.zeros(B, dtype=torch.float64, device=x.device) for x in xa]
+        bred = ws.bred
 
         def body():
             for u in range(B):  # B even: xa/xb roles return to the start
                 src, dst = (xa, xb) if u % 2 == 0 else (xb, xa)
                 step(src, dst, False, [r_[u:u + 1] for r_ in bred])
-        g = _capture(comm, body)
+        g = _graph_for(prob, ws, body)
         if g is not None:
             while k + B <= iters:
                 g.replay()
@@ -709,7 +744,7 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     comm.allreduce(red)
     norms = torch.sqrt(red[0]).cpu().numpy()
     prob.diverged = _diverged(prob, norms)
-    return xa, norms
+    return [x.clone() for x in xa], norms  # fresh arrays: the workspace is reused
 
 
 def pcg(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False, fused=None,
@@ -751,15 +786,25 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
     f64 = dict(dtype=torch.float64, device=dev)
     _reset_flags(ops)
     B = GRAPH_BATCH
-    xs = [x.clone() for x in xs0]
-    rs, us, ws, ps, ss = ([op.zeros() for op in ops] for _ in range(5))
-    ring = [torch.zeros((B, 4), **f64) for _ in ops]   # [gamma, delta, rr, alpha]
-    part = [torch.zeros(2, **f64) for _ in ops]        # interface / interior sweep w.u
-    ctl = [torch.zeros(4, dtype=torch.int32, device=dev) for _ in ops]
-    rr0 = [torch.zeros(1, **f64) for _ in ops]
-    zero = torch.zeros(1, **f64)
     fused = _fused_ok(ops) if fused is None else fused
     tol_ = -1.0 if tol is None else float(tol)
+    on_dev = dev.type == "cuda"
+    wsp = _workspace(prob, ("pcg1", tol_, bool(fused)), lambda: _Workspace(
+        xs=[op.zeros() for op in ops], rs=[op.zeros() for op in ops],
+        us=[op.zeros() for op in ops], ws=[op.zeros() for op in ops],
+        ps=[op.zeros() for op in ops], ss=[op.zeros() for op in ops],
+        ring=[torch.zeros((B, 4), **f64) for _ in ops],   # [gamma, delta, rr, alpha]
+        part=[torch.zeros(2, **f64) for _ in ops],        # interface / interior sweep w.u
+        ctl=[torch.zeros(4, dtype=torch.int32, device=dev) for _ in ops],
+        rr0=[torch.zeros(1, **f64) for _ in ops],
+        host_ctl=[torch.zeros((2, 4), dtype=torch.int32, pin_memory=on_dev) for _ in ops]))
+    xs, rs, us, ws, ps, ss = wsp.xs, wsp.rs, wsp.us, wsp.ws, wsp.ps, wsp.ss
+    ring, part, ctl, rr0, host_ctl = wsp.ring, wsp.part, wsp.ctl, wsp.rr0, wsp.host_ctl
+    for i in range(len(ops)):
+        xs[i].copy_(xs0[i])
+        for t in (us[i], ps[i], ss[i], ring[i], part[i], ctl[i]):
+            t.zero_()
+    zero = torch.zeros(1, **f64)
     for op, c in zip(ops, ctl):
         if hasattr(op, "set_stop"):
             op.set_stop(c if fused else None)
@@ -814,11 +859,9 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
         def body():
             for u in range(B):
                 step(u)
-        g = _capture(comm, body)  # recorded only: nothing ran, the ring is untouched
+        g = _graph_for(prob, wsp, body)  # recorded only: nothing ran, the ring is untouched
     # batches of B iterations (graph replay or eager); the stop flags of batch j are read
     # while batch j+1 is queued, so the device never waits for the host
-    on_dev = dev.type == "cuda"
-    host_ctl = [torch.zeros((2, 4), dtype=torch.int32, pin_memory=on_dev) for _ in ops]
     pending = None
     k, j = 0, 0
     while k < iters:
@@ -860,7 +903,7 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
     norms = torch.sqrt(norm2[0][:n]).cpu().numpy()
     diverged = _diverged(prob, norms)  # collective: every rank calls it
     prob.diverged = diverged or bool(int(c[3]))
-    return xs, norms
+    return [x.clone() for x in xs], norms  # fresh arrays: the workspace is reused
 
 
 def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: bool = False,
@@ -874,19 +917,28 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
     dev = xs0[0].device
     f64 = dict(dtype=torch.float64, device=dev)
     _reset_flags(ops)
-    xs = [x.clone() for x in xs0]
-    rs = [op.zeros() for op in ops]
-    ps = [op.zeros() for op in ops]
-    qs = [op.zeros() for op in ops]
-    ss = [op.zeros() for op in ops]
+    for op in ops:
+        if hasattr(op, "set_stop"):
+            op.set_stop(None)
+    fused = _fused_ok(ops) if fused is None else fused
+    B = GRAPH_BATCH
+    wsp = _workspace(prob, ("pcg2", bool(fused)), lambda: _Workspace(
+        xs=[op.zeros() for op in ops], rs=[op.zeros() for op in ops],
+        ps=[op.zeros() for op in ops], qs=[op.zeros() for op in ops],
+        ss=[op.zeros() for op in ops],
+        ring=[torch.zeros((B, 2), **f64) for _ in ops],   # iteration k: slot k % B
+        pq=[torch.zeros(1, **f64) for _ in ops],
+        part=[torch.zeros(2, **f64) for _ in ops]))       # interface / interior sweep p.q
+    xs, rs, ps, qs, ss = wsp.xs, wsp.rs, wsp.ps, wsp.qs, wsp.ss
+    ring, pq, part = wsp.ring, wsp.pq, wsp.part
+    for i in range(len(ops)):
+        xs[i].copy_(xs0[i])
+        for t in (ps[i], ring[i]):
+            t.zero_()
     zero = torch.zeros(1, **f64)
     for op, x, s in zip(ops, xs, ss):
         op.matvec_partial(x, s)
     halo(ops, comm, ss)
-    B = GRAPH_BATCH
-    ring = [torch.zeros((B, 2), **f64) for _ in ops]   # iteration k: slot k % B
-    pq = [torch.zeros(1, **f64) for _ in ops]
-    part = [torch.zeros(2, **f64) for _ in ops]        # interface / interior sweep p.q
     init = [rg[B - 1] for rg in ring]                  # iteration 0 reads its rz here
     for i, op in enumerate(ops):
         op.vec_jacobi(0.0, prob.b[i], ss[i], None, xs[i], None, rs[i], init[i][0:1])
@@ -896,8 +948,6 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
     norm2 = [torch.zeros(iters + 1, **f64) for _ in ops]  # ||r_k||^2
     for i in range(len(ops)):
         norm2[i][0:1].copy_(init[i][0:1])
-
-    fused = _fused_ok(ops) if fused is None else fused
 
     def step(u):
         slot = [rg[u] for rg in ring]
@@ -932,7 +982,7 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
         def body():
             for u in range(B):
                 step(u)
-        g = _capture(comm, body)
+        g = _graph_for(prob, wsp, body)
         if g is not None:
             while k + B <= iters:
                 g.replay()
@@ -954,7 +1004,7 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
     n = k_done + 1
     norms = torch.sqrt(norm2[0][:n]).cpu().numpy()
     prob.diverged = _diverged(prob, norms)
-    return xs, norms
+    return [x.clone() for x in xs], norms  # fresh arrays: the workspace is reused
 
 
 def gather_global(ops, vs, n_nodes, comm=None):
