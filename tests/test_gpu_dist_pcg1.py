@@ -121,3 +121,28 @@ def test_native_communicator_timeout_aborts(gpu):
     comm2.allreduce([t])
     comm2.sync()
     assert torch.equal(t, torch.ones_like(t))
+
+
+def test_native_transport_tolerance_and_reuse(gpu):
+    """libebs's own communicator (world 1) under the single-reduction loop with a
+    tolerance and CUDA-graph batches: same iterates and history as the device-copy
+    transport; a second solve on the same problem replays the cached graph (no new
+    capture) and gives the same result; results are fresh tensors."""
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    pr = config_problem(5, seed=3, size=8)
+    m = pr["mesh"]
+    op, _ = dist.rank_operator(m, pr["nu"], pr["f"], pr["dirichlet"], 1, 0)
+    prob_l = dist.setup([op], dist.LocalTransport())
+    prob_n = dist.setup([op], dist.NativeTransport(op))
+    x0 = op.zeros()
+    xl, nl = dist.pcg(prob_l, [x0], 3000, tol=1e-8, graph=True)
+    xn, nn = dist.pcg(prob_n, [x0], 3000, tol=1e-8, graph=True)
+    np.testing.assert_array_equal(nn, nl)
+    assert torch.equal(xn[0], xl[0])
+    before = dist.GRAPH_STATS["captured"]
+    xn2, nn2 = dist.pcg(prob_n, [x0], 3000, tol=1e-8, graph=True)
+    assert dist.GRAPH_STATS["captured"] == before  # cached graph replayed
+    np.testing.assert_array_equal(nn2, nn)
+    assert torch.equal(xn2[0], xn[0]) and xn2[0].data_ptr() != xn[0].data_ptr()
+    assert nn[-1] <= 1e-8 * nn[0] and not prob_n.diverged
