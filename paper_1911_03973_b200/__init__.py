@@ -22,12 +22,14 @@ from .operators import (DirichletData, apply_initial_guess, assemble_rhs, consta
 from .solvers import (ChebyshevCycle, ConvergenceHistory, SpectralBounds, cg, chebyshev2,
                       chebyshev3, chebyshev_roots, chebyshev_scaling_factor, jacobi, pcg,
                       richardson)
+from .reference import dense_interior_eigenvalues, solve_reference
 from .sparse import assemble_sparse
 from .spectrum import (mass_gershgorin, model_eigen_bounds, model_eigenvalues_all,
                        operator_bounds, power_iteration_lambda_max)
 
 __all__ = [
-    "ExperimentConfig", "ExperimentReport", "run_experiment",
+    "ExperimentConfig", "ExperimentReport", "run_experiment", "solve_reference",
+    "dense_interior_eigenvalues",
     "ChebyshevCycle", "chebyshev2", "chebyshev3", "chebyshev_roots", "chebyshev_scaling_factor",
     "mass_gershgorin", "operator_bounds", "power_iteration_lambda_max", "assemble_sparse",
     "uniform_refine", "export_mesh",
