@@ -214,7 +214,8 @@ int ebs_refine_tri(int64_t n_n, int64_t n_e, const double *coords, const int32_t
         CU(cudaStreamSynchronize(s));
     }
     int32_t n_edges = 0;
-    CU(cudaMemcpy(&n_edges, head.p + m - 1, sizeof n_edges, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&n_edges, head.p + m - 1, sizeof n_edges, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
     DevBuf<int32_t> mid(m);
     k_edge_mids<<<grid_for(m, 256), 256, 0, s>>>(m, n_n, ekey.p, eslot.p, head.p, coords, mid.p,
                                                  all_xy.p);

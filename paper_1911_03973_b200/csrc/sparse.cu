@@ -119,7 +119,8 @@ int ebs_csr_nnz(ebs_plan_t plan, const int32_t *conn, int64_t *crow, void *strea
         bump_launches(1);
     }
     int32_t bad = 0;
-    CU(cudaMemcpy(&bad, p->flag, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&bad, p->flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
     EBS_REQUIRE(bad == 0, "a row has more than %d element entries", MAX_ROW_ENTRIES);
     EBS_CATCH
 }
