@@ -335,6 +335,19 @@ int ebs_dist_jacobi_iface(int64_t n, const int64_t *idx, double omega, const dou
  * srcs is a HOST array of n_src (<= 8) device pointers. */
 int ebs_dist_combine(int64_t n_if, const int64_t *all_if, int n_src, const double *const *srcs,
                      const int32_t *pos, double *v, void *stream);
+/* The combine and the interface completion fused (one launch less per iteration):
+ * s[all_if[i]] = the rank-ordered sum as ebs_dist_combine, then the Jacobi completion of
+ * ebs_dist_jacobi_iface on that node (_jacobi), or q = free ? sum : 0 and red[0] = (prior[0]
+ * + prior[1]) + sum_owned p.q as ebs_dist_q_iface (_q).  srcs is a HOST array. */
+int ebs_dist_combine_jacobi(int64_t n_if, const int64_t *all_if, int n_src,
+                            const double *const *srcs, const int32_t *pos, double *s, double omega,
+                            const double *b, const double *dinv, const uint8_t *free_m,
+                            const uint8_t *owned, const double *x, double *x_out,
+                            const double *prior, double *red, void *ws, void *stream);
+int ebs_dist_combine_q(int64_t n_if, const int64_t *all_if, int n_src, const double *const *srcs,
+                       const int32_t *pos, double *q, const uint8_t *free_m, const uint8_t *owned,
+                       const double *pv, const double *prior, double *red, void *ws,
+                       void *stream);
 /* ... and red[0] = (prior[0] + prior[1]) + the interface nodes' owned p.q (prior, nullable:
  * the interface- and interior-chunk partials of the sweeps): the rank's whole p.q. */
 int ebs_dist_q_iface(int64_t n, const int64_t *idx, const uint8_t *free_m, const uint8_t *owned,

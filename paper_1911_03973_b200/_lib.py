@@ -119,6 +119,13 @@ SIGNATURES = {
     "ebs_dist_wait": (c_int, [c_void_p, c_void_p, c_double]),
     "ebs_dist_abort": (c_int, [c_void_p]),
     "ebs_dist_set_stop": (c_int, [c_void_p, c_void_p]),
+    "ebs_dist_combine_jacobi": (c_int, [c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                        c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p]),
+    "ebs_dist_combine_q": (c_int, [c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p]),
     "ebs_vec_cg1_update": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_double, c_void_p,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

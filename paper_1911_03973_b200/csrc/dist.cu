@@ -371,7 +371,10 @@ int ebs_vec_pcg_update(int64_t n, const double *rz, const double *pq, const uint
     EBS_REQUIRE(n >= 0 && rz && pq && owned && dinv && x && r && p && q && red && nonfinite && ws,
                 "null argument");
     Scratch sc = scratch(ws);
-    k_vec_pcg_update<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+    // one wave of resident CTAs (occupancy-sized, fixed per device: deterministic order);
+    // the capped 1184-CTA grid ran in 4 waves at these kernels' register counts
+    const int grid = persistent_grid((const void *)k_vec_pcg_update, 256, (n + 255) / 256, 0);
+    k_vec_pcg_update<<<grid, 256, 0, S(stream)>>>(
         n, rz, pq, owned, dinv, x, r, p, q, sc.partials, sc.counter, red, nonfinite);
     LAUNCHED();
     EBS_CATCH
@@ -396,7 +399,8 @@ int ebs_vec_cg1_update(int64_t n, double *cur, const double *prev, const double 
                     nonfinite && ws && (rr0 || tol < 0.0),
                 "null argument");
     Scratch sc = scratch(ws);
-    k_vec_cg1_update<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
+    const int grid = persistent_grid((const void *)k_vec_cg1_update, 256, (n + 255) / 256, 0);
+    k_vec_cg1_update<<<grid, 256, 0, S(stream)>>>(
         n, cur, prev, rr0, tol, ctl, owned, dinv, x, r, u, w, p, s, sc.partials, sc.counter,
         next, nonfinite);
     LAUNCHED();
@@ -583,6 +587,60 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// The combine and the interface completion in one pass (one launch less per iteration on
+// the latency-bound halo tail): thread i sums the contributions to shared node all_if[i] in
+// ascending rank order (as k_dist_combine) and completes that node at once (as
+// k_dist_jacobi_iface / k_dist_q_iface) -- each thread reads and writes only its own node.
+__global__ void __launch_bounds__(256)
+    k_dist_combine_jacobi(int64_t n_if, const int64_t *__restrict__ all_if, CombineSrc src,
+                          const int32_t *__restrict__ pos, double *s, double omega,
+                          const double *__restrict__ b, const double *__restrict__ dinv,
+                          const uint8_t *__restrict__ free_m, const uint8_t *__restrict__ owned,
+                          const double *__restrict__ x, double *__restrict__ x_out,
+                          double *partials, unsigned int *counter, const double *prior,
+                          double *red) {
+    double part[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = all_if[i];
+        double acc = 0.0;
+        for (int k = 0; k < src.n; ++k) {
+            const int32_t q = pos[i * src.n + k];
+            if (q >= 0) acc += src.p[k][q];
+        }
+        s[m] = acc;
+        const double r = free_m[m] ? b[m] - acc : 0.0;
+        if (owned[m]) part[0] += r * r;
+        if (x_out) x_out[m] = dinv ? x[m] + omega * (dinv[m] * r) : x[m] + omega * r;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0)
+        red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
+}
+
+__global__ void __launch_bounds__(256)
+    k_dist_combine_q(int64_t n_if, const int64_t *__restrict__ all_if, CombineSrc src,
+                     const int32_t *__restrict__ pos, double *q, const uint8_t *__restrict__ free_m,
+                     const uint8_t *__restrict__ owned, const double *__restrict__ p,
+                     double *partials, unsigned int *counter, const double *prior, double *red) {
+    double part[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = all_if[i];
+        double acc = 0.0;
+        for (int k = 0; k < src.n; ++k) {
+            const int32_t c = pos[i * src.n + k];
+            if (c >= 0) acc += src.p[k][c];
+        }
+        const double qm = free_m[m] ? acc : 0.0;
+        q[m] = qm;
+        if (owned[m]) part[0] += p[m] * qm;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0)
+        red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
+}
+
 }  // namespace ebs
 
 extern "C" {
@@ -682,6 +740,55 @@ int ebs_dist_q_iface(int64_t n, const int64_t *idx, const uint8_t *free_m, const
     Scratch sc = scratch(ws);
     k_dist_q_iface<<<grid_for(n, 256, RED_MAX_BLOCKS), 256, 0, S(stream)>>>(
         n, idx, free_m, owned, pv, q, sc.partials, sc.counter, prior, red);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+
+static CombineSrc combine_sources(int n_src, const double *const *srcs) {
+    EBS_REQUIRE(n_src >= 1 && n_src <= COMBINE_MAX && srcs, "1 <= n_src <= %d sources",
+                COMBINE_MAX);
+    CombineSrc cs{};
+    cs.n = n_src;
+    for (int k = 0; k < n_src; ++k) {
+        EBS_REQUIRE(srcs[k], "null source %d", k);
+        cs.p[k] = srcs[k];
+    }
+    return cs;
+}
+
+int ebs_dist_combine_jacobi(int64_t n_if, const int64_t *all_if, int n_src,
+                            const double *const *srcs, const int32_t *pos, double *s, double omega,
+                            const double *b, const double *dinv, const uint8_t *free_m,
+                            const uint8_t *owned, const double *x, double *x_out,
+                            const double *prior, double *red, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n_if >= 0 && s && b && free_m && owned && x && red && ws &&
+                    (n_if == 0 || (all_if && pos)),
+                "null argument");
+    const CombineSrc cs = combine_sources(n_src, srcs);
+    Scratch sc = scratch(ws);
+    const int grid = persistent_grid((const void *)k_dist_combine_jacobi, 256, (n_if + 255) / 256, 0);
+    k_dist_combine_jacobi<<<grid, 256, 0, S(stream)>>>(n_if, all_if, cs, pos, s, omega, b, dinv,
+                                                       free_m, owned, x, x_out, sc.partials,
+                                                       sc.counter, prior, red);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_dist_combine_q(int64_t n_if, const int64_t *all_if, int n_src, const double *const *srcs,
+                       const int32_t *pos, double *q, const uint8_t *free_m, const uint8_t *owned,
+                       const double *pv, const double *prior, double *red, void *ws,
+                       void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n_if >= 0 && q && free_m && owned && pv && red && ws &&
+                    (n_if == 0 || (all_if && pos)),
+                "null argument");
+    const CombineSrc cs = combine_sources(n_src, srcs);
+    Scratch sc = scratch(ws);
+    const int grid = persistent_grid((const void *)k_dist_combine_q, 256, (n_if + 255) / 256, 0);
+    k_dist_combine_q<<<grid, 256, 0, S(stream)>>>(n_if, all_if, cs, pos, q, free_m, owned, pv,
+                                                  sc.partials, sc.counter, prior, red);
     LAUNCHED();
     EBS_CATCH
 }

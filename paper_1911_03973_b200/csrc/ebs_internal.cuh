@@ -235,6 +235,9 @@ void dist_free(Plan *p);
 
 // ------------------------------------------------------ reductions ----------
 constexpr int RED_BLOCK = 256;
+// occupancy-sized grid of `kernel` (one wave of resident CTAs, cached per kernel and
+// device; sell.cuh repeats the declaration with smem defaulted to 0)
+int persistent_grid(const void *kernel, int block, int64_t work_blocks, size_t smem);
 constexpr int RED_MAX_BLOCKS = 1184;  // 148 SMs x 8: fixed -> deterministic order
 
 __device__ __forceinline__ double warp_sum(double v) {

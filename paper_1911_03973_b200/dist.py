@@ -433,6 +433,31 @@ class GpuRankOperator:
         call("ebs_dist_combine", self.all_if.numel(), D.ptr(self.all_if), len(srcs), ptrs,
              D.ptr(self.combine_pos), D.ptr(v), D.stream())
 
+    def _combine_srcs(self, v, recvs):
+        srcs = [v if r == self.rank else recvs[r] for r in self.combine_ranks]
+        return len(srcs), (ctypes.c_void_p * len(srcs))(*[t.data_ptr() for t in srcs])
+
+    def combine_jacobi(self, recvs, omega, b, s_part, dinv, x, x_out, red, prior=None):
+        """combine + jacobi_iface in one launch (ebs_dist_combine_jacobi)."""
+        if self.if_idx and len(self.combine_ranks) > 8:
+            self.combine(s_part, recvs)
+            return self.jacobi_iface(omega, b, s_part, dinv, x, x_out, red, prior=prior)
+        n_src, ptrs = self._combine_srcs(s_part, recvs)
+        call("ebs_dist_combine_jacobi", self.all_if.numel(), D.ptr(self.all_if), n_src, ptrs,
+             D.ptr(self.combine_pos), D.ptr(s_part), float(omega), D.ptr(b), D.ptr(dinv),
+             D.ptr(self.free), D.ptr(self.owned), D.ptr(x), D.ptr(x_out), D.ptr(prior),
+             D.ptr(red), D.ptr(self._ws), D.stream())
+
+    def combine_q(self, recvs, p, q, red, prior=None):
+        """combine + q_iface in one launch (ebs_dist_combine_q)."""
+        if self.if_idx and len(self.combine_ranks) > 8:
+            self.combine(q, recvs)
+            return self.q_iface(p, q, red, prior=prior)
+        n_src, ptrs = self._combine_srcs(q, recvs)
+        call("ebs_dist_combine_q", self.all_if.numel(), D.ptr(self.all_if), n_src, ptrs,
+             D.ptr(self.combine_pos), D.ptr(q), D.ptr(self.free), D.ptr(self.owned), D.ptr(p),
+             D.ptr(prior), D.ptr(red), D.ptr(self._ws), D.stream())
+
     def jacobi_sweep(self, chunks, omega, x, x_out, b, dinv, s_part, red):
         call("ebs_dist_jacobi_sweep", self.plan.handle, D.ptr(chunks), chunks.numel(),
              float(omega), D.ptr(x), D.ptr(x_out), D.ptr(b), D.ptr(dinv), D.ptr(self.iface),
@@ -710,9 +735,9 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
                                 None if richardson else prob.dinv[i], ss[i], r3[i][1:2])
             recvs = comm.exchange_finish(h)
             for i, op in enumerate(ops):
-                op.combine(ss[i], recvs[i])
-                op.jacobi_iface(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i],
-                                src[i], None if final else dst[i], rslot[i], prior=r3[i])
+                op.combine_jacobi(recvs[i], omega, prob.b[i], ss[i],
+                                  None if richardson else prob.dinv[i], src[i],
+                                  None if final else dst[i], rslot[i], prior=r3[i])
             return
         for op, x, s_ in zip(ops, src, ss):
             op.matvec_partial(x, s_)
@@ -818,8 +843,7 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
                 op.matvec_sweep(op.in_chunks, us[i], ws[i], part[i][1:2])
             recvs = comm.exchange_finish(h)
             for i, op in enumerate(ops):
-                op.combine(ws[i], recvs[i])
-                op.q_iface(us[i], ws[i], slot[i][1:2], prior=part[i])
+                op.combine_q(recvs[i], us[i], ws[i], slot[i][1:2], prior=part[i])
         else:
             for op, u_, w_ in zip(ops, us, ws):
                 op.matvec_partial(u_, w_)
@@ -961,8 +985,7 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
                 op.matvec_sweep(op.in_chunks, ps[i], qs[i], part[i][1:2])
             recvs = comm.exchange_finish(h)
             for i, op in enumerate(ops):
-                op.combine(qs[i], recvs[i])
-                op.q_iface(ps[i], qs[i], pq[i], prior=part[i])
+                op.combine_q(recvs[i], ps[i], qs[i], pq[i], prior=part[i])
         else:
             for op, p_, q_ in zip(ops, ps, qs):
                 op.matvec_partial(p_, q_)
