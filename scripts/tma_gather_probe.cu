@@ -26,6 +26,31 @@
 
 constexpr int ILP = 8;
 
+template <int IL>
+__global__ void __launch_bounds__(256) k_lsu_t(int n, const int *__restrict__ o2n,
+                                               const double *__restrict__ x, double *__restrict__ y) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < n; base += stride * IL) {
+        int idx[IL];
+        double v[IL];
+#pragma unroll
+        for (int u = 0; u < IL; ++u) {
+            const int m = base + u * stride;
+            idx[u] = m < n ? __ldcs(o2n + m) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < IL; ++u) {
+            const int m = base + u * stride;
+            v[u] = m < n ? __ldg(x + idx[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < IL; ++u) {
+            const int m = base + u * stride;
+            if (m < n) __stcs(y + m, v[u]);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_lsu(int n, const int *__restrict__ o2n,
                                              const double *__restrict__ x, double *__restrict__ y) {
     const int stride = gridDim.x * blockDim.x;
@@ -191,6 +216,15 @@ int main(int argc, char **argv) {
     timeit("lsu ilp8 8 CTA/SM", [&] {
         k_lsu<<<sms * 8, 256>>>(n, o2n, x, y);
     });
+#define LSU_CASE(IL_, B_)                                                                 \
+    {                                                                                     \
+        char name[64];                                                                    \
+        snprintf(name, sizeof name, "lsu ilp%d %d CTA/SM", IL_, B_);                      \
+        timeit(name, [&] { k_lsu_t<IL_><<<sms * B_, 256>>>(n, o2n, x, y); });             \
+    }
+    LSU_CASE(4, 8) LSU_CASE(8, 8) LSU_CASE(16, 8) LSU_CASE(8, 4) LSU_CASE(16, 4) LSU_CASE(4, 16)
+    LSU_CASE(8, 16) LSU_CASE(32, 2) LSU_CASE(16, 2)
+    if (argc > 2) return 0;
 #define TMA_CASE(S_, W_, B_)                                                              \
     {                                                                                     \
         auto kern = k_tma<S_, W_>;                                                        \
