@@ -386,6 +386,85 @@ int ebs_dist_poll(ebs_plan_t plan);
 int ebs_dist_wait(ebs_plan_t plan, void *stream, double timeout_s);
 int ebs_dist_abort(ebs_plan_t plan);
 
+/* ------------------------------------------------- peer-memory halo (peer.cu) ---- */
+/* The element-slab halo and the dot all-reduce without a collective library: every rank of
+ * a node (<= EBS_PEER_MAX) owns one device WINDOW that the other ranks map (CUDA IPC; NVLink
+ * P2P between GPUs) and write into; epoch flags in the window publish the data.  The fused
+ * slab sweeps (ebs_peer_*_sweep) store each interface node's partial sum straight into the
+ * neighbours' windows from the SELL epilogue, chunk by chunk, while the same launch sweeps
+ * the interior; ebs_peer_combine_* wait for the neighbours' flags, sum the shared nodes in
+ * ascending rank order (the values of ebs_dist_combine_*) and complete them.  All ranks must
+ * issue the same sequence of peer calls.  Waits are bounded by the timeout given to
+ * ebs_peer_create; a timed-out wait sets the window's error word (ebs_peer_status ->
+ * EBS_ENCCL) instead of hanging.  Replaces the reference's chunk loop + bincount over the
+ * whole mesh (operators.py:95-111) across slabs; no reference counterpart for the transport. */
+#define EBS_PEER_MAX 8
+#define EBS_PEER_HANDLE_BYTES 64
+typedef struct ebs_peer_s *ebs_peer_t;
+/* Window of a rank whose largest interface has `cap` nodes; zeroed.  handle_out (nullable,
+ * EBS_PEER_HANDLE_BYTES) receives its CUDA IPC handle for the other processes. */
+size_t ebs_peer_window_bytes(int64_t cap);
+int ebs_peer_window_alloc(int64_t cap, void **win, void *handle_out);
+int ebs_peer_window_open(const void *handle, void **win); /* another process's window */
+int ebs_peer_window_close(void *win);                     /* ... unmapped */
+int ebs_peer_window_free(void *win);                      /* own window freed */
+/* Peer group view of rank `rank`: wins[q] = rank q's window as mapped in this process
+ * (wins[rank] = the own window); every rank uses the same cap.  timeout_s < 0: wait forever. */
+int ebs_peer_create(int rank, int world, int64_t cap, void *const *wins, double timeout_s,
+                    ebs_peer_t *out);
+int ebs_peer_destroy(ebs_peer_t peer);
+/* Halo of a slab plan with n_local nodes: neighbours nb_ranks[0..n_nb) (ascending), and per
+ * neighbour the nb_len[k] local node ids (device int64, nb_idx[k]) it shares, in the order
+ * both sides agree on (ascending global id).  Host arrays of device pointers. */
+int ebs_peer_set_halo(ebs_peer_t peer, int64_t n_local, int n_nb, const int32_t *nb_ranks,
+                      const int64_t *nb_len, const int64_t *const *nb_idx, void *stream);
+/* EBS_ENCCL when a wait of this rank timed out (synchronises `stream`). */
+int ebs_peer_status(ebs_peer_t peer, void *stream);
+/* In-place sum over the ranks of n device doubles, added in rank order 0..world-1 (identical
+ * on every rank).  mode 0: one launch per 256 values; 1 / 2: only the put / only the
+ * wait-and-sum phase (n <= 256; for ranks emulated in one process, all puts first). */
+int ebs_peer_allreduce(ebs_peer_t peer, double *buf, int64_t n, int mode, void *stream);
+/* Generic halo: bufs[k] (nb_len[k] doubles, device) to neighbour k; recv: wait and copy
+ * neighbour k's values into out[k].  push: v at the interface nodes to every neighbour;
+ * combine: wait, then v[shared] = the rank-ordered sum.  ws: ebs_vec_workspace_bytes(). */
+int ebs_peer_send(ebs_peer_t peer, const double *const *bufs, void *stream);
+int ebs_peer_recv(ebs_peer_t peer, double *const *out, void *ws, void *stream);
+int ebs_peer_push(ebs_peer_t peer, const double *v, void *stream);
+int ebs_peer_combine(ebs_peer_t peer, double *v, void *ws, void *stream);
+/* Fused slab steps: as ebs_dist_jacobi_sweep / ebs_dist_matvec_sweep over ALL the rank's
+ * chunks in one launch, the n_if_chunks chunks holding interface nodes listed first; interface
+ * partials go to the neighbours' windows from the epilogue.  Then the combine + completion
+ * of ebs_dist_combine_jacobi / ebs_dist_combine_q after waiting for the neighbours. */
+int ebs_peer_jacobi_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks, int64_t n_list,
+                          int64_t n_if_chunks, double omega, const double *x, double *x_out,
+                          const double *b, const double *dinv, const uint8_t *iface,
+                          double *s_part, double *red, void *ws, void *stream);
+int ebs_peer_matvec_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks, int64_t n_list,
+                          int64_t n_if_chunks, const double *pv, double *q, const uint8_t *iface,
+                          double *red, void *ws, void *stream);
+int ebs_peer_combine_jacobi(ebs_peer_t peer, double *s, double omega, const double *b,
+                            const double *dinv, const uint8_t *free_m, const uint8_t *owned,
+                            const double *x, double *x_out, const double *prior, double *red,
+                            void *ws, void *stream);
+/* stop (device int32, nullable): as ebs_dist_set_stop -- a no-op once *stop != 0 (the matvec
+ * sweep sent nothing).  dots (device, nullable; red may point into it): after red[0] is
+ * written, dots[0..3) are put as this rank's contribution to the next all-reduce -- the
+ * single-reduction PCG's [r.u, w.u, r.r] -- consumed by ebs_peer_cg1_update (or by
+ * ebs_peer_allreduce mode 2). */
+int ebs_peer_combine_q(ebs_peer_t peer, double *q, const uint8_t *free_m, const uint8_t *owned,
+                       const double *pv, const double *prior, double *red, const int32_t *stop,
+                       const double *dots, void *ws, void *stream);
+/* ebs_vec_cg1_update whose cur[0..2] are all-reduced on the device: every block waits for the
+ * ranks' contributions (put by ebs_peer_combine_q with dots) and adds them in rank order; the
+ * sums are stored in cur[0..2] and the reduced r.r once more in cur[4] (cur holds 5 doubles
+ * here: [0..2] are later overwritten with partials when the slot is reused); at the first step
+ * (ctl[2] == 0) the reduced r.r is also stored in rr0[0] (it is only known there).  No all-reduce launch per iteration. */
+int ebs_peer_cg1_update(ebs_peer_t peer, int64_t n, double *cur, const double *prev,
+                        const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
+                        const double *dinv, double *x, double *r, double *u, const double *w,
+                        double *p, double *s, double *next, int32_t *nonfinite, void *ws,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

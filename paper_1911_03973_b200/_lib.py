@@ -155,6 +155,36 @@ SIGNATURES = {
     "ebs_plan_free_mask": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ebs_plan_internal_rhs": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ebs_plan_internal_diag": (c_int, [c_void_p, c_void_p, c_void_p]),
+    # peer-memory halo (peer.cu)
+    "ebs_peer_window_bytes": (c_size_t, [c_int64]),
+    "ebs_peer_window_alloc": (c_int, [c_int64, POINTER(c_void_p), c_void_p]),
+    "ebs_peer_window_open": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "ebs_peer_window_close": (c_int, [c_void_p]),
+    "ebs_peer_window_free": (c_int, [c_void_p]),
+    "ebs_peer_create": (c_int, [c_int, c_int, c_int64, c_void_p, c_double, POINTER(c_void_p)]),
+    "ebs_peer_destroy": (c_int, [c_void_p]),
+    "ebs_peer_set_halo": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p,
+                                  c_void_p]),
+    "ebs_peer_status": (c_int, [c_void_p, c_void_p]),
+    "ebs_peer_allreduce": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "ebs_peer_send": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_recv": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_push": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_combine": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_jacobi_sweep": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_matvec_sweep": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_combine_jacobi": (c_int, [c_void_p, c_void_p, c_double, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_combine_q": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_cg1_update": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double,
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p]),
 }
 
 _lib = None

@@ -8,6 +8,7 @@
 // (owner = lowest rank touching the node) and are then all-reduced.  All reductions here
 // are fixed-order (deterministic for a fixed launch configuration).
 #include "ebs_internal.cuh"
+#include "peer.cuh"
 
 namespace ebs {
 
@@ -177,29 +178,58 @@ __global__ void __launch_bounds__(256)
 // ctl = [stop, k_stop, k, diverged]: the loop rules of _iterate (solvers.py:117-160) on the
 // device -- stop when ||r_k|| <= tol ||r_0|| (tol >= 0) or ||r_k|| is not finite; every
 // later launch (and the plan's fused matvec sweeps, ebs_dist_set_stop) is a no-op.
+// rg.win != nullptr (ebs_peer_cg1_update): cur[0..2] are not reduced yet -- every block
+// waits for the ranks' contributions in the peer window (put by ebs_peer_combine_q) and adds
+// them in rank order; block 0 stores the sums in cur, the last block advances the window's
+// all-reduce epoch (also on the stopping launch, so every rank's epoch stays in step).
 #ifndef EBS_CG1_MINB
 #define EBS_CG1_MINB 1
 #endif
 __global__ void __launch_bounds__(256, EBS_CG1_MINB)
     k_vec_cg1_update(int64_t n, double *cur, const double *__restrict__ prev,
-                     const double *__restrict__ rr0, double tol, int32_t *ctl,
+                     double *rr0, double tol, int32_t *ctl,
                      const uint8_t *__restrict__ owned, const double *__restrict__ dinv,
                      double *__restrict__ x, double *__restrict__ r, double *__restrict__ u,
                      const double *__restrict__ w, double *__restrict__ p,
                      double *__restrict__ s, double *partials, unsigned int *counter,
-                     double *next, int32_t *nonfinite) {
+                     double *next, int32_t *nonfinite, const RedGet rg) {
     if (ctl && ctl[0]) return;
-    const double gamma = cur[0], delta = cur[1], rr = cur[2];
+    double gamma, delta, rr;
+    unsigned long long ep = 0;
+    if (rg.win) {
+        double v[3];
+        ep = red_get_block<3>(rg, v);
+        gamma = v[0];
+        delta = v[1];
+        rr = v[2];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            cur[0] = gamma;
+            cur[1] = delta;
+            cur[2] = rr;
+            cur[4] = rr;  // history copy: [0..2] are reused for partials B iterations on
+        }
+    } else {
+        gamma = cur[0];
+        delta = cur[1];
+        rr = cur[2];
+    }
+    bool stopping = false;
+    // peer all-reduce: ||r_0||^2 is known only here, at the first step (k = 0)
+    const bool first = rg.win && (ctl ? ctl[2] == 0 : prev[0] == 0.0);
+    const double rr0v = tol < 0.0 ? 0.0 : (first ? rr : rr0[0]);
+    if (first && rr0 && blockIdx.x == 0 && threadIdx.x == 0) rr0[0] = rr;
     if (ctl) {
         const double nk = sqrt(rr);
         const bool bad = !isfinite(nk);
-        if (bad || (tol >= 0.0 && nk <= tol * sqrt(rr0[0]))) {
+        if (bad || (tol >= 0.0 && nk <= tol * sqrt(rr0v))) {
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 ctl[1] = ctl[2];
                 ctl[3] = bad ? 1 : 0;
                 ctl[0] = 1;
             }
-            return;  // every block takes the same decision from the same scalars
+            // every block takes the same decision from the same scalars
+            if (!rg.win) return;
+            stopping = true;
         }
     }
     const double g_prev = prev[0], a_prev = prev[3];
@@ -209,7 +239,7 @@ __global__ void __launch_bounds__(256, EBS_CG1_MINB)
     double part[2] = {0.0, 0.0};
     bool bad = false;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < (stopping ? 0 : n);
          base += stride * VEC_ILP) {
         double uv[VEC_ILP], wv[VEC_ILP], pv[VEC_ILP], sv[VEC_ILP], xv[VEC_ILP], rv[VEC_ILP],
             dv[VEC_ILP];
@@ -252,10 +282,13 @@ __global__ void __launch_bounds__(256, EBS_CG1_MINB)
     if (bad) atomicOr(nonfinite, 1);
     double tot[2];
     if (grid_sum_last<2>(part, partials, counter, tot) && threadIdx.x == 0) {
-        next[0] = tot[0];
-        next[2] = tot[1];
-        cur[3] = alpha;
-        if (ctl) ctl[2] += 1;
+        if (rg.win) reinterpret_cast<WinHdr *>(rg.win)->red_epoch = ep + 1;
+        if (!stopping) {
+            next[0] = tot[0];
+            next[2] = tot[1];
+            cur[3] = alpha;
+            if (ctl) ctl[2] += 1;
+        }
     }
 }
 
@@ -291,6 +324,28 @@ static Scratch scratch(void *ws) {
     s.counter = reinterpret_cast<unsigned int *>(ws);
     s.partials = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256);
     return s;
+}
+
+}  // namespace ebs
+
+namespace ebs {
+// the same step with cur[0..2] all-reduced on the device from the peer window (ebs_peer_*)
+int peer_cg1_update(const ebs::RedGet &rg, int64_t n, double *cur, const double *prev,
+                    const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
+                    const double *dinv, double *x, double *r, double *u, const double *w,
+                    double *p, double *s, double *next, int32_t *nonfinite, void *ws,
+                    void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(n >= 0 && cur && prev && owned && dinv && x && r && u && w && p && s && next &&
+                    nonfinite && ws && (rr0 || tol < 0.0) && rg.win,
+                "null argument");
+    Scratch sc = scratch(ws);
+    const int grid = persistent_grid((const void *)k_vec_cg1_update, 256, (n + 255) / 256, 0);
+    k_vec_cg1_update<<<grid, 256, 0, S(stream)>>>(
+        n, cur, prev, const_cast<double *>(rr0), tol, ctl, owned, dinv, x, r, u, w, p, s,
+        sc.partials, sc.counter, next, nonfinite, rg);
+    LAUNCHED();
+    EBS_CATCH
 }
 
 }  // namespace ebs
@@ -401,8 +456,8 @@ int ebs_vec_cg1_update(int64_t n, double *cur, const double *prev, const double 
     Scratch sc = scratch(ws);
     const int grid = persistent_grid((const void *)k_vec_cg1_update, 256, (n + 255) / 256, 0);
     k_vec_cg1_update<<<grid, 256, 0, S(stream)>>>(
-        n, cur, prev, rr0, tol, ctl, owned, dinv, x, r, u, w, p, s, sc.partials, sc.counter,
-        next, nonfinite);
+        n, cur, prev, const_cast<double *>(rr0), tol, ctl, owned, dinv, x, r, u, w, p, s,
+        sc.partials, sc.counter, next, nonfinite, RedGet{nullptr, 0, 0});
     LAUNCHED();
     EBS_CATCH
 }

@@ -1,0 +1,898 @@
+// peer.cu -- the element-slab halo exchange and the dot all-reduce over PEER MEMORY
+// (SURVEY 8e): each rank owns one device window (cudaMalloc, exported by CUDA IPC and
+// mapped by every other rank of the node -- NVLink / NVSwitch P2P on an 8-GPU box); ranks
+// write into each other's windows with plain stores and publish with a release store of
+// an epoch flag; readers acquire the flag and read their own window.
+//
+// Hot path (the slab Jacobi / PCG iterations): the SELL sweep over a rank's chunks takes
+// the chunks holding interface nodes FIRST; the epilogue of an interface node stores its
+// partial sum straight into each sharing neighbour's window, and the last warp to finish
+// an interface chunk releases the neighbours' flags -- so the halo travels while the same
+// launch sweeps the interior chunks (the exchange overlaps the math chunk by chunk, no
+// collective launch, no gather).  The combine kernel that follows acquires the flags,
+// sums every shared node over the touching ranks in ascending rank order (own partial
+// among them: bitwise the values of the NCCL / device-copy transports) and completes the
+// node.  Per rank and iteration: 2 launches (Jacobi), 4 (single-reduction PCG, with the
+// all-reduce kernel) instead of 4-7 plus NCCL.
+//
+// Window layout (bytes): [0, 256) header (flags indexed by SOURCE rank, local epochs,
+// arrival counter, error word); [256, 256 + 32 KiB) all-reduce slots [parity][src][256
+// doubles]; then the halo slots [src][parity][cap doubles].  Double buffering by epoch
+// parity: a sender writes epoch e into slot e & 1 only after completing its own epoch
+// e-1 combine, which needed the receiver's epoch e-1 flag, which the receiver set after
+// finishing its epoch e-2 read of that slot (stream order) -- so a slot is never
+// overwritten while it is read.  Every rank runs the same sequence of exchanges, so
+// the local epoch counters agree.  Waits are bounded (globaltimer): on a timeout the
+// window's error word is set, the kernel proceeds, and ebs_peer_status reports EBS_ENCCL.
+#include "peer.cuh"
+#include "sell.cuh"
+
+#include <algorithm>
+#include <vector>
+
+namespace ebs {
+
+// ------------------------------------------------------------------ peer state --
+struct Peer {
+    int rank = 0, world = 1;
+    int64_t cap = 0;
+    long long timeout_ns = 0;
+    char *win[PEER_MAX] = {nullptr};  // mapped windows; win[rank] is this rank's own
+    // halo (ebs_peer_set_halo)
+    int n_nb = 0;
+    int nb[PEER_MAX] = {0};
+    int64_t len[PEER_MAX] = {0};
+    int64_t n_if = 0;
+    int64_t *all_if = nullptr;             // interface nodes (local ids, ascending)
+    int32_t *ifx = nullptr;                // [n_local]: position in all_if or -1
+    int32_t *snd_off = nullptr;            // [n_if + 1] send entries of interface node i
+    unsigned long long *snd_addr = nullptr;  // remote parity-0 slot address per entry
+    int32_t *pos = nullptr;                // [n_if][n_src]: index in source k or -1
+    int n_src = 0;
+    int src[PEER_MAX] = {0};               // combine sources, ascending rank (self included)
+    int64_t *gidx[PEER_MAX] = {nullptr};   // per neighbour: local ids in slot order (send)
+    int64_t n_local = 0;
+};
+
+WinHdr *hdr_of(const Peer *p) { return reinterpret_cast<WinHdr *>(p->win[p->rank]); }
+
+// ----------------------------------------------------------------- all-reduce --
+struct RedArgs {
+    char *win[PEER_MAX];
+    int rank, world, n;
+    long long timeout_ns;
+};
+
+// phase 1: this rank's n values into slot [parity][rank] of every window, flags released
+__device__ __forceinline__ void red_put(const RedArgs &a, const double *buf, unsigned long long ep) {
+    const int par = (int)(ep & 1);
+    for (int q = 0; q < a.world; ++q) {
+        double *dst = win_red(a.win[q], par, a.rank);
+        for (int i = threadIdx.x; i < a.n; i += blockDim.x) dst[i] = buf[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // the block's stores (barrier) before the flags
+        for (int q = 0; q < a.world; ++q)
+            st_relaxed_sys(&reinterpret_cast<WinHdr *>(a.win[q])->red_flag[a.rank], ep + 1);
+    }
+}
+
+// phase 2: wait for every rank's slot, buf = sum over src = 0..world-1 (fixed order)
+__device__ __forceinline__ void red_get(const RedArgs &a, double *buf, unsigned long long ep) {
+    WinHdr *h = reinterpret_cast<WinHdr *>(a.win[a.rank]);
+    if (threadIdx.x < a.world) peer_wait(&h->red_flag[threadIdx.x], ep + 1, a.timeout_ns, &h->error);
+    __syncthreads();
+    const int par = (int)(ep & 1);
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
+        double s = __ldcg(win_red(a.win[a.rank], par, 0) + i);
+        for (int q = 1; q < a.world; ++q) s += __ldcg(win_red(a.win[a.rank], par, q) + i);
+        buf[i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) h->red_epoch = ep + 1;
+}
+
+// mode 0: put + get (one launch, ranks in separate processes); 1: put only; 2: get only
+// (ranks emulated in one process: every put is enqueued before any get)
+__global__ void __launch_bounds__(256) k_peer_allreduce(__grid_constant__ const RedArgs a,
+                                                        double *buf, int mode) {
+    WinHdr *h = reinterpret_cast<WinHdr *>(a.win[a.rank]);
+    const unsigned long long ep = ld_volatile(&h->red_epoch);
+    if (mode != 2) red_put(a, buf, ep);
+    if (mode != 1) red_get(a, buf, ep);
+}
+
+// --------------------------------------------------------- generic halo put/get --
+struct PutArgs {
+    WinHdr *hdr;
+    int n_nb;
+    int64_t off[PEER_MAX + 1];          // prefix of the neighbours' lengths
+    const double *src[PEER_MAX];        // per neighbour: len doubles (slot order)
+    double *dst[PEER_MAX];              // remote parity-0 slot of this rank in neighbour k
+    unsigned long long *flag[PEER_MAX]; // remote halo_flag[rank] of neighbour k
+    int64_t cap;
+};
+
+__global__ void __launch_bounds__(256) k_peer_put(__grid_constant__ const PutArgs a) {
+    const unsigned long long ep = ld_volatile(&a.hdr->halo_epoch);
+    const int64_t par = (int64_t)(ep & 1);
+    const int64_t tot = a.off[a.n_nb];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (t >= a.off[k + 1]) ++k;
+        const int64_t i = t - a.off[k];
+        a.dst[k][par * a.cap + i] = a.src[k][i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&a.hdr->arrive, 1u);
+        if (prev == gridDim.x - 1) {
+            a.hdr->arrive = 0;
+            __threadfence_system();
+            for (int k = 0; k < a.n_nb; ++k) st_relaxed_sys(a.flag[k], ep + 1);
+        }
+    }
+}
+
+struct GetArgs {
+    WinHdr *hdr;
+    int n_nb;
+    int nb[PEER_MAX];
+    int64_t off[PEER_MAX + 1];
+    const double *slot[PEER_MAX];  // local parity-0 slot of neighbour k
+    double *out[PEER_MAX];
+    int64_t cap;
+    long long timeout_ns;
+};
+
+__global__ void __launch_bounds__(256) k_peer_get(__grid_constant__ const GetArgs a,
+                                                  unsigned int *counter) {
+    const unsigned long long ep = ld_volatile(&a.hdr->halo_epoch);
+    if (threadIdx.x < a.n_nb)
+        peer_wait(&a.hdr->halo_flag[a.nb[threadIdx.x]], ep + 1, a.timeout_ns, &a.hdr->error);
+    __syncthreads();
+    const int64_t par = (int64_t)(ep & 1);
+    const int64_t tot = a.off[a.n_nb];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (t >= a.off[k + 1]) ++k;
+        const int64_t i = t - a.off[k];
+        a.out[k][i] = __ldcg(a.slot[k] + par * a.cap + i);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(counter, 1u);
+        if (prev == gridDim.x - 1) {
+            *counter = 0;
+            a.hdr->halo_epoch = ep + 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------ fused slab sweeps --
+// Interface-node stores of the sweeps: node m's partial s goes to every neighbour that
+// shares m, at its slot position (snd_addr: parity-0 address; + parity * cap).
+struct PeerSend {
+    WinHdr *hdr;
+    const int32_t *ifx;
+    const int32_t *snd_off;
+    const unsigned long long *snd_addr;
+    int64_t cap;
+    int n_if_chunks;
+    int n_nb;
+    unsigned long long *flag[PEER_MAX];  // remote halo_flag[rank] of neighbour k
+};
+
+__device__ __forceinline__ void peer_push(const PeerSend &ps, int m, double s) {
+    const int i = ps.ifx[m];
+    const int64_t par = (int64_t)(ld_volatile(&ps.hdr->halo_epoch) & 1);
+    for (int e = ps.snd_off[i]; e < ps.snd_off[i + 1]; ++e)
+        reinterpret_cast<double *>(ps.snd_addr[e])[par * ps.cap] = s;
+}
+
+// after a warp finished an interface chunk: the last one releases the neighbours' flags
+__device__ __forceinline__ void peer_arrive(const PeerSend &ps, int lane) {
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) {
+        const unsigned prev = atomicAdd(&ps.hdr->arrive, 1u);
+        if (prev == (unsigned)ps.n_if_chunks - 1) {
+            ps.hdr->arrive = 0;
+            __threadfence_system();
+            const unsigned long long val = ld_volatile(&ps.hdr->halo_epoch) + 1;
+            for (int k = 0; k < ps.n_nb; ++k) st_relaxed_sys(ps.flag[k], val);
+        }
+    }
+}
+
+struct PeerJacobiEpi {
+    double omega;
+    const double *__restrict__ b;
+    const double *__restrict__ dinv;
+    const uint8_t *__restrict__ free_m;
+    const uint8_t *__restrict__ iface;
+    double *__restrict__ x_out;
+    double *__restrict__ s_part;
+    const PeerSend *ps;
+    double part[1];
+    __device__ __forceinline__ void operator()(int64_t m, double s, double xo) {
+        if (iface[m]) {
+            s_part[m] = s;
+            peer_push(*ps, (int)m, s);
+            return;
+        }
+        double r = free_m[m] ? b[m] - s : 0.0;
+        part[0] += r * r;
+        if (x_out) x_out[m] = dinv ? xo + omega * (dinv[m] * r) : xo + omega * r;
+    }
+};
+
+struct PeerMatvecEpi {
+    const uint8_t *__restrict__ free_m;
+    const uint8_t *__restrict__ iface;
+    double *__restrict__ q;
+    const PeerSend *ps;
+    double part[1];
+    __device__ __forceinline__ void operator()(int64_t m, double s, double po) {
+        if (iface[m]) {
+            q[m] = s;  // partial; completed after the halo
+            peer_push(*ps, (int)m, s);
+            return;
+        }
+        double qm = free_m[m] ? s : 0.0;
+        q[m] = qm;
+        part[0] += po * qm;
+    }
+};
+
+// The chunk list holds the interface chunks first (clist[0, n_if_chunks)): the first
+// warps of the persistent grid take them at launch, push their nodes and arrive.
+template <int NB, int IDS, bool PIPE, class Epi>
+__device__ __forceinline__ void peer_sweep(const SellView &v, const double *__restrict__ x,
+                                           Epi &epi, const PeerSend &ps) {
+    __shared__ __align__(16) int32_t stab_all[256 / LANES][SellStab<NB, IDS>::CAP];
+    const int lane = threadIdx.x & (LANES - 1);
+    int32_t *stab = sell_stab_init<NB, IDS>(v, stab_all);
+    const XLdg xl{x};
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+    const int nwarps = (int)((gridDim.x * blockDim.x) / LANES);
+    const int nlist = (int)v.nlist;
+    for (int ci = warp; ci < nlist; ci += nwarps) {
+        sell_chunk<NB, IDS, false, PIPE>(v, v.clist[ci], lane, stab, xl, epi);
+        if (ci < ps.n_if_chunks) peer_arrive(ps, lane);
+    }
+}
+
+template <int NB, int IDS>
+__global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
+    k_peer_jacobi_sweep(SellView v, const double *__restrict__ x, PeerJacobiEpi epi,
+                        __grid_constant__ const PeerSend ps, double *partials,
+                        unsigned int *counter, double *red) {
+    epi.ps = &ps;
+    peer_sweep<NB, IDS, NB == 3>(v, x, epi, ps);
+    double tot[1];
+    if (grid_sum_last<1>(epi.part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+template <int NB, int IDS>
+__global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
+    k_peer_matvec_sweep(SellView v, const double *__restrict__ p, PeerMatvecEpi epi,
+                        __grid_constant__ const PeerSend ps, double *partials,
+                        unsigned int *counter, double *red, const int32_t *stop) {
+    if (stop && *stop) return;  // single-reduction PCG already stopped (ebs_dist_set_stop)
+    epi.ps = &ps;
+    peer_sweep<NB, IDS, false>(v, p, epi, ps);
+    double tot[1];
+    if (grid_sum_last<1>(epi.part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
+}
+
+// ------------------------------------------------------- combine + completion --
+struct PeerRecv {
+    WinHdr *hdr;
+    const char *win;  // this rank's window
+    int64_t cap;
+    int64_t n_if;
+    const int64_t *all_if;
+    const int32_t *pos;
+    int n_src;
+    int src[PEER_MAX];
+    int rank;
+    long long timeout_ns;
+};
+
+// every block: wait for the neighbours' flags of epoch ep (thread k waits for source k)
+__device__ __forceinline__ unsigned long long recv_wait(const PeerRecv &r) {
+    const unsigned long long ep = ld_volatile(&r.hdr->halo_epoch);
+    if (threadIdx.x < r.n_src && r.src[threadIdx.x] != r.rank)
+        peer_wait(&r.hdr->halo_flag[r.src[threadIdx.x]], ep + 1, r.timeout_ns, &r.hdr->error);
+    __syncthreads();
+    return ep;
+}
+
+// sum of the contributions to shared node i in ascending rank order (own partial: v)
+__device__ __forceinline__ double recv_sum(const PeerRecv &r, int64_t i, const double *v,
+                                           int par) {
+    double acc = 0.0;
+    for (int k = 0; k < r.n_src; ++k) {
+        const int32_t q = r.pos[i * r.n_src + k];
+        if (q < 0) continue;
+        acc += r.src[k] == r.rank
+                   ? v[q]
+                   : __ldcg(win_recv(const_cast<char *>(r.win), r.cap, r.src[k], par) + q);
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(256)
+    k_peer_combine_jacobi(__grid_constant__ const PeerRecv r, double *s, double omega,
+                          const double *__restrict__ b, const double *__restrict__ dinv,
+                          const uint8_t *__restrict__ free_m, const uint8_t *__restrict__ owned,
+                          const double *__restrict__ x, double *__restrict__ x_out,
+                          double *partials, unsigned int *counter, const double *prior,
+                          double *red) {
+    const unsigned long long ep = recv_wait(r);
+    const int par = (int)(ep & 1);
+    double part[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = r.all_if[i];
+        const double acc = recv_sum(r, i, s, par);
+        s[m] = acc;
+        const double rr = free_m[m] ? b[m] - acc : 0.0;
+        if (owned[m]) part[0] += rr * rr;
+        if (x_out) x_out[m] = dinv ? x[m] + omega * (dinv[m] * rr) : x[m] + omega * rr;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) {
+        red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
+        r.hdr->halo_epoch = ep + 1;
+    }
+}
+
+// This rank's contribution to the fused all-reduce: dots[0..3) into slot [parity][rank] of
+// every window, then the flags (one thread; the put phase of ebs_peer_allreduce).
+struct RedPut {
+    char *win[PEER_MAX];
+    int rank, world;
+};
+
+__device__ __forceinline__ void red_put_thread(const RedPut &a, const double *dots) {
+    WinHdr *h = reinterpret_cast<WinHdr *>(a.win[a.rank]);
+    const unsigned long long ep = ld_volatile(&h->red_epoch);
+    const int par = (int)(ep & 1);
+    const double d0 = dots[0], d1 = dots[1], d2 = dots[2];
+    for (int q = 0; q < a.world; ++q) {
+        double *dst = win_red(a.win[q], par, a.rank);
+        dst[0] = d0;
+        dst[1] = d1;
+        dst[2] = d2;
+    }
+    __threadfence_system();
+    for (int q = 0; q < a.world; ++q)
+        st_relaxed_sys(&reinterpret_cast<WinHdr *>(a.win[q])->red_flag[a.rank], ep + 1);
+}
+
+__global__ void __launch_bounds__(256)
+    k_peer_combine_q(__grid_constant__ const PeerRecv r, double *q,
+                     const uint8_t *__restrict__ free_m, const uint8_t *__restrict__ owned,
+                     const double *__restrict__ p, double *partials, unsigned int *counter,
+                     const double *prior, double *red, const int32_t *stop,
+                     __grid_constant__ const RedPut rp, const double *dots) {
+    // a stopped single-reduction PCG: the sweep sent nothing (every rank stops at the same
+    // iteration -- the decision comes from all-reduced scalars), so nothing is awaited
+    if (stop && *stop) return;
+    const unsigned long long ep = recv_wait(r);
+    const int par = (int)(ep & 1);
+    double part[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = r.all_if[i];
+        const double acc = recv_sum(r, i, q, par);
+        const double qm = free_m[m] ? acc : 0.0;
+        q[m] = qm;
+        if (owned[m]) part[0] += p[m] * qm;
+    }
+    double tot[1];
+    if (grid_sum_last<1>(part, partials, counter, tot) && threadIdx.x == 0) {
+        red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
+        r.hdr->halo_epoch = ep + 1;
+        if (dots) red_put_thread(rp, dots);
+    }
+}
+
+// v[all_if[i]] = the rank-ordered sum (the halo of setup / residual vectors)
+__global__ void __launch_bounds__(256)
+    k_peer_combine(__grid_constant__ const PeerRecv r, double *v, unsigned int *counter) {
+    const unsigned long long ep = recv_wait(r);
+    const int par = (int)(ep & 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double acc = recv_sum(r, i, v, par);
+        v[r.all_if[i]] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(counter, 1u);
+        if (prev == gridDim.x - 1) {
+            *counter = 0;
+            r.hdr->halo_epoch = ep + 1;
+        }
+    }
+}
+
+// v at the interface nodes into the neighbours' slots (k_peer_put over per-node entries)
+__global__ void __launch_bounds__(256)
+    k_peer_push_vec(__grid_constant__ const PeerSend ps, int64_t n_if,
+                    const int64_t *__restrict__ all_if, const double *__restrict__ v) {
+    const unsigned long long ep = ld_volatile(&ps.hdr->halo_epoch);
+    const int64_t par = (int64_t)(ep & 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double val = v[all_if[i]];
+        for (int e = ps.snd_off[i]; e < ps.snd_off[i + 1]; ++e)
+            reinterpret_cast<double *>(ps.snd_addr[e])[par * ps.cap] = val;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&ps.hdr->arrive, 1u);
+        if (prev == gridDim.x - 1) {
+            ps.hdr->arrive = 0;
+            __threadfence_system();
+            for (int k = 0; k < ps.n_nb; ++k) st_relaxed_sys(ps.flag[k], ep + 1);
+        }
+    }
+}
+
+int peer_cg1_update(const RedGet &rg, int64_t n, double *cur, const double *prev,
+                    const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
+                    const double *dinv, double *x, double *r, double *u, const double *w,
+                    double *p, double *s, double *next, int32_t *nonfinite, void *ws,
+                    void *stream);  // dist.cu
+
+PeerSend peer_send_args(const Peer *p, int64_t n_if_chunks) {
+    PeerSend ps{};
+    ps.hdr = hdr_of(p);
+    ps.ifx = p->ifx;
+    ps.snd_off = p->snd_off;
+    ps.snd_addr = p->snd_addr;
+    ps.cap = p->cap;
+    ps.n_if_chunks = (int)n_if_chunks;
+    ps.n_nb = p->n_nb;
+    for (int k = 0; k < p->n_nb; ++k)
+        ps.flag[k] = &reinterpret_cast<WinHdr *>(p->win[p->nb[k]])->halo_flag[p->rank];
+    return ps;
+}
+
+PeerRecv peer_recv_args(const Peer *p) {
+    PeerRecv r{};
+    r.hdr = hdr_of(p);
+    r.win = p->win[p->rank];
+    r.cap = p->cap;
+    r.n_if = p->n_if;
+    r.all_if = p->all_if;
+    r.pos = p->pos;
+    r.n_src = p->n_src;
+    for (int k = 0; k < p->n_src; ++k) r.src[k] = p->src[k];
+    r.rank = p->rank;
+    r.timeout_ns = p->timeout_ns;
+    return r;
+}
+
+struct Scratch2 {
+    double *partials;
+    unsigned int *counter;
+};
+inline Scratch2 scratch2(void *ws) {  // the layout of dist.cu's ebs_vec_workspace_bytes
+    Scratch2 s;
+    s.counter = reinterpret_cast<unsigned int *>(ws);
+    s.partials = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256);
+    return s;
+}
+
+}  // namespace ebs
+
+using namespace ebs;
+
+extern "C" {
+
+size_t ebs_peer_window_bytes(int64_t cap) { return window_bytes(cap < 0 ? 0 : cap); }
+
+int ebs_peer_window_alloc(int64_t cap, void **win, void *handle_out) {
+    EBS_TRY
+    EBS_REQUIRE(cap >= 0 && win, "bad arguments");
+    void *p = nullptr;
+    CU(cudaMalloc(&p, window_bytes(cap)));
+    cudaError_t e = cudaMemset(p, 0, window_bytes(cap));
+    if (e == cudaSuccess && handle_out) {
+        cudaIpcMemHandle_t h;
+        e = cudaIpcGetMemHandle(&h, p);
+        if (e == cudaSuccess) std::memcpy(handle_out, &h, sizeof h);
+    }
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        CU(e);
+    }
+    CU(cudaDeviceSynchronize());
+    *win = p;
+    EBS_CATCH
+}
+
+int ebs_peer_window_open(const void *handle, void **win) {
+    EBS_TRY
+    EBS_REQUIRE(handle && win, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void *p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *win = p;
+    EBS_CATCH
+}
+
+int ebs_peer_window_close(void *win) {
+    EBS_TRY
+    if (win) CU(cudaIpcCloseMemHandle(win));
+    EBS_CATCH
+}
+
+int ebs_peer_window_free(void *win) {
+    EBS_TRY
+    if (win) CU(cudaFree(win));
+    EBS_CATCH
+}
+
+int ebs_peer_create(int rank, int world, int64_t cap, void *const *wins, double timeout_s,
+                    ebs_peer_t *out) {
+    EBS_TRY
+    EBS_REQUIRE(world >= 1 && world <= PEER_MAX && rank >= 0 && rank < world && cap >= 0 &&
+                    wins && out,
+                "bad arguments (1 <= world <= %d)", PEER_MAX);
+    for (int q = 0; q < world; ++q) EBS_REQUIRE(wins[q], "null window of rank %d", q);
+    Peer *p = new Peer();
+    p->rank = rank;
+    p->world = world;
+    p->cap = cap;
+    p->timeout_ns = timeout_s < 0 ? (long long)4e18 : (long long)(timeout_s * 1e9);
+    for (int q = 0; q < world; ++q) p->win[q] = static_cast<char *>(wins[q]);
+    p->n_src = 1;
+    p->src[0] = rank;
+    *out = reinterpret_cast<ebs_peer_t>(p);
+    EBS_CATCH
+}
+
+static void peer_clear_halo(Peer *p) {
+    dfree(p->all_if);
+    dfree(p->ifx);
+    dfree(p->snd_off);
+    dfree(p->snd_addr);
+    dfree(p->pos);
+    for (int k = 0; k < PEER_MAX; ++k) dfree(p->gidx[k]);
+    p->n_nb = 0;
+    p->n_if = 0;
+    p->n_src = 1;
+    p->src[0] = p->rank;
+}
+
+int ebs_peer_destroy(ebs_peer_t peer) {
+    EBS_TRY
+    if (!peer) return EBS_OK;
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    peer_clear_halo(p);
+    delete p;
+    EBS_CATCH
+}
+
+int ebs_peer_set_halo(ebs_peer_t peer, int64_t n_local, int n_nb, const int32_t *nb_ranks,
+                      const int64_t *nb_len, const int64_t *const *nb_idx, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && n_local >= 0 && n_nb >= 0 && (n_nb == 0 || (nb_ranks && nb_len && nb_idx)),
+                "bad arguments");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(n_nb < p->world, "more neighbours than ranks");
+    cudaStream_t s = S(stream);
+    std::vector<std::vector<int64_t>> idx(n_nb);
+    for (int k = 0; k < n_nb; ++k) {
+        EBS_REQUIRE(nb_ranks[k] >= 0 && nb_ranks[k] < p->world && nb_ranks[k] != p->rank &&
+                        (k == 0 || nb_ranks[k] > nb_ranks[k - 1]),
+                    "neighbour ranks must be ascending, distinct from the caller");
+        EBS_REQUIRE(nb_len[k] >= 0 && nb_len[k] <= p->cap, "interface %d longer than the window "
+                    "capacity (%lld > %lld)", k, (long long)nb_len[k], (long long)p->cap);
+        idx[k].resize(nb_len[k]);
+        if (nb_len[k])
+            CU(cudaMemcpyAsync(idx[k].data(), nb_idx[k], sizeof(int64_t) * nb_len[k],
+                               cudaMemcpyDeviceToHost, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    std::vector<int64_t> all;
+    for (int k = 0; k < n_nb; ++k) {
+        for (int64_t m : idx[k]) EBS_REQUIRE(m >= 0 && m < n_local, "interface node out of range");
+        all.insert(all.end(), idx[k].begin(), idx[k].end());
+    }
+    std::sort(all.begin(), all.end());
+    all.erase(std::unique(all.begin(), all.end()), all.end());
+    const int64_t n_if = (int64_t)all.size();
+    EBS_REQUIRE(n_local < (1ll << 31) && n_if < (1ll << 31), "slab too large");
+    std::vector<int32_t> ifx(n_local, -1);
+    for (int64_t i = 0; i < n_if; ++i) ifx[all[i]] = (int32_t)i;
+    // send entries per interface node (neighbours ascending) and the combine positions
+    std::vector<std::vector<std::pair<int, int64_t>>> ent(n_if);
+    for (int k = 0; k < n_nb; ++k)
+        for (int64_t j = 0; j < nb_len[k]; ++j) ent[ifx[idx[k][j]]].push_back({k, j});
+    std::vector<int32_t> off(n_if + 1, 0);
+    std::vector<unsigned long long> addr;
+    int srcs[PEER_MAX];
+    int n_src = 0;
+    {
+        std::vector<int> r(nb_ranks, nb_ranks + n_nb);
+        r.push_back(p->rank);
+        std::sort(r.begin(), r.end());
+        for (int v : r) srcs[n_src++] = v;
+    }
+    std::vector<int32_t> pos((size_t)n_if * n_src, -1);
+    for (int64_t i = 0; i < n_if; ++i) {
+        off[i + 1] = off[i] + (int32_t)ent[i].size();
+        for (auto &e : ent[i]) {
+            const int q = nb_ranks[e.first];
+            addr.push_back(reinterpret_cast<unsigned long long>(
+                win_recv(p->win[q], p->cap, p->rank, 0) + e.second));
+            const int ks = (int)(std::find(srcs, srcs + n_src, q) - srcs);
+            pos[(size_t)i * n_src + ks] = (int32_t)e.second;
+        }
+        const int self = (int)(std::find(srcs, srcs + n_src, p->rank) - srcs);
+        pos[(size_t)i * n_src + self] = (int32_t)all[i];
+    }
+    peer_clear_halo(p);
+    p->n_local = n_local;
+    p->n_nb = n_nb;
+    for (int k = 0; k < n_nb; ++k) {
+        p->nb[k] = nb_ranks[k];
+        p->len[k] = nb_len[k];
+        p->gidx[k] = dmalloc<int64_t>(nb_len[k]);
+        if (nb_len[k])
+            CU(cudaMemcpyAsync(p->gidx[k], idx[k].data(), sizeof(int64_t) * nb_len[k],
+                               cudaMemcpyHostToDevice, s));
+    }
+    p->n_if = n_if;
+    p->n_src = n_src;
+    for (int k = 0; k < n_src; ++k) p->src[k] = srcs[k];
+    p->all_if = dmalloc<int64_t>(n_if);
+    p->ifx = dmalloc<int32_t>(n_local);
+    p->snd_off = dmalloc<int32_t>(n_if + 1);
+    p->snd_addr = dmalloc<unsigned long long>(addr.size());
+    p->pos = dmalloc<int32_t>(pos.size());
+    if (n_if) CU(cudaMemcpyAsync(p->all_if, all.data(), sizeof(int64_t) * n_if, cudaMemcpyHostToDevice, s));
+    if (n_local) CU(cudaMemcpyAsync(p->ifx, ifx.data(), sizeof(int32_t) * n_local, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(p->snd_off, off.data(), sizeof(int32_t) * (n_if + 1), cudaMemcpyHostToDevice, s));
+    if (!addr.empty())
+        CU(cudaMemcpyAsync(p->snd_addr, addr.data(), sizeof(unsigned long long) * addr.size(),
+                           cudaMemcpyHostToDevice, s));
+    if (!pos.empty())
+        CU(cudaMemcpyAsync(p->pos, pos.data(), sizeof(int32_t) * pos.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));  // host vectors go out of scope
+    EBS_CATCH
+}
+
+int ebs_peer_status(ebs_peer_t peer, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    unsigned int err = 0;
+    CU(cudaMemcpyAsync(&err, &hdr_of(p)->error, sizeof err, cudaMemcpyDeviceToHost, S(stream)));
+    CU(cudaStreamSynchronize(S(stream)));
+    if (err) {
+        set_error("peer exchange timed out waiting for another rank (rank %d of %d)", p->rank,
+                  p->world);
+        return EBS_ENCCL;
+    }
+    EBS_CATCH
+}
+
+int ebs_peer_allreduce(ebs_peer_t peer, double *buf, int64_t n, int mode, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && (buf || n == 0) && n >= 0 && mode >= 0 && mode <= 2, "bad arguments");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    RedArgs a{};
+    for (int q = 0; q < p->world; ++q) a.win[q] = p->win[q];
+    a.rank = p->rank;
+    a.world = p->world;
+    a.timeout_ns = p->timeout_ns;
+    EBS_REQUIRE(mode == 0 || n <= PEER_RED_MAX, "split all-reduce phases take <= %d values",
+                PEER_RED_MAX);
+    for (int64_t o = 0; o < n; o += PEER_RED_MAX) {
+        a.n = (int)std::min<int64_t>(PEER_RED_MAX, n - o);
+        k_peer_allreduce<<<1, 256, 0, S(stream)>>>(a, buf + o, mode);
+        LAUNCHED();
+    }
+    EBS_CATCH
+}
+
+int ebs_peer_send(ebs_peer_t peer, const double *const *bufs, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(p->n_nb == 0 || bufs, "null buffers");
+    PutArgs a{};
+    a.hdr = hdr_of(p);
+    a.n_nb = p->n_nb;
+    a.cap = p->cap;
+    a.off[0] = 0;
+    for (int k = 0; k < p->n_nb; ++k) {
+        EBS_REQUIRE(bufs[k] || p->len[k] == 0, "null buffer %d", k);
+        a.src[k] = bufs[k];
+        a.dst[k] = win_recv(p->win[p->nb[k]], p->cap, p->rank, 0);
+        a.flag[k] = &reinterpret_cast<WinHdr *>(p->win[p->nb[k]])->halo_flag[p->rank];
+        a.off[k + 1] = a.off[k] + p->len[k];
+    }
+    k_peer_put<<<grid_for(a.off[p->n_nb], 256, sm_count()), 256, 0, S(stream)>>>(a);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_recv(ebs_peer_t peer, double *const *out, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && ws, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(p->n_nb == 0 || out, "null outputs");
+    GetArgs a{};
+    a.hdr = hdr_of(p);
+    a.n_nb = p->n_nb;
+    a.cap = p->cap;
+    a.timeout_ns = p->timeout_ns;
+    a.off[0] = 0;
+    for (int k = 0; k < p->n_nb; ++k) {
+        EBS_REQUIRE(out[k] || p->len[k] == 0, "null output %d", k);
+        a.nb[k] = p->nb[k];
+        a.slot[k] = win_recv(p->win[p->rank], p->cap, p->nb[k], 0);
+        a.out[k] = out[k];
+        a.off[k + 1] = a.off[k] + p->len[k];
+    }
+    k_peer_get<<<grid_for(a.off[p->n_nb], 256, sm_count()), 256, 0, S(stream)>>>(
+        a, scratch2(ws).counter);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_push(ebs_peer_t peer, const double *v, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && v, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    const PeerSend ps = peer_send_args(p, 0);
+    k_peer_push_vec<<<grid_for(p->n_if, 256, sm_count()), 256, 0, S(stream)>>>(ps, p->n_if,
+                                                                               p->all_if, v);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_combine(ebs_peer_t peer, double *v, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && v && ws, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    const PeerRecv r = peer_recv_args(p);
+    k_peer_combine<<<grid_for(p->n_if, 256, sm_count()), 256, 0, S(stream)>>>(
+        r, v, scratch2(ws).counter);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_jacobi_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks, int64_t n_list,
+                          int64_t n_if_chunks, double omega, const double *x, double *x_out,
+                          const double *b, const double *dinv, const uint8_t *iface,
+                          double *s_part, double *red, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && peer && x && b && iface && s_part && red && ws, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Peer *pr = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(n_list >= 1 && chunks && n_if_chunks >= 0 && n_if_chunks <= n_list,
+                "bad chunk list");
+    EBS_REQUIRE(pr->n_local == p->n_n, "peer halo set for %lld nodes, plan has %lld",
+                (long long)pr->n_local, (long long)p->n_n);
+    EBS_REQUIRE((n_if_chunks > 0) == (pr->n_nb > 0), "interface chunks without neighbours "
+                "(or the reverse)");
+    const Scratch2 sc = scratch2(ws);
+    const PeerSend ps = peer_send_args(pr, n_if_chunks);
+    PeerJacobiEpi epi{omega, b, dinv, p->free_int, iface, x_out, s_part, nullptr, {0.0}};
+    SellView v = sell_view(p, chunks, n_list);
+#define EBS_PJ(NB_, IDS_)                                                                  \
+    {                                                                                      \
+        auto kern = k_peer_jacobi_sweep<NB_, IDS_>;                                        \
+        const int grid = persistent_grid((const void *)kern, 256,                          \
+                                         (n_list * LANES + 255) / 256, 0);                 \
+        kern<<<grid, 256, 0, S(stream)>>>(v, x, epi, ps, sc.partials, sc.counter, red);    \
+    }
+    EBS_SELL_DISPATCH(p, EBS_PJ);
+#undef EBS_PJ
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_matvec_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks, int64_t n_list,
+                          int64_t n_if_chunks, const double *pv, double *q, const uint8_t *iface,
+                          double *red, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && peer && pv && q && iface && red && ws, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Peer *pr = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(n_list >= 1 && chunks && n_if_chunks >= 0 && n_if_chunks <= n_list,
+                "bad chunk list");
+    EBS_REQUIRE(pr->n_local == p->n_n, "peer halo set for %lld nodes, plan has %lld",
+                (long long)pr->n_local, (long long)p->n_n);
+    EBS_REQUIRE((n_if_chunks > 0) == (pr->n_nb > 0), "interface chunks without neighbours "
+                "(or the reverse)");
+    const Scratch2 sc = scratch2(ws);
+    const PeerSend ps = peer_send_args(pr, n_if_chunks);
+    PeerMatvecEpi epi{p->free_int, iface, q, nullptr, {0.0}};
+    SellView v = sell_view(p, chunks, n_list);
+#define EBS_PM(NB_, IDS_)                                                                  \
+    {                                                                                      \
+        auto kern = k_peer_matvec_sweep<NB_, IDS_>;                                        \
+        const int grid = persistent_grid((const void *)kern, 256,                          \
+                                         (n_list * LANES + 255) / 256, 0);                 \
+        kern<<<grid, 256, 0, S(stream)>>>(v, pv, epi, ps, sc.partials, sc.counter, red,    \
+                                          p->dist_stop);                                   \
+    }
+    EBS_SELL_DISPATCH(p, EBS_PM);
+#undef EBS_PM
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_combine_jacobi(ebs_peer_t peer, double *s, double omega, const double *b,
+                            const double *dinv, const uint8_t *free_m, const uint8_t *owned,
+                            const double *x, double *x_out, const double *prior, double *red,
+                            void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && s && b && free_m && owned && x && red && ws, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    const Scratch2 sc = scratch2(ws);
+    const PeerRecv r = peer_recv_args(p);
+    const int grid = persistent_grid((const void *)k_peer_combine_jacobi, 256,
+                                     (p->n_if + 255) / 256, 0);
+    k_peer_combine_jacobi<<<grid, 256, 0, S(stream)>>>(r, s, omega, b, dinv, free_m, owned, x,
+                                                       x_out, sc.partials, sc.counter, prior, red);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_combine_q(ebs_peer_t peer, double *q, const uint8_t *free_m, const uint8_t *owned,
+                       const double *pv, const double *prior, double *red, const int32_t *stop,
+                       const double *dots, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && q && free_m && owned && pv && red && ws, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    const Scratch2 sc = scratch2(ws);
+    const PeerRecv r = peer_recv_args(p);
+    const int grid = persistent_grid((const void *)k_peer_combine_q, 256, (p->n_if + 255) / 256, 0);
+    RedPut rp{};
+    for (int k = 0; k < p->world; ++k) rp.win[k] = p->win[k];
+    rp.rank = p->rank;
+    rp.world = p->world;
+    k_peer_combine_q<<<grid, 256, 0, S(stream)>>>(r, q, free_m, owned, pv, sc.partials,
+                                                  sc.counter, prior, red, stop, rp, dots);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_cg1_update(ebs_peer_t peer, int64_t n, double *cur, const double *prev,
+                        const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
+                        const double *dinv, double *x, double *r, double *u, const double *w,
+                        double *p, double *s, double *next, int32_t *nonfinite, void *ws,
+                        void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer, "null argument");
+    Peer *pr = reinterpret_cast<Peer *>(peer);
+    const RedGet rg{pr->win[pr->rank], pr->world, pr->timeout_ns};
+    return peer_cg1_update(rg, n, cur, prev, rr0, tol, ctl, owned, dinv, x, r, u, w, p, s, next,
+                           nonfinite, ws, stream);
+    EBS_CATCH
+}
+
+}  // extern "C"

@@ -222,6 +222,229 @@ class LocalTransport:
             t.copy_(total)
 
 
+def _peer_timeout() -> float:
+    import os
+    return float(os.environ.get("EBS_PEER_TIMEOUT", "600"))
+
+
+class _PeerBase:
+    """Halo exchange and dot all-reduce over peer memory (csrc/peer.cu): no collective
+    library on the data path.  The solver loops use the fused form (fused_peer): the slab
+    sweep pushes the interface partials into the neighbours' windows from its epilogue and
+    the combine kernel waits for them -- 2 launches per Jacobi iteration.  Subclasses hold
+    the ops' native peer views (op.peer) and say how the put and get phases are ordered."""
+
+    fused_peer = True
+    serialize = False
+
+    def after_put(self):
+        """Between the put phase of every local rank and the first get (serialize: host
+        barrier, for several rank processes sharing one GPU in tests)."""
+
+    def exchange_start(self, ops: list, sends: list):
+        keep = []
+        for op, snd in zip(ops, sends):
+            nbs = sorted(snd)
+            if nbs != sorted(op.if_idx):
+                raise ValueError("peer exchange: sends must cover exactly the slab neighbours")
+            bufs = [snd[q].contiguous() for q in nbs]
+            keep.append(bufs)
+            arr = (ctypes.c_void_p * max(len(bufs), 1))(*[b.data_ptr() for b in bufs])
+            call("ebs_peer_send", op.peer, arr, D.stream())
+        self.after_put()
+        return keep
+
+    def exchange_finish(self, handle) -> list:
+        out = []
+        for op in self._ops:
+            nbs = sorted(op.if_idx)
+            recvs = {q: D.empty(op.if_idx[q].numel()) for q in nbs}
+            arr = (ctypes.c_void_p * max(len(nbs), 1))(*[recvs[q].data_ptr() for q in nbs])
+            call("ebs_peer_recv", op.peer, arr, D.ptr(op._ws), D.stream())
+            out.append(recvs)
+        return out
+
+    def exchange(self, ops: list, sends: list) -> list:
+        return self.exchange_finish(self.exchange_start(ops, sends))
+
+    def halo(self, ops: list, vs: list):
+        """v[shared] = rank-ordered sum of the partials: push + combine, 2 launches."""
+        for op, v in zip(ops, vs):
+            op.peer_push(v)
+        self.after_put()
+        for op, v in zip(ops, vs):
+            op.peer_combine(v)
+
+    def allreduce_get(self, tensors: list):
+        """The get phase alone (mode 2) of an all-reduce whose put phase already ran (the
+        put of peer_combine_q with dots): tensors[i] (<= 256 values) := the rank-ordered sum."""
+        for op, t in zip(self._ops, tensors):
+            self._check(t)
+            call("ebs_peer_allreduce", op.peer, D.ptr(t), t.numel(), 2, D.stream())
+
+    def _check(self, t):
+        if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ValueError("peer all-reduce takes contiguous float64 device tensors")
+
+    def status(self):
+        """Raise (EBS_ENCCL) when a wait of a local rank timed out; synchronises."""
+        for op in self._ops:
+            call("ebs_peer_status", op.peer, D.stream())
+
+    def sync(self, timeout=None):
+        self.status()
+
+
+class PeerTransport(_PeerBase):
+    """One rank per process, the node's ranks mapping each other's windows through CUDA IPC
+    (NVLink P2P stores between GPUs; the handles travel through torch.distributed's object
+    collectives -- host plumbing only).  Waits time out after `timeout` s (EBS_PEER_TIMEOUT,
+    600) and report EBS_ENCCL instead of hanging.  serialize=True (tests: several rank
+    processes on ONE GPU): a host barrier after every put phase, so no kernel ever waits on
+    another process's kernels, and no CUDA graphs."""
+
+    def __init__(self, op, group=None, timeout: float | None = None, serialize: bool = False):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.serialize = serialize
+        self._ops = [op]
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if world > 8:
+            raise ValueError("PeerTransport spans at most 8 ranks (one NVSwitch node)")
+        if rank != op.rank:
+            raise ValueError(f"process rank {rank} runs slab {op.rank}")
+        cap = max([t.numel() for t in op.if_idx.values()] + [1])
+        if world > 1:
+            caps = [None] * world
+            dist.all_gather_object(caps, cap, group=group)
+            cap = max(caps)
+        self.world, self.rank, self.cap = world, rank, cap
+        own = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        call("ebs_peer_window_alloc", cap, ctypes.byref(own), handle)
+        self._own = own
+        handles = [bytes(handle.raw)]
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(handle.raw), group=group)
+        self._opened = []
+        wins = []
+        for q in range(world):
+            if q == rank:
+                wins.append(own.value)
+                continue
+            w = ctypes.c_void_p()
+            call("ebs_peer_window_open", ctypes.create_string_buffer(handles[q], 64),
+                 ctypes.byref(w))
+            self._opened.append(w)
+            wins.append(w.value)
+        arr = (ctypes.c_void_p * world)(*wins)
+        peer = ctypes.c_void_p()
+        t = _peer_timeout() if timeout is None else float(timeout)
+        call("ebs_peer_create", rank, world, cap, arr, ctypes.c_double(t), ctypes.byref(peer))
+        self.peer = peer
+        op.peer_attach(peer)
+        if world > 1:  # every window is mapped before anyone writes into it
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+
+    def after_put(self):
+        if self.serialize and self.world > 1:
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+
+    def allreduce(self, tensors: list):
+        (t,) = tensors
+        self._check(t)
+        (op,) = self._ops
+        if not self.serialize:
+            call("ebs_peer_allreduce", op.peer, D.ptr(t), t.numel(), 0, D.stream())
+            return
+        for a in range(0, t.numel(), 256):
+            piece = t[a:a + 256]
+            call("ebs_peer_allreduce", op.peer, D.ptr(piece), piece.numel(), 1, D.stream())
+            self.after_put()
+            call("ebs_peer_allreduce", op.peer, D.ptr(piece), piece.numel(), 2, D.stream())
+
+    def agree(self, ok: bool) -> bool:
+        if self.world == 1:
+            return bool(ok)
+        box = [None] * self.world
+        self.dist.all_gather_object(box, bool(ok), group=self.group)
+        return all(box)
+
+    def close(self):
+        """Release the window mappings (collective: every rank calls it)."""
+        if getattr(self, "peer", None) is None:
+            return
+        torch.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier(group=self.group)
+        call("ebs_peer_destroy", self.peer)
+        for w in self._opened:
+            call("ebs_peer_window_close", w)
+        call("ebs_peer_window_free", self._own)
+        self.peer = None
+        self._ops[0].peer = None
+
+
+class LocalPeerTransport(_PeerBase):
+    """All P ranks in this process on one GPU (emulation, tests): the same windows, kernels
+    and layout as PeerTransport, windows addressed directly; every put phase of all ranks is
+    enqueued before any get, so nothing waits."""
+
+    def __init__(self, ops, timeout: float | None = None):
+        if len(ops) > 8:
+            raise ValueError("peer groups span at most 8 ranks")
+        self._ops = list(ops)
+        P = len(ops)
+        cap = max([t.numel() for op in ops for t in op.if_idx.values()] + [1])
+        self.cap = cap
+        self._wins = []
+        for _ in range(P):
+            w = ctypes.c_void_p()
+            call("ebs_peer_window_alloc", cap, ctypes.byref(w), None)
+            self._wins.append(w)
+        arr = (ctypes.c_void_p * P)(*[w.value for w in self._wins])
+        t = _peer_timeout() if timeout is None else float(timeout)
+        self.peers = []
+        for op in ops:
+            peer = ctypes.c_void_p()
+            call("ebs_peer_create", op.rank, P, cap, arr, ctypes.c_double(t), ctypes.byref(peer))
+            self.peers.append(peer)
+            op.peer_attach(peer)
+
+    def allreduce(self, tensors: list):
+        if len(tensors) != len(self._ops):
+            raise ValueError(f"emulated all-reduce takes one tensor per rank ({len(self._ops)}), "
+                             f"got {len(tensors)}")
+        for t in tensors:
+            self._check(t)
+        n = tensors[0].numel()
+        for a in range(0, n, 256):
+            pieces = [t[a:a + 256] for t in tensors]
+            for op, p in zip(self._ops, pieces):
+                call("ebs_peer_allreduce", op.peer, D.ptr(p), p.numel(), 1, D.stream())
+            for op, p in zip(self._ops, pieces):
+                call("ebs_peer_allreduce", op.peer, D.ptr(p), p.numel(), 2, D.stream())
+
+    def agree(self, ok: bool) -> bool:
+        return bool(ok)
+
+    def close(self):
+        if not self.peers:
+            return
+        torch.cuda.synchronize()
+        for op, p in zip(self._ops, self.peers):
+            call("ebs_peer_destroy", p)
+            op.peer = None
+        for w in self._wins:
+            call("ebs_peer_window_free", w)
+        self.peers = []
+
+
 # ---------------------------------------------------------------- rank operator --
 def rank_operator(mesh, nu: float, f, d, P: int, rank: int, maps: dict | None = None):
     """Rank `rank` of P: partition maps of the mesh and a GpuRankOperator whose element
@@ -339,6 +562,8 @@ class GpuRankOperator:
         self._ws = D.zeros(int(load().ebs_vec_workspace_bytes()), torch.uint8)
         self._acc = D.zeros(n)
         self._flag = D.zeros(1, torch.int32)
+        self._stop = None   # device stop flag of a single-reduction PCG (set_stop)
+        self.peer = None    # native peer group view (peer_attach)
 
     # ---- primitives used by the generic loops ----
     def to_internal(self, x_global: torch.Tensor) -> torch.Tensor:
@@ -508,6 +733,60 @@ class GpuRankOperator:
     def set_stop(self, ctl):
         """Fused matvec sweeps of this rank's plan no-op while ctl[0] != 0 (None clears)."""
         call("ebs_dist_set_stop", self.plan.handle, D.ptr(ctl))
+        self._stop = ctl
+
+    # ---- peer-memory halo (PeerTransport / LocalPeerTransport; csrc/peer.cu) ----
+    def peer_attach(self, peer):
+        """Bind this rank's halo to a native peer group view (ebs_peer_set_halo): the
+        neighbours' slots hold the interface nodes in ascending global id (if_idx order)."""
+        self.peer = peer
+        nbs = sorted(self.if_idx)
+        n = len(nbs)
+        ranks = (ctypes.c_int32 * max(n, 1))(*nbs)
+        lens = (ctypes.c_int64 * max(n, 1))(*[self.if_idx[q].numel() for q in nbs])
+        idx = (ctypes.c_void_p * max(n, 1))(*[self.if_idx[q].data_ptr() for q in nbs])
+        call("ebs_peer_set_halo", peer, self.n, n, ranks, lens, idx, D.stream())
+        # the chunk list of the fused peer sweeps: interface chunks first
+        self.peer_chunks = torch.cat([self.if_chunks, self.in_chunks]).contiguous()
+        self._stop = getattr(self, "_stop", None)
+
+    def peer_jacobi_sweep(self, omega, x, x_out, b, dinv, s_part, red):
+        c = self.peer_chunks
+        call("ebs_peer_jacobi_sweep", self.plan.handle, self.peer, D.ptr(c), c.numel(),
+             self.if_chunks.numel(), float(omega), D.ptr(x), D.ptr(x_out), D.ptr(b), D.ptr(dinv),
+             D.ptr(self.iface), D.ptr(s_part), D.ptr(red), D.ptr(self._ws), D.stream())
+
+    def peer_matvec_sweep(self, p, q, red):
+        c = self.peer_chunks
+        call("ebs_peer_matvec_sweep", self.plan.handle, self.peer, D.ptr(c), c.numel(),
+             self.if_chunks.numel(), D.ptr(p), D.ptr(q), D.ptr(self.iface), D.ptr(red),
+             D.ptr(self._ws), D.stream())
+
+    def peer_combine_jacobi(self, omega, b, s_part, dinv, x, x_out, red, prior=None):
+        call("ebs_peer_combine_jacobi", self.peer, D.ptr(s_part), float(omega), D.ptr(b),
+             D.ptr(dinv), D.ptr(self.free), D.ptr(self.owned), D.ptr(x), D.ptr(x_out),
+             D.ptr(prior), D.ptr(red), D.ptr(self._ws), D.stream())
+
+    def peer_combine_q(self, p, q, red, prior=None, dots=None):
+        """dots: also put dots[0..3) (after red[0] is written) as this rank's contribution to
+        the fused all-reduce that peer_cg1_update consumes."""
+        call("ebs_peer_combine_q", self.peer, D.ptr(q), D.ptr(self.free), D.ptr(self.owned),
+             D.ptr(p), D.ptr(prior), D.ptr(red), D.ptr(self._stop), D.ptr(dots), D.ptr(self._ws),
+             D.stream())
+
+    def peer_cg1_update(self, cur, prev, rr0, tol, ctl, dinv, x, r, u, w, p, s_, nxt):
+        """vec_cg1_update with cur[0..2] all-reduced on the device (waits for every rank's
+        peer_combine_q put, adds the contributions in rank order)."""
+        call("ebs_peer_cg1_update", self.peer, self.n, D.ptr(cur), D.ptr(prev), D.ptr(rr0),
+             float(tol), D.ptr(ctl), D.ptr(self.owned), D.ptr(dinv), D.ptr(x), D.ptr(r), D.ptr(u),
+             D.ptr(w), D.ptr(p), D.ptr(s_), D.ptr(nxt), D.ptr(self._flag), D.ptr(self._ws),
+             D.stream())
+
+    def peer_push(self, v):
+        call("ebs_peer_push", self.peer, D.ptr(v), D.stream())
+
+    def peer_combine(self, v):
+        call("ebs_peer_combine", self.peer, D.ptr(v), D.ptr(self._ws), D.stream())
 
     def dot_owned(self, x, y, red):
         call("ebs_vec_dot_owned", self.n, D.ptr(x), D.ptr(y), D.ptr(self.owned), D.ptr(red),
@@ -518,8 +797,15 @@ class GpuRankOperator:
 
 
 # ------------------------------------------------------------------- loops --
+def _peer(comm) -> bool:
+    return bool(getattr(comm, "fused_peer", False))
+
+
 def halo(ops, comm, vs):
     """Exchange interface partials of vs[i] (rank ops[i]) and combine in rank order."""
+    if _peer(comm):
+        comm.halo(ops, vs)
+        return
     sends = [{q: op.gather(idx, v) for q, idx in op.if_idx.items()} for op, v in zip(ops, vs)]
     recvs = comm.exchange(ops, sends)
     for op, v, rc in zip(ops, vs, recvs):
@@ -667,7 +953,7 @@ def _capture(comm, body):
     run eagerly -- ranks never mix graph replay with eager steps, whose NCCL calls would
     not pair up.  EBS_DIST_GRAPH=0 disables capture."""
     import os
-    if os.environ.get("EBS_DIST_GRAPH", "1") == "0":
+    if os.environ.get("EBS_DIST_GRAPH", "1") == "0" or getattr(comm, "serialize", False):
         return None
     g, err = None, None
     try:
@@ -712,7 +998,8 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     fused = _fused_ok(ops) if fused is None else fused
     B = GRAPH_BATCH
     dev = xs0[0].device
-    ws = _workspace(prob, ("jacobi", float(omega), bool(richardson), bool(fused)),
+    peer = fused and _peer(comm)
+    ws = _workspace(prob, ("jacobi", float(omega), bool(richardson), bool(fused), peer),
                     lambda: _Workspace(
                         xa=[op.zeros() for op in ops], xb=[op.zeros() for op in ops],
                         ss=[op.zeros() for op in ops],
@@ -724,6 +1011,16 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
     red = [torch.zeros(iters + 1, dtype=torch.float64, device=dev) for _ in ops]
 
     def step(src, dst, final, rslot):
+        if peer:  # one sweep pushing the interface partials to the neighbours, combine
+            for i, op in enumerate(ops):
+                op.peer_jacobi_sweep(omega, src[i], None if final else dst[i], prob.b[i],
+                                     None if richardson else prob.dinv[i], ss[i], r3[i][0:1])
+            comm.after_put()
+            for i, op in enumerate(ops):
+                op.peer_combine_jacobi(omega, prob.b[i], ss[i],
+                                       None if richardson else prob.dinv[i], src[i],
+                                       None if final else dst[i], rslot[i], prior=r3[i])
+            return
         if fused:  # interface chunks, exchange || interior chunks, interface completion
             for i, op in enumerate(ops):
                 op.jacobi_sweep(op.if_chunks, omega, src[i], None if final else dst[i], prob.b[i],
@@ -767,6 +1064,9 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
         if not final:
             xa, xb = xb, xa
     comm.allreduce(red)
+    sync = getattr(comm, "sync", None)
+    if sync is not None:
+        sync()
     norms = torch.sqrt(red[0]).cpu().numpy()
     prob.diverged = _diverged(prob, norms)
     return [x.clone() for x in xa], norms  # fresh arrays: the workspace is reused
@@ -814,11 +1114,14 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
     fused = _fused_ok(ops) if fused is None else fused
     tol_ = -1.0 if tol is None else float(tol)
     on_dev = dev.type == "cuda"
-    wsp = _workspace(prob, ("pcg1", tol_, bool(fused)), lambda: _Workspace(
+    peer = fused and _peer(comm)
+    wsp = _workspace(prob, ("pcg1", tol_, bool(fused), peer), lambda: _Workspace(
         xs=[op.zeros() for op in ops], rs=[op.zeros() for op in ops],
         us=[op.zeros() for op in ops], ws=[op.zeros() for op in ops],
         ps=[op.zeros() for op in ops], ss=[op.zeros() for op in ops],
-        ring=[torch.zeros((B, 4), **f64) for _ in ops],   # [gamma, delta, rr, alpha]
+        # [gamma, delta, rr, alpha] (+ peer: the reduced rr again -- [0..2] of a slot are
+        # overwritten with the next-but-B iteration's partials before a graph batch ends)
+        ring=[torch.zeros((B, 5 if peer else 4), **f64) for _ in ops],
         part=[torch.zeros(2, **f64) for _ in ops],        # interface / interior sweep w.u
         ctl=[torch.zeros(4, dtype=torch.int32, device=dev) for _ in ops],
         rr0=[torch.zeros(1, **f64) for _ in ops],
@@ -835,7 +1138,14 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
             op.set_stop(c if fused else None)
 
     def matvec_w(slot):  # w = mask(A u), slot[1] = the rank's owned w.u
-        if fused:
+        if peer:  # ... and [r.u, w.u, r.r] put for the all-reduce the next update takes
+            for i, op in enumerate(ops):
+                op.peer_matvec_sweep(us[i], ws[i], part[i][0:1])
+            comm.after_put()
+            for i, op in enumerate(ops):
+                op.peer_combine_q(us[i], ws[i], slot[i][1:2], prior=part[i], dots=slot[i][0:3])
+            comm.after_put()
+        elif fused:
             for i, op in enumerate(ops):
                 op.matvec_sweep(op.if_chunks, us[i], ws[i], part[i][0:1])
             h = comm.exchange_start(ops, [op.gather_sends(w_) for op, w_ in zip(ops, ws)])
@@ -862,16 +1172,26 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
         op.dot_owned(rs[i], us[i], slot0[i][0:1])
         ss[i].zero_()
     matvec_w(slot0)
-    comm.allreduce([sl[0:3] for sl in slot0])
     norm2 = [torch.zeros(iters + 1, **f64) for _ in ops]
-    for i in range(len(ops)):
-        rr0[i].copy_(slot0[i][2:3])
-        norm2[i][0:1].copy_(slot0[i][2:3])
+    if not peer:
+        comm.allreduce([sl[0:3] for sl in slot0])
+        for i in range(len(ops)):
+            rr0[i].copy_(slot0[i][2:3])
+            norm2[i][0:1].copy_(slot0[i][2:3])
+    # peer: every put of matvec_w is consumed by the next update (ebs_peer_cg1_update: the
+    # slot it reads is reduced there, rr0 set at k = 0), so history entry k is recorded after
+    # step k, and the put of the last step by one get after the loop
 
     def step(k):
         cur = [rg[k % B] for rg in ring]
         prev = [rg[(k - 1) % B] for rg in ring]
         nxt = [rg[(k + 1) % B] for rg in ring]
+        if peer:  # the all-reduce of cur happens inside the update (fused get)
+            for i, op in enumerate(ops):
+                op.peer_cg1_update(cur[i], prev[i], rr0[i], tol_, ctl[i], prob.dinv[i], xs[i],
+                                   rs[i], us[i], ws[i], ps[i], ss[i], nxt[i])
+            matvec_w(nxt)
+            return
         for i, op in enumerate(ops):
             op.vec_cg1_update(cur[i], prev[i], rr0[i], tol_, ctl[i], prob.dinv[i], xs[i], rs[i],
                               us[i], ws[i], ps[i], ss[i], nxt[i])
@@ -892,14 +1212,20 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
         nb = min(B, iters - k)
         if g is not None and nb == B:
             g.replay()
-            for i in range(len(ops)):  # iterations k..k+B-1 wrote slots 1..B-1, 0
-                norm2[i][k + 1:k + B].copy_(ring[i][1:B, 2])
-                norm2[i][k + B:k + B + 1].copy_(ring[i][0:1, 2])
+            for i in range(len(ops)):
+                if peer:  # iterations k..k+B-1 reduced slots 0..B-1
+                    norm2[i][k:k + B].copy_(ring[i][0:B, 4])
+                else:  # iterations k..k+B-1 wrote slots 1..B-1, 0
+                    norm2[i][k + 1:k + B].copy_(ring[i][1:B, 2])
+                    norm2[i][k + B:k + B + 1].copy_(ring[i][0:1, 2])
         else:
             for kk in range(k, k + nb):
                 step(kk)
                 for i in range(len(ops)):
-                    norm2[i][kk + 1:kk + 2].copy_(ring[i][(kk + 1) % B, 2:3])
+                    if peer:
+                        norm2[i][kk:kk + 1].copy_(ring[i][kk % B, 4:5])
+                    else:
+                        norm2[i][kk + 1:kk + 2].copy_(ring[i][(kk + 1) % B, 2:3])
         k += nb
         if k >= iters:
             break
@@ -920,6 +1246,11 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
     if sync is not None:
         sync()
     c = ctl[0].cpu()
+    if peer and not int(c[0]):  # the last step's put (same decision on every rank)
+        last = [rg[iters % B] for rg in ring]
+        comm.allreduce_get([sl[0:3] for sl in last])
+        for i in range(len(ops)):
+            norm2[i][iters:iters + 1].copy_(last[i][2:3])
     for op in ops:
         if hasattr(op, "set_stop"):
             op.set_stop(None)
@@ -946,7 +1277,8 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
             op.set_stop(None)
     fused = _fused_ok(ops) if fused is None else fused
     B = GRAPH_BATCH
-    wsp = _workspace(prob, ("pcg2", bool(fused)), lambda: _Workspace(
+    peer = fused and _peer(comm)
+    wsp = _workspace(prob, ("pcg2", bool(fused), peer), lambda: _Workspace(
         xs=[op.zeros() for op in ops], rs=[op.zeros() for op in ops],
         ps=[op.zeros() for op in ops], qs=[op.zeros() for op in ops],
         ss=[op.zeros() for op in ops],
@@ -976,7 +1308,13 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
     def step(u):
         slot = [rg[u] for rg in ring]
         prev = [rg[(u - 1) % B] for rg in ring]
-        if fused:  # interface chunks, exchange || interior chunks, interface completion
+        if peer:
+            for i, op in enumerate(ops):
+                op.peer_matvec_sweep(ps[i], qs[i], part[i][0:1])
+            comm.after_put()
+            for i, op in enumerate(ops):
+                op.peer_combine_q(ps[i], qs[i], pq[i], prior=part[i])
+        elif fused:  # interface chunks, exchange || interior chunks, interface completion
             for i, op in enumerate(ops):
                 op.matvec_sweep(op.if_chunks, ps[i], qs[i], part[i][0:1])
             h = comm.exchange_start(ops, [op.gather_sends(q_)
@@ -1025,6 +1363,9 @@ def _pcg_two_reductions(prob: DistProblem, xs0, iters: int, tol=None, graph: boo
         for i in range(len(ops)):
             norm2[i][kk + 1:kk + 2].copy_(ring[i][kk % B, 0:1])
     n = k_done + 1
+    sync = getattr(comm, "sync", None)
+    if sync is not None:
+        sync()
     norms = torch.sqrt(norm2[0][:n]).cpu().numpy()
     prob.diverged = _diverged(prob, norms)
     return [x.clone() for x in xs], norms  # fresh arrays: the workspace is reused
@@ -1036,14 +1377,16 @@ def gather_global(ops, vs, n_nodes, comm=None):
     out = torch.zeros(n_nodes, dtype=torch.float64, device=vs[0].device)
     for op, v in zip(ops, vs):
         op.scatter_owned(v, out)
-    if comm is not None and not isinstance(comm, LocalTransport):
+    if comm is not None and not isinstance(comm, (LocalTransport, LocalPeerTransport)):
         comm.allreduce([out])  # owned parts are disjoint: the sum is the global vector
     return out
 
 
-def emulate(batch, n_nodes, d, P, precondition=True):
-    """P ranks in this process on the current GPU (tests; nothing waits on anything)."""
+def emulate(batch, n_nodes, d, P, precondition=True, peer: bool = False):
+    """P ranks in this process on the current GPU (tests; nothing waits on anything).
+    peer=True: the peer-memory transport (LocalPeerTransport: the windows, fused sweeps and
+    combine kernels of PeerTransport), else device copies (LocalTransport)."""
     maps = partition_maps(batch.index.indt, n_nodes, P)
     ops = [GpuRankOperator(batch, n_nodes, d, maps, p) for p in range(P)]
-    comm = LocalTransport()
+    comm = LocalPeerTransport(ops) if peer else LocalTransport()
     return setup(ops, comm, precondition=precondition), maps

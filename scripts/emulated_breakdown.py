@@ -1,6 +1,6 @@
 """Per-kernel device time per iteration of the emulated P-slab loop (one GPU, CUPTI via
 torch.profiler): where the partitioning overhead of scripts/emulated_scaling.py goes.
-Usage: python scripts/emulated_breakdown.py CFG P"""
+Usage: python scripts/emulated_breakdown.py CFG P [peer]"""
 import sys
 from collections import defaultdict
 
@@ -16,7 +16,8 @@ P = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 iters = 64
 p = config_problem(cfg)
 batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
-prob, _ = dist.emulate(batch, m.n_nodes, d, P)
+peer = len(sys.argv) > 3 and sys.argv[3] == "peer"
+prob, _ = dist.emulate(batch, m.n_nodes, d, P, peer=peer)
 x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
 xin = [op.to_internal(x0) for op in prob.ops]
 run = (lambda: dist.jacobi(prob, xin, iters, 0.8, graph=True)) if cfg == 4 else \

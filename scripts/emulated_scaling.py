@@ -4,7 +4,10 @@ process (dist.emulate: every rank's kernels run back to back on the one device, 
 device copy).  The emulated time of P ranks is the sum of their per-rank work, so
 E_compute(P) = T_1GPU / T_emulated(P) measures what partitioning itself costs (interface
 sweeps, halo gather / combine kernels, smaller grids) -- NOT the NVLink / NCCL latency,
-which one GPU cannot show.  Usage: python scripts/emulated_scaling.py [4|5]"""
+which one GPU cannot show.  Both transports: the device-copy one (the NCCL path's kernel
+sequence: interface sweep, send gather, interior sweep, combine) and the peer-memory one
+(one sweep pushing the interface partials, one combine).
+Usage: python scripts/emulated_scaling.py [4|5]"""
 import sys
 
 import torch
@@ -36,14 +39,17 @@ for cfg in [int(a) for a in sys.argv[1:]] or [4, 5]:
     t1 = tm(one)
     print(f"C{cfg}: 1-GPU {iters / t1:.0f} it/s", flush=True)
     for P in (1, 2, 4, 8):
-        prob, _ = dist.emulate(batch, m.n_nodes, d, P)
-        xin = [op.to_internal(x0) for op in prob.ops]
-        run = (lambda: dist.jacobi(prob, xin, iters, 0.8, graph=True)) if cfg == 4 else \
-            (lambda: dist.pcg(prob, xin, iters, graph=True))
-        t = tm(run)
-        print(f"  P={P}: emulated {iters / t:.0f} it/s (sum of the ranks' work), "
-              f"E_compute = {t1 / t:.3f}", flush=True)
-        del prob, xin
-        torch.cuda.empty_cache()
+        for peer in (False, True):
+            prob, _ = dist.emulate(batch, m.n_nodes, d, P, peer=peer)
+            xin = [op.to_internal(x0) for op in prob.ops]
+            run = (lambda: dist.jacobi(prob, xin, iters, 0.8, graph=True)) if cfg == 4 else \
+                (lambda: dist.pcg(prob, xin, iters, graph=True))
+            t = tm(run)
+            print(f"  P={P} {'peer' if peer else 'copy'}: emulated {iters / t:.0f} it/s (sum of "
+                  f"the ranks' work), E_compute = {t1 / t:.3f}", flush=True)
+            if peer:
+                prob.comm.close()
+            del prob, xin
+            torch.cuda.empty_cache()
     del p, batch
     torch.cuda.empty_cache()
