@@ -13,8 +13,32 @@ import numpy as np
 import torch
 
 from paper_1911_03973_b200._lib import load
-from paper_1911_03973_b200.dist import (GRAPH_BATCH, GRAPH_STATS, TorchTransport, _capture,
-                                        jacobi, pcg, rank_operator, setup)
+from paper_1911_03973_b200.dist import (GRAPH_BATCH, GRAPH_STATS, PeerTransport,
+                                        TorchTransport, _capture, jacobi, pcg, rank_operator,
+                                        setup)
+
+TRANSPORTS = {
+    "peer": "peer memory: CUDA-IPC windows, interface partials stored into the neighbours' "
+            "windows from the SELL sweep epilogue (NVLink P2P), flag-waiting combine, dot "
+            "all-reduce fused into the combine / update kernels (dist.PeerTransport)",
+    "nccl": "NCCL send/recv halo + all-reduce through torch.distributed (dist.TorchTransport)",
+}
+
+
+def _transport(op, gloo):
+    """EBS_TRANSPORT=peer (default) | nccl.  gloo (tests: ranks sharing one GPU): the peer
+    transport with a host barrier after every put phase, or NCCL's stand-in staged through
+    host memory -- no kernel ever waits on another process."""
+    kind = os.environ.get("EBS_TRANSPORT", "peer")
+    if kind == "peer":
+        return PeerTransport(op, serialize=gloo), "peer"
+    return TorchTransport(stage_host=gloo), "nccl"
+
+
+def _close(comm):
+    close = getattr(comm, "close", None)
+    if close is not None:
+        close()
 
 
 def _bench_module():
@@ -22,7 +46,7 @@ def _bench_module():
     return bench
 
 
-def _residual_measure(p, args, rank, world, comm, sampler):
+def _residual_measure(p, args, rank, world, gloo, sampler):
     """Time K residual steps r = b - A x on `world` element slabs of problem `p` (device
     time, max over ranks), x and r in each rank's caller order -- its local nodes in
     ascending global id (dist.residual_local).  Returns a dict for rank 0's JSON line:
@@ -37,6 +61,7 @@ def _residual_measure(p, args, rank, world, comm, sampler):
     lib = load()
     m = p["mesh"]
     op, maps = rank_operator(m, p["nu"], p["f"], None, world, rank)
+    comm, kind = _transport(op, gloo)
     setup([op], comm)
     x_local = torch.from_numpy(p["x"]).cuda()[op.global_ids].contiguous()
     x_int, s_raw, r_local = op.zeros(), op.zeros(), op.zeros()
@@ -167,6 +192,8 @@ def _residual_measure(p, args, rank, world, comm, sampler):
            "n_nodes": m.n_nodes, "n_elements": m.n_elements,
            "bytes_rank": _bench_module().residual_bytes(op.n, hi - lo),
            "graph": graph is not None, "graph_verified": verified}
+    out["transport"] = kind
+    _close(comm)
     del op, x_local, x_int, s_raw, r_local
     torch.cuda.empty_cache()
     return out
@@ -198,13 +225,12 @@ def bench_rank(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     peaks, peak_kind = B.load_peaks()
     sampler = B.ClockSampler(index=dev).start()
-    comm = TorchTransport(stage_host=gloo)
     strong = _residual_measure(config_problem(2, seed=args.seed, size=args.size, assemble=False),
-                               args, rank, world, comm, sampler)
+                               args, rank, world, gloo, sampler)
     weak = None
     if getattr(args, "extra", False):
         weak = _residual_measure(stacked_c2_problem(world, seed=args.seed, size=args.size), args,
-                                 rank, world, comm, sampler)
+                                 rank, world, gloo, sampler)
     sampler.stop()
     line = None
     if rank == 0:
@@ -237,6 +263,7 @@ def bench_rank(args, rank, world, local_rank):
                                "copies of consecutive steps overlapped (two buffer sets, copy "
                                "streams)"},
                 "gpu_launches": strong["launches"], "clocks": sampler.summary(),
+                "transport": TRANSPORTS[strong["transport"]],
                 "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=strong["graph_verified"]),
                 "cpu_baseline": None}
         line["config"]["cuda_graph"] = strong["graph"]
@@ -318,7 +345,7 @@ def _bench_solvers(args, rank, world):
             del p
             gc.collect()
             torch.cuda.empty_cache()
-            comm = TorchTransport(stage_host=os.environ.get("EBS_BENCH_GLOO") == "1")
+            comm, kind = _transport(op, os.environ.get("EBS_BENCH_GLOO") == "1")
             prob = setup([op], comm)
             x0 = op.zeros()
             solve = (lambda it, g: jacobi(prob, [x0], it, 0.8, graph=g)) if cfg == 4 else \
@@ -350,6 +377,7 @@ def _bench_solvers(args, rank, world):
                    "final_norm": float(norms[-1]), "n_nodes": m.n_nodes,
                    "n_elements": m.n_elements, "diverged": bool(prob.diverged),
                    "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=use_graph),
+                   "transport": kind,
                    "t1": "in-job single-GPU run of the same solve (eb.jacobi / eb.pcg, "
                          "ebs_solve) on rank 0"}
             if h1 is not None:
@@ -363,6 +391,7 @@ def _bench_solvers(args, rank, world):
                                           "entries_compared": int(live.sum()) if ok_len else 0,
                                           "ok_1e-8": bool(ok_len and dev_ <= 1e-8)}
             out[f"C{cfg}"] = row
+            _close(comm)
             del op, prob
         except Exception as e:  # noqa: BLE001
             out[f"C{cfg}"] = {"error": f"{type(e).__name__}: {e}"}

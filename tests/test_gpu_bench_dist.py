@@ -1,5 +1,7 @@
-"""bench.py --gpus 2 end to end on the one GPU of the box (EBS_BENCH_GLOO=1: gloo with
-host-staged halos, both ranks on cuda:0, no kernel waits on another process): every N > 1
+"""bench.py --gpus 2 end to end on the one GPU of the box (EBS_BENCH_GLOO=1: both ranks on
+cuda:0, gloo for the host plumbing, no kernel waits on another process -- the peer-memory
+transport with a host barrier after every put phase (CUDA-IPC windows between the two
+processes), or NCCL's stand-in with host-staged halos): every N > 1
 branch of bench_dist.py runs -- `value` = the fixed C2 mesh strong-scaled (the N=1
 workload), the weak-scaled C2 extra, C4 / C5 solver strong scaling with E(N) against the
 in-job single-GPU run and the C5 norm history checked against it, the JSON line."""
@@ -23,8 +25,9 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_bench_two_ranks_gloo(gpu):
-    env = dict(os.environ, EBS_BENCH_GLOO="1")
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_bench_two_ranks_gloo(gpu, transport):
+    env = dict(os.environ, EBS_BENCH_GLOO="1", EBS_TRANSPORT=transport, EBS_PEER_TIMEOUT="120")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
            "--gpus", "2", "--steps", "8", "--warmup", "3", "--size", "9", "--c4-size", "9",
@@ -37,12 +40,13 @@ def test_bench_two_ranks_gloo(gpu):
     assert line["config"]["parallelism"].startswith("element slabs x2")
     assert line["weak_c2"]["value"] > 0 and line["weak_c2"]["n_nodes"] == 513 * (512 * 2 + 1)
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    assert line["transport"].startswith("peer memory" if transport == "peer" else "NCCL")
     assert line["roofline"]["frac"] > 0
     ss = line["strong_scaling"]
     for cfg, its in (("C4", 200), ("C5", 500)):
         row = ss[cfg]
         assert "error" not in row, row
         assert row["ranks"] == 2 and row["iterations"] == its and row["efficiency"] > 0
-        assert row["t1_it_per_s"] > 0 and not row["diverged"]
+        assert row["t1_it_per_s"] > 0 and not row["diverged"] and row["transport"] == transport
     assert ss["C5"]["history_vs_1gpu"]["ok_1e-8"], ss["C5"]["history_vs_1gpu"]
     assert ss["C4"]["history_vs_1gpu"]["ok_1e-8"], ss["C4"]["history_vs_1gpu"]
