@@ -63,7 +63,7 @@ static __device__ __noinline__ bool peer_wait(const unsigned long long *flag, un
     while (ld_acquire_sys(flag) < want) {
         if (*reinterpret_cast<volatile unsigned int *>(err)) return false;
         __nanosleep(ns);
-        if (ns < 1024) ns *= 2;
+        if (ns < 256) ns *= 2;
         if (global_ns() - t0 > timeout_ns) {
             atomicExch(err, 1u);
             return false;
