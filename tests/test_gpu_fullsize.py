@@ -121,3 +121,38 @@ def test_c5_full_size(gpu):
         1e-9 * h.residual_norms[-1]
     del batch, p, x, b
     _free()
+
+
+def test_c4_c5_full_size_eight_peer_slabs(gpu):
+    """The BASELINE multi-GPU workloads on 8 element slabs through the peer-memory transport
+    (emulated on the one GPU): C4 200 damped-Jacobi sweeps and C5 500 single-reduction
+    Jacobi-PCG iterations (fused all-reduce) against the single-GPU solvers -- the checks
+    bench.py --gpus 8 makes (history within 1e-8; C4 norms and iterate within 1e-10)."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    for cfg, iters in ((4, 200), (5, 500)):
+        p = config_problem(cfg, seed=0)
+        batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+        x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+        if cfg == 4:
+            x1, h1 = eb.jacobi(batch, d, x0, iters, omega=0.8)
+        else:
+            x1, h1 = eb.pcg(batch, d, x0, iters)
+        prob, _ = dist.emulate(batch, m.n_nodes, d, 8, peer=True)
+        xin = [op.to_internal(x0) for op in prob.ops]
+        if cfg == 4:
+            xs, norms = dist.jacobi(prob, xin, iters, 0.8, graph=True)
+            np.testing.assert_allclose(norms, h1.residual_norms, rtol=1e-10)
+        else:
+            xs, norms = dist.pcg(prob, xin, iters, graph=True)
+            assert len(norms) == len(h1.residual_norms) == iters + 1
+            np.testing.assert_allclose(norms, h1.residual_norms, rtol=1e-8)
+        assert not prob.diverged
+        xg = dist.gather_global(prob.ops, xs, m.n_nodes, prob.comm)
+        tol = 1e-10 if cfg == 4 else 1e-8
+        assert float(torch.linalg.vector_norm(xg - x1)) <= tol * float(torch.linalg.vector_norm(x1))
+        prob.comm.status()
+        prob.comm.close()
+        del prob, xs, xin, batch, p, x1
+        _free()
