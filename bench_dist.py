@@ -71,8 +71,9 @@ def _residual_measure(p, args, rank, world, gloo, sampler):
 
     def step(ev=None, xl=None, rl=None):
         # x to the slab's internal order, r := -0.0, partial residual of the interface
-        # chunks added into r (caller order), NCCL halo of the interface partials in flight
-        # while the interior chunks are swept, owned interface entries completed
+        # chunks added into r (caller order), the halo of the interface partials in flight
+        # while the interior chunks are swept (peer: pushed from the same sweep), owned
+        # interface entries completed
         xl = x_local if xl is None else xl
         rl = r_local if rl is None else rl
         s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -80,6 +81,13 @@ def _residual_measure(p, args, rank, world, gloo, sampler):
         lib.ebs_fill(n, ctypes.c_double(-0.0), D.ptr(rl), s)
         if ev is not None:
             ev[0].record(stream)
+        if kind == "peer":  # one sweep pushing the interface partials, one combine
+            op.peer_residual_sweep(x_int, rl)
+            if ev is not None:
+                ev[1].record(stream)
+            comm.after_put()
+            op.peer_residual_combine(rl)
+            return
         op.residual_local_sweep(op.if_chunks, x_int, rl, s_raw)
         hd = comm.exchange_start([op], [op.gather_sends(s_raw)])
         op.residual_local_sweep(op.in_chunks, x_int, rl, s_raw)
@@ -251,8 +259,11 @@ def bench_rank(args, rank, world, local_rank):
                              "peak": peak, "unit": "GB/s",
                              "frac": strong["bytes_rank"] / strong["kern"] / 1e9 / peak,
                              "traffic": None,
-                             "kernel": "k_sell_op<3,1,1> over the slab's chunks (max over "
-                                       "ranks; bytes of the largest slab)",
+                             "kernel": ("k_peer_residual_sweep<3,1> over all the slab's "
+                                        "chunks, interface partials pushed from the epilogue"
+                                        if strong["transport"] == "peer" else
+                                        "k_sell_op<3,1,1> over the slab's chunks") +
+                                       " (max over ranks; bytes of the largest slab)",
                              "bytes_per_launch": strong["bytes_rank"],
                              "kernel_ms": strong["kern"] * 1e3, "peak_source": peak_kind},
                 "e2e": {"value": strong["n_nodes"] * args.steps / strong["te"] / 1e9,

@@ -176,6 +176,10 @@ SIGNATURES = {
                                       c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_peer_matvec_sweep": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_residual_sweep": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_residual_combine": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                          c_void_p]),
     "ebs_peer_combine_jacobi": (c_int, [c_void_p, c_void_p, c_double, c_void_p, c_void_p,
                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_void_p, c_void_p, c_void_p]),

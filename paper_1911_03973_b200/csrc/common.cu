@@ -86,6 +86,14 @@ int sm_count() {
 }
 
 // occupancy-sized persistent grid, cached per (kernel, device)
+bool pdl_enabled() {
+    static const bool v = [] {
+        const char *e = getenv("EBS_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 int persistent_grid(const void *kernel, int block, int64_t work_blocks, size_t smem) {
     struct Ent { const void *k; int dev; int block; size_t smem; int grid; };
     static Ent cache[64];

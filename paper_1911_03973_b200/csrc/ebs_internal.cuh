@@ -5,6 +5,7 @@
 
 #include <mutex>
 #include <type_traits>
+#include <utility>
 #include <stdint.h>
 #include <cmath>
 #include <cstdio>
@@ -232,6 +233,31 @@ void perm_apply(Plan *p, const Perm2 *P, const double *in, double *out, int32_t 
                 cudaStream_t s);
 void perm_free(Plan *p);
 void dist_free(Plan *p);
+
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream
+// serialisation is scheduled while its predecessor drains; griddepcontrol.wait at its
+// entry then blocks until the predecessor grid has completed and its writes are visible
+// (a no-op for a plain launch).  EBS_PDL=0 in the environment disables it everywhere.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// launch `kern` on `s`, with programmatic stream serialisation when pdl_enabled()
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CU(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // ------------------------------------------------------ reductions ----------
 constexpr int RED_BLOCK = 256;

@@ -50,17 +50,6 @@ struct OpEpi {
 // which triggers at its start) drains; griddepcontrol.wait then blocks until that grid
 // has completed and its writes are visible.  Without the attribute the wait is a no-op.
 // EBS_PDL=0 in the environment launches it the plain way (A/B in profiles/README.md).
-static bool use_pdl() {
-    static const bool v = [] {
-        const char *e = getenv("EBS_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return v;
-}
-
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
-
 template <int NB, int IDS, int MODE>
 __global__ void EBS_SELL_BOUNDS(NB)
     k_sell_op(SellView v, const double *__restrict__ x, OpEpi epi) {
@@ -74,7 +63,7 @@ void launch_sell_op_t(const Plan *p, const double *x_int, const OpEpi &epi, cuda
     auto kern = k_sell_op<NB, IDS, MODE>;
     const SellView v = sell_view(p, chunks, n_list);
     const SellLaunch SL = sell_launch((const void *)kern, NB, p->rowb, v.nlist);
-    if (use_pdl()) {
+    if (pdl_enabled()) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(SL.grid);
         cfg.blockDim = dim3(SL.block);

@@ -292,6 +292,33 @@ __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
     if (grid_sum_last<1>(epi.part, partials, counter, tot) && threadIdx.x == 0) red[0] = tot[0];
 }
 
+// The slab residual r = b_p - A_p x in the rank's caller order (dist.residual_local): one
+// sweep adds every node's partial residual into the -0.0-filled caller-order r (red.add, as
+// operators.cu's OpEpi) and pushes the interface nodes' partials to the neighbours; the
+// combine then adds the neighbours' partials onto the owned shared entries.
+struct PeerResidualEpi {
+    const double *__restrict__ b_int;
+    const uint8_t *__restrict__ iface;
+    const int32_t *__restrict__ old_of_new;
+    double *__restrict__ out;
+    const PeerSend *ps;
+    __device__ __forceinline__ void operator()(int64_t m, double s, double) {
+        s = b_int[m] - s;
+        atomicAdd(out + old_of_new[m], s);
+        if (iface[m]) peer_push(*ps, (int)m, s);
+    }
+};
+
+template <int NB, int IDS>
+__global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
+    k_peer_residual_sweep(SellView v, const double *__restrict__ x, PeerResidualEpi epi,
+                          __grid_constant__ const PeerSend ps) {
+    pdl_wait();  // PDL after the -0.0 fill (it triggers at its start), as the 1-GPU pass
+    epi.ps = &ps;
+    peer_sweep<NB, IDS, false>(v, x, epi, ps);
+    pdl_trigger();
+}
+
 // ------------------------------------------------------- combine + completion --
 struct PeerRecv {
     WinHdr *hdr;
@@ -403,6 +430,38 @@ __global__ void __launch_bounds__(256)
         red[0] = prior ? (prior[0] + prior[1]) + tot[0] : tot[0];
         r.hdr->halo_epoch = ep + 1;
         if (dots) red_put_thread(rp, dots);
+    }
+}
+
+// owned shared nodes of a caller-order residual: out[old_of_new[m]] (the own partial) +=
+// the neighbours' partials in ascending rank order (the owner is the lowest touching rank)
+__global__ void __launch_bounds__(256)
+    k_peer_residual_combine(__grid_constant__ const PeerRecv r, const uint8_t *__restrict__ owned,
+                            const int32_t *__restrict__ old_of_new, double *out,
+                            unsigned int *counter) {
+    pdl_wait();
+    const unsigned long long ep = recv_wait(r);
+    const int par = (int)(ep & 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n_if;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = r.all_if[i];
+        if (!owned[m]) continue;
+        double acc = out[old_of_new[m]];
+        for (int k = 0; k < r.n_src; ++k) {
+            const int32_t q = r.pos[i * r.n_src + k];
+            if (q < 0 || r.src[k] == r.rank) continue;
+            acc += __ldcg(win_recv(const_cast<char *>(r.win), r.cap, r.src[k], par) + q);
+        }
+        out[old_of_new[m]] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(counter, 1u);
+        if (prev == gridDim.x - 1) {
+            *counter = 0;
+            r.hdr->halo_epoch = ep + 1;
+        }
     }
 }
 
@@ -877,6 +936,48 @@ int ebs_peer_combine_q(ebs_peer_t peer, double *q, const uint8_t *free_m, const 
     rp.world = p->world;
     k_peer_combine_q<<<grid, 256, 0, S(stream)>>>(r, q, free_m, owned, pv, sc.partials,
                                                   sc.counter, prior, red, stop, rp, dots);
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_residual_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks,
+                            int64_t n_list, int64_t n_if_chunks, const double *x_int, double *out,
+                            const int32_t *out_map, const uint8_t *iface, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && peer && x_int && out && out_map && iface, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Peer *pr = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(p->has_A && p->has_be, "residual needs an operator loaded with b_e");
+    EBS_REQUIRE(n_list >= 1 && chunks && n_if_chunks >= 0 && n_if_chunks <= n_list,
+                "bad chunk list");
+    EBS_REQUIRE(pr->n_local == p->n_n, "peer halo set for %lld nodes, plan has %lld",
+                (long long)pr->n_local, (long long)p->n_n);
+    EBS_REQUIRE((n_if_chunks > 0) == (pr->n_nb > 0), "interface chunks without neighbours "
+                "(or the reverse)");
+    const PeerSend ps = peer_send_args(pr, n_if_chunks);
+    PeerResidualEpi epi{p->b_int, iface, out_map, out, nullptr};
+    SellView v = sell_view(p, chunks, n_list);
+#define EBS_PR(NB_, IDS_)                                                                  \
+    {                                                                                      \
+        auto kern = k_peer_residual_sweep<NB_, IDS_>;                                      \
+        const int grid = persistent_grid((const void *)kern, 256,                          \
+                                         (n_list * LANES + 255) / 256, 0);                 \
+        launch_pdl(kern, grid, 256, 0, S(stream), v, x_int, epi, ps);                      \
+    }
+    EBS_SELL_DISPATCH(p, EBS_PR);
+#undef EBS_PR
+    LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_residual_combine(ebs_peer_t peer, const uint8_t *owned, const int32_t *out_map,
+                              double *out, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && owned && out_map && out && ws, "null argument");
+    Peer *p = reinterpret_cast<Peer *>(peer);
+    const PeerRecv r = peer_recv_args(p);
+    launch_pdl(k_peer_residual_combine, grid_for(p->n_if, 256, sm_count()), 256, 0, S(stream),
+               r, owned, out_map, out, scratch2(ws).counter);
     LAUNCHED();
     EBS_CATCH
 }

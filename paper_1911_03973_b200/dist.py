@@ -782,6 +782,19 @@ class GpuRankOperator:
              D.ptr(w), D.ptr(p), D.ptr(s_), D.ptr(nxt), D.ptr(self._flag), D.ptr(self._ws),
              D.stream())
 
+    def peer_residual_sweep(self, x_int, r_local):
+        """residual_local_sweep over all chunks (interface chunks first) whose interface
+        partials go straight to the neighbours' windows (ebs_peer_residual_sweep)."""
+        c = self.peer_chunks
+        call("ebs_peer_residual_sweep", self.plan.handle, self.peer, D.ptr(c), c.numel(),
+             self.if_chunks.numel(), D.ptr(x_int), D.ptr(r_local), D.ptr(self.old_of_new32),
+             D.ptr(self.iface), D.stream())
+
+    def peer_residual_combine(self, r_local):
+        """correct_owned_local with the neighbours' partials from the window."""
+        call("ebs_peer_residual_combine", self.peer, D.ptr(self.owned), D.ptr(self.old_of_new32),
+             D.ptr(r_local), D.ptr(self._ws), D.stream())
+
     def peer_push(self, v):
         call("ebs_peer_push", self.peer, D.ptr(v), D.stream())
 
@@ -919,6 +932,15 @@ def residual_local(prob: DistProblem, x_locals: list, r_locals: list, x_ints: li
     owned interface entries completed in ascending rank order.  The owned entries
     (op.owned_local) are the residual within rounding of the reassociated sum."""
     ops, comm = prob.ops, prob.comm
+    if _peer(comm):  # one sweep pushing the interface partials, one combine (s_raws unused)
+        for op, xl, rl, xi in zip(ops, x_locals, r_locals, x_ints):
+            call("ebs_to_internal", op.plan.handle, D.ptr(xl), D.ptr(xi), None, D.stream())
+            call("ebs_fill", rl.numel(), -0.0, D.ptr(rl), D.stream())
+            op.peer_residual_sweep(xi, rl)
+        comm.after_put()
+        for op, rl in zip(ops, r_locals):
+            op.peer_residual_combine(rl)
+        return
     for op, xl, rl, xi, sr in zip(ops, x_locals, r_locals, x_ints, s_raws):
         call("ebs_to_internal", op.plan.handle, D.ptr(xl), D.ptr(xi), None, D.stream())
         call("ebs_fill", rl.numel(), -0.0, D.ptr(rl), D.stream())

@@ -20,8 +20,24 @@ peer = len(sys.argv) > 3 and sys.argv[3] == "peer"
 prob, _ = dist.emulate(batch, m.n_nodes, d, P, peer=peer)
 x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
 xin = [op.to_internal(x0) for op in prob.ops]
-run = (lambda: dist.jacobi(prob, xin, iters, 0.8, graph=True)) if cfg == 4 else \
-    (lambda: dist.pcg(prob, xin, iters, graph=True))
+if cfg == 2:  # the caller-order slab residual (bench value), graph of `iters` residuals
+    x = torch.from_numpy(p["x"]).cuda()
+    xl = [x[op.global_ids].contiguous() for op in prob.ops]
+    rl, xi, sr = ([op.zeros() for op in prob.ops] for _ in range(3))
+
+    def body():
+        for _ in range(iters):
+            dist.residual_local(prob, xl, rl, xi, sr)
+    body()
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        body()
+    run = g.replay
+elif cfg == 4:
+    run = lambda: dist.jacobi(prob, xin, iters, 0.8, graph=True)  # noqa: E731
+else:
+    run = lambda: dist.pcg(prob, xin, iters, graph=True)  # noqa: E731
 run()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:

@@ -121,6 +121,17 @@ def test_peer_residual_caller_order(gpu, P):
         assert torch.equal(a[own], b[own])
         gids = op.global_ids[own]
         assert float((b[own] - ref[gids]).abs().max()) <= 1e-12 * float(ref.abs().max())
+    # the global-vector variant through the generic peer send / recv (ebs_peer_send/_recv)
+    rg = []
+    for prob in (pa, pb):
+        r_ = [torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda") for _ in prob.ops]
+        dist.residual_caller(prob, x, r_, [op.zeros() for op in prob.ops],
+                             [op.zeros() for op in prob.ops])
+        rg.append(r_)
+    for op, a, b in zip(pb.ops, rg[0], rg[1]):
+        gids = op.global_ids[op.owned_local]
+        assert torch.equal(a[gids], b[gids])
+    pb.comm.status()
 
 
 def test_peer_allreduce_rank_order(gpu):
