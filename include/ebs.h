@@ -142,8 +142,8 @@ int ebs_plan_set_dirichlet(ebs_plan_t plan, const int64_t *nd, int64_t n_d, void
 /* ------------------------------------------------------------- operators ---- */
 /* operators.py:72-111 residual: r = b - A x (mode EBS_RES_EXACT reproduces the reference
  * bit for bit; EBS_RES_FAST uses the pre-assembled b).  masked != 0 also applies
- * mask_dirichlet (operators.py:114-118).  nonfinite (device int32, nullable) is set to
- * 1 when x has a non-finite entry (operators.py:90-91). */
+ * mask_dirichlet (operators.py:114-118).  nonfinite (device int32, nullable) is written:
+ * 1 when x has a non-finite entry (operators.py:90-91), else 0 (no reset needed). */
 int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int masked,
                  int32_t *nonfinite, void *stream);
 /* spectrum.py:54-61 _apply_masked: y = A x in (j,e) order; masked != 0 zeroes y[nd]. */

@@ -205,6 +205,8 @@ struct Plan {
     double *hist_dev = nullptr;  // device history (norms, errors)
     int64_t hist_cap = 0;
     int32_t *flag = nullptr;     // device scratch flag
+    int32_t *nf_state = nullptr; // [accumulator, block counter] of the self-resetting
+                                 // non-finite check of the x permutation (operators.cu)
     uint8_t *rowflag = nullptr;  // id layout 3 (3D): 1 per two-base row (sell.cuh IDS_DELTA2)
     int64_t two_base_rows = 0;   // id layout 3: rows coded with two bases
     // single-cluster solver launch (solve.cu k_pcg_cluster), decided once per plan:

@@ -100,10 +100,13 @@ void launch_sell_op(const Plan *p, const double *x_int, const uint8_t *free_int,
 // two-pass shared-memory schedule of perm.cu (profiles/README.md).
 constexpr int PERM_ILP = 8;
 
+// nonfinite (nullable) is WRITTEN, 0 or 1, by the last block to finish (a block counter and
+// an accumulator in the plan's nf_state, both reset by that block): no memset of the flag
+// before the launch -- one graph node less per residual.
 __global__ void __launch_bounds__(256)
     k_to_internal_ilp(int64_t n, const int32_t *__restrict__ old_of_new,
                       const double *__restrict__ x_user, double *__restrict__ x_int,
-                      int32_t *nonfinite) {
+                      int32_t *nonfinite, int32_t *state) {
     bool bad = false;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n;
@@ -130,8 +133,17 @@ __global__ void __launch_bounds__(256)
             }
         }
     }
-    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
-        atomicOr(nonfinite, 1);
+    const int any = __syncthreads_or(bad);
+    if (nonfinite && threadIdx.x == 0) {
+        if (any) atomicOr(state, 1);
+        __threadfence();
+        const unsigned prev = atomicAdd(reinterpret_cast<unsigned *>(state + 1), 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            *nonfinite = atomicExch(state, 0) ? 1 : 0;
+            state[1] = 0;
+        }
+    }
 }
 
 #ifndef EBS_PERM2
@@ -190,16 +202,20 @@ static void fill_negzero(int64_t n, double *out, cudaStream_t s) { fill_value(n,
 
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
                  cudaStream_t s) {
-    if (p->n_n == 0) return;
+    if (p->n_n == 0) {
+        if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
+        return;
+    }
     if (use_perm2(p)) {
         Plan *pm = const_cast<Plan *>(p);
         if (const Perm2 *P = perm_get(pm, 0, s)) {
+            if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
             perm_apply(pm, P, x_user, x_int, nonfinite, s);
             return;
         }
     }
     k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, sm_count() * 8), 256, 0, s>>>(
-        p->n_n, p->old_of_new, x_user, x_int, nonfinite);
+        p->n_n, p->old_of_new, x_user, x_int, nonfinite, p->nf_state);
     LAUNCHED();
 }
 
@@ -289,8 +305,7 @@ int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int mask
     EBS_REQUIRE(x != r, "x and r must not alias");
     cudaStream_t s = S(stream);
     double *x_int = plan_vec(p, 0);
-    if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
-    to_internal(p, x, x_int, nonfinite, s);
+    to_internal(p, x, x_int, nonfinite, s);  // writes *nonfinite (0 / 1)
     sell_apply(p, mode == EBS_RES_EXACT ? 2 : 1, x_int, masked ? p->free_int : nullptr,
                p->old_of_new, r, s);
     EBS_CATCH
@@ -316,8 +331,7 @@ int ebs_to_internal(ebs_plan_t plan, const double *x, double *x_int, int32_t *no
     EBS_REQUIRE(plan && x && x_int, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
     OrderGuard order(p->order, S(stream));
-    if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), S(stream)));
-    to_internal(p, x, x_int, nonfinite, S(stream));
+    to_internal(p, x, x_int, nonfinite, S(stream));  // writes *nonfinite (0 / 1)
     EBS_CATCH
 }
 

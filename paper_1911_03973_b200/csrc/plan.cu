@@ -735,7 +735,7 @@ static void plan_free(Plan *p) {
     dfree(p->new_of_old); dfree(p->old_of_new); dfree(p->cnt); dfree(p->cnt8); dfree(p->codes); dfree(p->tup); dfree(p->rowbase);
     dfree(p->width); dfree(p->slot_ej); dfree(p->slot); dfree(p->tab); dfree(p->taboff);
     dfree(p->slot_be); dfree(p->b_int); dfree(p->free_int); dfree(p->partials);
-    dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag); dfree(p->rowflag);
+    dfree(p->ctl); dfree(p->hist_dev); dfree(p->flag); dfree(p->nf_state); dfree(p->rowflag);
     for (auto &v : p->wvec) dfree(v);
     perm_free(p);
     dist_free(p);
@@ -779,6 +779,8 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     p->n_e = n_e;
     p->n_chunks = (n_n + LANES - 1) / LANES;
     p->flag = dmalloc<int32_t>(4);
+    p->nf_state = dmalloc<int32_t>(2);
+    CU(cudaMemsetAsync(p->nf_state, 0, 2 * sizeof(int32_t), s));
     const int64_t total = (int64_t)nb * n_e;
 
     // 1. valence + first appearance
