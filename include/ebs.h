@@ -442,6 +442,13 @@ int ebs_peer_jacobi_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunk
 int ebs_peer_matvec_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks, int64_t n_list,
                           int64_t n_if_chunks, const double *pv, double *q, const uint8_t *iface,
                           double *red, void *ws, void *stream);
+/* Protocol self-test (synchronises): P peer views of ONE process (emulated ranks, every
+ * window in this process) exercised by one cooperative kernel whose block groups act as the
+ * ranks, concurrently and skewed -- `iters` rounds of interface pushes / flag waits /
+ * rank-ordered sums and of the fused all-reduce, every value checked.  global_ids[r] (device
+ * int64) = the global id of each local node of rank r.  *n_errors = the mismatches (0). */
+int ebs_peer_selftest(ebs_peer_t const *peers, const int64_t *const *global_ids, int P,
+                      int iters, int64_t *n_errors, void *stream);
 /* The slab residual in the rank's caller order (its local nodes by ascending global id):
  * out (pre-filled with -0.0) += b_p - A_p x at out[out_map[m]] for every node (fast mode of
  * ebs_plan_apply_map_chunks with EBS_APPLY_ADD), interface partials pushed to the neighbours;

@@ -189,9 +189,13 @@ struct PeerSend {
     unsigned long long *flag[PEER_MAX];  // remote halo_flag[rank] of neighbour k
 };
 
+#ifndef EBS_PEER_BREAK_PARITY
+#define EBS_PEER_BREAK_PARITY 0  // negative control of ebs_peer_selftest only (one slot, no
+#endif                           // double buffering): must report errors (profiles/)
 __device__ __forceinline__ void peer_push(const PeerSend &ps, int m, double s) {
     const int i = ps.ifx[m];
-    const int64_t par = (int64_t)(ld_volatile(&ps.hdr->halo_epoch) & 1);
+    const int64_t par =
+        EBS_PEER_BREAK_PARITY ? 0 : (int64_t)(ld_volatile(&ps.hdr->halo_epoch) & 1);
     for (int e = ps.snd_off[i]; e < ps.snd_off[i + 1]; ++e)
         reinterpret_cast<double *>(ps.snd_addr[e])[par * ps.cap] = s;
 }
@@ -345,6 +349,7 @@ __device__ __forceinline__ unsigned long long recv_wait(const PeerRecv &r) {
 // sum of the contributions to shared node i in ascending rank order (own partial: v)
 __device__ __forceinline__ double recv_sum(const PeerRecv &r, int64_t i, const double *v,
                                            int par) {
+    if (EBS_PEER_BREAK_PARITY) par = 0;
     double acc = 0.0;
     for (int k = 0; k < r.n_src; ++k) {
         const int32_t q = r.pos[i * r.n_src + k];
@@ -554,6 +559,114 @@ inline Scratch2 scratch2(void *ws) {  // the layout of dist.cu's ebs_vec_workspa
     s.counter = reinterpret_cast<unsigned int *>(ws);
     s.partials = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256);
     return s;
+}
+
+// ----------------------------------------------------------------- self-test --
+// The peer protocol under real concurrency on ONE GPU (the emulation the profiling guide
+// prescribes: one cooperative kernel over all ranks' data, block groups as ranks), using the
+// product's device functions (peer_push / peer_arrive / recv_wait / recv_sum, red_put_thread
+// / red_get_block) on the ranks' real windows and halo maps.  Every iteration each rank
+// pushes code(rank, global id, k) for its shared nodes and one all-reduce triple; after the
+// waits it checks every shared-node sum (ascending rank order) and the reduced triple
+// against the expected values.  Ranks are skewed with rank-dependent sleeps so fast ranks
+// run ahead into the next epoch while slow ones still read -- any parity / epoch / fence
+// error shows up as a wrong value (or a timeout).
+struct StressRank {
+    PeerSend ps;
+    PeerRecv pr;
+    RedPut rp;
+    RedGet rg;
+    const int64_t *gid;  // global id of each local node
+    double *own;         // this rank's pushed values (the own source of recv_sum)
+    int n_chunks;        // interface "chunks" of 32 shared nodes
+    unsigned *bar;       // [count, generation] of the rank's block barrier
+};
+
+__device__ __forceinline__ double stress_code(int q, int64_t g, int k) {
+    return (double)((int64_t)(k + 1) * 1000003 + (int64_t)q * 10007 + g);  // exact in f64
+}
+
+__device__ void rank_sync(unsigned *bar, int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == (unsigned)nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256)
+    k_peer_selftest(const StressRank *__restrict__ ranks, int P, int iters,
+                    unsigned long long *errors) {
+    const int r = (int)((int64_t)blockIdx.x * P / gridDim.x);
+    const int b0 = (int)(((int64_t)r * gridDim.x + P - 1) / P);
+    const int b1 = (int)(((int64_t)(r + 1) * gridDim.x + P - 1) / P);
+    const int nb = b1 - b0, bi = blockIdx.x - b0;
+    const StressRank &R = ranks[r];
+    const int lane = threadIdx.x & 31;
+    const int warp = bi * (blockDim.x / 32) + threadIdx.x / 32, nwarps = nb * (blockDim.x / 32);
+    unsigned long long bad = 0;
+    for (int k = 0; k < iters; ++k) {
+        if ((r + k) % 3 == 0) __nanosleep(2000 * (r + 1));  // skew the ranks
+        // push: one warp per interface chunk, then the arrival that publishes the flags
+        for (int c = warp; c < R.n_chunks; c += nwarps) {
+            const int64_t i = (int64_t)c * 32 + lane;
+            if (i < R.pr.n_if) {
+                const int64_t m = R.pr.all_if[i];
+                const double val = stress_code(r, R.gid[m], k);
+                R.own[m] = val;
+                peer_push(R.ps, (int)m, val);
+            }
+            peer_arrive(R.ps, lane);
+        }
+        rank_sync(R.bar, nb);  // the own values (other blocks of the rank) before the sums
+        // combine: wait for the neighbours, check every shared node's rank-ordered sum
+        const unsigned long long ep = recv_wait(R.pr);
+        const int par = (int)(ep & 1);
+        for (int64_t i = bi * (int64_t)blockDim.x + threadIdx.x; i < R.pr.n_if;
+             i += (int64_t)nb * blockDim.x) {
+            const int64_t m = R.pr.all_if[i];
+            const double got = recv_sum(R.pr, i, R.own, par);
+            double want = 0.0;
+            for (int s = 0; s < R.pr.n_src; ++s)
+                if (R.pr.pos[i * R.pr.n_src + s] >= 0) want += stress_code(R.pr.src[s], R.gid[m], k);
+            if (got != want) ++bad;
+        }
+        rank_sync(R.bar, nb);
+        const bool reduce = k % 5 == 4;  // an all-reduce syncs the ranks: only now and then,
+                                         // so fast ranks can run an epoch ahead in between
+        if (bi == 0 && threadIdx.x == 0) {
+            R.pr.hdr->halo_epoch = ep + 1;
+            if (reduce) {
+                const double dots[3] = {(double)(r + 1), (double)k, (double)(2 * r)};
+                red_put_thread(R.rp, dots);
+            }
+        }
+        if (!reduce) {
+            rank_sync(R.bar, nb);
+            continue;
+        }
+        double v[3];
+        const unsigned long long rep = red_get_block<3>(R.rg, v);
+        if (threadIdx.x == 0) {
+            const double s0 = (double)P * (P + 1) / 2, s2 = (double)P * (P - 1);
+            if (v[0] != s0 || v[1] != (double)k * P || v[2] != s2) ++bad;
+        }
+        rank_sync(R.bar, nb);
+        if (bi == 0 && threadIdx.x == 0)
+            reinterpret_cast<WinHdr *>(R.rg.win)->red_epoch = rep + 1;
+        rank_sync(R.bar, nb);
+    }
+    if (bad) atomicAdd(errors, bad);
 }
 
 }  // namespace ebs
@@ -979,6 +1092,56 @@ int ebs_peer_residual_combine(ebs_peer_t peer, const uint8_t *owned, const int32
     launch_pdl(k_peer_residual_combine, grid_for(p->n_if, 256, sm_count()), 256, 0, S(stream),
                r, owned, out_map, out, scratch2(ws).counter);
     LAUNCHED();
+    EBS_CATCH
+}
+
+int ebs_peer_selftest(ebs_peer_t const *peers, const int64_t *const *global_ids, int P,
+                      int iters, int64_t *n_errors, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peers && global_ids && n_errors && P >= 1 && P <= PEER_MAX && iters >= 0,
+                "bad arguments");
+    cudaStream_t s = S(stream);
+    std::vector<StressRank> h(P);
+    std::vector<double *> owns(P, nullptr);
+    unsigned *bars = dmalloc<unsigned>(2 * P);
+    unsigned long long *err = dmalloc<unsigned long long>(1);
+    StressRank *d = dmalloc<StressRank>(P);
+    CU(cudaMemsetAsync(bars, 0, sizeof(unsigned) * 2 * P, s));
+    CU(cudaMemsetAsync(err, 0, sizeof(unsigned long long), s));
+    for (int r = 0; r < P; ++r) {
+        const Peer *p = reinterpret_cast<const Peer *>(peers[r]);
+        EBS_REQUIRE(p && p->rank == r && p->world == P && global_ids[r], "peer %d", r);
+        const int nc = (int)((p->n_if + 31) / 32);
+        h[r].ps = peer_send_args(p, nc);
+        h[r].pr = peer_recv_args(p);
+        for (int q = 0; q < P; ++q) h[r].rp.win[q] = p->win[q];
+        h[r].rp.rank = r;
+        h[r].rp.world = P;
+        h[r].rg = RedGet{p->win[r], P, p->timeout_ns};
+        h[r].gid = global_ids[r];
+        owns[r] = dmalloc<double>(p->n_local);
+        h[r].own = owns[r];
+        h[r].n_chunks = nc;
+        h[r].bar = bars + 2 * r;
+        EBS_REQUIRE((nc > 0) == (p->n_nb > 0), "peer %d: interface without neighbours", r);
+    }
+    CU(cudaMemcpyAsync(d, h.data(), sizeof(StressRank) * P, cudaMemcpyHostToDevice, s));
+    int per_sm = 0, sms = 0, dev = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peer_selftest, 256, 0));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = std::min(per_sm * sms, 16 * P);  // co-resident: ranks spin on each other
+    void *args[] = {(void *)&d, (void *)&P, (void *)&iters, (void *)&err};
+    CU(cudaLaunchCooperativeKernel((const void *)k_peer_selftest, dim3(grid), dim3(256), args, 0, s));
+    LAUNCHED();
+    unsigned long long e = 0;
+    CU(cudaMemcpyAsync(&e, err, sizeof e, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *n_errors = (int64_t)e;
+    for (double *o : owns) cudaFree(o);
+    cudaFree(bars);
+    cudaFree(err);
+    cudaFree(d);
     EBS_CATCH
 }
 

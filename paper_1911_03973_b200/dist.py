@@ -416,6 +416,17 @@ class LocalPeerTransport(_PeerBase):
             self.peers.append(peer)
             op.peer_attach(peer)
 
+    def selftest(self, iters: int = 200) -> int:
+        """The peer protocol under real concurrency (ebs_peer_selftest): one cooperative
+        kernel whose block groups act as these ranks on their real windows and halo maps,
+        skewed; returns the number of wrong values (0)."""
+        P = len(self._ops)
+        peers = (ctypes.c_void_p * P)(*[op.peer.value for op in self._ops])
+        gids = (ctypes.c_void_p * P)(*[op.global_of_int.data_ptr() for op in self._ops])
+        n = ctypes.c_int64(-1)
+        call("ebs_peer_selftest", peers, gids, P, int(iters), ctypes.byref(n), D.stream())
+        return int(n.value)
+
     def allreduce(self, tensors: list):
         if len(tensors) != len(self._ops):
             raise ValueError(f"emulated all-reduce takes one tensor per rank ({len(self._ops)}), "
