@@ -50,7 +50,6 @@ struct Peer {
     int32_t *pos = nullptr;                // [n_if][n_src]: index in source k or -1
     int n_src = 0;
     int src[PEER_MAX] = {0};               // combine sources, ascending rank (self included)
-    int64_t *gidx[PEER_MAX] = {nullptr};   // per neighbour: local ids in slot order (send)
     int64_t n_local = 0;
 };
 
@@ -745,7 +744,6 @@ static void peer_clear_halo(Peer *p) {
     dfree(p->snd_off);
     dfree(p->snd_addr);
     dfree(p->pos);
-    for (int k = 0; k < PEER_MAX; ++k) dfree(p->gidx[k]);
     p->n_nb = 0;
     p->n_if = 0;
     p->n_src = 1;
@@ -826,10 +824,6 @@ int ebs_peer_set_halo(ebs_peer_t peer, int64_t n_local, int n_nb, const int32_t 
     for (int k = 0; k < n_nb; ++k) {
         p->nb[k] = nb_ranks[k];
         p->len[k] = nb_len[k];
-        p->gidx[k] = dmalloc<int64_t>(nb_len[k]);
-        if (nb_len[k])
-            CU(cudaMemcpyAsync(p->gidx[k], idx[k].data(), sizeof(int64_t) * nb_len[k],
-                               cudaMemcpyHostToDevice, s));
     }
     p->n_if = n_if;
     p->n_src = n_src;
