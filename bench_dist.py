@@ -78,7 +78,8 @@ def _residual_measure(p, args, rank, world, gloo, sampler):
         rl = r_local if rl is None else rl
         s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         lib.ebs_to_internal(h, D.ptr(xl), D.ptr(x_int), None, s)
-        lib.ebs_fill(n, ctypes.c_double(-0.0), D.ptr(rl), s)
+        if kind != "peer":  # the NCCL path adds into -0.0 (the peer sweep fills if it adds)
+            lib.ebs_fill(n, ctypes.c_double(-0.0), D.ptr(rl), s)
         if ev is not None:
             ev[0].record(stream)
         if kind == "peer":  # one sweep pushing the interface partials, one combine

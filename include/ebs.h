@@ -450,13 +450,15 @@ int ebs_peer_matvec_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunk
 int ebs_peer_selftest(ebs_peer_t const *peers, const int64_t *const *global_ids, int P,
                       int iters, int64_t *n_errors, void *stream);
 /* The slab residual in the rank's caller order (its local nodes by ascending global id):
- * out (pre-filled with -0.0) += b_p - A_p x at out[out_map[m]] for every node (fast mode of
- * ebs_plan_apply_map_chunks with EBS_APPLY_ADD), interface partials pushed to the neighbours;
+ * out[out_map[m]] = b_p - A_p x for every node (fast mode of ebs_plan_apply_map_chunks;
+ * flags EBS_APPLY_ADD: added into a -0.0-filled out instead of stored), interface partials
+ * pushed to the neighbours;
  * then the combine adds the neighbours' partials (ascending rank) onto the owned shared
  * entries -- bitwise the NCCL path's ebs_index_add corrections. */
 int ebs_peer_residual_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks,
                             int64_t n_list, int64_t n_if_chunks, const double *x_int, double *out,
-                            const int32_t *out_map, const uint8_t *iface, void *stream);
+                            const int32_t *out_map, const uint8_t *iface, int flags,
+                            void *stream);
 int ebs_peer_residual_combine(ebs_peer_t peer, const uint8_t *owned, const int32_t *out_map,
                               double *out, void *ws, void *stream);
 int ebs_peer_combine_jacobi(ebs_peer_t peer, double *s, double omega, const double *b,

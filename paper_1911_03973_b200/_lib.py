@@ -177,7 +177,8 @@ SIGNATURES = {
     "ebs_peer_matvec_sweep": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_peer_residual_sweep": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64,
-                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                        c_void_p]),
     "ebs_peer_residual_combine": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                           c_void_p]),
     "ebs_peer_selftest": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_int64), c_void_p]),

@@ -296,18 +296,23 @@ __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
 }
 
 // The slab residual r = b_p - A_p x in the rank's caller order (dist.residual_local): one
-// sweep adds every node's partial residual into the -0.0-filled caller-order r (red.add, as
-// operators.cu's OpEpi) and pushes the interface nodes' partials to the neighbours; the
-// combine then adds the neighbours' partials onto the owned shared entries.
+// sweep stores every node's partial residual into the caller-order r and pushes the
+// interface nodes' partials to the neighbours; the combine then adds the neighbours'
+// partials onto the owned shared entries.  red = 0: a plain scattered store; red = 1: the
+// red.add into a -0.0-filled vector of the 1-GPU pass (operators.cu OpEpi) -- cheaper in the
+// L1tex pipe for large slabs, but the fill launch costs more than that at the size of an
+// 8-way C2 slab (emulated, profiles/r02_peer_scaling_c2.txt).
 struct PeerResidualEpi {
     const double *__restrict__ b_int;
     const uint8_t *__restrict__ iface;
     const int32_t *__restrict__ old_of_new;
     double *__restrict__ out;
     const PeerSend *ps;
+    int red;
     __device__ __forceinline__ void operator()(int64_t m, double s, double) {
         s = b_int[m] - s;
-        atomicAdd(out + old_of_new[m], s);
+        if (red) atomicAdd(out + old_of_new[m], s);
+        else out[old_of_new[m]] = s;
         if (iface[m]) peer_push(*ps, (int)m, s);
     }
 };
@@ -316,7 +321,7 @@ template <int NB, int IDS>
 __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
     k_peer_residual_sweep(SellView v, const double *__restrict__ x, PeerResidualEpi epi,
                           __grid_constant__ const PeerSend ps) {
-    pdl_wait();  // PDL after the -0.0 fill (it triggers at its start), as the 1-GPU pass
+    pdl_wait();  // PDL-launched after the x permutation
     epi.ps = &ps;
     peer_sweep<NB, IDS, false>(v, x, epi, ps);
     pdl_trigger();
@@ -1049,8 +1054,10 @@ int ebs_peer_combine_q(ebs_peer_t peer, double *q, const uint8_t *free_m, const 
 
 int ebs_peer_residual_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks,
                             int64_t n_list, int64_t n_if_chunks, const double *x_int, double *out,
-                            const int32_t *out_map, const uint8_t *iface, void *stream) {
+                            const int32_t *out_map, const uint8_t *iface, int flags,
+                            void *stream) {
     EBS_TRY
+    EBS_REQUIRE(flags == 0 || flags == EBS_APPLY_ADD, "bad flags %d", flags);
     EBS_REQUIRE(plan && peer && x_int && out && out_map && iface, "null argument");
     Plan *p = reinterpret_cast<Plan *>(plan);
     Peer *pr = reinterpret_cast<Peer *>(peer);
@@ -1062,7 +1069,7 @@ int ebs_peer_residual_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chu
     EBS_REQUIRE((n_if_chunks > 0) == (pr->n_nb > 0), "interface chunks without neighbours "
                 "(or the reverse)");
     const PeerSend ps = peer_send_args(pr, n_if_chunks);
-    PeerResidualEpi epi{p->b_int, iface, out_map, out, nullptr};
+    PeerResidualEpi epi{p->b_int, iface, out_map, out, nullptr, flags == EBS_APPLY_ADD ? 1 : 0};
     SellView v = sell_view(p, chunks, n_list);
 #define EBS_PR(NB_, IDS_)                                                                  \
     {                                                                                      \

@@ -793,13 +793,21 @@ class GpuRankOperator:
              D.ptr(w), D.ptr(p), D.ptr(s_), D.ptr(nxt), D.ptr(self._flag), D.ptr(self._ws),
              D.stream())
 
+    # slabs of at least this many nodes add into a -0.0-filled r (red.add, as the 1-GPU
+    # pass); smaller ones store (the fill launch costs more than the stores' L1tex cost)
+    PEER_RED_MIN_NODES = 3 << 20
+
     def peer_residual_sweep(self, x_int, r_local):
         """residual_local_sweep over all chunks (interface chunks first) whose interface
-        partials go straight to the neighbours' windows (ebs_peer_residual_sweep)."""
+        partials go straight to the neighbours' windows (ebs_peer_residual_sweep): r_local
+        filled with -0.0 and added into on large slabs, stored directly on small ones."""
         c = self.peer_chunks
+        add = self.n >= self.PEER_RED_MIN_NODES
+        if add:
+            call("ebs_fill", r_local.numel(), -0.0, D.ptr(r_local), D.stream())
         call("ebs_peer_residual_sweep", self.plan.handle, self.peer, D.ptr(c), c.numel(),
              self.if_chunks.numel(), D.ptr(x_int), D.ptr(r_local), D.ptr(self.old_of_new32),
-             D.ptr(self.iface), D.stream())
+             D.ptr(self.iface), EBS_APPLY_ADD if add else 0, D.stream())
 
     def peer_residual_combine(self, r_local):
         """correct_owned_local with the neighbours' partials from the window."""
@@ -946,7 +954,6 @@ def residual_local(prob: DistProblem, x_locals: list, r_locals: list, x_ints: li
     if _peer(comm):  # one sweep pushing the interface partials, one combine (s_raws unused)
         for op, xl, rl, xi in zip(ops, x_locals, r_locals, x_ints):
             call("ebs_to_internal", op.plan.handle, D.ptr(xl), D.ptr(xi), None, D.stream())
-            call("ebs_fill", rl.numel(), -0.0, D.ptr(rl), D.stream())
             op.peer_residual_sweep(xi, rl)
         comm.after_put()
         for op, rl in zip(ops, r_locals):

@@ -114,6 +114,18 @@ def test_peer_residual_caller_order(gpu, P):
         dist.residual_local(prob, xl, rl, [op.zeros() for op in prob.ops],
                             [op.zeros() for op in prob.ops])
         out.append((prob, rl))
+    # the large-slab variant of the peer sweep (red.add into a -0.0-filled r): same bits
+    pb = out[1][0]
+    try:
+        dist.GpuRankOperator.PEER_RED_MIN_NODES = 0
+        xl = [x[op.global_ids].contiguous() for op in pb.ops]
+        ra_ = [torch.full_like(r_, float("nan")) for r_ in out[1][1]]
+        dist.residual_local(pb, xl, ra_, [op.zeros() for op in pb.ops], [None] * P)
+    finally:
+        dist.GpuRankOperator.PEER_RED_MIN_NODES = 3 << 20
+    for op, a, b in zip(pb.ops, ra_, out[1][1]):
+        own = op.owned_local
+        assert torch.equal(a[own], b[own])
     ref = eb.residual(batch, x, deterministic=False)
     (pa, ra), (pb, rb) = out
     for op, a, b in zip(pb.ops, ra, rb):
