@@ -511,6 +511,48 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
+def emulated_slabs(batch, d, m, cfg, iters, t1, h1, P=8):
+    """The C4 / C5 slab solve on P element slabs EMULATED on this one GPU through the
+    peer-memory transport (dist.emulate(..., peer=True): the ranks' windows, fused sweeps,
+    combines and fused all-reduce, every rank's kernels back to back, CUDA-graph batches):
+    the emulated time is the sum of the ranks' work, so E = T1 / T_emulated is the
+    compute-side strong-scaling efficiency at P GPUs before any NVLink latency.  The slab
+    norm history is checked against the 1-GPU solve (h1)."""
+    import numpy as np
+    import torch
+
+    from paper_1911_03973_b200 import dist
+    prob, _ = dist.emulate(batch, m.n_nodes, d, P, peer=True)
+    try:
+        x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+        xin = [op.to_internal(x0) for op in prob.ops]
+        run = (lambda: dist.jacobi(prob, xin, iters, 0.8, graph=True)) if cfg == 4 else \
+            (lambda: dist.pcg(prob, xin, iters, graph=True))
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, norms = run()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        h1 = np.asarray(h1)
+        live = np.abs(h1) >= 1e-10 * abs(h1[0]) if len(h1) == len(norms) else None
+        dev = (float(np.max(np.abs(norms[live] - h1[live]) / np.abs(h1[live])))
+               if live is not None else None)
+        return {"slabs": P, "it_per_s": iters / t, "e_compute": t1 / t,
+                "history_vs_1gpu_max_rel": dev, "diverged": bool(prob.diverged),
+                "transport": "peer memory (LocalPeerTransport: windows, fused sweeps, combines, "
+                             "fused all-reduce)",
+                "note": f"{P} element slabs emulated on this ONE GPU, ranks back to back: "
+                        "the time is the sum of the ranks' work, e_compute = T_1GPU / T_emulated "
+                        "(compute-side strong-scaling efficiency, no NVLink latency)"}
+    finally:
+        prob.comm.close()
+        del prob
+        torch.cuda.empty_cache()
+
+
 def solver_extras(args):
     """Solver throughput on the other BASELINE configs (C3 JPCG, C4 Jacobi, C5 JPCG)."""
     import numpy as np
@@ -575,6 +617,12 @@ def solver_extras(args):
                 "frac_of_peak_stored": per_it_stored * its / t / 1e9 / float(peaks["hbm_gbs"]),
                 "final_rel_residual": float(h.residual_norms[-1] / h.residual_norms[0]),
                 "n_nodes": n_n, "n_elements": n_e, "setup_s": setup}
+            if cfg in (4, 5) and not permuted and getattr(args, "emulate", True):
+                try:
+                    out[f"C{cfg}"]["emulated_8_slabs"] = emulated_slabs(
+                        batch, d, m, cfg, iters, t, h.residual_norms)
+                except Exception as e:  # noqa: BLE001
+                    out[f"C{cfg}"]["emulated_8_slabs"] = {"error": f"{type(e).__name__}: {e}"}
             del p, batch, pl, x
             torch.cuda.empty_cache()
         except Exception as e:  # report, never kill the headline line
@@ -653,6 +701,8 @@ def main():
     ap.add_argument("--extra", action=argparse.BooleanOptionalAction, default=True,
                     help="also time the C3/C4/C5 solvers (default on; --no-extra to skip)")
     ap.add_argument("--solver-configs", type=int, nargs="*", default=[3, 4, 5])
+    ap.add_argument("--emulate", action=argparse.BooleanOptionalAction, default=True,
+                    help="C4 / C5 on 8 element slabs emulated on this GPU (peer transport)")
     ap.add_argument("--c4-size", type=int, default=None, help="override the C4 level (tests)")
     ap.add_argument("--c5-size", type=int, default=None, help="override the C5 N (tests)")
     args = ap.parse_args()
