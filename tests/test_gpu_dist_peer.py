@@ -184,6 +184,41 @@ def test_peer_protocol_under_concurrency(gpu, cfg, size, P):
     prob.comm.close()
 
 
+def test_peer_transport_world_one(gpu):
+    """PeerTransport in a single process (world 1, no torch.distributed): its own window
+    through the IPC-handle path, the one-launch all-reduce (mode 0: put + get in one kernel,
+    the form every real multi-GPU Jacobi norm / two-reduction PCG / gather uses), the fused
+    loops -- against the single-GPU solvers."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    for cfg, size in ((4, 6), (5, 8)):
+        pr = config_problem(cfg, seed=4, size=size)
+        m = pr["mesh"]
+        op, _ = dist.rank_operator(m, pr["nu"], pr["f"], pr["dirichlet"], 1, 0)
+        comm = dist.PeerTransport(op, timeout=60)
+        assert comm.world == 1
+        prob = dist.setup([op], comm)
+        x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+        t = torch.arange(600, dtype=torch.float64, device="cuda")
+        comm.allreduce([t])  # 3 launches of mode 0 on one rank: the identity
+        assert torch.equal(t, torch.arange(600, dtype=torch.float64, device="cuda"))
+        if cfg == 4:
+            xs, norms = dist.jacobi(prob, [op.to_internal(x0)], 30, 0.8, graph=True)
+            x1, h1 = eb.jacobi(pr["batch"], pr["dirichlet"], x0, 30, omega=0.8)
+            np.testing.assert_allclose(norms, h1.residual_norms, rtol=1e-12)
+        else:
+            for red in (1, 2):
+                xs, norms = dist.pcg(prob, [op.to_internal(x0)], 500, tol=1e-8, reductions=red)
+                x1, h1 = eb.pcg(pr["batch"], pr["dirichlet"], x0, 500, tol=1e-8)
+                assert len(norms) == len(h1.residual_norms)
+        xg = dist.gather_global([op], xs, m.n_nodes, comm).cpu().numpy()
+        x1 = x1.cpu().numpy()
+        assert np.linalg.norm(xg - x1) <= 1e-10 * np.linalg.norm(x1)
+        comm.status()
+        comm.close()
+
+
 def test_peer_wait_times_out(gpu):
     """A combine whose neighbour never publishes: the device wait gives up after the
     timeout, sets the window's error word, and the transport raises instead of hanging."""
