@@ -12,11 +12,15 @@ rank touching the node) and are all-reduced.  Maps (local node sets, interfaces,
 match oracle/ebs_oracle.py halo_maps bit for bit.
 
 The solver loops are written against two small protocols so the same code runs
-  * distributed: one ``GpuRankOperator`` per process, ``TorchTransport`` (NCCL / gloo
+  * distributed: one ``GpuRankOperator`` per process and ``PeerTransport`` (peer memory:
+                 CUDA-IPC windows of the node's ranks, the halo pushed from the SELL sweep
+                 epilogue and the PCG dot all-reduce fused into the combine / update kernels,
+                 csrc/peer.cu -- the default of bench.py), ``TorchTransport`` (NCCL / gloo
                  through torch.distributed) or ``NativeTransport`` (libebs.so's own NCCL
                  communicator, ebs_dist_*);
-  * emulated:    P ``GpuRankOperator``s in one process on one GPU, ``LocalTransport``
-                 (device copies; used by the GPU tests -- nothing waits on anything);
+  * emulated:    P ``GpuRankOperator``s in one process on one GPU, ``LocalPeerTransport``
+                 (the peer kernels and windows, every put before any get) or
+                 ``LocalTransport`` (device copies) -- nothing waits on anything;
   * CPU tests:   a torch-CPU rank operator (tests/) over gloo, world size 2.
 """
 
