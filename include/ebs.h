@@ -394,7 +394,8 @@ int ebs_dist_abort(ebs_plan_t plan);
  * neighbours' windows from the SELL epilogue, chunk by chunk, while the same launch sweeps
  * the interior; ebs_peer_combine_* wait for the neighbours' flags, sum the shared nodes in
  * ascending rank order (the values of ebs_dist_combine_*) and complete them.  All ranks must
- * issue the same sequence of peer calls.  Waits are bounded by the timeout given to
+ * issue the same sequence of peer calls, each rank on one stream (a peer view holds device
+ * epoch counters: it is not for concurrent use from several streams).  Waits are bounded by the timeout given to
  * ebs_peer_create; a timed-out wait sets the window's error word (ebs_peer_status ->
  * EBS_ENCCL) instead of hanging.  Replaces the reference's chunk loop + bincount over the
  * whole mesh (operators.py:95-111) across slabs; no reference counterpart for the transport. */
