@@ -8,14 +8,15 @@ Kept beside bench.py (not in the package): it is measurement code, not library c
 from __future__ import annotations
 
 import os
+import sys
 
 import numpy as np
 import torch
 
 from paper_1911_03973_b200._lib import load
 from paper_1911_03973_b200.dist import (GRAPH_BATCH, GRAPH_STATS, PeerTransport,
-                                        TorchTransport, _capture, jacobi, pcg, rank_operator,
-                                        setup)
+                                        PeerUnavailable, TorchTransport, _capture, jacobi, pcg,
+                                        rank_operator, setup)
 
 TRANSPORTS = {
     "peer": "peer memory: CUDA-IPC windows, interface partials stored into the neighbours' "
@@ -31,7 +32,10 @@ def _transport(op, gloo):
     host memory -- no kernel ever waits on another process."""
     kind = os.environ.get("EBS_TRANSPORT", "peer")
     if kind == "peer":
-        return PeerTransport(op, serialize=gloo), "peer"
+        try:
+            return PeerTransport(op, serialize=gloo), "peer"
+        except PeerUnavailable as e:  # raised on every rank together: NCCL instead
+            print(f"peer transport unavailable, NCCL instead: {e}", file=sys.stderr, flush=True)
     return TorchTransport(stage_host=gloo), "nccl"
 
 

@@ -707,7 +707,11 @@ int ebs_peer_window_open(const void *handle, void **win) {
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle, sizeof h);
     void *p = nullptr;
-    CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // not sticky: clear it, so the next launch check does not see it
+        CU(e);
+    }
     *win = p;
     EBS_CATCH
 }

@@ -299,6 +299,11 @@ class _PeerBase:
         self.status()
 
 
+class PeerUnavailable(RuntimeError):
+    """Raised on EVERY rank (a collective decision) when some rank cannot map the others'
+    windows (no CUDA IPC / peer access between the node's GPUs): fall back to NCCL."""
+
+
 class PeerTransport(_PeerBase):
     """One rank per process, the node's ranks mapping each other's windows through CUDA IPC
     (NVLink P2P stores between GPUs; the handles travel through torch.distributed's object
@@ -335,15 +340,28 @@ class PeerTransport(_PeerBase):
             dist.all_gather_object(handles, bytes(handle.raw), group=group)
         self._opened = []
         wins = []
-        for q in range(world):
-            if q == rank:
-                wins.append(own.value)
-                continue
-            w = ctypes.c_void_p()
-            call("ebs_peer_window_open", ctypes.create_string_buffer(handles[q], 64),
-                 ctypes.byref(w))
-            self._opened.append(w)
-            wins.append(w.value)
+        err = None
+        try:
+            for q in range(world):
+                if q == rank:
+                    wins.append(own.value)
+                    continue
+                w = ctypes.c_void_p()
+                call("ebs_peer_window_open", ctypes.create_string_buffer(handles[q], 64),
+                     ctypes.byref(w))
+                self._opened.append(w)
+                wins.append(w.value)
+        except Exception as e:  # noqa: BLE001 -- decided collectively below
+            err = f"{type(e).__name__}: {e}"
+        if world > 1:  # every rank mapped every window, or all of them give up together
+            errs = [None] * world
+            dist.all_gather_object(errs, err, group=group)
+            err = next((f"rank {q}: {e}" for q, e in enumerate(errs) if e), None)
+        if err is not None:
+            for w in self._opened:
+                call("ebs_peer_window_close", w)
+            call("ebs_peer_window_free", own)
+            raise PeerUnavailable(f"peer windows cannot be mapped ({err})")
         arr = (ctypes.c_void_p * world)(*wins)
         peer = ctypes.c_void_p()
         t = _peer_timeout() if timeout is None else float(timeout)

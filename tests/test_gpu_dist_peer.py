@@ -219,6 +219,18 @@ def test_peer_transport_world_one(gpu):
         comm.close()
 
 
+def test_peer_window_open_failure_is_reported(gpu):
+    """A handle that maps nothing fails loudly (EbsError) -- PeerTransport turns that into a
+    collective PeerUnavailable so the bench falls back to NCCL on every rank together."""
+    import ctypes
+
+    from paper_1911_03973_b200._lib import EbsError, call
+    w = ctypes.c_void_p()
+    with pytest.raises(EbsError):
+        call("ebs_peer_window_open", ctypes.create_string_buffer(b"\x00" * 64, 64),
+             ctypes.byref(w))
+
+
 def test_peer_wait_times_out(gpu):
     """A combine whose neighbour never publishes: the device wait gives up after the
     timeout, sets the window's error word, and the transport raises instead of hanging."""
