@@ -59,6 +59,7 @@ struct Fail {
     do {                                                                          \
         cudaError_t err_ = (call);                                                \
         if (err_ != cudaSuccess) {                                                \
+            cudaGetLastError(); /* a non-sticky error must not resurface later */ \
             ebs::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
                            cudaGetErrorString(err_));                             \
             throw ebs::Fail{err_ == cudaErrorMemoryAllocation ? EBS_ENOMEM       \

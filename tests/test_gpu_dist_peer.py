@@ -231,6 +231,23 @@ def test_peer_window_open_failure_is_reported(gpu):
              ctypes.byref(w))
 
 
+def test_failed_allocation_leaves_no_stale_error(gpu):
+    """A device allocation that fails (a window of 2^36 doubles per slot) raises MemoryError,
+    and the next library call works: the non-sticky CUDA error is cleared where it is
+    reported (ebs_internal.cuh CU), not picked up by an unrelated later launch check."""
+    import ctypes
+
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200._lib import call
+    w = ctypes.c_void_p()
+    with pytest.raises(MemoryError):
+        call("ebs_peer_window_alloc", 1 << 36, ctypes.byref(w), None)
+    m = eb.build_unit_square_mesh(3)
+    batch = eb.build_element_batch(m, nu=1.0)
+    r = eb.residual(batch, torch.ones(m.n_nodes, dtype=torch.float64, device="cuda"))
+    assert torch.isfinite(r).all()
+
+
 def test_peer_wait_times_out(gpu):
     """A combine whose neighbour never publishes: the device wait gives up after the
     timeout, sets the window's error word, and the transport raises instead of hanging."""
