@@ -462,6 +462,21 @@ int ebs_peer_residual_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chu
                             void *stream);
 int ebs_peer_residual_combine(ebs_peer_t peer, const uint8_t *owned, const int32_t *out_map,
                               double *out, void *ws, void *stream);
+/* One damped-Jacobi iteration k >= 1 in ONE launch, no grid barrier: the first
+ * ceil(n_shared/32) warps complete iteration k-1's shared nodes (ebs_peer_combine_jacobi's
+ * work: s_part totals, x_cur = x_k there from x_prev = x_{k-1}, red_prev[0] = (prior[0] +
+ * prior[1]) + their owned r^2) while the other warps sweep the interior chunks of iteration
+ * k from x_cur; the chunk list is [n_if_chunks interface chunks | interior | n_near chunks
+ * with a node that shares an element with a shared node], and the interface and near chunks
+ * wait for the completion (the interface ones then push their partials, as
+ * ebs_peer_jacobi_sweep).  Its partial norm goes to part_out[0] (may alias prior[0]); x_out
+ * may alias x_prev (ping-pong buffers). */
+int ebs_peer_jacobi_step(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks, int64_t n_list,
+                         int64_t n_if_chunks, int64_t n_near, double omega, const double *x_prev,
+                         double *x_cur, double *x_out, const double *b, const double *dinv,
+                         const uint8_t *iface, const uint8_t *owned, double *s_part,
+                         const double *prior, double *red_prev, double *part_out, void *ws,
+                         void *stream);
 int ebs_peer_combine_jacobi(ebs_peer_t peer, double *s, double omega, const double *b,
                             const double *dinv, const uint8_t *free_m, const uint8_t *owned,
                             const double *x, double *x_out, const double *prior, double *red,

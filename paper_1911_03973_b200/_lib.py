@@ -182,6 +182,10 @@ SIGNATURES = {
     "ebs_peer_residual_combine": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                           c_void_p]),
     "ebs_peer_selftest": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_int64), c_void_p]),
+    "ebs_peer_jacobi_step": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
+                                     c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_void_p, c_void_p]),
     "ebs_peer_combine_jacobi": (c_int, [c_void_p, c_void_p, c_double, c_void_p, c_void_p,
                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_void_p, c_void_p, c_void_p]),

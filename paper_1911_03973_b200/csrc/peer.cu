@@ -414,6 +414,109 @@ __device__ __forceinline__ void red_put_thread(const RedPut &a, const double *do
         st_relaxed_sys(&reinterpret_cast<WinHdr *>(a.win[q])->red_flag[a.rank], ep + 1);
 }
 
+// One damped-Jacobi iteration k >= 1 per launch, the previous iteration's shared-node
+// completion overlapped with this iteration's interior sweep (no grid barrier):
+//   * the first ceil(n_if/32) warps complete iteration k-1's shared nodes (wait for the
+//     neighbours' flags, rank-ordered sums, x_k there -- k_peer_combine_jacobi's work) and
+//     arrive; the last one advances the halo epoch;
+//   * the chunk list is [interface chunks | interior | chunks next to an interface node]:
+//     interface and near-interface chunks read x_k at shared nodes, so their warps wait for
+//     the arrivals (the near ones come last: by then there is nothing to wait for); the
+//     interior chunks start at once -- the completion's latency hides under the interior
+//     sweep.  Interface partials are pushed as in k_peer_jacobi_sweep.
+// Balance: warp w sweeps the list positions w, w + nwarps, ...; when the chunk count is
+// not a multiple of the warps, the warps from nlist % nwarps on have one chunk fewer, and
+// the completion work and the interface chunks go to those warps (the list is read with
+// the interface chunks moved to logical positions [pos0, pos0 + n_if_chunks)) -- the
+// completion then costs no tail.  Waiting warps wait only for completion warps that are
+// already running (resident persistent grid), never the reverse.
+struct PrevJacobi {
+    double *s;              // the previous sweep's own partials at the shared nodes -> totals
+    const double *x_prev;   // x_{k-1}
+    double *x_cur;          // x_k: the sweep's input, completed here at the shared nodes
+    const uint8_t *owned;
+    const double *prior;    // [previous sweep's partial, 0]
+    double *red;            // ||r_{k-1}||^2 slot
+    double *part_out;       // [this sweep's partial] for the next step (may alias prior[0])
+    int n_near;             // near-interface chunks at the end of the list
+};
+
+__device__ __forceinline__ void wait_done_a(WinHdr *h, unsigned target) {
+    if ((threadIdx.x & 31) == 0)
+        while (*reinterpret_cast<volatile unsigned *>(&h->done_a) < target) __nanosleep(64);
+    __syncwarp();
+    __threadfence();
+}
+
+template <int NB, int IDS>
+__global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
+    k_peer_jacobi_step(SellView v, PeerJacobiEpi epi, __grid_constant__ const PeerSend ps,
+                       __grid_constant__ const PeerRecv pr, PrevJacobi pv, double *partials,
+                       unsigned int *counter) {
+    __shared__ double part_a[256];  // completion partials, parked outside the sweep's registers
+    __shared__ __align__(16) int32_t stab_all[256 / LANES][SellStab<NB, IDS>::CAP];
+    const int lane = threadIdx.x & (LANES - 1);
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+    const int nwarps = (int)((gridDim.x * blockDim.x) / LANES);
+    const unsigned n_a = (unsigned)((pr.n_if + LANES - 1) / LANES);
+    const int nlist = (int)v.nlist;
+    const int n_ifc = ps.n_if_chunks;
+    const int rem = nlist % nwarps;
+    const int need = n_ifc > (int)n_a ? n_ifc : (int)n_a;
+    // the short warps exist only when the list spans more than one round of the grid
+    const int pos0 = nlist > nwarps && rem > 0 && nwarps - rem >= need ? rem : 0;
+    part_a[threadIdx.x] = 0.0;
+    if ((unsigned)(warp - pos0) < n_a) {  // ---- completion of iteration k-1's shared nodes ----
+        const unsigned long long ep = ld_volatile(&pr.hdr->halo_epoch);
+        if (lane < pr.n_src && pr.src[lane] != pr.rank)
+            peer_wait(&pr.hdr->halo_flag[pr.src[lane]], ep + 1, pr.timeout_ns, &pr.hdr->error);
+        __syncwarp();
+        const int par = (int)(ep & 1);
+        const int64_t i = (int64_t)(warp - pos0) * LANES + lane;
+        if (i < pr.n_if) {
+            const int64_t m = pr.all_if[i];
+            const double acc = recv_sum(pr, i, pv.s, par);
+            pv.s[m] = acc;
+            const double rr = epi.free_m[m] ? epi.b[m] - acc : 0.0;
+            if (pv.owned[m]) part_a[threadIdx.x] = rr * rr;
+            pv.x_cur[m] = epi.dinv ? pv.x_prev[m] + epi.omega * (epi.dinv[m] * rr)
+                                   : pv.x_prev[m] + epi.omega * rr;
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            const unsigned prev = atomicAdd(&pr.hdr->arrive, 1u) + 1;  // arrive: free here
+            if (prev == n_a) {
+                pr.hdr->arrive = 0;
+                pr.hdr->halo_epoch = ep + 1;  // every completion warp has read ep
+                __threadfence();
+                atomicExch(&pr.hdr->done_a, n_a);
+            }
+        }
+    }
+    // ---- the sweep of iteration k from x_k ----
+    epi.ps = &ps;
+    int32_t *stab = sell_stab_init<NB, IDS>(v, stab_all);
+    const XLdg xl{pv.x_cur};
+    const int first_near = nlist - pv.n_near;
+    for (int ci = warp; ci < nlist; ci += nwarps) {
+        // logical position -> list index: [pos0, pos0 + n_ifc) holds the interface chunks
+        // (list[0, n_ifc)), the positions before them the list's next pos0 entries
+        const bool is_if = (unsigned)(ci - pos0) < (unsigned)n_ifc;
+        const int li = is_if ? ci - pos0 : (ci < pos0 ? n_ifc + ci : ci);
+        if (is_if || li >= first_near) wait_done_a(pr.hdr, n_a);
+        sell_chunk<NB, IDS, false, NB == 3>(v, v.clist[li], lane, stab, xl, epi);
+        if (is_if) peer_arrive(ps, lane);
+    }
+    double part[2] = {part_a[threadIdx.x], epi.part[0]};
+    double tot[2];
+    if (grid_sum_last<2>(part, partials, counter, tot) && threadIdx.x == 0) {
+        pv.red[0] = (pv.prior[0] + pv.prior[1]) + tot[0];
+        pv.part_out[0] = tot[1];
+        pr.hdr->done_a = 0;  // every waiter has passed
+    }
+}
+
 __global__ void __launch_bounds__(256)
     k_peer_combine_q(__grid_constant__ const PeerRecv r, double *q,
                      const uint8_t *__restrict__ free_m, const uint8_t *__restrict__ owned,
@@ -1147,6 +1250,47 @@ int ebs_peer_selftest(ebs_peer_t const *peers, const int64_t *const *global_ids,
     cudaFree(bars);
     cudaFree(err);
     cudaFree(d);
+    EBS_CATCH
+}
+
+int ebs_peer_jacobi_step(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks, int64_t n_list,
+                         int64_t n_if_chunks, int64_t n_near, double omega, const double *x_prev,
+                         double *x_cur, double *x_out, const double *b, const double *dinv,
+                         const uint8_t *iface, const uint8_t *owned, double *s_part,
+                         const double *prior, double *red_prev, double *part_out, void *ws,
+                         void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && peer && x_prev && x_cur && b && iface && owned && s_part && prior &&
+                    red_prev && part_out && ws,
+                "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Peer *pr = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(n_list >= 1 && chunks && n_if_chunks >= 0 && n_near >= 0 &&
+                    n_if_chunks + n_near <= n_list,
+                "bad chunk list");
+    EBS_REQUIRE(pr->n_local == p->n_n, "peer halo set for %lld nodes, plan has %lld",
+                (long long)pr->n_local, (long long)p->n_n);
+    EBS_REQUIRE((n_if_chunks > 0) == (pr->n_nb > 0), "interface chunks without neighbours "
+                "(or the reverse)");
+    const Scratch2 sc = scratch2(ws);
+    const PeerSend ps = peer_send_args(pr, n_if_chunks);
+    const PeerRecv rv = peer_recv_args(pr);
+    PeerJacobiEpi epi{omega, b, dinv, p->free_int, iface, x_out, s_part, nullptr, {0.0}};
+    PrevJacobi pv{s_part, x_prev, x_cur, owned, prior, red_prev, part_out, (int)n_near};
+    SellView v = sell_view(p, chunks, n_list);
+#define EBS_PS(NB_, IDS_)                                                                  \
+    {                                                                                      \
+        auto kern = k_peer_jacobi_step<NB_, IDS_>;                                         \
+        const int grid = persistent_grid((const void *)kern, 256,                          \
+                                         (n_list * LANES + 255) / 256, 0);                 \
+        EBS_REQUIRE((int64_t)grid * 8 >= (rv.n_if + LANES - 1) / LANES,                    \
+                    "more shared nodes than the grid's completion warps");                 \
+        kern<<<grid, 256, 0, S(stream)>>>(v, epi, ps, rv, pv, sc.partials, sc.counter);    \
+    }
+    EBS_SELL_DISPATCH(p, EBS_PS);
+#undef EBS_PS
+    LAUNCHED();
     EBS_CATCH
 }
 

@@ -15,7 +15,8 @@ struct WinHdr {
     unsigned long long red_epoch;            // local: all-reduces completed
     unsigned int arrive;                     // interface chunks / blocks done (running put)
     unsigned int error;                      // 1: a wait timed out
-    unsigned int pad[26];
+    unsigned int done_a;                     // k_peer_jacobi_step: completion warps done
+    unsigned int pad[25];
 };
 static_assert(sizeof(WinHdr) == 256, "window header is 256 bytes");
 constexpr size_t RED_OFF = 256;

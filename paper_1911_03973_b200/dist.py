@@ -518,6 +518,7 @@ class GpuRankOperator:
         self.n = n
         indt = batch.index.indt
         conn = torch.searchsorted(gl, indt[:, lo:hi].to(torch.int64)).to(torch.int32).contiguous()
+        self._conn_local = conn
         A_store = batch._A_store()[lo:hi]
         b_e = batch.b_e[:, lo:hi].contiguous()
         self.batch = ElementBatch(K_e=A_store.permute(1, 2, 0), M_e=A_store.permute(1, 2, 0),
@@ -779,8 +780,19 @@ class GpuRankOperator:
         lens = (ctypes.c_int64 * max(n, 1))(*[self.if_idx[q].numel() for q in nbs])
         idx = (ctypes.c_void_p * max(n, 1))(*[self.if_idx[q].data_ptr() for q in nbs])
         call("ebs_peer_set_halo", peer, self.n, n, ranks, lens, idx, D.stream())
-        # the chunk list of the fused peer sweeps: interface chunks first
-        self.peer_chunks = torch.cat([self.if_chunks, self.in_chunks]).contiguous()
+        # the chunk list of the fused peer sweeps: interface chunks first, then the interior,
+        # then the chunks with a node sharing an element with a shared node ("near": they
+        # read shared-node values, so ebs_peer_jacobi_step sweeps them last)
+        near = torch.zeros((self.n + 31) // 32, dtype=torch.bool, device=self.iface.device)
+        if self.all_if.numel():
+            ci = self.new_of_old[self._conn_local.to(torch.int64)]      # (nb, n_e) internal
+            touch = self.iface[ci].bool().any(dim=0)
+            near[torch.unique(ci[:, touch]) // 32] = True
+        near[self.if_chunks.to(torch.int64)] = False
+        deep = self.in_chunks[~near[self.in_chunks.to(torch.int64)]]
+        nearc = self.in_chunks[near[self.in_chunks.to(torch.int64)]]
+        self.peer_chunks = torch.cat([self.if_chunks, deep, nearc]).contiguous()
+        self.n_near = int(nearc.numel())
         self._stop = getattr(self, "_stop", None)
 
     def peer_jacobi_sweep(self, omega, x, x_out, b, dinv, s_part, red):
@@ -794,6 +806,18 @@ class GpuRankOperator:
         call("ebs_peer_matvec_sweep", self.plan.handle, self.peer, D.ptr(c), c.numel(),
              self.if_chunks.numel(), D.ptr(p), D.ptr(q), D.ptr(self.iface), D.ptr(red),
              D.ptr(self._ws), D.stream())
+
+    def peer_jacobi_step(self, omega, x_prev, x_cur, x_out, b, dinv, s_part, prior, red_prev,
+                         part_out):
+        """Iteration k >= 1 in one launch: iteration k-1's shared nodes completed (x_cur there,
+        red_prev) by the first warps while the interior chunks of iteration k are swept
+        (ebs_peer_jacobi_step)."""
+        c = self.peer_chunks
+        call("ebs_peer_jacobi_step", self.plan.handle, self.peer, D.ptr(c), c.numel(),
+             self.if_chunks.numel(), self.n_near, float(omega), D.ptr(x_prev), D.ptr(x_cur),
+             D.ptr(x_out), D.ptr(b), D.ptr(dinv), D.ptr(self.iface), D.ptr(self.owned),
+             D.ptr(s_part), D.ptr(prior), D.ptr(red_prev), D.ptr(part_out), D.ptr(self._ws),
+             D.stream())
 
     def peer_combine_jacobi(self, omega, b, s_part, dinv, x, x_out, red, prior=None):
         call("ebs_peer_combine_jacobi", self.peer, D.ptr(s_part), float(omega), D.ptr(b),
@@ -1105,6 +1129,9 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
             op.vec_jacobi(omega, prob.b[i], ss[i], None if richardson else prob.dinv[i], src[i],
                           None if final else dst[i], None, rslot[i])
 
+    if peer:
+        return _jacobi_peer(prob, ws, xa, xb, ss, r3, red, iters, omega, richardson, graph)
+
     k = 0
     if graph and iters >= B and _graph_ok(ops):
         bred = ws.bred
@@ -1125,6 +1152,60 @@ def jacobi(prob: DistProblem, xs0, iters: int, omega: float = 0.8, richardson: b
         step(xa, xb, final, [r_[kk:kk + 1] for r_ in red])
         if not final:
             xa, xb = xb, xa
+    comm.allreduce(red)
+    sync = getattr(comm, "sync", None)
+    if sync is not None:
+        sync()
+    norms = torch.sqrt(red[0]).cpu().numpy()
+    prob.diverged = _diverged(prob, norms)
+    return [x.clone() for x in xa], norms  # fresh arrays: the workspace is reused
+
+
+def _jacobi_peer(prob, ws, xa, xb, ss, r3, red, iters, omega, richardson, graph):
+    """The peer-transport Jacobi loop: ONE launch per iteration (ebs_peer_jacobi_step: the
+    first warps complete iteration k-1's shared nodes while the interior chunks of iteration
+    k are swept; the interface chunks push their partials), the first sweep alone and the
+    last completion alone.  Iterates are bitwise those of the other transports (same
+    per-node sums, same rank order)."""
+    ops, comm = prob.ops, prob.comm
+    B = GRAPH_BATCH
+    dinv = [None if richardson else d for d in prob.dinv]
+
+    def step(src, dst, final, red_prev):  # iteration k >= 1: x_{k-1} in dst, x_k in src
+        for i, op in enumerate(ops):
+            op.peer_jacobi_step(omega, dst[i], src[i], None if final else dst[i], prob.b[i],
+                                dinv[i], ss[i], r3[i], red_prev[i], r3[i][0:1])
+        comm.after_put()
+
+    for i, op in enumerate(ops):  # iteration 0: the sweep alone
+        op.peer_jacobi_sweep(omega, xa[i], None if iters == 0 else xb[i], prob.b[i], dinv[i],
+                             ss[i], r3[i][0:1])
+    comm.after_put()
+    if iters > 0:
+        xa, xb = xb, xa
+    k = 1
+    if graph and iters >= B + 1 and _graph_ok(ops):
+        bred = ws.bred
+
+        def body():  # iterations k..k+B-1 (none final); B even: xa/xb roles return
+            for u in range(B):
+                src, dst = (xa, xb) if u % 2 == 0 else (xb, xa)
+                step(src, dst, False, [r_[u:u + 1] for r_ in bred])
+        g = _graph_for(prob, ws, body)
+        if g is not None:
+            while k + B <= iters:  # the final iteration stays eager
+                g.replay()
+                for i in range(len(ops)):
+                    red[i][k - 1:k - 1 + B].copy_(bred[i])
+                k += B
+    for kk in range(k, iters + 1):
+        final = kk == iters
+        step(xa, xb, final, [r_[kk - 1:kk] for r_ in red])
+        if not final:
+            xa, xb = xb, xa
+    for i, op in enumerate(ops):  # the last iteration's shared nodes (x_iters, ||r_iters||)
+        op.peer_combine_jacobi(omega, prob.b[i], ss[i], dinv[i], xa[i], None,
+                               red[i][iters:iters + 1], prior=r3[i])
     comm.allreduce(red)
     sync = getattr(comm, "sync", None)
     if sync is not None:
