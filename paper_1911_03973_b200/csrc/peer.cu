@@ -453,6 +453,7 @@ __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
     k_peer_jacobi_step(SellView v, PeerJacobiEpi epi, __grid_constant__ const PeerSend ps,
                        __grid_constant__ const PeerRecv pr, PrevJacobi pv, double *partials,
                        unsigned int *counter) {
+    pdl_wait();  // PDL-launched after the previous iteration's step (a no-op otherwise)
     __shared__ double part_a[256];  // completion partials, parked outside the sweep's registers
     __shared__ __align__(16) int32_t stab_all[256 / LANES][SellStab<NB, IDS>::CAP];
     const int lane = threadIdx.x & (LANES - 1);
@@ -508,6 +509,7 @@ __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
         sell_chunk<NB, IDS, false, NB == 3>(v, v.clist[li], lane, stab, xl, epi);
         if (is_if) peer_arrive(ps, lane);
     }
+    pdl_trigger();  // the next iteration's step may be scheduled (it waits for this grid)
     double part[2] = {part_a[threadIdx.x], epi.part[0]};
     double tot[2];
     if (grid_sum_last<2>(part, partials, counter, tot) && threadIdx.x == 0) {
@@ -1286,7 +1288,8 @@ int ebs_peer_jacobi_step(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks
                                          (n_list * LANES + 255) / 256, 0);                 \
         EBS_REQUIRE((int64_t)grid * 8 >= (rv.n_if + LANES - 1) / LANES,                    \
                     "more shared nodes than the grid's completion warps");                 \
-        kern<<<grid, 256, 0, S(stream)>>>(v, epi, ps, rv, pv, sc.partials, sc.counter);    \
+        launch_pdl(kern, grid, 256, 0, S(stream), v, epi, ps, rv, pv, sc.partials,         \
+                   sc.counter);                                                            \
     }
     EBS_SELL_DISPATCH(p, EBS_PS);
 #undef EBS_PS
