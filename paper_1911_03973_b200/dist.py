@@ -332,12 +332,21 @@ class PeerTransport(_PeerBase):
         self.world, self.rank, self.cap = world, rank, cap
         own = ctypes.c_void_p()
         handle = ctypes.create_string_buffer(64)
-        call("ebs_peer_window_alloc", cap, ctypes.byref(own), handle)
+        try:
+            call("ebs_peer_window_alloc", cap, ctypes.byref(own), handle)
+            mine = bytes(handle.raw)
+        except Exception as e:  # noqa: BLE001 -- decided collectively below
+            own, mine = None, f"{type(e).__name__}: {e}"
         self._own = own
-        handles = [bytes(handle.raw)]
+        handles = [mine]
         if world > 1:
             handles = [None] * world
-            dist.all_gather_object(handles, bytes(handle.raw), group=group)
+            dist.all_gather_object(handles, mine, group=group)
+        bad = next((f"rank {q}: {h}" for q, h in enumerate(handles) if isinstance(h, str)), None)
+        if bad is not None:  # some rank has no window: every rank gives up together
+            if own is not None:
+                call("ebs_peer_window_free", own)
+            raise PeerUnavailable(f"peer window allocation failed ({bad})")
         self._opened = []
         wins = []
         err = None
