@@ -10,7 +10,7 @@ adds the ranks' slots in rank order.  On the one GPU of the box:
   the same ascending rank order), norms within 1e-12; single- and two-reduction PCG against
   the oracle (same iteration count to 1e-8, solution within 1e-8); the caller-order residual
   bitwise; CUDA-graph replay bitwise equal to eager;
-* two real processes on the one GPU mapping each other's windows through CUDA IPC
+* two and three real processes on the one GPU mapping each other's windows through CUDA IPC
   (PeerTransport, serialize=True: a host barrier after every put phase, so no kernel waits
   on the other process) against the single-GPU solvers;
 * a wait that never completes times out on the device and is reported (EBS_ENCCL)."""
@@ -304,13 +304,15 @@ def _ipc_worker(rank, world, port, out):
         tdist.destroy_process_group()
 
 
-def test_two_processes_cuda_ipc_windows(gpu):
+@pytest.mark.parametrize("world", [2, 3])
+def test_processes_cuda_ipc_windows(gpu, world):
+    """world 3: the middle rank maps and writes two neighbours' windows."""
     import paper_1911_03973_b200 as eb
     from paper_1911_03973_b200.inputs import config_problem
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=300)
