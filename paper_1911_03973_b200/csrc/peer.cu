@@ -195,6 +195,7 @@ __device__ __forceinline__ void peer_push(const PeerSend &ps, int m, double s) {
     const int i = ps.ifx[m];
     const int64_t par =
         EBS_PEER_BREAK_PARITY ? 0 : (int64_t)(ld_volatile(&ps.hdr->halo_epoch) & 1);
+    EBS_DCHECK(i >= 0);
     for (int e = ps.snd_off[i]; e < ps.snd_off[i + 1]; ++e)
         reinterpret_cast<double *>(ps.snd_addr[e])[par * ps.cap] = s;
 }
@@ -358,6 +359,7 @@ __device__ __forceinline__ double recv_sum(const PeerRecv &r, int64_t i, const d
     for (int k = 0; k < r.n_src; ++k) {
         const int32_t q = r.pos[i * r.n_src + k];
         if (q < 0) continue;
+        EBS_DCHECK(r.src[k] == r.rank || q < r.cap);
         acc += r.src[k] == r.rank
                    ? v[q]
                    : __ldcg(win_recv(const_cast<char *>(r.win), r.cap, r.src[k], par) + q);
