@@ -70,6 +70,37 @@ def test_peer_jacobi_bitwise_vs_device_copy(gpu, P):
         peer.comm.status()
 
 
+@pytest.mark.parametrize("level,P", [(2, 8), (3, 7), (2, 5)])
+def test_peer_thin_slabs_many_sharers(gpu, level, P):
+    """Slabs thinner than a row of cells: shared nodes touched by 3-5 ranks (multi-source
+    combines, ranks with several neighbours, tiny grids where no warp has a chunk fewer)."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import dist
+    m = eb.build_unit_square_mesh(level)
+    batch = eb.build_element_batch(m, nu=1.0)
+    d = eb.constant_dirichlet(m, 0.0)
+    maps = dist.partition_maps(batch.index.indt, m.n_nodes, P)
+    sharers = torch.zeros(m.n_nodes, dtype=torch.int64)
+    for loc in maps["local"]:
+        sharers[loc.cpu()] += 1
+    assert int(sharers.max()) >= 3
+    ref, _ = dist.emulate(batch, m.n_nodes, d, P)
+    peer, _ = dist.emulate(batch, m.n_nodes, d, P, peer=True)
+    x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+    xr, nr = dist.jacobi(ref, [op.to_internal(x0) for op in ref.ops], 25, 0.8)
+    xp, npe = dist.jacobi(peer, [op.to_internal(x0) for op in peer.ops], 25, 0.8, graph=True)
+    for a_, b_ in zip(xr, xp):
+        assert torch.equal(a_, b_)
+    np.testing.assert_allclose(npe, nr, rtol=1e-12)
+    x1, h1 = eb.pcg(batch, d, x0, 500, tol=1e-10)
+    xs, ns = dist.pcg(peer, [op.to_internal(x0) for op in peer.ops], 500, tol=1e-10)
+    assert len(ns) == len(h1.residual_norms)
+    xg = dist.gather_global(peer.ops, xs, m.n_nodes, peer.comm)
+    assert float((xg - x1).norm()) <= 1e-8 * float(x1.norm())
+    peer.comm.status()
+    peer.comm.close()
+
+
 @pytest.mark.parametrize("P", [2, 4])
 def test_peer_pcg_matches_oracle(gpu, P):
     from paper_1911_03973_b200 import dist
