@@ -206,7 +206,15 @@ def _residual_measure(p, args, rank, world, gloo, sampler):
            "bytes_rank": _bench_module().residual_bytes(op.n, hi - lo),
            "graph": graph is not None, "graph_verified": verified}
     out["transport"] = kind
-    _close(comm)
+    status, err = getattr(comm, "status", None), None
+    if status is not None:  # a timed-out peer wait raises here (EBS_ENCCL) ...
+        try:
+            status()
+        except Exception as e:  # noqa: BLE001
+            err = e
+    _close(comm)  # ... after the collective close, so every rank gets there
+    if err is not None:
+        raise err
     del op, x_local, x_int, s_raw, r_local
     torch.cuda.empty_cache()
     return out
@@ -238,8 +246,20 @@ def bench_rank(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     peaks, peak_kind = B.load_peaks()
     sampler = B.ClockSampler(index=dev).start()
-    strong = _residual_measure(config_problem(2, seed=args.seed, size=args.size, assemble=False),
-                               args, rank, world, gloo, sampler)
+    # a lost or broken peer link must not hang an unattended run: bounded waits, and the
+    # strong-scaling line falls back to NCCL on every rank if the peer run reported an error
+    os.environ.setdefault("EBS_PEER_TIMEOUT", "60")
+    c2 = config_problem(2, seed=args.seed, size=args.size, assemble=False)
+    try:
+        strong, err = _residual_measure(c2, args, rank, world, gloo, sampler), None
+    except Exception as e:  # noqa: BLE001 -- decided collectively below
+        strong, err = None, f"{type(e).__name__}: {e}"
+    errs = [None] * world
+    dist.all_gather_object(errs, err)
+    if any(errs):
+        os.environ["EBS_TRANSPORT"] = "nccl"
+        strong = _residual_measure(c2, args, rank, world, gloo, sampler)
+        strong["fallback"] = next(e for e in errs if e)
     weak = None
     if getattr(args, "extra", False):
         weak = _residual_measure(stacked_c2_problem(world, seed=args.seed, size=args.size), args,
@@ -279,7 +299,8 @@ def bench_rank(args, rank, world, local_rank):
                                "copies of consecutive steps overlapped (two buffer sets, copy "
                                "streams)"},
                 "gpu_launches": strong["launches"], "clocks": sampler.summary(),
-                "transport": TRANSPORTS[strong["transport"]],
+                "transport": TRANSPORTS[strong["transport"]] + (
+                    f" (peer run failed: {strong['fallback']})" if "fallback" in strong else ""),
                 "cuda_graph": dict(GRAPH_STATS, replay_matches_eager=strong["graph_verified"]),
                 "cpu_baseline": None}
         line["config"]["cuda_graph"] = strong["graph"]
