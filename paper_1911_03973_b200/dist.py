@@ -386,6 +386,22 @@ class PeerTransport(_PeerBase):
             torch.cuda.synchronize()
             self.dist.barrier(group=self.group)
 
+    def sync(self, timeout=None):
+        """status() decided collectively: every rank raises when any rank's wait timed out,
+        so no rank is left alone in the next collective."""
+        err = None
+        try:
+            self.status()
+        except Exception as e:  # noqa: BLE001
+            err = str(e)
+        if self.world > 1:
+            errs = [None] * self.world
+            self.dist.all_gather_object(errs, err, group=self.group)
+            err = next((f"rank {q}: {e}" for q, e in enumerate(errs) if e), None)
+        if err is not None:
+            from ._lib import EbsError
+            raise EbsError(err)
+
     def allreduce(self, tensors: list):
         (t,) = tensors
         self._check(t)
