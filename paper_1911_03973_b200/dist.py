@@ -899,6 +899,163 @@ class GpuRankOperator:
         return D.zeros(self.n if n is None else n)
 
 
+# ------------------------------------------------ exact residual on P slabs --
+class ExactSlab:
+    """Rank p's slab with a ghost layer, for the EXACT (reference-order) residual on P slabs,
+    bit for bit the single-GPU / reference `residual(..., deterministic=True)` at every node
+    of the slab ("for bitwise identity across P ...").
+
+    The slab's elements are augmented with every element of another slab that touches one of
+    its shared nodes (a one-element ghost layer), kept in ascending GLOBAL element order --
+    so the plan's per-node slot order (j, then element) is the global (j, e) bincount order
+    of operators.py:98 restricted to ALL the elements at that node: the node sums are the
+    reference's, not rank-partial sums.  The price is the ghost elements' bytes (one cell row
+    per neighbour) and an exchange of x at the ghost-only nodes before the pass (instead of
+    the partial sums after it).  Construction is from the global mesh (+ its f) or, in
+    emulation, the global ElementBatch."""
+
+    def __init__(self, maps: dict, p: int, indt: torch.Tensor, n_nodes: int, batch=None,
+                 mesh=None, nu=None, f=None):
+        from .elements import ElementBatch, build_element_batch
+        from .mesh import IndexArrays, Mesh
+        self.rank, self.P = p, len(maps["local"])
+        dev = D.device()
+        indt = indt.to(dev)
+        lo, hi = int(maps["bounds"][p]), int(maps["bounds"][p + 1])
+        own = maps["local"][p].to(dev)
+        shared = (torch.unique(torch.cat(list(maps["interface"][p].values()))).to(dev)
+                  if maps["interface"][p] else torch.empty(0, dtype=torch.int64, device=dev))
+        is_sh = torch.zeros(n_nodes, dtype=torch.bool, device=dev)
+        is_sh[shared] = True
+        touch = is_sh[indt.to(torch.int64)].any(dim=0)
+        touch[lo:hi] = True                                   # own elements
+        self.elements = torch.nonzero(touch).reshape(-1)     # ascending global element id
+        nodes = torch.unique(indt[:, self.elements].reshape(-1).to(torch.int64))
+        self.global_ids = nodes                               # the plan's caller numbering
+        self.n = nodes.numel()
+        conn = torch.searchsorted(nodes, indt[:, self.elements].to(torch.int64)).to(torch.int32)
+        if batch is not None:
+            A = batch._A_store()[self.elements]
+            b_e = batch.b_e[:, self.elements].contiguous()
+            self.batch = ElementBatch(K_e=A.permute(1, 2, 0), M_e=A.permute(1, 2, 0),
+                                      A_e=A.permute(1, 2, 0), b_e=b_e, nu=batch.nu,
+                                      index=IndexArrays(None, conn.contiguous(), n_nodes=self.n))
+        else:
+            sub = Mesh(mesh.nodes, None, mesh.boundary_nodes,
+                       conn=mesh.conn[:, self.elements].contiguous())
+            full = build_element_batch(sub, nu=nu, f=f)
+            self.batch = ElementBatch(K_e=full.K_e, M_e=full.M_e, A_e=full.A_e, b_e=full.b_e,
+                                      nu=full.nu,
+                                      index=IndexArrays(None, conn.contiguous(), n_nodes=self.n))
+        self.plan = self.batch.operator(self.n)
+        # where the slab's own local nodes (its caller order) sit in the augmented numbering,
+        # and the ghost-only nodes with the rank that supplies each (their owner)
+        self.own_pos = torch.searchsorted(nodes, own)
+        ghost = torch.ones(self.n, dtype=torch.bool, device=dev)
+        ghost[self.own_pos] = False
+        self.ghost_pos = torch.nonzero(ghost).reshape(-1)
+        gids = nodes[self.ghost_pos]
+        src = maps["owner"].to(dev)[gids]
+        self.recv = {}   # q -> positions (in the augmented numbering) filled from rank q
+        self.recv_g = {}  # q -> their global ids (ascending)
+        for q in torch.unique(src).tolist():
+            sel = src == q
+            self.recv[int(q)] = self.ghost_pos[sel]
+            self.recv_g[int(q)] = gids[sel]
+        self._own_global = own
+        self.send = {}   # q -> positions in this rank's own local order sent to rank q
+
+    def link(self, slabs_or_recv_g: dict):
+        """Send lists: for each rank q, the nodes q needs from this rank (q's recv_g[p]),
+        as positions in this rank's own local order.  slabs_or_recv_g: {q: global ids}."""
+        for q, g in slabs_or_recv_g.items():
+            self.send[q] = torch.searchsorted(self._own_global, g.to(self._own_global.device))
+
+
+def exact_slabs(maps: dict, indt, n_nodes: int, batch=None, mesh=None, nu=None, f=None,
+                ranks=None):
+    """ExactSlab of each rank in `ranks` (default all), send lists linked (every rank can
+    compute every rank's ghost set from the global connectivity)."""
+    P = len(maps["local"])
+    allr = list(range(P))
+    views = [ExactSlab(maps, p, indt, n_nodes, batch=batch, mesh=mesh, nu=nu, f=f)
+             if (ranks is None or p in ranks) else None for p in allr]
+    need = {}  # need[q][p] = global ids rank p needs from rank q
+    for p in allr:  # remote ranks: only their ghost bookkeeping
+        v = views[p] if views[p] is not None else _ghost_only(maps, p, indt, n_nodes)
+        for q, g in v.recv_g.items():
+            need.setdefault(q, {})[p] = g
+    for p in allr:
+        if views[p] is not None:
+            views[p].link(need.get(p, {}))
+    return [v for v in views if v is not None]
+
+
+def _ghost_only(maps, p, indt, n_nodes):
+    """The ghost-node bookkeeping of rank p without building its plan."""
+    class _G:
+        pass
+    dev = D.device()
+    indt = indt.to(dev)
+    lo, hi = int(maps["bounds"][p]), int(maps["bounds"][p + 1])
+    own = maps["local"][p].to(dev)
+    shared = (torch.unique(torch.cat(list(maps["interface"][p].values()))).to(dev)
+              if maps["interface"][p] else torch.empty(0, dtype=torch.int64, device=dev))
+    is_sh = torch.zeros(n_nodes, dtype=torch.bool, device=dev)
+    is_sh[shared] = True
+    touch = is_sh[indt.to(torch.int64)].any(dim=0)
+    touch[lo:hi] = True
+    nodes = torch.unique(indt[:, torch.nonzero(touch).reshape(-1)].reshape(-1).to(torch.int64))
+    isown = torch.zeros(n_nodes, dtype=torch.bool, device=dev)
+    isown[own] = True
+    gids = nodes[~isown[nodes]]
+    src = maps["owner"].to(dev)[gids]
+    g = _G()
+    g.recv_g = {int(q): gids[src == q] for q in torch.unique(src).tolist()}
+    return g
+
+
+def residual_exact(slabs: list, comm, x_locals: list) -> list:
+    """r = b - A x in the reference's exact order on P slabs: each rank's x_locals[i] holds
+    its slab's local nodes (ascending global id, as residual_local); returns each rank's r at
+    the same nodes, bit for bit the single-GPU / reference residual there.  The ghost x
+    values travel through comm's generic exchange (padded to equal sizes both ways)."""
+    sends, xa = [], []
+    for sl, xl in zip(slabs, x_locals):
+        buf = {}
+        for q, pos in sl.send.items():
+            m = max(pos.numel(), _peer_count(slabs, sl, q))
+            t = torch.zeros(m, dtype=torch.float64, device=xl.device)
+            t[:pos.numel()] = xl[pos]
+            buf[q] = t
+        for q in sl.recv:
+            if q not in buf:  # receive-only direction: an empty send of the right size
+                buf[q] = torch.zeros(sl.recv[q].numel(), dtype=torch.float64, device=xl.device)
+        sends.append(buf)
+        x_aug = torch.empty(sl.n, dtype=torch.float64, device=xl.device)
+        x_aug[sl.own_pos] = xl
+        xa.append(x_aug)
+    if getattr(comm, "fused_peer", False):
+        raise ValueError("residual_exact needs a transport with a generic exchange "
+                         "(LocalTransport / TorchTransport / NativeTransport)")
+    recvs = comm.exchange(slabs, sends)
+    out = []
+    for sl, x_aug, rc in zip(slabs, xa, recvs):
+        for q, pos in sl.recv.items():
+            x_aug[pos] = rc[q][:pos.numel()]
+        r_aug = D.empty(sl.n)
+        with sl.batch.using(sl.n) as pl:
+            call("ebs_residual", pl.handle, D.ptr(x_aug), D.ptr(r_aug), 0, 0, None, D.stream())
+        out.append(r_aug[sl.own_pos])
+    return out
+
+
+def _peer_count(slabs, sl, q):
+    """Size of what rank q sends to this rank (for the symmetric padding)."""
+    n = sl.recv.get(q)
+    return 0 if n is None else n.numel()
+
+
 # ------------------------------------------------------------------- loops --
 def _peer(comm) -> bool:
     return bool(getattr(comm, "fused_peer", False))

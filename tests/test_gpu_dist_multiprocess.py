@@ -48,8 +48,17 @@ def _worker(rank, world, port, out):
                 xs, norms = D.pcg(prob, [op.to_internal(x0)], 500, tol=1e-8)
             xg = D.gather_global([op], xs, m.n_nodes, comm)
             res[cfg] = (xg.cpu().numpy(), norms)
+            # the exact (reference-order) residual on the slabs: ghost layer built rank-locally
+            # from the mesh, ghost x values through the host-staged gloo exchange
+            sl, = D.exact_slabs(maps, batch.index.indt, m.n_nodes, mesh=m, nu=p["nu"], f=p["f"],
+                                ranks=[rank])
+            x = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, m.n_nodes)).cuda()
+            r_ex, = D.residual_exact([sl], comm, [x[maps["local"][rank].cuda()]])
+            res[("exact", cfg, rank)] = r_ex.cpu().numpy()
         if rank == 0:
             out.put(res)
+        else:
+            out.put({k: v for k, v in res.items() if isinstance(k, tuple)})
     finally:
         dist.destroy_process_group()
 
@@ -63,7 +72,9 @@ def test_two_gpu_rank_processes_match_single_gpu(gpu):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = q.get(timeout=300)
+    res = {}
+    for _ in range(2):
+        res.update(q.get(timeout=300))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -79,3 +90,9 @@ def test_two_gpu_rank_processes_match_single_gpu(gpu):
             assert len(res[cfg][1]) == len(h1.residual_norms)
         x1 = x1.cpu().numpy()
         assert np.linalg.norm(res[cfg][0] - x1) <= 1e-8 * np.linalg.norm(x1)
+        x = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, pr["mesh"].n_nodes)).cuda()
+        ref = eb.residual(pr["batch"], x).cpu().numpy()
+        from paper_1911_03973_b200 import dist as D
+        maps = D.partition_maps(pr["batch"].index.indt, pr["mesh"].n_nodes, 2)
+        for rank in range(2):
+            assert np.array_equal(res[("exact", cfg, rank)], ref[maps["local"][rank].cpu().numpy()])

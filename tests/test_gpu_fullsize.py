@@ -156,3 +156,24 @@ def test_c4_c5_full_size_eight_peer_slabs(gpu):
         prob.comm.close()
         del prob, xs, xin, batch, p, x1
         _free()
+
+
+def test_c2_exact_residual_eight_slabs_bitwise(gpu):
+    """The full C2 mesh (8.4M triangles, permuted numbering) on 8 element slabs with the
+    ghost layer (dist.residual_exact): bit for bit the single-GPU exact residual -- i.e. the
+    reference's -- at every node of every slab."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(2, seed=0)
+    m, batch = p["mesh"], p["batch"]
+    x = torch.from_numpy(p["x"]).cuda()
+    ref = eb.residual(batch, x)
+    maps = dist.partition_maps(batch.index.indt, m.n_nodes, 8)
+    slabs = dist.exact_slabs(maps, batch.index.indt, m.n_nodes, batch=batch)
+    rs = dist.residual_exact(slabs, dist.LocalTransport(),
+                             [x[maps["local"][sl.rank].cuda()] for sl in slabs])
+    for sl, r in zip(slabs, rs):
+        assert torch.equal(r, ref[maps["local"][sl.rank].cuda()]), sl.rank
+    del slabs, rs, batch, p
+    _free()
