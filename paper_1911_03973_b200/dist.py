@@ -963,6 +963,7 @@ class ExactSlab:
             self.recv[int(q)] = self.ghost_pos[sel]
             self.recv_g[int(q)] = gids[sel]
         self._own_global = own
+        self._owner = maps["owner"].to(dev)
         self.send = {}   # q -> positions in this rank's own local order sent to rank q
 
     def link(self, slabs_or_recv_g: dict):
@@ -1048,6 +1049,85 @@ def residual_exact(slabs: list, comm, x_locals: list) -> list:
             call("ebs_residual", pl.handle, D.ptr(x_aug), D.ptr(r_aug), 0, 0, None, D.stream())
         out.append(r_aug[sl.own_pos])
     return out
+
+
+def _ghost_exchange(slabs, comm, x_augs):
+    """Fill every slab's ghost-only entries of x_aug (the augmented numbering) from the ranks
+    that own those nodes (the transport's generic exchange, padded to equal sizes)."""
+    if getattr(comm, "fused_peer", False):
+        raise ValueError("the ghost-layer slabs need a transport with a generic exchange "
+                         "(LocalTransport / TorchTransport / NativeTransport)")
+    sends = []
+    for sl, xa in zip(slabs, x_augs):
+        buf = {}
+        own = xa[sl.own_pos]
+        for q, pos in sl.send.items():
+            m = max(pos.numel(), _peer_count(slabs, sl, q))
+            t = torch.zeros(m, dtype=torch.float64, device=xa.device)
+            t[:pos.numel()] = own[pos]
+            buf[q] = t
+        for q in sl.recv:
+            if q not in buf:
+                buf[q] = torch.zeros(sl.recv[q].numel(), dtype=torch.float64, device=xa.device)
+        sends.append(buf)
+    recvs = comm.exchange(slabs, sends)
+    for sl, xa, rc in zip(slabs, x_augs, recvs):
+        for q, pos in sl.recv.items():
+            xa[pos] = rc[q][:pos.numel()]
+
+
+def jacobi_exact(slabs: list, comm, d, x_locals0: list, iters: int, omega: float = 0.8):
+    """Damped Jacobi on P ghost-layer slabs (ExactSlab) whose iterates are BIT FOR BIT the
+    single-GPU solver's (eb.jacobi, fast residual) at every slab node, for any P: each
+    iteration exchanges x at the ghost-only nodes, then every slab evaluates the masked
+    residual over all the elements at its nodes in the global (j, e) order (the same SELL
+    arithmetic as the solver's step) and the update x + omega (dinv r) with dinv from the
+    slot-order diagonal.  Returns (x_locals, norms): x on each slab's own local nodes; the
+    norms sum the owned nodes in rank order (within rounding of the 1-GPU history)."""
+    if iters < 0:
+        raise ValueError(f"iteration count must be nonnegative, got {iters}")
+    dev = x_locals0[0].device
+    xa, rs, dinvs, owned = [], [], [], []
+    for sl, x0 in zip(slabs, x_locals0):
+        nd = d.nd.to(dev) if d is not None else torch.empty(0, dtype=torch.int64, device=dev)
+        is_d = torch.zeros(int(max(int(sl.global_ids.max()) + 1, 1)), dtype=torch.bool,
+                           device=dev)
+        if nd.numel():
+            is_d[nd[nd < is_d.numel()]] = True
+        local_d = torch.nonzero(is_d[sl.global_ids]).reshape(-1)
+        from .operators import DirichletData
+        sl.plan.ensure_dirichlet(DirichletData(local_d, torch.zeros(local_d.numel(),
+                                                                   dtype=torch.float64,
+                                                                   device=dev)))
+        diag = D.empty(sl.n)
+        call("ebs_diagonal", sl.plan.handle, D.ptr(diag), D.stream())
+        free = torch.ones(sl.n, dtype=torch.bool, device=dev)
+        free[local_d] = False
+        ok = free & (diag != 0.0)
+        dinvs.append(torch.where(ok, 1.0 / torch.where(ok, diag, torch.ones_like(diag)),
+                                 torch.zeros_like(diag)))
+        x = torch.zeros(sl.n, dtype=torch.float64, device=dev)
+        x[sl.own_pos] = x0.to(dev, torch.float64)
+        xa.append(x)
+        rs.append(D.empty(sl.n))
+        own_g = sl.global_ids[sl.own_pos]
+        owned.append(sl.own_pos[sl._owner[own_g] == sl.rank])
+    norm2 = [torch.zeros(iters + 1, dtype=torch.float64, device=dev) for _ in slabs]
+    for k in range(iters + 1):
+        _ghost_exchange(slabs, comm, xa)
+        for i, sl in enumerate(slabs):
+            with sl.batch.using(sl.n) as pl:
+                call("ebs_residual", pl.handle, D.ptr(xa[i]), D.ptr(rs[i]), 1, 1, None,
+                     D.stream())
+            r_o = rs[i][owned[i]]
+            norm2[i][k] = torch.dot(r_o, r_o)
+            if k < iters:  # x + omega (dinv r): the solver's rounding, op by op
+                t = dinvs[i] * rs[i]
+                t = t * float(omega)
+                xa[i] = xa[i] + t
+    comm.allreduce(norm2)
+    norms = torch.sqrt(norm2[0]).cpu().numpy()
+    return [x[sl.own_pos] for sl, x in zip(slabs, xa)], norms
 
 
 def _peer_count(slabs, sl, q):

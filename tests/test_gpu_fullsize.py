@@ -177,3 +177,24 @@ def test_c2_exact_residual_eight_slabs_bitwise(gpu):
         assert torch.equal(r, ref[maps["local"][sl.rank].cuda()]), sl.rank
     del slabs, rs, batch, p
     _free()
+
+
+def test_c4_exact_jacobi_eight_slabs_bitwise(gpu):
+    """Full C4 (33.5M triangles, jittered + permuted, nu = 10, sin sin) on 8 ghost-layer slabs:
+    20 damped-Jacobi iterates bit for bit the single-GPU solver's at every slab node."""
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import dist
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(4, seed=0)
+    batch, d, m = p["batch"], p["dirichlet"], p["mesh"]
+    x0 = torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda")
+    x1, h1 = eb.jacobi(batch, d, x0, 20, omega=0.8)
+    maps = dist.partition_maps(batch.index.indt, m.n_nodes, 8)
+    slabs = dist.exact_slabs(maps, batch.index.indt, m.n_nodes, batch=batch)
+    xs, norms = dist.jacobi_exact(slabs, dist.LocalTransport(), d,
+                                  [x0[maps["local"][sl.rank].cuda()] for sl in slabs], 20, 0.8)
+    for sl, x in zip(slabs, xs):
+        assert torch.equal(x, x1[maps["local"][sl.rank].cuda()]), sl.rank
+    np.testing.assert_allclose(norms, h1.residual_norms, rtol=1e-12)
+    del slabs, xs, batch, p, x1
+    _free()
