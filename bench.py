@@ -163,9 +163,11 @@ def reference_c2_inputs(eb_ref, seed, size):
 
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation of the path on this host's
-    cores -- the unmodified `ebsolve.residual(batch, x, threads=T, deterministic=True)`
-    (operators.py:72-111) from baseline/_ref when installed ("kind": "reference"), else the
-    oracle port of the same algorithm (oracle/ebs_oracle.py, "kind": "port")."""
+    cores -- the unmodified `ebsolve.residual(batch, x, threads=T, deterministic=False)`
+    (operators.py:72-111; its fast mode, like the GPU arm's value; the default bit-exact
+    mode timed beside it under exact_mode) from baseline/_ref when installed ("kind":
+    "reference"), else the oracle port of the same algorithm (oracle/ebs_oracle.py, "kind":
+    "port").  Under torchrun only rank 0 runs it."""
     import numpy as np
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
