@@ -489,6 +489,20 @@ int ebs_peer_combine_jacobi(ebs_peer_t peer, double *s, double omega, const doub
 int ebs_peer_combine_q(ebs_peer_t peer, double *q, const uint8_t *free_m, const uint8_t *owned,
                        const double *pv, const double *prior, double *red, const int32_t *stop,
                        const double *dots, void *ws, void *stream);
+/* The two-launch single-reduction PCG iteration: the matvec sweep with delta = the slab's
+ * element energies sum_e u_e^T A_e u_e (summed over the ranks: u.mask(A u), u being 0 at
+ * constrained nodes) and the put of [dots[0], delta, dots[2]] (dots[1] := delta) by its last
+ * block -- no halo wait before the put; w's shared nodes keep their partials (pushed) --
+ * then the update kernel that first completes w's shared nodes from the neighbours' pushes
+ * (rank-ordered sums, masked; a grid barrier) and reduces the dots (_halo). */
+int ebs_peer_matvec_sweep_put(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks,
+                              int64_t n_list, int64_t n_if_chunks, const double *pv, double *q,
+                              const uint8_t *iface, double *dots, void *ws, void *stream);
+int ebs_peer_cg1_update_halo(ebs_peer_t peer, int64_t n, double *cur, const double *prev,
+                             const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
+                             const uint8_t *free_m, const double *dinv, double *x, double *r,
+                             double *u, double *w, double *p, double *s, double *next,
+                             int32_t *nonfinite, void *ws, void *stream);
 /* ebs_vec_cg1_update whose cur[0..2] are all-reduced on the device: every block waits for the
  * ranks' contributions (put by ebs_peer_combine_q with dots) and adds them in rank order; the
  * sums are stored in cur[0..2] and the reduced r.r once more in cur[4] (cur holds 5 doubles

@@ -191,6 +191,13 @@ SIGNATURES = {
                                         c_void_p, c_void_p, c_void_p]),
     "ebs_peer_combine_q": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ebs_peer_matvec_sweep_put": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                          c_void_p]),
+    "ebs_peer_cg1_update_halo": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                         c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_peer_cg1_update": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double,
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

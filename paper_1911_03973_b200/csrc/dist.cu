@@ -190,10 +190,38 @@ __global__ void __launch_bounds__(256, EBS_CG1_MINB)
                      double *rr0, double tol, int32_t *ctl,
                      const uint8_t *__restrict__ owned, const double *__restrict__ dinv,
                      double *__restrict__ x, double *__restrict__ r, double *__restrict__ u,
-                     const double *__restrict__ w, double *__restrict__ p,
+                     double *w, double *__restrict__ p,
                      double *__restrict__ s, double *partials, unsigned int *counter,
-                     double *next, int32_t *nonfinite, const RedGet rg) {
+                     double *next, int32_t *nonfinite, const RedGet rg,
+                     const PeerRecv hr, const uint8_t *__restrict__ free_m) {
     if (ctl && ctl[0]) return;
+    if (hr.hdr) {
+        // the previous sweep's shared nodes of w (ebs_peer_matvec_sweep_put pushed the
+        // partials and put the dots without waiting): rank-ordered sums, masked, then a grid
+        // barrier so every thread sees the completed w
+        const unsigned long long hep = recv_wait(hr);
+        const int hpar = (int)(hep & 1);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hr.n_if;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t m = hr.all_if[i];
+            const double acc = recv_sum(hr, i, w, hpar);
+            w[m] = free_m[m] ? acc : 0.0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const unsigned arrived = atomicAdd(&hr.hdr->done_a, 1u) + 1;
+            if (arrived == gridDim.x) {  // every block has read hep and finished its nodes
+                hr.hdr->halo_epoch = hep + 1;
+                __threadfence();
+                atomicAdd(&hr.hdr->done_a, 1u);
+            }
+            while (*reinterpret_cast<volatile unsigned *>(&hr.hdr->done_a) < gridDim.x + 1)
+                __nanosleep(64);
+            __threadfence();
+        }
+        __syncthreads();
+    }
     double gamma, delta, rr;
     unsigned long long ep = 0;
     if (rg.win) {
@@ -283,6 +311,7 @@ __global__ void __launch_bounds__(256, EBS_CG1_MINB)
     double tot[2];
     if (grid_sum_last<2>(part, partials, counter, tot) && threadIdx.x == 0) {
         if (rg.win) reinterpret_cast<WinHdr *>(rg.win)->red_epoch = ep + 1;
+        if (hr.hdr) hr.hdr->done_a = 0;  // every block is past the barrier
         if (!stopping) {
             next[0] = tot[0];
             next[2] = tot[1];
@@ -330,7 +359,8 @@ static Scratch scratch(void *ws) {
 
 namespace ebs {
 // the same step with cur[0..2] all-reduced on the device from the peer window (ebs_peer_*)
-int peer_cg1_update(const ebs::RedGet &rg, int64_t n, double *cur, const double *prev,
+int peer_cg1_update(const ebs::RedGet &rg, const ebs::PeerRecv &hr, const uint8_t *free_m,
+                    int64_t n, double *cur, const double *prev,
                     const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
                     const double *dinv, double *x, double *r, double *u, const double *w,
                     double *p, double *s, double *next, int32_t *nonfinite, void *ws,
@@ -342,8 +372,9 @@ int peer_cg1_update(const ebs::RedGet &rg, int64_t n, double *cur, const double 
     Scratch sc = scratch(ws);
     const int grid = persistent_grid((const void *)k_vec_cg1_update, 256, (n + 255) / 256, 0);
     k_vec_cg1_update<<<grid, 256, 0, S(stream)>>>(
-        n, cur, prev, const_cast<double *>(rr0), tol, ctl, owned, dinv, x, r, u, w, p, s,
-        sc.partials, sc.counter, next, nonfinite, rg);
+        n, cur, prev, const_cast<double *>(rr0), tol, ctl, owned, dinv, x, r, u,
+        const_cast<double *>(w), p, s, sc.partials, sc.counter, next, nonfinite, rg, hr,
+        free_m);
     LAUNCHED();
     EBS_CATCH
 }
@@ -456,8 +487,9 @@ int ebs_vec_cg1_update(int64_t n, double *cur, const double *prev, const double 
     Scratch sc = scratch(ws);
     const int grid = persistent_grid((const void *)k_vec_cg1_update, 256, (n + 255) / 256, 0);
     k_vec_cg1_update<<<grid, 256, 0, S(stream)>>>(
-        n, cur, prev, const_cast<double *>(rr0), tol, ctl, owned, dinv, x, r, u, w, p, s,
-        sc.partials, sc.counter, next, nonfinite, RedGet{nullptr, 0, 0});
+        n, cur, prev, const_cast<double *>(rr0), tol, ctl, owned, dinv, x, r, u,
+        const_cast<double *>(w), p, s, sc.partials, sc.counter, next, nonfinite,
+        RedGet{nullptr, 0, 0}, PeerRecv{}, nullptr);
     LAUNCHED();
     EBS_CATCH
 }

@@ -188,9 +188,6 @@ struct PeerSend {
     unsigned long long *flag[PEER_MAX];  // remote halo_flag[rank] of neighbour k
 };
 
-#ifndef EBS_PEER_BREAK_PARITY
-#define EBS_PEER_BREAK_PARITY 0  // negative control of ebs_peer_selftest only (one slot, no
-#endif                           // double buffering): must report errors (profiles/)
 __device__ __forceinline__ void peer_push(const PeerSend &ps, int m, double s) {
     const int i = ps.ifx[m];
     const int64_t par =
@@ -237,6 +234,10 @@ struct PeerJacobiEpi {
     }
 };
 
+// ENERGY: part sums p_m s_m over EVERY node, the shared ones with their slab-partial s --
+// i.e. the slab's element energies sum_e p_e^T A_e p_e (p = 0 at constrained nodes), whose
+// sum over the ranks is p.mask(A p) without waiting for the halo (ebs_peer_matvec_sweep_put).
+template <bool ENERGY = false>
 struct PeerMatvecEpi {
     const uint8_t *__restrict__ free_m;
     const uint8_t *__restrict__ iface;
@@ -247,6 +248,7 @@ struct PeerMatvecEpi {
         if (iface[m]) {
             q[m] = s;  // partial; completed after the halo
             peer_push(*ps, (int)m, s);
+            if (ENERGY) part[0] += po * s;
             return;
         }
         double qm = free_m[m] ? s : 0.0;
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
 
 template <int NB, int IDS>
 __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
-    k_peer_matvec_sweep(SellView v, const double *__restrict__ p, PeerMatvecEpi epi,
+    k_peer_matvec_sweep(SellView v, const double *__restrict__ p, PeerMatvecEpi<> epi,
                         __grid_constant__ const PeerSend ps, double *partials,
                         unsigned int *counter, double *red, const int32_t *stop) {
     if (stop && *stop) return;  // single-reduction PCG already stopped (ebs_dist_set_stop)
@@ -329,44 +331,6 @@ __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
 }
 
 // ------------------------------------------------------- combine + completion --
-struct PeerRecv {
-    WinHdr *hdr;
-    const char *win;  // this rank's window
-    int64_t cap;
-    int64_t n_if;
-    const int64_t *all_if;
-    const int32_t *pos;
-    int n_src;
-    int src[PEER_MAX];
-    int rank;
-    long long timeout_ns;
-};
-
-// every block: wait for the neighbours' flags of epoch ep (thread k waits for source k)
-__device__ __forceinline__ unsigned long long recv_wait(const PeerRecv &r) {
-    const unsigned long long ep = ld_volatile(&r.hdr->halo_epoch);
-    if (threadIdx.x < r.n_src && r.src[threadIdx.x] != r.rank)
-        peer_wait(&r.hdr->halo_flag[r.src[threadIdx.x]], ep + 1, r.timeout_ns, &r.hdr->error);
-    __syncthreads();
-    return ep;
-}
-
-// sum of the contributions to shared node i in ascending rank order (own partial: v)
-__device__ __forceinline__ double recv_sum(const PeerRecv &r, int64_t i, const double *v,
-                                           int par) {
-    if (EBS_PEER_BREAK_PARITY) par = 0;
-    double acc = 0.0;
-    for (int k = 0; k < r.n_src; ++k) {
-        const int32_t q = r.pos[i * r.n_src + k];
-        if (q < 0) continue;
-        EBS_DCHECK(r.src[k] == r.rank || q < r.cap);
-        acc += r.src[k] == r.rank
-                   ? v[q]
-                   : __ldcg(win_recv(const_cast<char *>(r.win), r.cap, r.src[k], par) + q);
-    }
-    return acc;
-}
-
 __global__ void __launch_bounds__(256)
     k_peer_combine_jacobi(__grid_constant__ const PeerRecv r, double *s, double omega,
                           const double *__restrict__ b, const double *__restrict__ dinv,
@@ -521,6 +485,28 @@ __global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
     }
 }
 
+// The single-reduction PCG's matvec sweep with the dot and the all-reduce put folded in:
+// w = A u (interface partials pushed), delta = sum_e u_e^T A_e u_e over the slab's elements
+// (the ENERGY epilogue: summed over the ranks it is u.mask(A u), u being 0 at constrained
+// nodes), and the last block puts [gamma, delta, rr] = dots[0..3) with dots[1] := delta for
+// the update kernel, which completes the shared nodes itself (ebs_peer_cg1_update_halo):
+// no combine launch, and the put does not wait for the neighbours.
+template <int NB, int IDS>
+__global__ void __launch_bounds__(256, (NB) == 3 ? EBS_MINB2 : EBS_MINB3)
+    k_peer_matvec_sweep_put(SellView v, const double *__restrict__ p, PeerMatvecEpi<true> epi,
+                            __grid_constant__ const PeerSend ps, double *partials,
+                            unsigned int *counter, __grid_constant__ const RedPut rp,
+                            double *dots, const int32_t *stop) {
+    if (stop && *stop) return;  // single-reduction PCG already stopped
+    epi.ps = &ps;
+    peer_sweep<NB, IDS, false>(v, p, epi, ps);
+    double tot[1];
+    if (grid_sum_last<1>(epi.part, partials, counter, tot) && threadIdx.x == 0) {
+        dots[1] = tot[0];
+        red_put_thread(rp, dots);
+    }
+}
+
 __global__ void __launch_bounds__(256)
     k_peer_combine_q(__grid_constant__ const PeerRecv r, double *q,
                      const uint8_t *__restrict__ free_m, const uint8_t *__restrict__ owned,
@@ -626,7 +612,8 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-int peer_cg1_update(const RedGet &rg, int64_t n, double *cur, const double *prev,
+int peer_cg1_update(const RedGet &rg, const PeerRecv &hr, const uint8_t *free_m, int64_t n,
+                    double *cur, const double *prev,
                     const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
                     const double *dinv, double *x, double *r, double *u, const double *w,
                     double *p, double *s, double *next, int32_t *nonfinite, void *ws,
@@ -1111,7 +1098,7 @@ int ebs_peer_matvec_sweep(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunk
                 "(or the reverse)");
     const Scratch2 sc = scratch2(ws);
     const PeerSend ps = peer_send_args(pr, n_if_chunks);
-    PeerMatvecEpi epi{p->free_int, iface, q, nullptr, {0.0}};
+    PeerMatvecEpi<> epi{p->free_int, iface, q, nullptr, {0.0}};
     SellView v = sell_view(p, chunks, n_list);
 #define EBS_PM(NB_, IDS_)                                                                  \
     {                                                                                      \
@@ -1299,6 +1286,42 @@ int ebs_peer_jacobi_step(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks
     EBS_CATCH
 }
 
+int ebs_peer_matvec_sweep_put(ebs_plan_t plan, ebs_peer_t peer, const int32_t *chunks,
+                              int64_t n_list, int64_t n_if_chunks, const double *pv, double *q,
+                              const uint8_t *iface, double *dots, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && peer && pv && q && iface && dots && ws, "null argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Peer *pr = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(p->has_A, "no operator loaded (ebs_plan_load)");
+    EBS_REQUIRE(n_list >= 1 && chunks && n_if_chunks >= 0 && n_if_chunks <= n_list,
+                "bad chunk list");
+    EBS_REQUIRE(pr->n_local == p->n_n, "peer halo set for %lld nodes, plan has %lld",
+                (long long)pr->n_local, (long long)p->n_n);
+    EBS_REQUIRE((n_if_chunks > 0) == (pr->n_nb > 0), "interface chunks without neighbours "
+                "(or the reverse)");
+    const Scratch2 sc = scratch2(ws);
+    const PeerSend ps = peer_send_args(pr, n_if_chunks);
+    RedPut rp{};
+    for (int k = 0; k < pr->world; ++k) rp.win[k] = pr->win[k];
+    rp.rank = pr->rank;
+    rp.world = pr->world;
+    PeerMatvecEpi<true> epi{p->free_int, iface, q, nullptr, {0.0}};
+    SellView v = sell_view(p, chunks, n_list);
+#define EBS_PMP(NB_, IDS_)                                                                 \
+    {                                                                                      \
+        auto kern = k_peer_matvec_sweep_put<NB_, IDS_>;                                    \
+        const int grid = persistent_grid((const void *)kern, 256,                          \
+                                         (n_list * LANES + 255) / 256, 0);                 \
+        kern<<<grid, 256, 0, S(stream)>>>(v, pv, epi, ps, sc.partials, sc.counter, rp,     \
+                                          dots, p->dist_stop);                             \
+    }
+    EBS_SELL_DISPATCH(p, EBS_PMP);
+#undef EBS_PMP
+    LAUNCHED();
+    EBS_CATCH
+}
+
 int ebs_peer_cg1_update(ebs_peer_t peer, int64_t n, double *cur, const double *prev,
                         const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
                         const double *dinv, double *x, double *r, double *u, const double *w,
@@ -1308,8 +1331,25 @@ int ebs_peer_cg1_update(ebs_peer_t peer, int64_t n, double *cur, const double *p
     EBS_REQUIRE(peer, "null argument");
     Peer *pr = reinterpret_cast<Peer *>(peer);
     const RedGet rg{pr->win[pr->rank], pr->world, pr->timeout_ns};
-    return peer_cg1_update(rg, n, cur, prev, rr0, tol, ctl, owned, dinv, x, r, u, w, p, s, next,
-                           nonfinite, ws, stream);
+    return peer_cg1_update(rg, PeerRecv{}, nullptr, n, cur, prev, rr0, tol, ctl, owned, dinv, x,
+                           r, u, w, p, s, next, nonfinite, ws, stream);
+    EBS_CATCH
+}
+
+int ebs_peer_cg1_update_halo(ebs_peer_t peer, int64_t n, double *cur, const double *prev,
+                             const double *rr0, double tol, int32_t *ctl, const uint8_t *owned,
+                             const uint8_t *free_m, const double *dinv, double *x, double *r,
+                             double *u, double *w, double *p, double *s, double *next,
+                             int32_t *nonfinite, void *ws, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(peer && free_m && w, "null argument");
+    Peer *pr = reinterpret_cast<Peer *>(peer);
+    EBS_REQUIRE(pr->n_local == n, "peer halo set for %lld nodes, vectors have %lld",
+                (long long)pr->n_local, (long long)n);
+    const RedGet rg{pr->win[pr->rank], pr->world, pr->timeout_ns};
+    const PeerRecv hr = peer_recv_args(pr);
+    return peer_cg1_update(rg, hr, free_m, n, cur, prev, rr0, tol, ctl, owned, dinv, x, r, u, w,
+                           p, s, next, nonfinite, ws, stream);
     EBS_CATCH
 }
 

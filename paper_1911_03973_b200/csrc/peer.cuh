@@ -73,6 +73,49 @@ static __device__ __noinline__ bool peer_wait(const unsigned long long *flag, un
     return true;
 }
 
+#ifndef EBS_PEER_BREAK_PARITY
+#define EBS_PEER_BREAK_PARITY 0  // negative control of ebs_peer_selftest only (one slot, no
+#endif                           // double buffering): must report errors (profiles/)
+
+// The receiving side of a rank's halo (peer.cu builds it from the peer view).
+struct PeerRecv {
+    WinHdr *hdr;
+    const char *win;  // this rank's window
+    int64_t cap;
+    int64_t n_if;
+    const int64_t *all_if;
+    const int32_t *pos;
+    int n_src;
+    int src[PEER_MAX];
+    int rank;
+    long long timeout_ns;
+};
+
+// every block: wait for the neighbours' flags of epoch ep (thread k waits for source k)
+__device__ __forceinline__ unsigned long long recv_wait(const PeerRecv &r) {
+    const unsigned long long ep = ld_volatile(&r.hdr->halo_epoch);
+    if (threadIdx.x < r.n_src && r.src[threadIdx.x] != r.rank)
+        peer_wait(&r.hdr->halo_flag[r.src[threadIdx.x]], ep + 1, r.timeout_ns, &r.hdr->error);
+    __syncthreads();
+    return ep;
+}
+
+// sum of the contributions to shared node i in ascending rank order (own partial: v)
+__device__ __forceinline__ double recv_sum(const PeerRecv &r, int64_t i, const double *v,
+                                           int par) {
+    if (EBS_PEER_BREAK_PARITY) par = 0;
+    double acc = 0.0;
+    for (int k = 0; k < r.n_src; ++k) {
+        const int32_t q = r.pos[i * r.n_src + k];
+        if (q < 0) continue;
+        EBS_DCHECK(r.src[k] == r.rank || q < r.cap);
+        acc += r.src[k] == r.rank
+                   ? v[q]
+                   : __ldcg(win_recv(const_cast<char *>(r.win), r.cap, r.src[k], par) + q);
+    }
+    return acc;
+}
+
 // Fused all-reduce consumer: the ranks' contributions were put into this window's slots
 // (ebs_peer_allreduce mode 1, or the put of ebs_peer_combine_q); wait for every rank's flag
 // of the current epoch and add the slots in rank order 0..world-1 (identical on every rank).

@@ -856,6 +856,23 @@ class GpuRankOperator:
              D.ptr(p), D.ptr(prior), D.ptr(red), D.ptr(self._stop), D.ptr(dots), D.ptr(self._ws),
              D.stream())
 
+    def peer_matvec_sweep_put(self, p, q, dots):
+        """q = A p with the interface partials pushed, dots[1] = the slab's element energies
+        (p.mask(A p) summed over the ranks) and [dots[0..3)] put for the all-reduce -- the
+        shared nodes of q are completed by peer_cg1_update_halo."""
+        c = self.peer_chunks
+        call("ebs_peer_matvec_sweep_put", self.plan.handle, self.peer, D.ptr(c), c.numel(),
+             self.if_chunks.numel(), D.ptr(p), D.ptr(q), D.ptr(self.iface), D.ptr(dots),
+             D.ptr(self._ws), D.stream())
+
+    def peer_cg1_update_halo(self, cur, prev, rr0, tol, ctl, dinv, x, r, u, w, p, s_, nxt):
+        """peer_cg1_update that first completes w's shared nodes (the previous sweep's
+        pushed partials, rank-ordered, masked)."""
+        call("ebs_peer_cg1_update_halo", self.peer, self.n, D.ptr(cur), D.ptr(prev), D.ptr(rr0),
+             float(tol), D.ptr(ctl), D.ptr(self.owned), D.ptr(self.free), D.ptr(dinv), D.ptr(x),
+             D.ptr(r), D.ptr(u), D.ptr(w), D.ptr(p), D.ptr(s_), D.ptr(nxt), D.ptr(self._flag),
+             D.ptr(self._ws), D.stream())
+
     def peer_cg1_update(self, cur, prev, rr0, tol, ctl, dinv, x, r, u, w, p, s_, nxt):
         """vec_cg1_update with cur[0..2] all-reduced on the device (waits for every rank's
         peer_combine_q put, adds the contributions in rank order)."""
@@ -1543,12 +1560,10 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
             op.set_stop(c if fused else None)
 
     def matvec_w(slot):  # w = mask(A u), slot[1] = the rank's owned w.u
-        if peer:  # ... and [r.u, w.u, r.r] put for the all-reduce the next update takes
+        if peer:  # ... w.u from the element energies and [r.u, w.u, r.r] put for the
+            # all-reduce the next update takes, which also completes w's shared nodes
             for i, op in enumerate(ops):
-                op.peer_matvec_sweep(us[i], ws[i], part[i][0:1])
-            comm.after_put()
-            for i, op in enumerate(ops):
-                op.peer_combine_q(us[i], ws[i], slot[i][1:2], prior=part[i], dots=slot[i][0:3])
+                op.peer_matvec_sweep_put(us[i], ws[i], slot[i][0:3])
             comm.after_put()
         elif fused:
             for i, op in enumerate(ops):
@@ -1591,10 +1606,10 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
         cur = [rg[k % B] for rg in ring]
         prev = [rg[(k - 1) % B] for rg in ring]
         nxt = [rg[(k + 1) % B] for rg in ring]
-        if peer:  # the all-reduce of cur happens inside the update (fused get)
+        if peer:  # the all-reduce of cur and w's halo completion happen inside the update
             for i, op in enumerate(ops):
-                op.peer_cg1_update(cur[i], prev[i], rr0[i], tol_, ctl[i], prob.dinv[i], xs[i],
-                                   rs[i], us[i], ws[i], ps[i], ss[i], nxt[i])
+                op.peer_cg1_update_halo(cur[i], prev[i], rr0[i], tol_, ctl[i], prob.dinv[i],
+                                        xs[i], rs[i], us[i], ws[i], ps[i], ss[i], nxt[i])
             matvec_w(nxt)
             return
         for i, op in enumerate(ops):
@@ -1651,9 +1666,11 @@ def _pcg_single_reduction(prob: DistProblem, xs0, iters: int, tol=None, graph: b
     if sync is not None:
         sync()
     c = ctl[0].cpu()
-    if peer and not int(c[0]):  # the last step's put (same decision on every rank)
+    if peer and not int(c[0]):  # the last sweep's put and halo (same decision on every rank)
         last = [rg[iters % B] for rg in ring]
         comm.allreduce_get([sl[0:3] for sl in last])
+        for op, w_ in zip(ops, ws):
+            op.peer_combine(w_)
         for i in range(len(ops)):
             norm2[i][iters:iters + 1].copy_(last[i][2:3])
     for op in ops:
