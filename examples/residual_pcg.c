@@ -94,6 +94,17 @@ int main(int argc, char **argv) {
     printf("level %d: %lld nodes, %lld triangles; residual bitwise mismatches: %lld\n", level,
            (long long)nn, (long long)ne, (long long)mismatches);
 
+    /* the same residual on host buffers, 3 times through the pipelined host entry point
+     * (x read from one host row: ldx = 0) -- each row bit-identical to the device call */
+    double *hr3 = malloc(sizeof(double) * 3 * nn);
+    int32_t hbad[3] = {-1, -1, -1};
+    EBS(ebs_residual_many_host(plan, hx, 0, hr3, nn, 3, EBS_RES_EXACT, 0, hbad, NULL));
+    int64_t host_mismatches = hbad[0] + hbad[1] + hbad[2];
+    for (int64_t i = 0; i < 3 * nn; ++i) host_mismatches += memcmp(&hr3[i], &hr[i % nn], sizeof(double)) != 0;
+    printf("host-buffer residuals (3 rows): bitwise mismatches vs the device call: %lld\n",
+           (long long)host_mismatches);
+    free(hr3);
+
     /* Dirichlet u = 0 on the boundary, Jacobi-PCG to 1e-10 */
     uint8_t *hf = malloc(nn);
     EBS(ebs_mesh_flags(2, nn, nodes, 0, flags, NULL));

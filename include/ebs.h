@@ -146,6 +146,16 @@ int ebs_plan_set_dirichlet(ebs_plan_t plan, const int64_t *nd, int64_t n_d, void
  * 1 when x has a non-finite entry (operators.py:90-91), else 0 (no reset needed). */
 int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int masked,
                  int32_t *nonfinite, void *stream);
+/* NEW: ebs_residual on k caller-numbered vectors in HOST memory (x_i at x_host + i*ldx,
+ * ldx 0 or >= n_nodes; r_i written to r_host + i*ldr, ldr >= n_nodes).  The host->device
+ * copy of x_{i+1}, the residual of x_i and the device->host copy of r_{i-1} overlap
+ * (copy streams + device buffers kept by the plan); pinned host memory lets the copies
+ * run asynchronously.  Each r_i is bit-identical to ebs_residual on x_i.  nonfinite
+ * (HOST int32[k], nullable): the per-vector flag of ebs_residual.  Returns once every r_i
+ * is in r_host (host-synchronous; not capturable); ordered after prior work on stream. */
+int ebs_residual_many_host(ebs_plan_t plan, const double *x_host, int64_t ldx, double *r_host,
+                           int64_t ldr, int64_t k, int mode, int masked, int32_t *nonfinite_host,
+                           void *stream);
 /* spectrum.py:54-61 _apply_masked: y = A x in (j,e) order; masked != 0 zeroes y[nd]. */
 int ebs_matvec(ebs_plan_t plan, const double *x, double *y, int masked, void *stream);
 /* NEW diag(A) = assemble_rhs(stack_j A_e[j,j,:]), caller numbering. */

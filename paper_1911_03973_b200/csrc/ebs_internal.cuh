@@ -223,6 +223,7 @@ struct Plan {
     uint8_t *codes = nullptr;
     int4 *tup = nullptr;
     int n_tup = 0;
+    void *hostpipe = nullptr;    // host-buffer residual pipeline (hostpipe.cu), lazy
 };
 
 double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)
@@ -236,6 +237,7 @@ void perm_apply(Plan *p, const Perm2 *P, const double *in, double *out, int32_t 
                 cudaStream_t s);
 void perm_free(Plan *p);
 void dist_free(Plan *p);
+void hostpipe_free(Plan *p);
 
 // Programmatic dependent launch (PDL): a kernel launched with programmatic stream
 // serialisation is scheduled while its predecessor drains; griddepcontrol.wait at its

@@ -739,6 +739,7 @@ static void plan_free(Plan *p) {
     for (auto &v : p->wvec) dfree(v);
     perm_free(p);
     dist_free(p);
+    hostpipe_free(p);
     if (p->ctl_host) cudaFreeHost(p->ctl_host);
     p->ctl_host = nullptr;
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);

@@ -116,14 +116,15 @@ def residual_many(batch: ElementBatch, xs, out=None, deterministic: bool = True,
     memory -- the k-fold ``residual`` with the PCIe traffic overlapped.
 
     ``xs``: a (k, n) CPU tensor / array (pinned memory lets the copies run
-    asynchronously) or a sequence of k such vectors.  ``out``: an optional (k, n)
-    CPU float64 tensor (pinned: asynchronous read-back), else one is allocated
-    (pinned).  Each x_i goes host->device on a copy stream, its residual runs on the
-    current stream, r_i goes device->host on a second copy stream; two device
-    buffers per side, so the H2D of x_{i+1}, the kernels of x_i and the D2H of r_{i-1}
-    overlap.  Each r_i is bit-identical to ``residual(batch, x_i, deterministic=...)``.
-    Non-finite entries in any x_i raise ValueError (after all copies complete), as
-    ``residual`` does (operators.py:87-91)."""
+    asynchronously; a broadcast (0, 1)-strided batch is read as is) or a sequence of k
+    such vectors.  ``out``: an optional (k, n) contiguous CPU float64 tensor (pinned:
+    asynchronous read-back), else one is allocated (pinned).  One native call
+    (``ebs_residual_many_host``, csrc/hostpipe.cu): x_i goes host->device on a copy
+    stream, its residual runs on the current stream, r_i goes device->host on a second
+    copy stream, with device buffers kept by the plan, so the H2D of x_{i+1}, the kernels
+    of x_i and the D2H of r_{i-1} overlap.  Each r_i is bit-identical to
+    ``residual(batch, x_i, deterministic=...)``.  Non-finite entries in any x_i raise
+    ValueError (after all residuals complete), as ``residual`` does (operators.py:87-91)."""
     import torch as _t
     seq = list(xs) if not isinstance(xs, (_t.Tensor, np.ndarray)) else None
     if seq is not None:
@@ -135,9 +136,9 @@ def residual_many(batch: ElementBatch, xs, out=None, deterministic: bool = True,
         raise ValueError(f"xs must be (k, n), got shape {tuple(xs.shape)}")
     if xs.dtype != _t.float64 or xs.device.type != "cpu":
         xs = xs.to(device="cpu", dtype=_t.float64)
-    if xs.stride(1) != 1:                            # rows must be contiguous (a broadcast
-        xs = xs.contiguous()                         # (0, 1)-strided batch is fine)
     k, n = xs.shape
+    if xs.stride(1) != 1 or (k > 1 and xs.stride(0) != 0 and xs.stride(0) < n):
+        xs = xs.contiguous()
     if out is None:
         out = _t.empty((k, n), dtype=_t.float64, pin_memory=True)
     elif (tuple(out.shape) != (k, n) or out.dtype != _t.float64 or out.device.type != "cpu"
@@ -145,47 +146,16 @@ def residual_many(batch: ElementBatch, xs, out=None, deterministic: bool = True,
         raise ValueError("out must be a contiguous (k, n) float64 CPU tensor")
     if k == 0:
         return out
+    flags = _t.zeros(k, dtype=_t.int32) if check_finite else None
+    mode = EBS_RES_EXACT if deterministic else EBS_RES_FAST
     with using_operator(batch, n) as pl:  # the plan's operator stays loaded
-        comp = _t.cuda.current_stream()
-        h2d, d2h = _t.cuda.Stream(), _t.cuda.Stream()
-        h2d.wait_stream(comp)                            # stream semantics: after prior work
-        d2h.wait_stream(comp)
-        xb = [D.empty(n), D.empty(n)]
-        rb = [D.empty(n), D.empty(n)]
-        flags = D.zeros(k, _t.int32)
-        ev = lambda: _t.cuda.Event()
-        x_ready, used, r_ready, read = ([ev() for _ in range(k)] for _ in range(4))
-        mode = EBS_RES_EXACT if deterministic else EBS_RES_FAST
-        s = D.stream()
-        for i in range(k):
-            j = i & 1
-            with _t.cuda.stream(h2d):
-                if i >= 2:
-                    h2d.wait_event(used[i - 2])          # compute of step i-2 done with xb[j]
-                xb[j].copy_(xs[i], non_blocking=True)
-                x_ready[i].record(h2d)
-            comp.wait_event(x_ready[i])
-            if i >= 2:
-                comp.wait_event(read[i - 2])             # rb[j] read back
-            fl = flags[i:i + 1] if check_finite else None
-            call("ebs_residual", pl.handle, D.ptr(xb[j]), D.ptr(rb[j]), mode, 0, D.ptr(fl), s)
-            used[i].record(comp)
-            r_ready[i].record(comp)
-            with _t.cuda.stream(d2h):
-                d2h.wait_event(r_ready[i])
-                out[i].copy_(rb[j], non_blocking=True)
-                read[i].record(d2h)
-        comp.wait_stream(d2h)
-        comp.wait_stream(h2d)
-        for t in xb + rb:                                # buffers used on the side streams
-            t.record_stream(h2d)
-            t.record_stream(d2h)
+        call("ebs_residual_many_host", pl.handle, xs.data_ptr(), xs.stride(0) if k > 1 else 0,
+             out.data_ptr(), n, k, mode, 0, flags.data_ptr() if check_finite else None,
+             D.stream())
     if check_finite:
         bad = _t.nonzero(flags).flatten()
         if bad.numel():
             raise ValueError(f"x[{int(bad[0])}] contains non-finite entries")
-    else:
-        comp.synchronize()
     return out
 
 

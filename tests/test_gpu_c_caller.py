@@ -24,7 +24,8 @@ def test_c_program_through_the_c_abi(gpu, tmp_path):
     for level in ("3", "7"):
         r = subprocess.run([str(exe), level], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout + r.stderr
-        assert "mismatches: 0" in r.stdout and r.stdout.strip().endswith("OK"), r.stdout
+        assert "residual bitwise mismatches: 0" in r.stdout and r.stdout.strip().endswith("OK"), r.stdout
+        assert "vs the device call: 0" in r.stdout, r.stdout
 
 
 def test_c_program_slab_jacobi_through_peer_memory(gpu, tmp_path):

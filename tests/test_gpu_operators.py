@@ -263,6 +263,11 @@ def test_residual_many_pipelined(gpu):
     bcast = torch.from_numpy(xs[2]).pin_memory().unsqueeze(0).expand(5, n)
     npt.assert_array_equal(eb.residual_many(batch, bcast).numpy(),
                            np.broadcast_to(to_np(eb.residual(batch, xs[2])), (5, n)))
+    wide = torch.from_numpy(np.pad(xs, ((0, 0), (0, 5))))[:, :n]   # rows n + 5 apart
+    assert wide.stride(0) == n + 5
+    npt.assert_array_equal(eb.residual_many(batch, wide, deterministic=False).numpy(),
+                           np.stack([to_np(eb.residual(batch, x, deterministic=False)) for x in xs]))
+    npt.assert_array_equal(eb.residual_many(batch, xs[5:6]).numpy()[0], to_np(eb.residual(batch, xs[5])))
     bad = xs.copy()
     bad[4, 3] = np.nan
     with pytest.raises(ValueError, match=r"x\[4\]"):
