@@ -153,6 +153,105 @@ __global__ void __launch_bounds__(W * 32) k_tma(const __grid_constant__ CUtensor
     }
 }
 
+// Hybrid: in each CTA, WL warps gather nodes [0, split) through the LSU (ILP-8), WT warps
+// gather [split, n) through TMA gather4 (S-stage ring per warp) -- the two paths have
+// separate throughput limits (L1tex wavefronts vs the TMA unit).
+template <int S, int WL, int WT>
+__global__ void __launch_bounds__((WL + WT) * 32) k_hyb(const __grid_constant__ CUtensorMap tm, int n,
+                                                        int split, const int *__restrict__ o2n,
+                                                        const double *__restrict__ x,
+                                                        double *__restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[WT > 0 ? WT : 1][S];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    if (wib < WL) {
+        const int stride = gridDim.x * WL * 32;
+        for (int base = blockIdx.x * WL * 32 + threadIdx.x; base < split; base += stride * ILP) {
+            int idx[ILP];
+            double v[ILP];
+#pragma unroll
+            for (int u = 0; u < ILP; ++u) {
+                const int m = base + u * stride;
+                idx[u] = m < split ? __ldcs(o2n + m) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < ILP; ++u) {
+                const int m = base + u * stride;
+                v[u] = m < split ? __ldg(x + idx[u]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < ILP; ++u) {
+                const int m = base + u * stride;
+                if (m < split) y[m] = v[u];
+            }
+        }
+        return;
+    }
+    if constexpr (WT > 0) {
+    const int tw = wib - WL;
+    double *ring = reinterpret_cast<double *>(smem) + (size_t)tw * S * 512;
+    uint64_t *bar = bars[tw];
+    if (lane == 0)
+        for (int s = 0; s < S; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const int warp = blockIdx.x * WT + tw, nwarps = gridDim.x * WT;
+    const int nst = (n - split + 127) / 128;
+    int idx_keep[S][4];
+    auto issue = [&](int st, int slot) {
+        const int base = split + st * 128 + lane * 4;
+        int r[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int m = base + q;
+            const int id = m < n ? __ldcs(o2n + m) : 0;
+            idx_keep[slot][q] = id;
+            r[q] = id >> 2;
+        }
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             smem_u32(&bar[slot])),
+                         "r"(128 * 32)
+                         : "memory");
+        __syncwarp();
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(ring + slot * 512 + lane * 16)),
+            "l"(&tm), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]),
+            "r"(smem_u32(&bar[slot]))
+            : "memory");
+    };
+    uint32_t phase = 0;
+    int k = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int st = warp + s * nwarps;
+        if (st < nst) issue(st, s);
+    }
+    for (int st = warp; st < nst; st += nwarps, ++k) {
+        const int slot = k % S;
+        asm volatile(
+            "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra W_%=;\n}\n" ::"r"(smem_u32(&bar[slot])),
+            "r"((phase >> slot) & 1u)
+            : "memory");
+        phase ^= 1u << slot;
+        const double *rs = ring + slot * 512 + lane * 16;
+        const int base = split + st * 128 + lane * 4;
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = rs[q * 4 + (idx_keep[slot][q] & 3)];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (base + q < n) y[base + q] = v[q];
+        const int nxt = st + S * nwarps;
+        if (nxt < nst) issue(nxt, slot);
+    }
+    }
+}
+
 int main(int argc, char **argv) {
     const int n = argc > 1 ? atoi(argv[1]) : 4198401;
     const int n2 = (n + 3) / 4 * 4;
@@ -185,6 +284,10 @@ int main(int argc, char **argv) {
     }
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const bool flush = getenv("FLUSH") && atoi(getenv("FLUSH"));
+    const size_t fbytes = 512ull << 20;
+    void *fbuf = nullptr;
+    if (flush) CK(cudaMalloc(&fbuf, fbytes));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -205,13 +308,29 @@ int main(int argc, char **argv) {
         CK(cudaDeviceSynchronize());
         check(what);
         const int R = 50;
-        CK(cudaEventRecord(e0));
-        for (int i = 0; i < R; ++i) launch();
-        CK(cudaEventRecord(e1));
-        CK(cudaEventSynchronize(e1));
         float ms = 0;
-        CK(cudaEventElapsedTime(&ms, e0, e1));
-        printf("%-28s %8.2f us\n", what, ms / R * 1e3);
+        if (flush) {
+            std::vector<float> t;
+            for (int i = 0; i < R; ++i) {
+                CK(cudaMemsetAsync(fbuf, i & 0xff, fbytes));
+                CK(cudaEventRecord(e0));
+                launch();
+                CK(cudaEventRecord(e1));
+                CK(cudaEventSynchronize(e1));
+                float m1 = 0;
+                CK(cudaEventElapsedTime(&m1, e0, e1));
+                t.push_back(m1);
+            }
+            std::sort(t.begin(), t.end());
+            ms = t[R / 2] * R;
+        } else {
+            CK(cudaEventRecord(e0));
+            for (int i = 0; i < R; ++i) launch();
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+        }
+        printf("%-28s %8.2f us%s\n", what, ms / R * 1e3, flush ? " (x flushed from L2, median)" : "");
     };
     timeit("lsu ilp8 8 CTA/SM", [&] {
         k_lsu<<<sms * 8, 256>>>(n, o2n, x, y);
@@ -224,6 +343,22 @@ int main(int argc, char **argv) {
     }
     LSU_CASE(4, 8) LSU_CASE(8, 8) LSU_CASE(16, 8) LSU_CASE(8, 4) LSU_CASE(16, 4) LSU_CASE(4, 16)
     LSU_CASE(8, 16) LSU_CASE(32, 2) LSU_CASE(16, 2)
+    if (argc > 2 && argv[2][0] == 'q') return 0;
+#define HYB_CASE(S_, WL_, WT_, B_, F_)                                                   \
+    {                                                                                     \
+        auto kern = k_hyb<S_, WL_, WT_>;                                                  \
+        const size_t sm = (size_t)(WT_ > 0 ? WT_ : 1) * S_ * 512 * 8;                     \
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+        const int split = (int)((long long)n * F_ / 100) / 128 * 128;                     \
+        char name[64];                                                                    \
+        snprintf(name, sizeof name, "hyb S=%d L%d T%d %d/SM f=%d%%", S_, WL_, WT_, B_, F_); \
+        timeit(name, [&] { kern<<<sms * B_, (WL_ + WT_) * 32, sm>>>(tm, n, split, o2n, x, y); }); \
+    }
+    HYB_CASE(2, 8, 0, 6, 100)
+    HYB_CASE(2, 8, 2, 5, 85) HYB_CASE(2, 8, 2, 5, 75) HYB_CASE(2, 8, 2, 5, 65)
+    HYB_CASE(2, 8, 4, 4, 75) HYB_CASE(2, 8, 4, 4, 65) HYB_CASE(2, 8, 4, 4, 55)
+    HYB_CASE(3, 8, 4, 4, 65) HYB_CASE(2, 6, 4, 4, 60) HYB_CASE(2, 8, 8, 3, 55)
+    HYB_CASE(2, 8, 8, 3, 45) HYB_CASE(2, 4, 4, 6, 60)
     if (argc > 2) return 0;
 #define TMA_CASE(S_, W_, B_)                                                              \
     {                                                                                     \
