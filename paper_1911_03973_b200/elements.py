@@ -25,6 +25,13 @@ EPS_AREA = 1e-14      # elements.py:19
 EPS_VOLUME = 1e-18    # tetrahedra (restatement)
 
 
+def _host_tensor(a) -> torch.Tensor:
+    """A float64 CPU tensor over a host array (read-only arrays, e.g. the reference's frozen
+    fields, are copied: torch needs a writable buffer)."""
+    a = np.asarray(a, dtype=np.float64)
+    return torch.from_numpy(a if a.flags.writeable else a.copy())
+
+
 @dataclass(frozen=True, eq=False)
 class ElementBatch:
     """elements.py:25-53: everything the element operator needs."""
@@ -41,13 +48,13 @@ class ElementBatch:
         vals = {}
         for name in ("K_e", "M_e", "A_e"):
             arr = getattr(self, name)
-            t = arr if isinstance(arr, torch.Tensor) else torch.from_numpy(np.asarray(arr, dtype=np.float64))
+            t = arr if isinstance(arr, torch.Tensor) else _host_tensor(arr)
             if tuple(t.shape) != (n_b, n_b, n_e):
                 raise ValueError(f"{name} must have shape ({n_b}, {n_b}, {n_e}), got {tuple(t.shape)}")
             if t.device != D.device() or t.dtype != torch.float64:
                 t = t.to(device=D.device(), dtype=torch.float64)
             vals[name] = t
-        b = self.b_e if isinstance(self.b_e, torch.Tensor) else torch.from_numpy(np.asarray(self.b_e, dtype=np.float64))
+        b = self.b_e if isinstance(self.b_e, torch.Tensor) else _host_tensor(self.b_e)
         if tuple(b.shape) != (n_b, n_e):
             raise ValueError(f"b_e must have shape ({n_b}, {n_e}), got {tuple(b.shape)}")
         if self.nu < 0:

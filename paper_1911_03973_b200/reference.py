@@ -23,6 +23,10 @@ import torch
 from . import _device as D
 from .operators import DirichletData
 
+# reference.py:20: the size above which the reference switches from a sparse direct solve to
+# CG.  The device solve has one path (Jacobi-PCG to _CG_RTOL) at every size; the name is
+# kept so callers that set it keep working.
+_DIRECT_LIMIT = 200_000
 _DENSE_EIG_LIMIT = 2000   # reference.py:21
 _CG_RTOL = 1e-13          # reference.py:22
 
