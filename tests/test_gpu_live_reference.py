@@ -33,6 +33,8 @@ def ref():
         yield mod
     finally:
         sys.path.remove(REF)
+        for name in [m for m in sys.modules if m == "ebsolve" or m.startswith("ebsolve.")]:
+            del sys.modules[name]
 
 
 @pytest.fixture(scope="module")
