@@ -206,18 +206,16 @@ def _facade_class(dev_cls: type) -> type:
     return cls
 
 
+# the device data classes whose fields hold tensors (directly or through one another): seen
+# through the facade they are facade classes, so constructing one from host arrays and reading
+# its fields both follow the reference's convention
+_TENSOR_CLASSES = frozenset({"Mesh", "IndexArrays", "ElementBatch", "DirichletData", "SolverRun",
+                             "ExperimentReport"})
+
+
 def _tensor_dataclass(cls) -> bool:
-    """Statically: a data class of the device package declared with a tensor field, or
-    with a field of such a class."""
-    if not (isinstance(cls, type) and dataclasses.is_dataclass(cls)):
-        return False
-    if not cls.__module__.startswith(_PKG):
-        return False
-    for f in dataclasses.fields(cls):
-        t = f.type if isinstance(f.type, str) else getattr(f.type, "__name__", str(f.type))
-        if "Tensor" in t or t in ("IndexArrays", "Mesh", "ElementBatch", "DirichletData"):
-            return True
-    return False
+    return (isinstance(cls, type) and dataclasses.is_dataclass(cls)
+            and cls.__module__.startswith(_PKG) and cls.__name__ in _TENSOR_CLASSES)
 
 
 class _FacadeModule(types.ModuleType):
