@@ -26,7 +26,6 @@ import time
 from dataclasses import dataclass
 
 import numpy as np
-import torch
 
 from . import _device as D
 from ._lib import (CALLBACK, EBS_CG, EBS_CHEB2, EBS_CHEB3, EBS_ECALLBACK, EBS_JACOBI, EBS_PCG,
