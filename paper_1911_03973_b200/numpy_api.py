@@ -300,22 +300,21 @@ _SUBMODULES = ("cli", "mesh", "elements", "operators", "solvers", "spectrum", "r
 
 
 def install(alias: str = "ebsolve", package_dir: str | None = None) -> types.ModuleType:
-    """Register the facade in ``sys.modules`` under the reference's import name.
+    """Register the facade in ``sys.modules`` under the reference's import name: ``alias`` for
+    the package and ``alias.<module>`` for its modules.
 
-    With ``package_dir`` (the ``compat/ebsolve`` shim) the package facade gets that
-    directory as its ``__path__`` and the submodules are found there as files (so
-    ``python -m ebsolve.cli`` has a spec to run); without it ``alias.<module>`` are
-    registered directly."""
+    With ``package_dir`` (the ``compat/ebsolve`` shim) the package facade gets that directory
+    as its ``__path__`` and ``alias.cli`` is left to the shim's ``cli.py`` file, so that
+    ``python -m ebsolve.cli`` (test_cli.py:218-225) has a module spec to run."""
     root = facade("")
     sys.modules[alias] = root
     if package_dir is not None:
         root.__dict__["__path__"] = [package_dir]
         root.__dict__["__package__"] = alias
-    else:
-        for sub in _SUBMODULES:
-            sys.modules[f"{alias}.{sub}"] = facade(sub)
     for sub in _SUBMODULES:
         root.__dict__[sub] = facade(sub)
+        if package_dir is None or sub != "cli":
+            sys.modules[f"{alias}.{sub}"] = facade(sub)
     return root
 
 
