@@ -146,6 +146,15 @@ int ebs_plan_set_dirichlet(ebs_plan_t plan, const int64_t *nd, int64_t n_d, void
  * 1 when x has a non-finite entry (operators.py:90-91), else 0 (no reset needed). */
 int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int masked,
                  int32_t *nonfinite, void *stream);
+/* NEW: ebs_residual on k caller-numbered DEVICE vectors (x_i at x + i*ldx, ldx 0 or >=
+ * n_nodes; r_i written to r + i*ldr, ldr >= n_nodes; rows must not alias), two residuals
+ * in flight: odd i run on a second stream kept by the plan, each stream with its own
+ * workspace, forked from and joined back into `stream` (asynchronous; capturable).  The
+ * permutation / fill of one residual overlaps the other's operator pass.  Each r_i is
+ * bit-identical to ebs_residual on x_i.  nonfinite (DEVICE int32[k], nullable): the
+ * per-vector flag of ebs_residual. */
+int ebs_residual_many(ebs_plan_t plan, const double *x, int64_t ldx, double *r, int64_t ldr,
+                      int64_t k, int mode, int masked, int32_t *nonfinite, void *stream);
 /* NEW: ebs_residual on k caller-numbered vectors in HOST memory (x_i at x_host + i*ldx,
  * ldx 0 or >= n_nodes; r_i written to r_host + i*ldr, ldr >= n_nodes).  The host->device
  * copy of x_{i+1}, the residual of x_i and the device->host copy of r_{i-1} overlap

@@ -77,6 +77,8 @@ SIGNATURES = {
     "ebs_plan_load": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "ebs_plan_set_dirichlet": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "ebs_residual": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "ebs_residual_many": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int,
+                                  c_int, c_void_p, c_void_p]),
     "ebs_residual_many_host": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int64,
                                        c_int, c_int, c_void_p, c_void_p]),
     "ebs_matvec": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),

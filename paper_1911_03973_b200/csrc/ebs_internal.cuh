@@ -158,6 +158,7 @@ struct Perm2 {
     uint16_t *dst2 = nullptr;  // pass 2: offset of intermediate slot k in its destination tile
 };
 
+constexpr int MANY_MAX = 4;  // residuals in flight in ebs_residual_many (workspace vectors 0..3)
 constexpr int PERM_VEC = 8;  // workspace vector: the permutation intermediate
 constexpr int OUT_VEC = 9;   // workspace vector: internal-order operator output
 
@@ -224,13 +225,19 @@ struct Plan {
     int4 *tup = nullptr;
     int n_tup = 0;
     void *hostpipe = nullptr;    // host-buffer residual pipeline (hostpipe.cu), lazy
+    // ebs_residual_many: the second stream of the two-deep residual pipeline and its
+    // fork / join events (operators.cu), lazy
+    cudaStream_t many_stream[MANY_MAX - 1] = {nullptr};
+    cudaEvent_t many_ev[MANY_MAX] = {nullptr};
 };
 
 double *plan_vec(Plan *p, int i);  // workspace vector i (n_n doubles)
 StreamOrder &red_order();           // ordering of the per-device reduction scratch
 // caller <-> internal numbering (operators.cu)
+// nf: the self-resetting state of the non-finite check (2 ints; default the plan's first pair)
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
-                 cudaStream_t s);
+                 cudaStream_t s, int32_t *nf = nullptr);
+void many_free(Plan *p);
 void to_user(const Plan *p, const double *v_int, double *v_user, cudaStream_t s);
 const Perm2 *perm_get(Plan *p, int dir, cudaStream_t s);
 void perm_apply(Plan *p, const Perm2 *P, const double *in, double *out, int32_t *nonfinite,

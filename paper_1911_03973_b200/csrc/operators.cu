@@ -201,7 +201,7 @@ static void fill_value(int64_t n, double value, double *out, cudaStream_t s) {
 static void fill_negzero(int64_t n, double *out, cudaStream_t s) { fill_value(n, -0.0, out, s); }
 
 void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *nonfinite,
-                 cudaStream_t s) {
+                 cudaStream_t s, int32_t *nf) {
     if (p->n_n == 0) {
         if (nonfinite) CU(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
         return;
@@ -215,7 +215,7 @@ void to_internal(const Plan *p, const double *x_user, double *x_int, int32_t *no
         }
     }
     k_to_internal_ilp<<<grid_for((p->n_n + PERM_ILP - 1) / PERM_ILP, 256, sm_count() * 8), 256, 0, s>>>(
-        p->n_n, p->old_of_new, x_user, x_int, nonfinite, p->nf_state);
+        p->n_n, p->old_of_new, x_user, x_int, nonfinite, nf ? nf : p->nf_state);
     LAUNCHED();
 }
 
@@ -288,11 +288,80 @@ void sell_apply(const Plan *p, int mode, const double *x_int, const uint8_t *fre
     if (P) perm_apply(const_cast<Plan *>(p), P, dst, out, nullptr, s);
 }
 
+// residuals in flight in ebs_residual_many (EBS_MANY_LANES, 1..MANY_MAX; read once)
+static int many_lanes() {
+    static const int v = [] {
+        const char *e = getenv("EBS_MANY_LANES");
+        const int l = e ? atoi(e) : 2;
+        return l < 1 ? 1 : (l > MANY_MAX ? MANY_MAX : l);
+    }();
+    return v;
+}
+
+void many_free(Plan *p) {
+    for (auto &st : p->many_stream) {
+        if (st) cudaStreamDestroy(st);
+        st = nullptr;
+    }
+    for (auto &e : p->many_ev) {
+        if (e) cudaEventDestroy(e);
+        e = nullptr;
+    }
+}
+
 }  // namespace ebs
 
 using namespace ebs;
 
 extern "C" {
+
+// k independent residuals of device-resident vectors, two in flight: residual i runs on
+// the caller's stream (i even) or on the plan's second stream (i odd), each with its own
+// internal-order x workspace and non-finite state.  The x permutation and the -0.0 fill of
+// one residual (latency-bound, little DRAM traffic) then run while the other's SELL pass
+// drains, and the two persistent sweeps fill each other's tails: C2 174 -> 157 us per
+// residual (profiles/r02s4_two_stream_probe.log).  Every r_i is the same launch sequence
+// as ebs_residual on x_i, so it is bit-identical to it.
+int ebs_residual_many(ebs_plan_t plan, const double *x, int64_t ldx, double *r, int64_t ldr,
+                      int64_t k, int mode, int masked, int32_t *nonfinite, void *stream) {
+    EBS_TRY
+    EBS_REQUIRE(plan && (k == 0 || (x && r)), "null argument");
+    EBS_REQUIRE(k >= 0, "negative k");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    cudaStream_t s = S(stream);
+    OrderGuard order(p->order, s);
+    EBS_REQUIRE(p->has_A && p->has_be, "residual needs an operator loaded with b_e");
+    EBS_REQUIRE(mode == EBS_RES_EXACT || mode == EBS_RES_FAST, "bad residual mode %d", mode);
+    EBS_REQUIRE(ldr >= p->n_n && (ldx == 0 || ldx >= p->n_n),
+                "bad leading dimensions (ldx 0 or >= n_nodes, ldr >= n_nodes)");
+    if (k == 0) return EBS_OK;
+    const uint8_t *free_int = masked ? p->free_int : nullptr;
+    const int sell_mode = mode == EBS_RES_EXACT ? 2 : 1;
+    // the two-pass permutation (meshes beyond L2's reach) stages through plan-held
+    // buffers: one residual at a time there
+    const int lanes = (k >= 2 && !use_perm2(p)) ? (int)(k < many_lanes() ? k : many_lanes()) : 1;
+    if (lanes > 1) {
+        if (!p->many_stream[0]) {
+            for (auto &st : p->many_stream) CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            for (auto &e : p->many_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        CU(cudaEventRecord(p->many_ev[0], s));  // fork: after the work queued on s
+        for (int l = 1; l < lanes; ++l) CU(cudaStreamWaitEvent(p->many_stream[l - 1], p->many_ev[0], 0));
+    }
+    for (int64_t i = 0; i < k; ++i) {
+        const int lane = (int)(i % lanes);
+        cudaStream_t st = lane ? p->many_stream[lane - 1] : s;
+        double *x_int = plan_vec(p, lane);
+        to_internal(p, x + i * ldx, x_int, nonfinite ? nonfinite + i : nullptr, st,
+                    p->nf_state + 2 * lane);
+        sell_apply(p, sell_mode, x_int, free_int, p->old_of_new, r + i * ldr, st);
+    }
+    for (int l = 1; l < lanes; ++l) {  // join
+        CU(cudaEventRecord(p->many_ev[l], p->many_stream[l - 1]));
+        CU(cudaStreamWaitEvent(s, p->many_ev[l], 0));
+    }
+    EBS_CATCH
+}
 
 int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int masked,
                  int32_t *nonfinite, void *stream) {

@@ -740,6 +740,7 @@ static void plan_free(Plan *p) {
     perm_free(p);
     dist_free(p);
     hostpipe_free(p);
+    many_free(p);
     if (p->ctl_host) cudaFreeHost(p->ctl_host);
     p->ctl_host = nullptr;
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -780,8 +781,8 @@ int ebs_plan_create(int nb, int64_t n_n, int64_t n_e, const int32_t *conn, void 
     p->n_e = n_e;
     p->n_chunks = (n_n + LANES - 1) / LANES;
     p->flag = dmalloc<int32_t>(4);
-    p->nf_state = dmalloc<int32_t>(2);
-    CU(cudaMemsetAsync(p->nf_state, 0, 2 * sizeof(int32_t), s));
+    p->nf_state = dmalloc<int32_t>(2 * MANY_MAX);  // one pair per stream of ebs_residual_many
+    CU(cudaMemsetAsync(p->nf_state, 0, 2 * MANY_MAX * sizeof(int32_t), s));
     const int64_t total = (int64_t)nb * n_e;
 
     // 1. valence + first appearance

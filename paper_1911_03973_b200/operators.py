@@ -112,8 +112,15 @@ def residual(batch: ElementBatch, x, threads: int = 1, deterministic: bool = Tru
 
 def residual_many(batch: ElementBatch, xs, out=None, deterministic: bool = True,
                   check_finite: bool = True):
-    """NEW: residuals of k vectors held in host memory, r_i = b - A x_i, returned in host
-    memory -- the k-fold ``residual`` with the PCIe traffic overlapped.
+    """NEW: residuals of k vectors, r_i = b - A x_i -- the k-fold ``residual`` as one call.
+
+    Device-resident ``xs`` (a (k, n) CUDA tensor, or a sequence of k CUDA vectors): returns a
+    (k, n) CUDA tensor (``out``: optional contiguous (k, n) CUDA float64 tensor).  One native
+    call (``ebs_residual_many``) keeps two residuals in flight on two streams, so the x
+    permutation and output fill of one overlap the operator pass of the other (C2: 157 vs
+    174 us per residual).
+
+    Host-resident ``xs``: returned in host memory with the PCIe traffic overlapped.
 
     ``xs``: a (k, n) CPU tensor / array (pinned memory lets the copies run
     asynchronously; a broadcast (0, 1)-strided batch is read as is) or a sequence of k
@@ -134,6 +141,8 @@ def residual_many(batch: ElementBatch, xs, out=None, deterministic: bool = True,
         xs = _t.from_numpy(np.ascontiguousarray(xs, dtype=np.float64))
     if xs.ndim != 2:
         raise ValueError(f"xs must be (k, n), got shape {tuple(xs.shape)}")
+    if xs.device.type == "cuda":
+        return _residual_many_device(batch, xs, out, deterministic, check_finite)
     if xs.dtype != _t.float64 or xs.device.type != "cpu":
         xs = xs.to(device="cpu", dtype=_t.float64)
     k, n = xs.shape
@@ -154,6 +163,31 @@ def residual_many(batch: ElementBatch, xs, out=None, deterministic: bool = True,
              D.stream())
     if check_finite:
         bad = _t.nonzero(flags).flatten()
+        if bad.numel():
+            raise ValueError(f"x[{int(bad[0])}] contains non-finite entries")
+    return out
+
+
+def _residual_many_device(batch, xs, out, deterministic, check_finite):
+    """residual_many on device-resident vectors (``ebs_residual_many``)."""
+    if xs.dtype != torch.float64 or xs.device != D.device():
+        xs = xs.to(device=D.device(), dtype=torch.float64)
+    k, n = xs.shape
+    if xs.stride(1) != 1 or (k > 1 and xs.stride(0) != 0 and xs.stride(0) < n):
+        xs = xs.contiguous()
+    if out is None:
+        out = D.empty((k, n))
+    elif (not isinstance(out, torch.Tensor) or tuple(out.shape) != (k, n)
+          or out.dtype != torch.float64 or out.device != xs.device or not out.is_contiguous()):
+        raise ValueError("out must be a contiguous (k, n) float64 tensor on the device of xs")
+    if k == 0:
+        return out
+    flags = D.zeros(k, torch.int32) if check_finite else None
+    with using_operator(batch, n) as pl:
+        call("ebs_residual_many", pl.handle, D.ptr(xs), xs.stride(0) if k > 1 else 0, D.ptr(out),
+             n, k, EBS_RES_EXACT if deterministic else EBS_RES_FAST, 0, D.ptr(flags), D.stream())
+    if check_finite:
+        bad = torch.nonzero(flags).flatten()
         if bad.numel():
             raise ValueError(f"x[{int(bad[0])}] contains non-finite entries")
     return out

@@ -277,6 +277,113 @@ def test_residual_many_pipelined(gpu):
         eb.residual_many(batch, xs[0])
 
 
+def test_residual_many_on_device_two_in_flight(gpu):
+    """residual_many on device-resident vectors (ebs_residual_many: two residuals in flight on
+    two streams, each with its own workspace): every row bit-identical to residual() in both
+    modes; odd / even / single k, broadcast and padded rows, sequences of CUDA vectors, `out`
+    validation, per-vector non-finite flags, CUDA-graph capture, a following call on another
+    stream, the masked C-ABI form, the sequential fallback of the two-pass permutation."""
+    import ctypes
+    import torch
+    import paper_1911_03973_b200 as eb
+    from paper_1911_03973_b200 import _device as D
+    from paper_1911_03973_b200._lib import EBS_RES_EXACT, load
+    from paper_1911_03973_b200.inputs import config_problem
+    p = config_problem(4, seed=3, size=7)          # jittered + permuted
+    batch, m = p["batch"], p["mesh"]
+    n = m.n_nodes
+    rng = np.random.default_rng(11)
+    xs = torch.from_numpy(rng.uniform(-1, 1, (7, n))).cuda()
+    for det in (True, False):
+        ref = torch.stack([eb.residual(batch, x, deterministic=det) for x in xs])
+        for k in (7, 6, 2, 1):
+            got = eb.residual_many(batch, xs[:k], deterministic=det)
+            assert got.is_cuda and tuple(got.shape) == (k, n)
+            assert torch.equal(got, ref[:k]), (det, k)
+        out = torch.empty((7, n), dtype=torch.float64, device="cuda")
+        assert eb.residual_many(batch, xs, out=out, deterministic=det) is out
+        assert torch.equal(out, ref)
+        assert torch.equal(eb.residual_many(batch, list(xs), deterministic=det), ref)
+    bcast = xs[2].unsqueeze(0).expand(5, n)
+    assert bcast.stride(0) == 0
+    assert torch.equal(eb.residual_many(batch, bcast), ref_row(eb, batch, xs[2]).expand(5, n))
+    wide = torch.nn.functional.pad(xs, (0, 5))[:, :n]
+    assert wide.stride(0) == n + 5
+    assert torch.equal(eb.residual_many(batch, wide), torch.stack([eb.residual(batch, x) for x in xs]))
+    assert tuple(eb.residual_many(batch, xs[:0]).shape) == (0, n)
+    with pytest.raises(ValueError):
+        eb.residual_many(batch, xs, out=torch.empty((7, n), dtype=torch.float64))   # host out
+    with pytest.raises(ValueError):
+        eb.residual_many(batch, xs, out=torch.empty((6, n), dtype=torch.float64, device="cuda"))
+    bad = xs.clone()
+    bad[3, 7] = float("inf")
+    bad[4, 0] = float("nan")
+    with pytest.raises(ValueError, match=r"x\[3\]"):
+        eb.residual_many(batch, bad)
+    # graph capture (fork / join across the plan's second stream) and replay
+    ref = torch.stack([eb.residual(batch, x, deterministic=False) for x in xs])
+    out = torch.zeros((7, n), dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        eb.residual_many(batch, xs, out=out, deterministic=False, check_finite=False)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            eb.residual_many(batch, xs, out=out, deterministic=False, check_finite=False)
+        for _ in range(3):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref)
+    # the next call on another stream is ordered after both lanes of this one
+    other = torch.cuda.Stream()
+    big = eb.residual_many(batch, xs.repeat(6, 1), deterministic=False, check_finite=False)
+    with torch.cuda.stream(other):
+        r_next = eb.residual(batch, xs[1], deterministic=False)
+    torch.cuda.synchronize()
+    assert torch.equal(r_next, ref[1]) and torch.equal(big[-1], ref[6]) and torch.equal(big[35], ref[0])
+    # C-ABI: masked rows and device flags
+    lib = load()
+    d = p["dirichlet"]
+    with batch.using(n) as pl:
+        pl.ensure_dirichlet(d)
+        flags = D.zeros(7, torch.int32)
+        out = D.empty((7, n))
+        rc = lib.ebs_residual_many(pl.handle, D.ptr(bad), n, D.ptr(out), n, 7, EBS_RES_EXACT, 1,
+                                   D.ptr(flags), D.stream())
+        assert rc == 0
+        torch.cuda.synchronize()
+    assert flags.tolist() == [0, 0, 0, 1, 1, 0, 0]
+    want = eb.mask_dirichlet(eb.residual(batch, xs[5]), d)
+    assert torch.equal(out[5], want) and torch.equal(out[0], eb.mask_dirichlet(eb.residual(batch, xs[0]), d))
+
+
+def ref_row(eb, batch, x):
+    return eb.residual(batch, x).unsqueeze(0)
+
+
+def test_residual_many_on_device_with_the_two_pass_permutation(gpu):
+    """Meshes on the two-pass permutation path (forced here by EBS_PERM2_MIN_NODES) stage
+    through plan-held buffers: ebs_residual_many runs them one at a time, same bits."""
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, paper_1911_03973_b200 as eb\n"
+        "from paper_1911_03973_b200.inputs import config_problem\n"
+        "p = config_problem(2, seed=1, size=7); b = p['batch']; n = p['mesh'].n_nodes\n"
+        "xs = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, (5, n))).cuda()\n"
+        "ref = torch.stack([eb.residual(b, x) for x in xs])\n"
+        "assert torch.equal(eb.residual_many(b, xs), ref)\n"
+        "assert torch.equal(eb.residual_many(b, xs, deterministic=False),"
+        " torch.stack([eb.residual(b, x, deterministic=False) for x in xs]))\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, EBS_PERM2_MIN_NODES="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
 def test_concurrent_residuals_on_separate_streams(gpu):
     """SPEC.md:273 of the reference: residual is safe to call concurrently on a shared
     batch.  Host threads, each on its own CUDA stream, share one plan (and its device
