@@ -149,7 +149,8 @@ int ebs_residual(ebs_plan_t plan, const double *x, double *r, int mode, int mask
 /* NEW: ebs_residual on k caller-numbered DEVICE vectors (x_i at x + i*ldx, ldx 0 or >=
  * n_nodes; r_i written to r + i*ldr, ldr >= n_nodes; rows must not alias), two residuals
  * in flight: odd i run on a second stream kept by the plan, each stream with its own
- * workspace, forked from and joined back into `stream` (asynchronous; capturable).  The
+ * workspace, forked from and joined back into `stream` (asynchronous; capturable once a
+ * first, uncaptured call has created the plan's second stream and workspace).  The
  * permutation / fill of one residual overlaps the other's operator pass.  Each r_i is
  * bit-identical to ebs_residual on x_i.  nonfinite (DEVICE int32[k], nullable): the
  * per-vector flag of ebs_residual. */

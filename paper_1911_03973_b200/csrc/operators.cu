@@ -334,6 +334,7 @@ int ebs_residual_many(ebs_plan_t plan, const double *x, int64_t ldx, double *r, 
     EBS_REQUIRE(mode == EBS_RES_EXACT || mode == EBS_RES_FAST, "bad residual mode %d", mode);
     EBS_REQUIRE(ldr >= p->n_n && (ldx == 0 || ldx >= p->n_n),
                 "bad leading dimensions (ldx 0 or >= n_nodes, ldr >= n_nodes)");
+    EBS_REQUIRE(x != r, "x and r must not alias");
     if (k == 0) return EBS_OK;
     const uint8_t *free_int = masked ? p->free_int : nullptr;
     const int sell_mode = mode == EBS_RES_EXACT ? 2 : 1;
