@@ -1,3 +1,5 @@
+# A/B of the dynamic-tail experiment (profiles/r02s4_dyn_tail_experiment.patch must be applied:
+# it adds EBS_DYN_ROUNDS; the product build ignores the variable).  Result: profiles/r02s4_dyn_tail_ab.log
 for rep in 1 2; do
 for r in 0 1 2 3 5 8 100; do
   EBS_DYN_ROUNDS=$r python bench.py --no-cpu --no-extra --steps 100 --warmup 5 2>/dev/null | python -c "
