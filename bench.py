@@ -368,6 +368,8 @@ def run_ours(args):
     # steps on a second stream with their own workspace, so the x permutation and -0.0 fill
     # of one step overlap the SELL pass of the other); every step writes its own output row
     total_many = None
+    total_many_ex = None
+    r_exact_many = None
     launches_many = None
     try:
         rows = min(args.steps, 128)   # output rows per call (4.3 GB at most)
@@ -375,8 +377,8 @@ def run_ours(args):
         flags_many = D.zeros(rows, torch.int32)
         rrp, fmp = (ctypes.c_void_p(t.data_ptr()) for t in (r_rows, flags_many))
 
-        def many(k):
-            rc = lib.ebs_residual_many(h, xp, 0, rrp, n_n, k, EBS_RES_FAST, 0, fmp, s)
+        def many(k, mode=EBS_RES_FAST):
+            rc = lib.ebs_residual_many(h, xp, 0, rrp, n_n, k, mode, 0, fmp, s)
             assert rc == 0, rc
 
         many(rows)
@@ -396,11 +398,28 @@ def run_ours(args):
         assert torch.equal(r_rows[0], r_fast) and torch.equal(r_rows[k - 1], r_fast), \
             "ebs_residual_many and ebs_residual disagree"
         assert not bool(flags_many.any())
+        # the bit-exact mode the same way
+        many(rows, EBS_RES_EXACT)
+        torch.cuda.synchronize()
+        em0.record(stream)
+        done = 0
+        while done < args.steps:
+            k = min(rows, args.steps - done)
+            many(k, EBS_RES_EXACT)
+            done += k
+        em1.record(stream)
+        torch.cuda.synchronize()
+        total_many_ex = em0.elapsed_time(em1) / 1e3
+        r_exact_many = r_rows[k - 1].clone()
         del r_rows
     except Exception as e:  # noqa: BLE001 -- report, keep the one-at-a-time number
         print(f"ebs_residual_many unavailable: {e}", file=sys.stderr)
         total_many = None
     total_ex, gather_ex, sell_ex, _ = timed(2, args.steps)
+    total_ex_seq = total_ex
+    if total_many_ex is not None:
+        assert torch.equal(r_exact_many, r_dev), "exact ebs_residual_many and ebs_residual disagree"
+        total_ex = total_many_ex
     # the solver path's operator: matvec on internal-numbered vectors (no permutation in
     # or out, coalesced output) -- what Jacobi / CG / PCG iterate on
     y_int = D.empty(n_n)
@@ -543,8 +562,9 @@ def run_ours(args):
                             "note": "y = A x on plan-internal vectors (solver path), "
                                     "matvec bytes n_e(8nb^2+4nb)+16n_n"},
         "exact_mode": {"value": n_n * args.steps / total_ex / 1e9, "unit": "GDoF/s",
+                       "sequential_value": n_n * args.steps / total_ex_seq / 1e9,
                        "kernel_ms": sell_ex * 1e3,
-                       "note": "bit-identical to ebsolve.residual (b_e streamed per slot)"},
+                       "note": "bit-identical to ebsolve.residual (b_e streamed per slot); value: two in flight (ebs_residual_many), sequential_value: one at a time"},
         "e2e": {"value": n_n * args.steps / t_e2e / 1e9, "unit": "GDoF/s",
                 "h2d_bytes_per_step": 8 * n_n, "d2h_bytes_per_step": 8 * n_n,
                 "wall_s": wall_e2e,
