@@ -268,12 +268,7 @@ class _FacadeModule(types.ModuleType):
         elif inspect.isfunction(value) or inspect.ismethod(value):
             # a host-convention replacement for a device function (monkeypatch): the device
             # code calls it with device objects and uses what it returns
-            host_fn = value
-
-            @functools.wraps(host_fn)
-            def value(*args, __fn=host_fn, **kwargs):
-                return to_device_arg(__fn(*[to_host(a) for a in args],
-                                          **{k: to_host(a) for k, a in kwargs.items()}))
+            value = _host_callback(value)
         setattr(dev, name, value)
 
     def __delattr__(self, name):
